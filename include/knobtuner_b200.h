@@ -1,0 +1,169 @@
+/*
+ * knobtuner_b200.h — C ABI of the B200 search-step engine (libknobtuner_b200.so).
+ *
+ * Drop-in boundary for the data-parallel search step of the reference knob
+ * tuner (/root/reference/pkg/src/knobtuner).  The reference is pure Python;
+ * its "plugin API" is the set of module-level functions the driver imports
+ * by name (driver.py:12-23).  Each entry point below replaces one of them (or
+ * the array kernel inside one of them) and is bound from Python by
+ * paper_1905_12799_b200/_lib.py (ctypes); INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *   - Plain C types only: pointers + sizes.  "_dev" pointers are CUDA device
+ *     memory on the engine's device; everything else is host memory.
+ *   - A configuration is a "row": knob i's index in byte i of a uint64
+ *     (n_knobs <= 8, every cardinality <= 255).  Unused high bytes are 0.
+ *   - Every call returns KT_OK or an error code; kt_last_error() gives the
+ *     message.  Error codes map 1:1 onto the reference's exception types so
+ *     the Python shim re-raises the same class with the same message
+ *     (errors.py:4-41, agent.py:274-277, sampler.py:86-87, cost_model.py:183-184).
+ *   - Calls are stream-ordered on the engine's stream; functions that return
+ *     host results synchronise that stream before returning.
+ */
+#ifndef KNOBTUNER_B200_H
+#define KNOBTUNER_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------ status */
+enum {
+    KT_OK = 0,
+    KT_ERR_VALUE = 1,       /* -> ValueError                                   */
+    KT_ERR_DIMENSION = 2,   /* -> knobtuner.errors.DimensionMismatchError       */
+    KT_ERR_SPACE = 3,       /* -> knobtuner.errors.SpaceValidationError         */
+    KT_ERR_UNSUPPORTED = 4, /* -> NotImplementedError (outside the engine's scope) */
+    KT_ERR_CUDA = 10,       /* -> RuntimeError                                  */
+    KT_ERR_INTERNAL = 11    /* -> RuntimeError                                  */
+};
+
+const char* kt_last_error(void);
+const char* kt_version(void);
+
+/* ------------------------------------------------------------------ engine */
+/* One engine per device: owns a CUDA stream and a growable device workspace. */
+typedef struct kt_engine kt_engine;
+
+int kt_engine_create(int device, kt_engine** out);
+int kt_engine_destroy(kt_engine* e);
+/* Use a caller-owned stream (cudaStream_t) instead of the engine's own; NULL restores it. */
+int kt_engine_set_stream(kt_engine* e, void* cuda_stream);
+int kt_engine_synchronize(kt_engine* e);
+/* Number of engine kernels launched since creation (evidence counter for the bench). */
+int64_t kt_engine_launch_count(const kt_engine* e);
+
+/* ------------------------------------------------------- host RNG streams */
+/* numpy SeedSequence(entropy, spawn_key) -> PCG64 -> random()/integers(0, n)
+ * (numpy/random/bit_generator.pyx SeedSequence, _pcg64.pyx, pcg64.h), used for
+ * the seeds the reference derives at sampler.py:89, sa.py:79-81, agent.py:292-296.
+ * words = little-endian 32-bit words of the entropy int (at least one word).   */
+int kt_pcg64_draw(const uint32_t* entropy_words, int n_entropy_words,
+                  const uint32_t* spawn_words, int n_spawn_words,
+                  int kind /* 0: random() doubles, 1: integers(0, bound) */,
+                  uint64_t bound, int64_t count, void* out /* double[] or int64[] */);
+
+/* --------------------------------------------------- surrogate scoring (K2) */
+/* Replaces CostModel._packed + predict_features (cost_model.py:157-201) and
+ * predict (cost_model.py:401-409).  The forest is given in the reference's
+ * flat per-tree arrays (Tree, cost_model.py:69-77) concatenated; node_offset
+ * has n_trees+1 entries.  feature_table is the (n_knobs x max_card) table of
+ * log2(1 + knob value) computed by the host exactly as feature_table() does
+ * (cost_model.py:235-249); thresholds become per-node index cut points.      */
+typedef struct kt_forest kt_forest;
+
+int kt_forest_create(kt_engine* e, int n_knobs, const int32_t* cards,
+                     const double* feature_table, int max_card,
+                     int n_trees, const int32_t* node_offset,
+                     const int32_t* feature, const double* threshold,
+                     const int32_t* child_left, const int32_t* child_right,
+                     const double* value, double base_score, kt_forest** out);
+int kt_forest_destroy(kt_forest* f);
+int kt_forest_depth(const kt_forest* f);
+/* scores_dev[i] = surrogate fitness of rows_dev[i] (bit-exact with predict_features). */
+int kt_score_trees(kt_engine* e, const kt_forest* f, const uint64_t* rows_dev,
+                   int64_t count, double* scores_dev);
+
+/* ------------------------------------------------ landscape scoring (K3) */
+/* Replaces synthetic_runtime/_hash_unit (backends.py:157-174) and
+ * SyntheticBackend.batch_runtimes (backends.py:272-273).  seed_text is
+ * str(landscape.seed) (the blake2b payload prefix).                        */
+typedef struct kt_landscape kt_landscape;
+
+int kt_landscape_create(kt_engine* e, int n_knobs, int n_centers, const int32_t* centers,
+                        const double* depths, const double* radii, double base_runtime,
+                        double noise_rel, const char* seed_text, kt_landscape** out);
+int kt_landscape_destroy(kt_landscape* l);
+int kt_score_landscape(kt_engine* e, const kt_landscape* l, const uint64_t* rows_dev,
+                       int64_t count, double* runtime_dev);
+
+/* ---------------------------------------------------- adaptive sampling */
+/* First-occurrence dedup (sampler.py:187-192): distinct_dev receives the
+ * distinct rows in order of first occurrence; *n_distinct their count.     */
+int kt_dedup(kt_engine* e, const uint64_t* rows_dev, int64_t count,
+             uint64_t* distinct_dev, int64_t* n_distinct);
+
+/* Per-knob mode over all rows, ties -> smallest index (mode_config, sampler.py:151-158). */
+int kt_mode_vote(kt_engine* e, const uint64_t* rows_dev, int64_t count,
+                 int n_knobs, int32_t* mode_out);
+
+/* Seeded k-means on lattice points (kmeans, sampler.py:72-122).
+ * assignment_out: host int64[m] (may be NULL); centroids_out: host double[k*n];
+ * history_out: host double[100] (may be NULL: then only the final loss is
+ * computed); returns the number of Lloyd passes in *n_passes.               */
+int kt_kmeans(kt_engine* e, const uint64_t* points_dev, int64_t m, int n_knobs,
+              int k, uint64_t seed, double* centroids_out, int64_t* assignment_out,
+              double* loss_out, double* history_out, int32_t* n_passes);
+
+/* Knee scan (knee_scan, sampler.py:125-148): grows k from 8 until
+ * knee_constant * L_k > L_{k-1}; returns the breaking k's clustering.
+ * scanned_k/scanned_loss: host arrays of capacity 56.                       */
+int kt_knee_scan(kt_engine* e, const uint64_t* points_dev, int64_t m, int n_knobs,
+                 uint64_t seed, double knee_constant, int k_max,
+                 int32_t* scanned_k, double* scanned_loss, int32_t* n_scanned,
+                 double* centroids_out /* k_max*n */, int64_t* assignment_out /* m or NULL */);
+
+/* Statistics of one adaptive_sample call. */
+typedef struct kt_sample_info {
+    int64_t n_distinct;     /* m */
+    int32_t chosen_k;       /* 0 when the <=8-distinct bypass was taken */
+    int32_t n_scanned;
+    int32_t scanned_k[56];
+    double scanned_loss[56];
+    int32_t lloyd_passes;   /* sum over scanned k */
+    int32_t used_mode;      /* 1 if a visited centroid was replaced by the mode */
+} kt_sample_info;
+
+/* The whole adaptive_sample (sampler.py:173-215): dedup -> knee k-means ->
+ * round centroids -> visited/mode replacement -> dedup of the batch.
+ * visited_rows: host array of measured configurations (VisitedSet).
+ * batch_out: host, capacity 63 rows.                                        */
+int kt_adaptive_sample(kt_engine* e, const uint64_t* rows_dev, int64_t count,
+                       int n_knobs, const int32_t* cards,
+                       const uint64_t* visited_rows, int64_t n_visited,
+                       uint64_t seed, double knee_constant,
+                       uint64_t* batch_out, int32_t* batch_len, kt_sample_info* info);
+
+/* ------------------------------------------------ simulated annealing (K10) */
+/* run_sa_round (sa.py:62-122).  The first min(n_starts, chains) rows of
+ * starts_dev are used; missing starts are padded from the parent stream
+ * exactly like sa.py:83-85.  Chain c's PCG64 stream is derived on the device
+ * from SeedSequence(seed, spawn_key=(c,)) (sa.py:79-81).  Outputs are the
+ * reference's chain-major trajectory (start, then each accepted move), compact:
+ * rows/scores/step indices, *n_out entries; capacity chains * (steps + 1).
+ * seed_words: little-endian 32-bit words of seed & (2^64 - 1).            */
+int kt_sa_chains(kt_engine* e, const kt_forest* f, const uint64_t* starts_dev, int32_t n_starts,
+                 int32_t chains, int32_t steps, const int32_t* cards, int n_knobs,
+                 const uint32_t* seed_words, int n_seed_words,
+                 int has_initial_temperature, double initial_temperature, double cooling,
+                 uint64_t* rows_out_dev, double* scores_out_dev, int32_t* steps_out_dev,
+                 int64_t* n_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KNOBTUNER_B200_H */

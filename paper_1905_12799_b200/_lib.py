@@ -1,0 +1,183 @@
+"""ctypes binding of libknobtuner_b200.so (include/knobtuner_b200.h).
+
+There is no CPU fallback: if the library or a CUDA device is missing, every
+engine call raises ``EngineUnavailable`` (a RuntimeError) with the reason.
+"""
+
+from __future__ import annotations
+
+import contextlib
+import ctypes as C
+import re
+import threading
+from pathlib import Path
+
+from . import errors
+
+PKG = Path(__file__).resolve().parent
+LIB_PATH = PKG / "lib" / "libknobtuner_b200.so"
+HEADER = PKG.parent / "include" / "knobtuner_b200.h"
+
+KT_OK, KT_ERR_VALUE, KT_ERR_DIMENSION, KT_ERR_SPACE, KT_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
+
+P = C.c_void_p
+i32, i64, u64, f64 = C.c_int32, C.c_int64, C.c_uint64, C.c_double
+pi32, pi64, pu64, pf64, pu32 = (C.POINTER(t) for t in (C.c_int32, C.c_int64, C.c_uint64, C.c_double, C.c_uint32))
+
+
+class EngineUnavailable(RuntimeError):
+    """The CUDA engine library or device is not available (no CPU fallback exists)."""
+
+
+class SampleInfo(C.Structure):
+    _fields_ = [
+        ("n_distinct", C.c_int64),
+        ("chosen_k", C.c_int32),
+        ("n_scanned", C.c_int32),
+        ("scanned_k", C.c_int32 * 56),
+        ("scanned_loss", C.c_double * 56),
+        ("lloyd_passes", C.c_int32),
+        ("used_mode", C.c_int32),
+    ]
+
+
+# name -> (restype, argtypes); every entry must exist in the header and the .so
+SIGNATURES = {
+    "kt_last_error": (C.c_char_p, []),
+    "kt_version": (C.c_char_p, []),
+    "kt_engine_create": (C.c_int, [C.c_int, C.POINTER(P)]),
+    "kt_engine_destroy": (C.c_int, [P]),
+    "kt_engine_set_stream": (C.c_int, [P, P]),
+    "kt_engine_synchronize": (C.c_int, [P]),
+    "kt_engine_launch_count": (C.c_int64, [P]),
+    "kt_pcg64_draw": (C.c_int, [pu32, C.c_int, pu32, C.c_int, C.c_int, u64, i64, P]),
+    "kt_forest_create": (C.c_int, [P, C.c_int, pi32, pf64, C.c_int, C.c_int, pi32, pi32, pf64, pi32, pi32, pf64,
+                                   f64, C.POINTER(P)]),
+    "kt_forest_destroy": (C.c_int, [P]),
+    "kt_forest_depth": (C.c_int, [P]),
+    "kt_score_trees": (C.c_int, [P, P, P, i64, P]),
+    "kt_landscape_create": (C.c_int, [P, C.c_int, C.c_int, pi32, pf64, pf64, f64, f64, C.c_char_p, C.POINTER(P)]),
+    "kt_landscape_destroy": (C.c_int, [P]),
+    "kt_score_landscape": (C.c_int, [P, P, P, i64, P]),
+    "kt_dedup": (C.c_int, [P, P, i64, P, pi64]),
+    "kt_mode_vote": (C.c_int, [P, P, i64, C.c_int, pi32]),
+    "kt_kmeans": (C.c_int, [P, P, i64, C.c_int, C.c_int, u64, pf64, pi64, pf64, pf64, pi32]),
+    "kt_knee_scan": (C.c_int, [P, P, i64, C.c_int, u64, f64, C.c_int, pi32, pf64, pi32, pf64, pi64]),
+    "kt_adaptive_sample": (C.c_int, [P, P, i64, C.c_int, pi32, pu64, i64, u64, f64, pu64, pi32,
+                                     C.POINTER(SampleInfo)]),
+    "kt_sa_chains": (C.c_int, [P, P, P, i32, i32, i32, pi32, C.c_int, pu32, C.c_int, C.c_int, f64, f64, P, P, P,
+                               pi64]),
+}
+
+_lock = threading.Lock()
+_lib = None
+_load_error: str | None = None
+_engines: dict[int, "Engine"] = {}
+
+
+def header_symbols() -> list[str]:
+    """Function names declared by include/knobtuner_b200.h."""
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"\b(kt_[a-z0-9_]+)\s*\(", text)))
+
+
+def load(path: Path | None = None):
+    """Load the shared library (no GPU needed).  Raises EngineUnavailable if absent."""
+    global _lib, _load_error
+    with _lock:
+        if _lib is not None:
+            return _lib
+        p = Path(path) if path else LIB_PATH
+        if not p.exists():
+            _load_error = f"{p} not built (run __graft_entry__.build() or python -m paper_1905_12799_b200.build)"
+            raise EngineUnavailable(_load_error)
+        lib = C.CDLL(str(p))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def raise_for(code: int) -> None:
+    if code == KT_OK:
+        return
+    msg = (_lib.kt_last_error() or b"").decode("utf-8", "replace")
+    if code == KT_ERR_VALUE:
+        raise ValueError(msg)
+    if code == KT_ERR_DIMENSION:
+        raise errors.DimensionMismatchError(msg)
+    if code == KT_ERR_SPACE:
+        raise errors.SpaceValidationError(msg)
+    if code == KT_ERR_UNSUPPORTED:
+        raise NotImplementedError(msg)
+    raise RuntimeError(f"knobtuner_b200 engine error {code}: {msg}")
+
+
+def call(name: str, *args) -> None:
+    raise_for(getattr(load(), name)(*args))
+
+
+class Engine:
+    """One per CUDA device; wraps kt_engine (stream + workspace)."""
+
+    def __init__(self, device: int):
+        import torch
+
+        lib = load()
+        h = P()
+        raise_for(lib.kt_engine_create(int(device), C.byref(h)))
+        self.handle = h
+        self.device = int(device)
+        # all engine work is ordered on one torch-visible stream
+        self.stream = torch.cuda.Stream(device=self.device)
+        raise_for(lib.kt_engine_set_stream(h, P(self.stream.cuda_stream)))
+
+    @contextlib.contextmanager
+    def scope(self):
+        """Run a block on the engine stream, ordered after/before the caller's stream."""
+        import torch
+
+        caller = torch.cuda.current_stream(self.device)
+        self.stream.wait_stream(caller)
+        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
+            yield self
+        caller.wait_stream(self.stream)
+
+    @property
+    def launches(self) -> int:
+        return int(load().kt_engine_launch_count(self.handle))
+
+    def synchronize(self) -> None:
+        call("kt_engine_synchronize", self.handle)
+
+    def set_stream(self, stream_ptr: int | None) -> None:
+        call("kt_engine_set_stream", self.handle, P(stream_ptr) if stream_ptr else None)
+
+
+def engine(device: int | None = None) -> Engine:
+    """The engine for ``device`` (default: torch's current CUDA device)."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise EngineUnavailable("no CUDA device visible; the B200 engine has no CPU fallback")
+    dev = torch.cuda.current_device() if device is None else int(device)
+    with _lock:
+        e = _engines.get(dev)
+    if e is None:
+        e = Engine(dev)
+        with _lock:
+            _engines[dev] = e
+    return e
+
+
+def ptr(t) -> P:
+    """Raw device/host pointer of a torch tensor or numpy array."""
+    if hasattr(t, "data_ptr"):
+        return P(t.data_ptr())
+    return P(t.ctypes.data)
+
+
+def as_ptr(arr, ctype):
+    return arr.ctypes.data_as(C.POINTER(ctype))

@@ -1,0 +1,199 @@
+"""Boosted-tree surrogate scoring on the B200 (K2) — drop-in for the scoring half of
+knobtuner/cost_model.py.
+
+* ``CostModel`` / ``Tree``  — mirror of the reference's frozen model types
+  (cost_model.py:69-218, JSON format included) so models round-trip.
+* ``device_forest(model, space)`` — the model packed for the engine
+  (complete-heap trees with integer cut points, see csrc/trees.cu), cached on
+  the model object like the reference caches ``_packed_arrays``
+  (cost_model.py:157-179).
+* ``predict(model, space, configs)`` — same signature, checks, errors and
+  bit-exact results as cost_model.py:401-409.
+* ``predict_rows(model, space, rows)`` — the array path: device rows in,
+  device float64 scores out (no Python objects on the hot path).
+"""
+
+from __future__ import annotations
+
+import json
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib, errors
+from . import space as sp
+
+
+@dataclass(frozen=True)
+class Tree:
+    feature: np.ndarray  # (nodes,) int32, -1 = leaf
+    threshold: np.ndarray  # (nodes,) float64
+    child_left: np.ndarray  # (nodes,) int32
+    child_right: np.ndarray  # (nodes,) int32
+    value: np.ndarray  # (nodes,) float64
+
+    @classmethod
+    def from_dict(cls, obj: dict) -> "Tree":
+        cols: dict[str, list] = {"f": [], "t": [], "l": [], "r": [], "v": []}
+
+        def visit(node: dict) -> int:
+            me = len(cols["f"])
+            for key, init in (("f", -1), ("t", 0.0), ("l", -1), ("r", -1), ("v", 0.0)):
+                cols[key].append(init)
+            if "value" in node:
+                cols["v"][me] = float(node["value"])
+            else:
+                cols["f"][me] = int(node["feature"])
+                cols["t"][me] = float(node["threshold"])
+                cols["l"][me] = visit(node["left"])
+                cols["r"][me] = visit(node["right"])
+            return me
+
+        visit(obj)
+        return cls(np.array(cols["f"], dtype=np.int32), np.array(cols["t"], dtype=np.float64),
+                   np.array(cols["l"], dtype=np.int32), np.array(cols["r"], dtype=np.int32),
+                   np.array(cols["v"], dtype=np.float64))
+
+    def to_dict(self) -> dict:
+        def node(i: int) -> dict:
+            if self.feature[i] < 0:
+                return {"value": float(self.value[i])}
+            return {"feature": int(self.feature[i]), "threshold": float(self.threshold[i]),
+                    "left": node(int(self.child_left[i])), "right": node(int(self.child_right[i]))}
+
+        return node(0)
+
+
+@dataclass(frozen=True)
+class CostModel:
+    trees: tuple
+    base_score: float
+    feature_count: int
+
+    @classmethod
+    def sentinel(cls, feature_count: int, base_score: float = 0.0) -> "CostModel":
+        return cls(trees=(), base_score=base_score, feature_count=feature_count)
+
+    @classmethod
+    def from_json(cls, text: str) -> "CostModel":
+        return cls.from_dict(json.loads(text))
+
+    @classmethod
+    def from_dict(cls, obj: dict) -> "CostModel":
+        return cls(trees=tuple(Tree.from_dict(t) for t in obj["trees"]), base_score=float(obj["base_score"]),
+                   feature_count=int(obj["feature_count"]))
+
+    def to_json(self) -> str:
+        return json.dumps({"base_score": self.base_score, "feature_count": self.feature_count,
+                           "trees": [t.to_dict() for t in self.trees]}, sort_keys=True)
+
+
+def feature_table(space) -> tuple[np.ndarray, np.ndarray]:
+    """log2(1 + value) lookup and negative-prefix counts (cost_model.py:235-249)."""
+    vals = sp.knob_values(space)
+    width = max(len(v) for v in vals)
+    table = np.zeros((len(vals), width), dtype=np.float64)
+    neg = np.zeros(len(vals), dtype=np.int64)
+    for j, v in enumerate(vals):
+        a = np.asarray(v, dtype=np.float64)
+        neg[j] = int((a < 0).sum())
+        with np.errstate(invalid="ignore", divide="ignore"):
+            table[j, : a.size] = np.log2(1.0 + a)
+    return table, neg
+
+
+class DeviceForest:
+    """kt_forest handle: the model packed for one space on one device."""
+
+    def __init__(self, model, space, engine: _lib.Engine):
+        cards = sp.check_engine_space(space)
+        table, neg = feature_table(space)
+        table = table.copy()
+        for j, k in enumerate(neg):  # negative settings are rejected before scoring;
+            table[j, :k] = -np.inf   # -inf keeps the cut-point search monotone
+        trees = list(model.trees)
+        offs = [0]
+        for t in trees:
+            offs.append(offs[-1] + int(np.asarray(t.feature).size))
+        cat = lambda attr, dt: (np.ascontiguousarray(np.concatenate([np.asarray(getattr(t, attr), dtype=dt) for t in trees]))
+                                if trees else np.zeros(1, dtype=dt))
+        feat, thr = cat("feature", np.int32), cat("threshold", np.float64)
+        left, right, val = cat("child_left", np.int32), cat("child_right", np.int32), cat("value", np.float64)
+        node_off = np.asarray(offs, dtype=np.int32)
+        table = np.ascontiguousarray(table)
+        h = _lib.P()
+        _lib.call("kt_forest_create", engine.handle, int(cards.size), _lib.as_ptr(cards, _lib.C.c_int32),
+                  _lib.as_ptr(table, _lib.C.c_double), int(table.shape[1]), len(trees),
+                  _lib.as_ptr(node_off, _lib.C.c_int32), _lib.as_ptr(feat, _lib.C.c_int32),
+                  _lib.as_ptr(thr, _lib.C.c_double), _lib.as_ptr(left, _lib.C.c_int32),
+                  _lib.as_ptr(right, _lib.C.c_int32), _lib.as_ptr(val, _lib.C.c_double),
+                  float(model.base_score), _lib.C.byref(h))
+        self.handle = h
+        self.neg_prefix = neg
+        self.n_knobs = int(cards.size)
+        self.depth = int(_lib.load().kt_forest_depth(h))
+        self.device = engine.device
+
+    def __del__(self):
+        try:
+            _lib.load().kt_forest_destroy(self.handle)
+        except Exception:
+            pass
+
+
+def _space_key(space) -> tuple:
+    return (space.name, tuple(tuple(v) for v in sp.knob_values(space)))
+
+
+def device_forest(model, space, engine: _lib.Engine | None = None) -> DeviceForest:
+    engine = engine or _lib.engine()
+    key = (engine.device, _space_key(space))
+    cache = getattr(model, "__dict__", {}).get("_b200_forests")
+    if cache is None:
+        cache = {}
+        try:
+            object.__setattr__(model, "_b200_forests", cache)
+        except (AttributeError, TypeError):
+            pass
+    f = cache.get(key)
+    if f is None:
+        f = DeviceForest(model, space, engine)
+        cache[key] = f
+    return f
+
+
+def _check_model(model, space) -> None:
+    if model.feature_count != len(space.knobs):
+        raise errors.DimensionMismatchError(
+            f"model expects {model.feature_count} features, space {space.name!r} has {len(space.knobs)} knobs")
+
+
+def predict_rows(model, space, rows, out=None, engine: _lib.Engine | None = None):
+    """Device path: ``rows`` is a CUDA int64/uint64 tensor of packed rows; returns CUDA float64 scores."""
+    import torch
+
+    _check_model(model, space)
+    engine = engine or _lib.engine()
+    f = device_forest(model, space, engine)
+    n = int(rows.numel())
+    with engine.scope():
+        if out is None:
+            out = torch.empty(n, dtype=torch.float64, device=rows.device)
+        _lib.call("kt_score_trees", engine.handle, f.handle, _lib.ptr(rows), n, _lib.ptr(out))
+    return out
+
+
+def predict(model, space, configs) -> np.ndarray:
+    """Surrogate fitness per configuration, in input order (cost_model.py:401-409)."""
+    import torch
+
+    _check_model(model, space)
+    if not configs:
+        return np.empty(0, dtype=np.float64)
+    idx = sp.index_matrix(space, configs)
+    engine = _lib.engine()
+    f = device_forest(model, space, engine)
+    if (idx < f.neg_prefix[None, :]).any():
+        raise ValueError("featurize requires non-negative knob values")
+    rows = torch.from_numpy(sp.pack(idx).view(np.int64)).to(f"cuda:{engine.device}")
+    return predict_rows(model, space, rows, engine=engine).cpu().numpy()

@@ -1,0 +1,138 @@
+// common.cuh — shared types, error plumbing and numpy-order float helpers.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <unordered_map>
+
+#include "../../include/knobtuner_b200.h"
+
+namespace kt {
+
+// ---------------------------------------------------------------- errors
+struct Error {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg);
+void set_last_error(const std::string& msg);
+
+#define KT_CUDA(call)                                                                   \
+    do {                                                                                \
+        cudaError_t _e = (call);                                                        \
+        if (_e != cudaSuccess)                                                          \
+            ::kt::fail(KT_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+// Wrap an extern "C" body: converts exceptions into status codes.
+#define KT_API_BEGIN try {
+#define KT_API_END                                        \
+    }                                                     \
+    catch (const ::kt::Error& err) {                      \
+        ::kt::set_last_error(err.msg);                    \
+        return err.code;                                  \
+    }                                                     \
+    catch (const std::exception& ex) {                    \
+        ::kt::set_last_error(ex.what());                  \
+        return KT_ERR_INTERNAL;                           \
+    }                                                     \
+    return KT_OK;
+
+// ---------------------------------------------------------------- layout
+constexpr int kMaxKnobs = 8;      // a row is one uint64: knob i in byte i
+constexpr int kMaxCard = 255;     // index 255 never occurs -> usable as a sentinel
+constexpr uint64_t kEmptyRow = ~0ull;
+
+__host__ __device__ __forceinline__ int row_byte(uint64_t row, int i) {
+    return int((row >> (8 * i)) & 0xffu);
+}
+
+// ---------------------------------------------------------- numpy sums
+// numpy's pairwise_sum for a contiguous run of n <= 8 float64 values
+// (numpy/_core/src/umath/loops_utils.h.src): n < 8 sums sequentially from
+// 0.0, n == 8 uses the 8-accumulator tree.  All ops are explicit _rn
+// intrinsics so no FMA contraction can change the rounding.
+__device__ __forceinline__ double np_sum_small(const double* t, int n) {
+    if (n == 8) {
+        double a = __dadd_rn(__dadd_rn(t[0], t[1]), __dadd_rn(t[2], t[3]));
+        double b = __dadd_rn(__dadd_rn(t[4], t[5]), __dadd_rn(t[6], t[7]));
+        return __dadd_rn(a, b);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        if (i < n) s = __dadd_rn(s, t[i]);
+    return s;
+}
+
+// ((p - c)**2).sum(axis=-1) for a lattice point p (row) and float64 centroid c.
+__device__ __forceinline__ double np_sq_dist(uint64_t row, const double* c, int n) {
+    double t[kMaxKnobs];
+#pragma unroll
+    for (int i = 0; i < kMaxKnobs; ++i) {
+        if (i < n) {
+            double d = __dsub_rn(double(row_byte(row, i)), c[i]);
+            t[i] = __dmul_rn(d, d);
+        }
+    }
+    return np_sum_small(t, n);
+}
+
+__device__ __forceinline__ int int_sq_dist(uint64_t a, uint64_t b, int n) {
+    int s = 0;
+#pragma unroll
+    for (int i = 0; i < kMaxKnobs; ++i) {
+        if (i < n) {
+            int d = row_byte(a, i) - row_byte(b, i);
+            s += d * d;
+        }
+    }
+    return s;
+}
+
+// 64-bit mixer (murmur3 finaliser) for the dedup hash tables.
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t k) {
+    k ^= k >> 33;
+    k *= 0xff51afd7ed558ccdull;
+    k ^= k >> 33;
+    k *= 0xc4ceb9fe1a85ec53ull;
+    k ^= k >> 33;
+    return k;
+}
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace kt
+
+// ------------------------------------------------------------------ engine
+struct kt_engine {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    int64_t launches = 0;
+    struct Buf {
+        void* ptr = nullptr;
+        size_t bytes = 0;
+    };
+    std::unordered_map<std::string, Buf> dev;
+    std::unordered_map<std::string, Buf> pinned;
+
+    // Named, growable device scratch (contents undefined after growth).
+    void* scratch(const std::string& name, size_t bytes);
+    // Named, growable pinned host staging buffer.
+    void* staging(const std::string& name, size_t bytes);
+    void note_launch(int n = 1) { launches += n; }
+    void check_launch(const char* what);
+    void sync();
+};
+
+namespace kt {
+// Launch helpers shared across translation units.
+int occupancy_blocks(const void* kernel, int threads, size_t smem);
+// out[i] = sum(in[0..i)), out[n] = total; n <= 16M (single-block scan).
+void exclusive_scan(kt_engine* e, const int64_t* in, int64_t* out, int n);
+}  // namespace kt

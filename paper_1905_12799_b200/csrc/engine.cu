@@ -1,0 +1,132 @@
+// engine.cu — engine lifetime, workspace, error plumbing, host RNG entry point.
+#include <cstring>
+#include <stdexcept>
+#include <vector>
+
+#include "common.cuh"
+#include "rng.cuh"
+
+namespace kt {
+
+static thread_local std::string g_last_error;
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+
+int occupancy_blocks(const void* kernel, int threads, size_t smem) {
+    int blocks = 0;
+    KT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, threads, smem));
+    return blocks;
+}
+
+}  // namespace kt
+
+void* kt_engine::scratch(const std::string& name, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    Buf& b = dev[name];
+    if (b.bytes < bytes) {
+        if (b.ptr) KT_CUDA(cudaFreeAsync(b.ptr, stream));
+        size_t grow = bytes + bytes / 4;
+        KT_CUDA(cudaMallocAsync(&b.ptr, grow, stream));
+        b.bytes = grow;
+    }
+    return b.ptr;
+}
+
+void* kt_engine::staging(const std::string& name, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    Buf& b = pinned[name];
+    if (b.bytes < bytes) {
+        if (b.ptr) {
+            KT_CUDA(cudaStreamSynchronize(stream));
+            KT_CUDA(cudaFreeHost(b.ptr));
+        }
+        size_t grow = bytes + bytes / 4;
+        KT_CUDA(cudaMallocHost(&b.ptr, grow));
+        b.bytes = grow;
+    }
+    return b.ptr;
+}
+
+void kt_engine::check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) kt::fail(KT_ERR_CUDA, std::string("launch of ") + what + ": " + cudaGetErrorString(e));
+    note_launch();
+}
+
+void kt_engine::sync() { KT_CUDA(cudaStreamSynchronize(stream)); }
+
+extern "C" {
+
+const char* kt_last_error(void) { return kt::g_last_error.c_str(); }
+
+const char* kt_version(void) { return "knobtuner_b200 0.1 (sm_100a)"; }
+
+int kt_engine_create(int device, kt_engine** out) {
+    KT_API_BEGIN
+    if (!out) kt::fail(KT_ERR_VALUE, "out is NULL");
+    int count = 0;
+    KT_CUDA(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) kt::fail(KT_ERR_VALUE, "no CUDA device " + std::to_string(device));
+    KT_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    KT_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) kt::fail(KT_ERR_UNSUPPORTED, std::string("engine is built for sm_100a; device is ") + prop.name);
+    auto* e = new kt_engine();
+    e->device = device;
+    e->num_sms = prop.multiProcessorCount;
+    KT_CUDA(cudaStreamCreateWithFlags(&e->own_stream, cudaStreamNonBlocking));
+    e->stream = e->own_stream;
+    *out = e;
+    KT_API_END
+}
+
+int kt_engine_destroy(kt_engine* e) {
+    KT_API_BEGIN
+    if (!e) return KT_OK;
+    cudaSetDevice(e->device);
+    cudaStreamSynchronize(e->stream);
+    for (auto& kv : e->dev)
+        if (kv.second.ptr) cudaFree(kv.second.ptr);
+    for (auto& kv : e->pinned)
+        if (kv.second.ptr) cudaFreeHost(kv.second.ptr);
+    if (e->own_stream) cudaStreamDestroy(e->own_stream);
+    delete e;
+    KT_API_END
+}
+
+int kt_engine_set_stream(kt_engine* e, void* s) {
+    KT_API_BEGIN
+    KT_CUDA(cudaStreamSynchronize(e->stream));
+    e->stream = s ? static_cast<cudaStream_t>(s) : e->own_stream;
+    KT_API_END
+}
+
+int kt_engine_synchronize(kt_engine* e) {
+    KT_API_BEGIN
+    e->sync();
+    KT_API_END
+}
+
+int64_t kt_engine_launch_count(const kt_engine* e) { return e ? e->launches : 0; }
+
+int kt_pcg64_draw(const uint32_t* entropy, int ne, const uint32_t* spawn, int ns, int kind,
+                  uint64_t bound, int64_t count, void* out) {
+    KT_API_BEGIN
+    if (ne < 1 || ne > 16 || ns < 0 || ns > 16) kt::fail(KT_ERR_VALUE, "entropy/spawn word counts out of range");
+    kt::Pcg64 g = kt::pcg64_from_seed_sequence(entropy, ne, spawn, ns);
+    if (kind == 0) {
+        double* o = static_cast<double*>(out);
+        for (int64_t i = 0; i < count; ++i) o[i] = g.random();
+    } else if (kind == 1) {
+        if (bound == 0 || bound > 0x100000000ull) kt::fail(KT_ERR_VALUE, "bound must be in [1, 2^32]");
+        int64_t* o = static_cast<int64_t*>(out);
+        for (int64_t i = 0; i < count; ++i) o[i] = int64_t(g.bounded32(uint32_t(bound - 1)));
+    } else {
+        kt::fail(KT_ERR_VALUE, "kind must be 0 (random) or 1 (integers)");
+    }
+    KT_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,46 @@
+// forest.cuh — packed forest handle and the device tree walk (shared by K2 and K10).
+#pragma once
+
+#include <vector>
+
+#include "common.cuh"
+
+struct kt_forest {
+    int n_knobs = 0;
+    int depth = 1;
+    int n_trees = 0;
+    int words_per_tree = 0;  // 8-byte words: super nodes then leaves
+    double base = 0.0;
+    uint64_t* dev = nullptr;  // n_trees * words_per_tree words
+    std::vector<uint64_t> host;
+    int device = 0;
+};
+
+namespace kt {
+
+// One tree of depth D: super nodes (two levels per 64-bit load), then leaves.
+template <int D>
+__device__ __forceinline__ double walk_tree(const uint64_t* __restrict__ t, uint32_t lo, uint32_t hi) {
+    int pos = 0;     // index within the current level
+    int base = 0;    // offset of the current super-node level
+#pragma unroll
+    for (int d = 0; d < D; d += 2) {
+        uint64_t w = t[base + pos];
+        uint32_t e = uint32_t(w) & 0xffffu;
+        uint32_t b = __byte_perm(lo, hi, e & 7u) & 0xffu;
+        int go = b >= (e >> 8);
+        pos = 2 * pos + go;
+        if (d + 1 < D) {
+            uint32_t e1 = uint32_t(w >> (16 * (1 + go))) & 0xffffu;
+            uint32_t b1 = __byte_perm(lo, hi, e1 & 7u) & 0xffu;
+            pos = 2 * pos + int(b1 >= (e1 >> 8));
+        }
+        base += 1 << d;
+    }
+    return __longlong_as_double((long long)t[base + pos]);
+}
+
+
+void score_trees(kt_engine* e, const kt_forest* f, const uint64_t* rows, int64_t count, double* out);
+
+}  // namespace kt

@@ -1,0 +1,190 @@
+// landscape.cu — K3 score_landscape: the synthetic "fake hardware" oracle.
+//
+// Replaces synthetic_runtime / _hash_unit (backends.py:157-174):
+//   runtime = base * (1 - sum_j depth_j * exp(-|x - c_j|^2 / r_j^2))
+//   runtime *= 1 + noise * u,  u = 2 * (blake2b64("seed:i0,i1,...") / 2^64) - 1
+//   runtime = max(runtime, 0.01 * base)
+// |x - c_j|^2 is an integer (lattice points), so it is exact in any order; the
+// remaining float64 ops follow the reference's evaluation order with explicit
+// _rn intrinsics.  exp() is CUDA's (<= 1 ulp from glibc's), hence the
+// north-star tolerance for runtimes rather than bit equality.
+//
+// blake2b (RFC 7693), unkeyed, 8-byte digest, one 128-byte block: the payload
+// "seed:" + decimal indices joined by ',' is at most 21 + 1 + 8 * 4 bytes.
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+constexpr int kMaxCenters = 16;
+
+struct kt_landscape {
+    int n = 0;
+    int n_centers = 0;
+    double base = 1.0;
+    double noise = 0.0;
+    std::string prefix;  // str(seed) + ":"
+    int32_t centers[kMaxCenters][8] = {};
+    double depths[kMaxCenters] = {};
+    double radii[kMaxCenters] = {};
+};
+
+namespace kt {
+
+struct LandscapeArgs {
+    int n, n_centers, prefix_len;
+    double base, noise;
+    int32_t centers[kMaxCenters][8];
+    double depths[kMaxCenters];
+    double r2[kMaxCenters];
+    unsigned char prefix[64];
+};
+
+__device__ __constant__ uint64_t kBlakeIV[8] = {0x6a09e667f3bcc908ull, 0xbb67ae8584caa73bull, 0x3c6ef372fe94f82bull,
+                                               0xa54ff53a5f1d36f1ull, 0x510e527fade682d1ull, 0x9b05688c2b3e6c1full,
+                                               0x1f83d9abfb41bd6bull, 0x5be0cd19137e2179ull};
+
+__device__ __forceinline__ uint64_t rotr64(uint64_t x, int r) { return (x >> r) | (x << (64 - r)); }
+
+#define KT_G(a, b, c, d, x, y)      \
+    a = a + b + x;                  \
+    d = rotr64(d ^ a, 32);          \
+    c = c + d;                      \
+    b = rotr64(b ^ c, 24);          \
+    a = a + b + y;                  \
+    d = rotr64(d ^ a, 16);          \
+    c = c + d;                      \
+    b = rotr64(b ^ c, 63);
+
+// blake2b-64 of a single final block m[16] holding `len` bytes.
+__device__ uint64_t blake2b64_one_block(const uint64_t m[16], uint64_t len) {
+    constexpr unsigned char sigma[12][16] = {
+        {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15}, {14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3},
+        {11, 8, 12, 0, 5, 2, 15, 13, 10, 14, 3, 6, 7, 1, 9, 4}, {7, 9, 3, 1, 13, 12, 11, 14, 2, 6, 5, 10, 4, 0, 15, 8},
+        {9, 0, 5, 7, 2, 4, 10, 15, 14, 1, 11, 12, 6, 8, 3, 13}, {2, 12, 6, 10, 0, 11, 8, 3, 4, 13, 7, 5, 15, 14, 1, 9},
+        {12, 5, 1, 15, 14, 13, 4, 10, 0, 7, 6, 3, 9, 2, 8, 11}, {13, 11, 7, 14, 12, 1, 3, 9, 5, 0, 15, 4, 8, 6, 2, 10},
+        {6, 15, 14, 9, 11, 3, 0, 8, 12, 2, 13, 7, 1, 4, 10, 5}, {10, 2, 8, 4, 7, 6, 1, 5, 15, 11, 9, 14, 3, 12, 13, 0},
+        {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15}, {14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3}};
+    const uint64_t h0 = kBlakeIV[0] ^ 0x01010008ull;  // digest 8 bytes, no key
+    uint64_t v0 = h0, v1 = kBlakeIV[1], v2 = kBlakeIV[2], v3 = kBlakeIV[3];
+    uint64_t v4 = kBlakeIV[4], v5 = kBlakeIV[5], v6 = kBlakeIV[6], v7 = kBlakeIV[7];
+    uint64_t v8 = kBlakeIV[0], v9 = kBlakeIV[1], v10 = kBlakeIV[2], v11 = kBlakeIV[3];
+    uint64_t v12 = kBlakeIV[4] ^ len, v13 = kBlakeIV[5], v14 = ~kBlakeIV[6], v15 = kBlakeIV[7];
+#pragma unroll
+    for (int r = 0; r < 12; ++r) {
+        const unsigned char* s = sigma[r];
+        KT_G(v0, v4, v8, v12, m[s[0]], m[s[1]]);
+        KT_G(v1, v5, v9, v13, m[s[2]], m[s[3]]);
+        KT_G(v2, v6, v10, v14, m[s[4]], m[s[5]]);
+        KT_G(v3, v7, v11, v15, m[s[6]], m[s[7]]);
+        KT_G(v0, v5, v10, v15, m[s[8]], m[s[9]]);
+        KT_G(v1, v6, v11, v12, m[s[10]], m[s[11]]);
+        KT_G(v2, v7, v8, v13, m[s[12]], m[s[13]]);
+        KT_G(v3, v4, v9, v14, m[s[14]], m[s[15]]);
+    }
+    return h0 ^ v0 ^ v8;
+}
+
+__device__ __forceinline__ void put_byte(uint64_t m[16], int pos, unsigned v) {
+    m[pos >> 3] |= uint64_t(v & 0xffu) << (8 * (pos & 7));
+}
+
+__global__ void __launch_bounds__(256) landscape_kernel(const LandscapeArgs a, const uint64_t* __restrict__ rows,
+                                                        int64_t count, double* __restrict__ out) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x) {
+        const uint64_t row = rows[i];
+        double depth_term = 0.0;
+        for (int j = 0; j < a.n_centers; ++j) {
+            int d2 = 0;
+            for (int q = 0; q < a.n; ++q) {
+                const int d = row_byte(row, q) - a.centers[j][q];
+                d2 += d * d;
+            }
+            const double e = exp(__ddiv_rn(-double(d2), a.r2[j]));
+            depth_term = __dadd_rn(depth_term, __dmul_rn(a.depths[j], e));
+        }
+        double rt = __dmul_rn(a.base, __dsub_rn(1.0, depth_term));
+        if (a.noise > 0.0) {
+            uint64_t m[16];
+#pragma unroll
+            for (int w = 0; w < 16; ++w) m[w] = 0;
+            int pos = 0;
+            for (; pos < a.prefix_len; ++pos) put_byte(m, pos, a.prefix[pos]);
+            for (int q = 0; q < a.n; ++q) {
+                if (q) put_byte(m, pos++, ',');
+                const int v = row_byte(row, q);
+                if (v >= 100) put_byte(m, pos++, '0' + v / 100);
+                if (v >= 10) put_byte(m, pos++, '0' + (v / 10) % 10);
+                put_byte(m, pos++, '0' + v % 10);
+            }
+            const uint64_t h = blake2b64_one_block(m, uint64_t(pos));
+            const uint64_t word = __byte_perm(uint32_t(h >> 32), 0, 0x0123) | (uint64_t(__byte_perm(uint32_t(h), 0, 0x0123)) << 32);
+            const double unit = __dsub_rn(2.0 * (__ull2double_rn(word) * 5.421010862427522e-20), 1.0);  // 2^-64
+            rt = __dmul_rn(rt, __dadd_rn(1.0, __dmul_rn(a.noise, unit)));
+        }
+        const double floor_rt = __dmul_rn(0.01, a.base);
+        out[i] = floor_rt > rt ? floor_rt : rt;
+    }
+}
+
+}  // namespace kt
+
+extern "C" {
+
+int kt_landscape_create(kt_engine* e, int n_knobs, int n_centers, const int32_t* centers, const double* depths,
+                        const double* radii, double base_runtime, double noise_rel, const char* seed_text,
+                        kt_landscape** out) {
+    KT_API_BEGIN
+    using namespace kt;
+    (void)e;
+    if (n_knobs < 1 || n_knobs > kMaxKnobs) fail(KT_ERR_UNSUPPORTED, "1..8 knobs supported");
+    if (n_centers < 1 || n_centers > kMaxCenters) fail(KT_ERR_UNSUPPORTED, "1..16 landscape centers supported");
+    auto* l = new kt_landscape();
+    l->n = n_knobs;
+    l->n_centers = n_centers;
+    l->base = base_runtime;
+    l->noise = noise_rel;
+    l->prefix = std::string(seed_text ? seed_text : "") + ":";
+    if (l->prefix.size() + 4 * size_t(n_knobs) > 128 || l->prefix.size() > 64) {
+        delete l;
+        fail(KT_ERR_UNSUPPORTED, "landscape seed text too long for a one-block blake2b payload");
+    }
+    for (int j = 0; j < n_centers; ++j) {
+        for (int q = 0; q < n_knobs; ++q) l->centers[j][q] = centers[j * n_knobs + q];
+        l->depths[j] = depths[j];
+        l->radii[j] = radii[j];
+    }
+    *out = l;
+    KT_API_END
+}
+
+int kt_landscape_destroy(kt_landscape* l) {
+    delete l;
+    return KT_OK;
+}
+
+int kt_score_landscape(kt_engine* e, const kt_landscape* l, const uint64_t* rows_dev, int64_t count,
+                       double* runtime_dev) {
+    KT_API_BEGIN
+    using namespace kt;
+    if (count <= 0) return KT_OK;
+    LandscapeArgs a{};
+    a.n = l->n;
+    a.n_centers = l->n_centers;
+    a.base = l->base;
+    a.noise = l->noise;
+    a.prefix_len = int(l->prefix.size());
+    std::memcpy(a.prefix, l->prefix.data(), l->prefix.size());
+    for (int j = 0; j < l->n_centers; ++j) {
+        for (int q = 0; q < 8; ++q) a.centers[j][q] = l->centers[j][q];
+        a.depths[j] = l->depths[j];
+        a.r2[j] = l->radii[j] * l->radii[j];
+    }
+    const int grid = int(std::min<int64_t>(ceil_div(count, 256), int64_t(e->num_sms) * 8));
+    landscape_kernel<<<grid, 256, 0, e->stream>>>(a, rows_dev, count, runtime_dev);
+    e->check_launch("score_landscape");
+    KT_API_END
+}
+
+}  // extern "C"

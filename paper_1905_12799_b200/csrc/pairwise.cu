@@ -1,0 +1,195 @@
+// pairwise.cu — see pairwise.cuh.
+#include <algorithm>
+#include <map>
+#include <string>
+
+#include "pairwise.cuh"
+
+namespace kt {
+
+struct Builder {
+    PairwiseTree& t;
+    struct Tmp {
+        int32_t l, r, h;
+    };
+    std::vector<Tmp> tmp;
+    // returns encoded id: leaf -> (id), internal -> -(tmp index) - 1
+    int64_t build(int64_t s, int64_t n, int* height) {
+        if (n <= 128) {
+            t.leaf_start.push_back(s);
+            t.leaf_len.push_back(int32_t(n));
+            *height = 0;
+            return int64_t(t.leaf_start.size()) - 1;
+        }
+        int64_t n2 = n / 2;
+        n2 -= n2 % 8;
+        int hl, hr;
+        int64_t a = build(s, n2, &hl);
+        int64_t b = build(s + n2, n - n2, &hr);
+        *height = 1 + std::max(hl, hr);
+        tmp.push_back({int32_t(a), int32_t(b), *height});
+        return -int64_t(tmp.size());
+    }
+};
+
+std::shared_ptr<PairwiseTree> make_tree(int64_t m) {
+    auto t = std::make_shared<PairwiseTree>();
+    t->m = m;
+    Builder b{*t, {}};
+    int h;
+    int64_t root = b.build(0, m, &h);
+    const int L = int(t->leaf_start.size());
+    // final ids: leaves 0..L-1; internal nodes L.. ordered by height
+    const int I = int(b.tmp.size());
+    std::vector<int> order(I);
+    for (int i = 0; i < I; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return b.tmp[x].h < b.tmp[y].h; });
+    std::vector<int> final_id(I);
+    for (int i = 0; i < I; ++i) final_id[order[i]] = L + i;
+    auto enc = [&](int64_t v) -> int32_t { return v >= 0 ? int32_t(v) : final_id[-v - 1]; };
+    t->node_left.resize(I);
+    t->node_right.resize(I);
+    int cur_h = -1;
+    for (int i = 0; i < I; ++i) {
+        const auto& nd = b.tmp[order[i]];
+        t->node_left[i] = enc(nd.l);
+        t->node_right[i] = enc(nd.r);
+        if (nd.h != cur_h) {
+            t->level_start.push_back(i);
+            cur_h = nd.h;
+        }
+    }
+    t->level_start.push_back(I);
+    t->n_levels = int(t->level_start.size()) - 1;
+    t->root = enc(root);
+    KT_CUDA(cudaMalloc(&t->d_leaf_start, std::max<size_t>(1, L) * 8));
+    KT_CUDA(cudaMalloc(&t->d_leaf_len, std::max<size_t>(1, L) * 4));
+    KT_CUDA(cudaMalloc(&t->d_left, std::max<size_t>(1, I) * 4));
+    KT_CUDA(cudaMalloc(&t->d_right, std::max<size_t>(1, I) * 4));
+    KT_CUDA(cudaMemcpy(t->d_leaf_start, t->leaf_start.data(), L * 8, cudaMemcpyHostToDevice));
+    KT_CUDA(cudaMemcpy(t->d_leaf_len, t->leaf_len.data(), L * 4, cudaMemcpyHostToDevice));
+    if (I) {
+        KT_CUDA(cudaMemcpy(t->d_left, t->node_left.data(), I * 4, cudaMemcpyHostToDevice));
+        KT_CUDA(cudaMemcpy(t->d_right, t->node_right.data(), I * 4, cudaMemcpyHostToDevice));
+    }
+    return t;
+}
+
+static std::map<std::pair<int, int64_t>, std::shared_ptr<PairwiseTree>> g_trees;
+
+const PairwiseTree& pairwise_tree(int device, int64_t m) {
+    auto key = std::make_pair(device, m);
+    auto it = g_trees.find(key);
+    if (it != g_trees.end()) return *it->second;
+    if (g_trees.size() > 64) g_trees.clear();
+    auto t = make_tree(m);
+    g_trees[key] = t;
+    return *t;
+}
+
+// One thread per leaf: the squared distance of each point to its assigned
+// centroid, summed numpy-style (n<8: sequential from 0; else 8 accumulators).
+__global__ void loss_leaf_kernel(const uint64_t* __restrict__ pts, const uint8_t* __restrict__ assign,
+                                 const double* __restrict__ cent, int n, const int64_t* leaf_start,
+                                 const int32_t* leaf_len, int L, double* vals) {
+    const int l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= L) return;
+    const int64_t s = leaf_start[l];
+    const int len = leaf_len[l];
+    auto v = [&](int i) { return np_sq_dist(pts[s + i], cent + int(assign[s + i]) * kMaxKnobs, n); };
+    double res;
+    if (len < 8) {
+        res = 0.0;
+        for (int i = 0; i < len; ++i) res = __dadd_rn(res, v(i));
+    } else {
+        double r[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = v(j);
+        int i = 8;
+        for (; i < len - (len % 8); i += 8) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], v(i + j));
+        }
+        res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                        __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+        for (; i < len; ++i) res = __dadd_rn(res, v(i));
+    }
+    vals[l] = res;
+}
+
+__global__ void __launch_bounds__(1024) loss_combine_kernel(double* vals, int L, const int32_t* left,
+                                                            const int32_t* right, const int32_t* level_start,
+                                                            int n_levels, int root, double* out) {
+    for (int lv = 0; lv < n_levels; ++lv) {
+        const int a = level_start[lv], b = level_start[lv + 1];
+        for (int i = a + threadIdx.x; i < b; i += blockDim.x) vals[L + i] = __dadd_rn(vals[left[i]], vals[right[i]]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = vals[root];
+}
+
+// loss of one run (centroids cent[k][8], assignment assign[m]) -> *out_dev
+void pairwise_loss(kt_engine* e, const uint64_t* pts, int64_t m, int n, const uint8_t* assign,
+                          const double* cent, double* out_dev) {
+    const PairwiseTree& t = pairwise_tree(e->device, m);
+    const int L = int(t.leaf_start.size());
+    const int I = int(t.node_left.size());
+    auto* vals = static_cast<double*>(e->scratch("loss.vals", size_t(L + I) * 8));
+    auto* lvl = static_cast<int32_t*>(e->scratch("loss.levels", t.level_start.size() * 4));
+    KT_CUDA(cudaMemcpyAsync(lvl, t.level_start.data(), t.level_start.size() * 4, cudaMemcpyHostToDevice, e->stream));
+    loss_leaf_kernel<<<int(ceil_div(L, 128)), 128, 0, e->stream>>>(pts, assign, cent, n, t.d_leaf_start, t.d_leaf_len,
+                                                                    L, vals);
+    e->check_launch("loss_leaf");
+    loss_combine_kernel<<<1, 1024, 0, e->stream>>>(vals, L, t.d_left, t.d_right, lvl, t.n_levels, t.root, out_dev);
+    e->check_launch("loss_combine");
+}
+
+
+// ---------------------------------------------------------- plain arrays
+__global__ void array_leaf_kernel(const double* __restrict__ x, const double* center, const int64_t* leaf_start,
+                                  const int32_t* leaf_len, int L, double* vals) {
+    const int l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= L) return;
+    const int64_t s = leaf_start[l];
+    const int len = leaf_len[l];
+    const double c = center ? *center : 0.0;
+    auto v = [&](int i) {
+        const double a = x[s + i];
+        if (!center) return a;
+        const double d = __dsub_rn(a, c);
+        return __dmul_rn(d, d);
+    };
+    double res;
+    if (len < 8) {
+        res = 0.0;
+        for (int i = 0; i < len; ++i) res = __dadd_rn(res, v(i));
+    } else {
+        double r[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = v(j);
+        int i = 8;
+        for (; i < len - (len % 8); i += 8) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], v(i + j));
+        }
+        res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                        __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+        for (; i < len; ++i) res = __dadd_rn(res, v(i));
+    }
+    vals[l] = res;
+}
+
+void pairwise_sum(kt_engine* e, const double* x, int64_t m, const double* center, double* out_dev) {
+    const PairwiseTree& t = pairwise_tree(e->device, m);
+    const int L = int(t.leaf_start.size());
+    const int I = int(t.node_left.size());
+    auto* vals = static_cast<double*>(e->scratch("psum.vals", size_t(L + I) * 8));
+    auto* lvl = static_cast<int32_t*>(e->scratch("psum.levels", t.level_start.size() * 4));
+    KT_CUDA(cudaMemcpyAsync(lvl, t.level_start.data(), t.level_start.size() * 4, cudaMemcpyHostToDevice, e->stream));
+    array_leaf_kernel<<<int(ceil_div(L, 128)), 128, 0, e->stream>>>(x, center, t.d_leaf_start, t.d_leaf_len, L, vals);
+    e->check_launch("psum_leaf");
+    loss_combine_kernel<<<1, 1024, 0, e->stream>>>(vals, L, t.d_left, t.d_right, lvl, t.n_levels, t.root, out_dev);
+    e->check_launch("psum_combine");
+}
+
+}  // namespace kt

@@ -1,0 +1,1025 @@
+// sampler.cu — adaptive sampling on the device: K6 dedup, K9 mode vote,
+// K7 k-means++ init, K8 multi-k Lloyd, pairwise loss, knee scan, batch assembly.
+//
+// Reference: knobtuner/sampler.py (dedup :187-192, _plus_plus_init :56-69,
+// kmeans :72-122, knee_scan :125-148, mode_config :151-158,
+// round_to_config :161-170, adaptive_sample :173-215).
+//
+// Exactness strategy (the parity contract is bit-exact k, assignments, batch):
+//   * dedup / mode vote are integer work;
+//   * k-means++ weights are squared distances between lattice points, i.e.
+//     integers, so cumsum / total / searchsorted are done exactly in int64;
+//     the only float op is u * total, done in IEEE double like numpy;
+//   * centroids are mean = (exact int64 sum) / count in IEEE double, which is
+//     what numpy's mean of integer-valued float64 rows rounds to;
+//   * assignment: a fast fp32 argmin with a proven error bound; any point whose
+//     best/second-best gap is inside the bound is re-evaluated with the
+//     reference's own float64 expression (numpy pairwise order, no FMA);
+//   * the loss is numpy's pairwise sum over points, reproduced with the same
+//     128-element blocks, 8 accumulators and split points.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cstring>
+#include <cmath>
+#include <map>
+#include <memory>
+#include <unordered_set>
+#include <vector>
+
+#include "common.cuh"
+#include "pairwise.cuh"
+#include "rng.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace kt {
+
+// ============================================================== dedup (K6)
+constexpr int kDedupRowsPerBlock = 1024;  // 256 threads x 4
+
+__global__ void dedup_insert_kernel(const uint64_t* __restrict__ rows, int64_t count, uint64_t* keys,
+                                    uint32_t* first, uint64_t mask) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x) {
+        const uint64_t key = rows[i];
+        uint64_t h = mix64(key) & mask;
+        while (true) {
+            uint64_t cur = keys[h];
+            if (cur == kEmptyRow) {
+                cur = atomicCAS((unsigned long long*)&keys[h], (unsigned long long)kEmptyRow, (unsigned long long)key);
+                if (cur == kEmptyRow) cur = key;
+            }
+            if (cur == key) {
+                atomicMin(&first[h], uint32_t(i));
+                break;
+            }
+            h = (h + 1) & mask;
+        }
+    }
+}
+
+__device__ __forceinline__ uint32_t dedup_lookup_first(const uint64_t* keys, const uint32_t* first, uint64_t mask,
+                                                       uint64_t key) {
+    uint64_t h = mix64(key) & mask;
+    while (__ldcg(keys + h) != key) h = (h + 1) & mask;
+    return __ldcg(first + h);
+}
+
+// One block = 1024 rows: ballot bitmask of first occurrences + block count.
+__global__ void __launch_bounds__(256) dedup_flag_kernel(const uint64_t* __restrict__ rows, int64_t count,
+                                                         const uint64_t* keys, const uint32_t* first, uint64_t mask,
+                                                         uint32_t* bits, int64_t* block_counts) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t base = int64_t(blockIdx.x) * kDedupRowsPerBlock;
+    int local = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int64_t w0 = base + j * 256 + warp * 32;
+        const int64_t i = w0 + lane;
+        bool is_first = false;
+        if (i < count) is_first = dedup_lookup_first(keys, first, mask, rows[i]) == uint32_t(i);
+        uint32_t b = __ballot_sync(0xffffffffu, is_first);
+        if (lane == 0 && w0 < count) bits[w0 >> 5] = b;
+        local += __popc(b);
+    }
+    __shared__ int s_cnt[8];
+    if (lane == 0) s_cnt[warp] = local;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int64_t t = 0;
+        for (int w = 0; w < 8; ++w) t += s_cnt[w];
+        block_counts[blockIdx.x] = t;
+    }
+}
+
+// Exclusive scan of up to ~16M/1024 block counts in one block; total -> out[n].
+__global__ void __launch_bounds__(1024) exclusive_scan_kernel(const int64_t* in, int64_t* out, int n) {
+    __shared__ int64_t s_part[1024];
+    const int per = (n + blockDim.x - 1) / blockDim.x;
+    const int lo = min(n, int(threadIdx.x) * per), hi = min(n, lo + per);
+    int64_t sum = 0;
+    for (int i = lo; i < hi; ++i) sum += in[i];
+    s_part[threadIdx.x] = sum;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {
+        int64_t v = threadIdx.x >= off ? s_part[threadIdx.x - off] : 0;
+        __syncthreads();
+        s_part[threadIdx.x] += v;
+        __syncthreads();
+    }
+    int64_t run = s_part[threadIdx.x] - sum;
+    for (int i = lo; i < hi; ++i) {
+        int64_t v = in[i];
+        out[i] = run;
+        run += v;
+    }
+    if (threadIdx.x == blockDim.x - 1) out[n] = s_part[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(256) dedup_scatter_kernel(const uint64_t* __restrict__ rows, int64_t count,
+                                                            const uint32_t* bits, const int64_t* offsets,
+                                                            uint64_t* __restrict__ out) {
+    __shared__ int s_prefix[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t base = int64_t(blockIdx.x) * kDedupRowsPerBlock;
+    const int64_t nwords = (count + 31) >> 5;
+    if (warp == 0) {
+        const int64_t w = (base >> 5) + lane;
+        int c = w < nwords ? __popc(bits[w]) : 0;
+        int incl = c;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            int v = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += v;
+        }
+        s_prefix[lane] = incl - c;
+    }
+    __syncthreads();
+    const int64_t off0 = offsets[blockIdx.x];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int word_in_block = j * 8 + warp;
+        const int64_t i = base + int64_t(word_in_block) * 32 + lane;
+        if (i >= count) continue;
+        const uint32_t b = bits[i >> 5];
+        if ((b >> lane) & 1u) out[off0 + s_prefix[word_in_block] + __popc(b & ((1u << lane) - 1u))] = rows[i];
+    }
+}
+
+void exclusive_scan(kt_engine* e, const int64_t* in, int64_t* out, int n) {
+    exclusive_scan_kernel<<<1, 1024, 0, e->stream>>>(in, out, n);
+    e->check_launch("exclusive_scan");
+}
+
+static uint64_t table_capacity(int64_t count) {
+    uint64_t cap = 1024;
+    while (cap < uint64_t(count) * 2) cap <<= 1;
+    return cap;
+}
+
+int64_t dedup(kt_engine* e, const uint64_t* rows, int64_t count, uint64_t* out) {
+    if (count <= 0) return 0;
+    if (count >= (int64_t(1) << 31)) fail(KT_ERR_UNSUPPORTED, "dedup supports < 2^31 rows per call");
+    const uint64_t cap = table_capacity(count);
+    auto* keys = static_cast<uint64_t*>(e->scratch("dedup.keys", cap * 8));
+    auto* first = static_cast<uint32_t*>(e->scratch("dedup.first", cap * 4));
+    KT_CUDA(cudaMemsetAsync(keys, 0xff, cap * 8, e->stream));
+    KT_CUDA(cudaMemsetAsync(first, 0xff, cap * 4, e->stream));
+    const int nb = int(ceil_div(count, kDedupRowsPerBlock));
+    auto* bits = static_cast<uint32_t*>(e->scratch("dedup.bits", size_t(ceil_div(count, 32)) * 4 + 128));
+    auto* counts = static_cast<int64_t*>(e->scratch("dedup.counts", size_t(nb) * 8));
+    auto* offsets = static_cast<int64_t*>(e->scratch("dedup.offsets", size_t(nb + 1) * 8));
+    int grid = int(std::min<int64_t>(ceil_div(count, 256), int64_t(e->num_sms) * 8));
+    dedup_insert_kernel<<<grid, 256, 0, e->stream>>>(rows, count, keys, first, cap - 1);
+    e->check_launch("dedup_insert");
+    dedup_flag_kernel<<<nb, 256, 0, e->stream>>>(rows, count, keys, first, cap - 1, bits, counts);
+    e->check_launch("dedup_flag");
+    exclusive_scan(e, counts, offsets, nb);
+    dedup_scatter_kernel<<<nb, 256, 0, e->stream>>>(rows, count, bits, offsets, out);
+    e->check_launch("dedup_scatter");
+    auto* h_total = static_cast<int64_t*>(e->staging("dedup.total", 8));
+    KT_CUDA(cudaMemcpyAsync(h_total, offsets + nb, 8, cudaMemcpyDeviceToHost, e->stream));
+    e->sync();
+    return *h_total;
+}
+
+// ============================================================== mode vote (K9)
+__global__ void __launch_bounds__(256) mode_hist_kernel(const uint64_t* __restrict__ rows, int64_t count, int n,
+                                                        unsigned int* __restrict__ hist /* [8][256] */) {
+    __shared__ unsigned int s_hist[kMaxKnobs * 256];
+    for (int i = threadIdx.x; i < kMaxKnobs * 256; i += blockDim.x) s_hist[i] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t warps_total = int64_t(gridDim.x) * (blockDim.x >> 5);
+    const int64_t gw = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    for (int64_t base = gw * 32; base < count; base += warps_total * 32) {
+        const int64_t i = base + lane;
+        const bool valid = i < count;
+        const unsigned active = __ballot_sync(0xffffffffu, valid);
+        if (!valid) continue;
+        const uint64_t row = rows[i];
+        for (int d = 0; d < n; ++d) {
+            const int v = row_byte(row, d);
+            const unsigned peers = __match_any_sync(active, v);
+            if (lane == __ffs(peers) - 1) atomicAdd(&s_hist[d * 256 + v], unsigned(__popc(peers)));
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n * 256; i += blockDim.x)
+        if (s_hist[i]) atomicAdd(&hist[i], s_hist[i]);
+}
+
+void mode_vote(kt_engine* e, const uint64_t* rows, int64_t count, int n, int32_t* mode_out) {
+    if (count <= 0) fail(KT_ERR_VALUE, "mode vote needs at least one row");
+    if (count >= (int64_t(1) << 32)) fail(KT_ERR_UNSUPPORTED, "mode vote supports < 2^32 rows");
+    auto* hist = static_cast<unsigned int*>(e->scratch("mode.hist", kMaxKnobs * 256 * 4));
+    KT_CUDA(cudaMemsetAsync(hist, 0, kMaxKnobs * 256 * 4, e->stream));
+    int grid = int(std::min<int64_t>(ceil_div(count, 256), int64_t(e->num_sms) * 4));
+    mode_hist_kernel<<<grid, 256, 0, e->stream>>>(rows, count, n, hist);
+    e->check_launch("mode_hist");
+    auto* h = static_cast<unsigned int*>(e->staging("mode.hist", kMaxKnobs * 256 * 4));
+    KT_CUDA(cudaMemcpyAsync(h, hist, kMaxKnobs * 256 * 4, cudaMemcpyDeviceToHost, e->stream));
+    e->sync();
+    for (int d = 0; d < n; ++d) {
+        int best = 0;
+        for (int v = 1; v < 256; ++v)
+            if (h[d * 256 + v] > h[d * 256 + best]) best = v;  // ties -> smallest index
+        mode_out[d] = best;
+    }
+}
+
+// ====================================================== k-means++ init (K7)
+constexpr int kInitChunk = 4096;  // points per init block (256 threads x 16)
+
+// d2[p] = min(d2[p], |p - c_j|^2) (exact int) and per-chunk int64 sums.
+__global__ void __launch_bounds__(256) init_update_kernel(const uint64_t* __restrict__ pts, int64_t m, int n,
+                                                          uint64_t* cent_rows, int j, int64_t first_idx,
+                                                          int* __restrict__ d2, long long* __restrict__ chunk_sums) {
+    uint64_t c;
+    if (j == 0) {
+        c = pts[first_idx];
+        if (blockIdx.x == 0 && threadIdx.x == 0) cent_rows[0] = c;
+    } else {
+        c = cent_rows[j];
+    }
+    const int64_t base = int64_t(blockIdx.x) * kInitChunk;
+    long long s = 0;
+    for (int t = threadIdx.x; t < kInitChunk; t += blockDim.x) {
+        const int64_t p = base + t;
+        if (p >= m) break;
+        int v = int_sq_dist(pts[p], c, n);
+        if (j > 0) v = min(v, d2[p]);
+        d2[p] = v;
+        s += v;
+    }
+    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    __shared__ long long s_w[8];
+    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long t = 0;
+        for (int w = 0; w < 8; ++w) t += s_w[w];
+        chunk_sums[blockIdx.x] = t;
+    }
+}
+
+// Pick centroid j: first index whose inclusive prefix of d2 exceeds
+// floor(u_j * total) — numpy's searchsorted(cumsum(d2), u * total, 'right').
+__global__ void __launch_bounds__(1024) init_select_kernel(const uint64_t* __restrict__ pts, int64_t m,
+                                                           const int* __restrict__ d2,
+                                                           const long long* __restrict__ chunk_sums, int nchunks,
+                                                           const double* __restrict__ uniforms, int j,
+                                                           uint64_t* cent_rows) {
+    __shared__ long long s_scan[1024];
+    __shared__ long long s_thresh;
+    __shared__ int s_chunk;
+    __shared__ long long s_before;
+    __shared__ unsigned long long s_found;
+    const int tid = threadIdx.x;
+    // 1) inclusive scan of chunk sums (each thread owns a contiguous slice)
+    const int per = (nchunks + 1023) / 1024;
+    const int lo = min(nchunks, tid * per), hi = min(nchunks, lo + per);
+    long long mine = 0;
+    for (int i = lo; i < hi; ++i) mine += chunk_sums[i];
+    s_scan[tid] = mine;
+    if (tid == 0) {
+        s_chunk = -1;
+        s_found = ~0ull;
+    }
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {
+        long long v = tid >= off ? s_scan[tid - off] : 0;
+        __syncthreads();
+        s_scan[tid] += v;
+        __syncthreads();
+    }
+    if (tid == 1023) {
+        const long long total = s_scan[1023];
+        const double u = __dmul_rn(uniforms[j - 1], double(total));
+        s_thresh = (long long)floor(u);
+    }
+    __syncthreads();
+    const long long T = s_thresh;
+    // 2) the chunk where the running total first exceeds T
+    long long run = s_scan[tid] - mine;
+    for (int i = lo; i < hi; ++i) {
+        const long long next = run + chunk_sums[i];
+        if (run <= T && next > T) {
+            s_chunk = i;
+            s_before = run;
+        }
+        run = next;
+    }
+    __syncthreads();
+    const int ch = s_chunk;
+    if (ch >= 0) {
+        // 3) inside the chunk: 4 consecutive points per thread
+        const int64_t p0 = int64_t(ch) * kInitChunk + tid * 4;
+        long long v[4];
+        long long tsum = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            v[q] = (p0 + q < m) ? d2[p0 + q] : 0;
+            tsum += v[q];
+        }
+        __syncthreads();
+        s_scan[tid] = tsum;
+        __syncthreads();
+        for (int off = 1; off < 1024; off <<= 1) {
+            long long x = tid >= off ? s_scan[tid - off] : 0;
+            __syncthreads();
+            s_scan[tid] += x;
+            __syncthreads();
+        }
+        long long acc = s_before + s_scan[tid] - tsum;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            acc += v[q];
+            if (acc > T && p0 + q < m) {
+                atomicMin(&s_found, (unsigned long long)(p0 + q));
+                break;
+            }
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int64_t idx = s_found == ~0ull ? m - 1 : int64_t(s_found);
+        if (idx > m - 1) idx = m - 1;
+        cent_rows[j] = pts[idx];
+    }
+}
+
+// ================================================================= Lloyd (K8)
+constexpr int kMaxRuns = 8;
+constexpr int kMaxClusters = 256;  // sum of k over the runs of one launch
+constexpr int kSumW = 9;           // 8 coordinate sums + count
+enum RunState : int { kActiveFromSums = 0, kActiveGiven = 1, kConverged = 2, kMaxed = 3, kNeedsReseed = 4 };
+
+struct LloydArgs {
+    const uint64_t* pts;
+    int64_t m;
+    int n;
+    int R;
+    int k[kMaxRuns];
+    int coff[kMaxRuns];
+    int K;  // total clusters
+    int it0, it_end, max_iters;
+    uint8_t* assign;         // [R][m], 255 = unassigned
+    double* cent;            // [K][8]
+    long long* S;            // [K][9]
+    unsigned long long* D;   // [3][K][9]
+    unsigned int* chg;       // [3][kMaxRuns]
+    int* run_state;          // [R]
+    int* run_iter;           // [R]
+    int* ctrl;               // [0] next iteration
+};
+
+// Conservative |fp32 - exact| bound for sum_i (p_i - c_i)^2 with p_i, |c_i| <= 255
+// (derivation in DESIGN.md §K8).
+__device__ __forceinline__ float d2_bound(float d) {
+    return 6.5e-5f * sqrtf(8.0f * d + 8.0f) + 5.5e-7f * d + 1e-6f;
+}
+
+struct LloydSmem {
+    long long S[kMaxClusters][kSumW];
+    double c64[kMaxClusters][kMaxKnobs];
+    float c32[kMaxClusters][kMaxKnobs];
+    int delta[kMaxClusters][kSumW];
+    int state[kMaxRuns];
+    int changed[kMaxRuns];
+    int exit_flag;
+    int n_active;
+};
+
+__device__ __forceinline__ void unpack_row(uint64_t row, float p[kMaxKnobs]) {
+    const uint32_t lo = uint32_t(row), hi = uint32_t(row >> 32);
+    p[0] = float(lo & 0xff);
+    p[1] = float((lo >> 8) & 0xff);
+    p[2] = float((lo >> 16) & 0xff);
+    p[3] = float(lo >> 24);
+    p[4] = float(hi & 0xff);
+    p[5] = float((hi >> 8) & 0xff);
+    p[6] = float((hi >> 16) & 0xff);
+    p[7] = float(hi >> 24);
+}
+
+__device__ __forceinline__ int assign_point(const LloydSmem& sm, uint64_t row, const float p[kMaxKnobs], int coff,
+                                            int k, int n) {
+    float best = INFINITY, second = INFINITY;
+    int bj = 0;
+    for (int j = 0; j < k; ++j) {
+        const float4 c0 = *reinterpret_cast<const float4*>(&sm.c32[coff + j][0]);
+        const float4 c1 = *reinterpret_cast<const float4*>(&sm.c32[coff + j][4]);
+        float t, d = 0.0f;
+        t = p[0] - c0.x; d = fmaf(t, t, d);
+        t = p[1] - c0.y; d = fmaf(t, t, d);
+        t = p[2] - c0.z; d = fmaf(t, t, d);
+        t = p[3] - c0.w; d = fmaf(t, t, d);
+        t = p[4] - c1.x; d = fmaf(t, t, d);
+        t = p[5] - c1.y; d = fmaf(t, t, d);
+        t = p[6] - c1.z; d = fmaf(t, t, d);
+        t = p[7] - c1.w; d = fmaf(t, t, d);
+        if (d < best) {
+            second = best;
+            best = d;
+            bj = j;
+        } else if (d < second) {
+            second = d;
+        }
+    }
+    if (k > 1 && !(second - best > d2_bound(best) + d2_bound(second))) {
+        // ambiguous: the reference's own float64 expression decides (ties -> lowest j)
+        double bd = INFINITY;
+        for (int j = 0; j < k; ++j) {
+            const double d = np_sq_dist(row, sm.c64[coff + j], n);
+            if (d < bd) {
+                bd = d;
+                bj = j;
+            }
+        }
+    }
+    return bj;
+}
+
+__global__ void __launch_bounds__(256) lloyd_kernel(LloydArgs a) {
+    extern __shared__ __align__(16) unsigned char s_raw[];
+    LloydSmem& sm = *reinterpret_cast<LloydSmem*>(s_raw);
+    cg::grid_group grid = cg::this_grid();
+    const int tid = threadIdx.x;
+    const int K = a.K, R = a.R, n = a.n;
+
+    for (int i = tid; i < K * kSumW; i += blockDim.x) sm.S[i / kSumW][i % kSumW] = a.S[i];
+    if (tid < R) sm.state[tid] = a.run_state[tid];
+    __syncthreads();
+
+    int it = a.it0;
+    while (it < a.it_end) {
+        // ---- centroids used by this pass
+        for (int r = 0; r < R; ++r) {
+            const int st = sm.state[r];
+            if (st != kActiveFromSums && st != kActiveGiven) continue;
+            for (int x = tid; x < a.k[r] * kMaxKnobs; x += blockDim.x) {
+                const int j = a.coff[r] + x / kMaxKnobs, i = x % kMaxKnobs;
+                double c;
+                if (i >= n) c = 0.0;
+                else if (st == kActiveFromSums) c = __ddiv_rn(double(sm.S[j][i]), double(sm.S[j][8]));
+                else c = a.cent[j * kMaxKnobs + i];
+                sm.c64[j][i] = c;
+                sm.c32[j][i] = float(c);
+                if (blockIdx.x == 0) a.cent[j * kMaxKnobs + i] = c;
+            }
+        }
+        for (int i = tid; i < K * kSumW; i += blockDim.x) sm.delta[i / kSumW][i % kSumW] = 0;
+        if (tid < kMaxRuns) sm.changed[tid] = 0;
+        __syncthreads();
+
+        // ---- assignment pass (phase A)
+        const int64_t gstride = int64_t(gridDim.x) * blockDim.x;
+        for (int64_t pidx = int64_t(blockIdx.x) * blockDim.x + tid; pidx < a.m; pidx += gstride) {
+            const uint64_t row = a.pts[pidx];
+            float p[kMaxKnobs];
+            unpack_row(row, p);
+            for (int r = 0; r < R; ++r) {
+                const int st = sm.state[r];
+                if (st != kActiveFromSums && st != kActiveGiven) continue;
+                const int j = assign_point(sm, row, p, a.coff[r], a.k[r], n);
+                uint8_t* as = a.assign + int64_t(r) * a.m + pidx;
+                const int old = *as;
+                if (old != j) {
+                    *as = uint8_t(j);
+                    sm.changed[r] = 1;
+                    int* dn = sm.delta[a.coff[r] + j];
+                    for (int i = 0; i < n; ++i) atomicAdd(dn + i, row_byte(row, i));
+                    atomicAdd(dn + 8, 1);
+                    if (old != 255) {
+                        int* dold = sm.delta[a.coff[r] + old];
+                        for (int i = 0; i < n; ++i) atomicSub(dold + i, row_byte(row, i));
+                        atomicSub(dold + 8, 1);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        const int buf = it % 3;
+        unsigned long long* Dcur = a.D + size_t(buf) * K * kSumW;
+        for (int i = tid; i < K * kSumW; i += blockDim.x) {
+            const int v = sm.delta[i / kSumW][i % kSumW];
+            if (v) atomicAdd(Dcur + i, (unsigned long long)(long long)v);
+        }
+        if (tid < R && sm.changed[tid]) atomicOr(a.chg + buf * kMaxRuns + tid, 1u);
+        if (blockIdx.x == 0) {
+            const int nb = (it + 1) % 3;
+            for (int i = tid; i < K * kSumW; i += blockDim.x) a.D[size_t(nb) * K * kSumW + i] = 0ull;
+            if (tid < kMaxRuns) a.chg[nb * kMaxRuns + tid] = 0u;
+        }
+        grid.sync();
+
+        // ---- decisions (identical in every block)
+        for (int i = tid; i < K * kSumW; i += blockDim.x) {
+            const long long v = (long long)__ldcg(Dcur + i);
+            if (v) sm.S[i / kSumW][i % kSumW] += v;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            sm.exit_flag = 0;
+            sm.n_active = 0;
+            for (int r = 0; r < R; ++r) {
+                int st = sm.state[r];
+                if (st != kActiveFromSums && st != kActiveGiven) continue;
+                const unsigned changed = __ldcg(a.chg + buf * kMaxRuns + r);
+                if (!changed) {
+                    st = kConverged;
+                } else if (it == a.max_iters - 1) {
+                    st = kMaxed;
+                } else {
+                    bool empty = false;
+                    for (int j = 0; j < a.k[r]; ++j) empty |= sm.S[a.coff[r] + j][8] == 0;
+                    if (empty) {
+                        st = kNeedsReseed;
+                        sm.exit_flag = 1;
+                    } else {
+                        st = kActiveFromSums;
+                        ++sm.n_active;
+                    }
+                }
+                if (st != kActiveFromSums && blockIdx.x == 0) a.run_iter[r] = it;
+                sm.state[r] = st;
+            }
+        }
+        __syncthreads();
+        ++it;
+        if (sm.exit_flag || sm.n_active == 0) break;
+    }
+    if (blockIdx.x == 0) {
+        for (int i = tid; i < K * kSumW; i += blockDim.x) a.S[i] = sm.S[i / kSumW][i % kSumW];
+        if (tid < R) a.run_state[tid] = sm.state[tid];
+        if (tid == 0) a.ctrl[0] = it;
+    }
+}
+
+// ============================================================ reseed helpers
+__global__ void point_d2_kernel(const uint64_t* __restrict__ pts, int64_t m, int n, const uint8_t* __restrict__ assign,
+                                const double* __restrict__ cent, double* __restrict__ out) {
+    for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < m; p += int64_t(gridDim.x) * blockDim.x)
+        out[p] = np_sq_dist(pts[p], cent + int(assign[p]) * kMaxKnobs, n);
+}
+
+// argmax of d2 over points not in `blocked` (ties -> lowest index); per-block partials.
+__global__ void __launch_bounds__(256) argmax_kernel(const double* __restrict__ d2, int64_t m,
+                                                     const int64_t* blocked, int n_blocked, double* part_v,
+                                                     int64_t* part_i) {
+    double bv = -1.0;
+    int64_t bi = -1;
+    for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < m; p += int64_t(gridDim.x) * blockDim.x) {
+        bool skip = false;
+        for (int q = 0; q < n_blocked; ++q) skip |= blocked[q] == p;
+        if (skip) continue;
+        const double v = d2[p];
+        if (v > bv) {
+            bv = v;
+            bi = p;
+        }
+    }
+    __shared__ double s_v[256];
+    __shared__ int64_t s_i[256];
+    s_v[threadIdx.x] = bv;
+    s_i[threadIdx.x] = bi;
+    __syncthreads();
+    for (int off = 128; off; off >>= 1) {
+        if (threadIdx.x < off) {
+            const double ov = s_v[threadIdx.x + off];
+            const int64_t oi = s_i[threadIdx.x + off];
+            const double mv = s_v[threadIdx.x];
+            const int64_t mi = s_i[threadIdx.x];
+            if (oi >= 0 && (mi < 0 || ov > mv || (ov == mv && oi < mi))) {
+                s_v[threadIdx.x] = ov;
+                s_i[threadIdx.x] = oi;
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        part_v[blockIdx.x] = s_v[0];
+        part_i[blockIdx.x] = s_i[0];
+    }
+}
+
+__global__ void rows_to_centroids_kernel(const uint64_t* rows, int count, int n, double* cent) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= count * kMaxKnobs) return;
+    const int j = x / kMaxKnobs, i = x % kMaxKnobs;
+    cent[x] = i < n ? double(row_byte(rows[j], i)) : 0.0;
+}
+
+// ============================================================ orchestration
+struct KmeansSession {
+    kt_engine* e;
+    const uint64_t* pts;
+    int64_t m;
+    int n;
+    uint64_t seed;
+    // incremental k-means++ state
+    int chosen = 0;  // centroids chosen so far
+    int64_t first_idx = 0;
+    std::vector<double> uniforms;  // u_1..u_62
+    uint64_t* cent_rows = nullptr;
+    int* d2 = nullptr;
+    long long* chunk_sums = nullptr;
+    double* d_uniforms = nullptr;
+    int nchunks = 0;
+
+    KmeansSession(kt_engine* e_, const uint64_t* p, int64_t m_, int n_, uint64_t s) : e(e_), pts(p), m(m_), n(n_), seed(s) {
+        uint32_t w[2];
+        int nw = u64_words(seed, w);
+        Pcg64 g = pcg64_from_seed_sequence(w, nw, nullptr, 0);
+        if (m > 0xffffffffll) fail(KT_ERR_UNSUPPORTED, "k-means supports < 2^32 points");
+        first_idx = int64_t(g.bounded32(uint32_t(m - 1)));
+        uniforms.resize(64);
+        for (auto& u : uniforms) u = g.random();
+        cent_rows = static_cast<uint64_t*>(e->scratch("km.cent_rows", 64 * 8));
+        d2 = static_cast<int*>(e->scratch("km.d2", size_t(m) * 4));
+        nchunks = int(ceil_div(m, kInitChunk));
+        chunk_sums = static_cast<long long*>(e->scratch("km.chunk_sums", size_t(nchunks) * 8));
+        d_uniforms = static_cast<double*>(e->scratch("km.uniforms", 64 * 8));
+        auto* h = static_cast<double*>(e->staging("km.uniforms", 64 * 8));
+        std::copy(uniforms.begin(), uniforms.end(), h);
+        KT_CUDA(cudaMemcpyAsync(d_uniforms, h, 64 * 8, cudaMemcpyHostToDevice, e->stream));
+    }
+
+    void ensure_init(int k) {
+        if (nchunks > 1024 * 16) fail(KT_ERR_UNSUPPORTED, "k-means++ init supports < 64M points");
+        while (chosen < k) {
+            const int j = chosen;
+            if (j > 0) {
+                init_select_kernel<<<1, 1024, 0, e->stream>>>(pts, m, d2, chunk_sums, nchunks, d_uniforms, j, cent_rows);
+                e->check_launch("init_select");
+            }
+            if (j + 1 < 64) {  // d2 update needed only if another centroid follows
+                init_update_kernel<<<nchunks, 256, 0, e->stream>>>(pts, m, n, cent_rows, j, first_idx, d2, chunk_sums);
+                e->check_launch("init_update");
+            }
+            ++chosen;
+        }
+    }
+
+    struct RunResult {
+        int k;
+        int passes;
+        double loss;
+    };
+
+    // Lloyd for the given ks (ascending); results in cent (device, [K][8]) and assign ([R][m]).
+    std::vector<RunResult> run(const std::vector<int>& ks, std::vector<double>* history /* R==1 only */) {
+        const int R = int(ks.size());
+        if (R < 1 || R > kMaxRuns) fail(KT_ERR_INTERNAL, "bad run count");
+        LloydArgs a{};
+        a.pts = pts;
+        a.m = m;
+        a.n = n;
+        a.R = R;
+        int K = 0;
+        for (int r = 0; r < R; ++r) {
+            a.k[r] = ks[r];
+            a.coff[r] = K;
+            K += ks[r];
+        }
+        if (K > kMaxClusters) fail(KT_ERR_INTERNAL, "too many clusters in one launch");
+        a.K = K;
+        a.max_iters = 100;
+        ensure_init(ks.back());
+        a.assign = static_cast<uint8_t*>(e->scratch("km.assign", size_t(R) * m));
+        a.cent = static_cast<double*>(e->scratch("km.cent", size_t(K) * kMaxKnobs * 8));
+        a.S = static_cast<long long*>(e->scratch("km.S", size_t(K) * kSumW * 8));
+        a.D = static_cast<unsigned long long*>(e->scratch("km.D", size_t(3) * K * kSumW * 8));
+        a.chg = static_cast<unsigned int*>(e->scratch("km.chg", 3 * kMaxRuns * 4));
+        a.run_state = static_cast<int*>(e->scratch("km.state", kMaxRuns * 4));
+        a.run_iter = static_cast<int*>(e->scratch("km.iter", kMaxRuns * 4));
+        a.ctrl = static_cast<int*>(e->scratch("km.ctrl", 16));
+        double* d_loss = static_cast<double*>(e->scratch("km.loss", kMaxRuns * 8));
+        KT_CUDA(cudaMemsetAsync(a.assign, 0xff, size_t(R) * m, e->stream));
+        KT_CUDA(cudaMemsetAsync(a.S, 0, size_t(K) * kSumW * 8, e->stream));
+        for (int r = 0; r < R; ++r) {
+            rows_to_centroids_kernel<<<int(ceil_div(ks[r] * kMaxKnobs, 256)), 256, 0, e->stream>>>(
+                cent_rows, ks[r], n, a.cent + size_t(a.coff[r]) * kMaxKnobs);
+            e->check_launch("rows_to_centroids");
+        }
+        auto* h_state = static_cast<int*>(e->staging("km.state", 64));
+        for (int r = 0; r < R; ++r) h_state[r] = kActiveGiven;
+        KT_CUDA(cudaMemcpyAsync(a.run_state, h_state, R * 4, cudaMemcpyHostToDevice, e->stream));
+
+        const size_t smem = sizeof(LloydSmem);
+        KT_CUDA(cudaFuncSetAttribute(lloyd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        const int occ = std::max(1, occupancy_blocks((const void*)lloyd_kernel, 256, smem));
+        const int grid = int(std::max<int64_t>(1, std::min<int64_t>(int64_t(occ) * e->num_sms, ceil_div(m, 256))));
+        int it = 0;
+        auto* h_ctrl = static_cast<int*>(e->staging("km.ctrl", 64));
+        auto* h_iter = static_cast<int*>(e->staging("km.iter", 64));
+        auto* h_S = static_cast<long long*>(e->staging("km.S", size_t(kMaxClusters) * kSumW * 8));
+        auto* h_loss = static_cast<double*>(e->staging("km.loss", 64 * 8));
+        while (true) {
+            KT_CUDA(cudaMemsetAsync(a.D, 0, size_t(3) * K * kSumW * 8, e->stream));
+            KT_CUDA(cudaMemsetAsync(a.chg, 0, 3 * kMaxRuns * 4, e->stream));
+            a.it0 = it;
+            a.it_end = history ? it + 1 : a.max_iters;
+            void* params[] = {&a};
+            KT_CUDA(cudaLaunchCooperativeKernel((const void*)lloyd_kernel, grid, 256, params, smem, e->stream));
+            e->check_launch("lloyd");
+            KT_CUDA(cudaMemcpyAsync(h_ctrl, a.ctrl, 4, cudaMemcpyDeviceToHost, e->stream));
+            KT_CUDA(cudaMemcpyAsync(h_state, a.run_state, R * 4, cudaMemcpyDeviceToHost, e->stream));
+            if (history) {
+                pairwise_loss(e, pts, m, n, a.assign, a.cent, d_loss);
+                KT_CUDA(cudaMemcpyAsync(h_loss, d_loss, 8, cudaMemcpyDeviceToHost, e->stream));
+            }
+            e->sync();
+            it = h_ctrl[0];
+            if (history) history->push_back(h_loss[0]);
+            bool reseed = false, active = false;
+            for (int r = 0; r < R; ++r) {
+                reseed |= h_state[r] == kNeedsReseed;
+                active |= h_state[r] == kActiveFromSums || h_state[r] == kActiveGiven;
+            }
+            if (reseed) {
+                KT_CUDA(cudaMemcpyAsync(h_S, a.S, size_t(K) * kSumW * 8, cudaMemcpyDeviceToHost, e->stream));
+                e->sync();
+                for (int r = 0; r < R; ++r)
+                    if (h_state[r] == kNeedsReseed) reseed_run(a, r, h_S);
+                for (int r = 0; r < R; ++r)
+                    if (h_state[r] == kNeedsReseed) h_state[r] = kActiveGiven;
+                KT_CUDA(cudaMemcpyAsync(a.run_state, h_state, R * 4, cudaMemcpyHostToDevice, e->stream));
+                continue;
+            }
+            if (!active) break;
+        }
+        std::vector<RunResult> out(R);
+        for (int r = 0; r < R; ++r)
+            pairwise_loss(e, pts, m, n, a.assign + size_t(r) * m, a.cent + size_t(a.coff[r]) * kMaxKnobs, d_loss + r);
+        KT_CUDA(cudaMemcpyAsync(h_loss, d_loss, R * 8, cudaMemcpyDeviceToHost, e->stream));
+        KT_CUDA(cudaMemcpyAsync(h_iter, a.run_iter, R * 4, cudaMemcpyDeviceToHost, e->stream));
+        e->sync();
+        for (int r = 0; r < R; ++r) out[r] = {ks[r], h_iter[r] + 1, h_loss[r]};
+        last_args = a;
+        return out;
+    }
+
+    // Empty clusters after pass `it`: non-empty -> mean, empty -> farthest
+    // unblocked points by the pass's own point distances (sampler.py:104-115).
+    void reseed_run(LloydArgs& a, int r, const long long* h_S) {
+        const int k = a.k[r], co = a.coff[r];
+        const uint8_t* asg = a.assign + size_t(r) * m;
+        double* cent = a.cent + size_t(co) * kMaxKnobs;  // centroids used by the pass
+        auto* pd2 = static_cast<double*>(e->scratch("km.pd2", size_t(m) * 8));
+        const int grid = int(std::min<int64_t>(ceil_div(m, 256), int64_t(e->num_sms) * 4));
+        point_d2_kernel<<<grid, 256, 0, e->stream>>>(pts, m, n, asg, cent, pd2);
+        e->check_launch("point_d2");
+        std::vector<int64_t> blocked;
+        auto* d_blocked = static_cast<int64_t*>(e->scratch("km.blocked", 64 * 8));
+        auto* pv = static_cast<double*>(e->scratch("km.part_v", size_t(grid) * 8));
+        auto* pi = static_cast<int64_t*>(e->scratch("km.part_i", size_t(grid) * 8));
+        auto* h_pv = static_cast<double*>(e->staging("km.part_v", size_t(grid) * 8));
+        auto* h_pi = static_cast<int64_t*>(e->staging("km.part_i", size_t(grid) * 8));
+        auto* h_rows = static_cast<uint64_t*>(e->staging("km.reseed_rows", 64 * 8));
+        std::vector<double> newc(size_t(k) * kMaxKnobs, 0.0);
+        std::vector<int> empties;
+        for (int j = 0; j < k; ++j) {
+            const long long* s = h_S + size_t(co + j) * kSumW;
+            if (s[8] == 0) {
+                empties.push_back(j);
+                continue;
+            }
+            for (int i = 0; i < n; ++i) newc[size_t(j) * kMaxKnobs + i] = double(s[i]) / double(s[8]);
+        }
+        for (size_t q = 0; q < empties.size(); ++q) {
+            if (!blocked.empty())
+                KT_CUDA(cudaMemcpyAsync(d_blocked, blocked.data(), blocked.size() * 8, cudaMemcpyHostToDevice, e->stream));
+            argmax_kernel<<<grid, 256, 0, e->stream>>>(pd2, m, d_blocked, int(blocked.size()), pv, pi);
+            e->check_launch("argmax");
+            KT_CUDA(cudaMemcpyAsync(h_pv, pv, size_t(grid) * 8, cudaMemcpyDeviceToHost, e->stream));
+            KT_CUDA(cudaMemcpyAsync(h_pi, pi, size_t(grid) * 8, cudaMemcpyDeviceToHost, e->stream));
+            e->sync();
+            double bv = -1.0;
+            int64_t bi = -1;
+            for (int b = 0; b < grid; ++b)
+                if (h_pi[b] >= 0 && (bi < 0 || h_pv[b] > bv || (h_pv[b] == bv && h_pi[b] < bi))) {
+                    bv = h_pv[b];
+                    bi = h_pi[b];
+                }
+            if (bi < 0) fail(KT_ERR_INTERNAL, "no point left to reseed an empty cluster");
+            blocked.push_back(bi);
+        }
+        // fetch the chosen points' rows
+        for (size_t q = 0; q < blocked.size(); ++q)
+            KT_CUDA(cudaMemcpyAsync(h_rows + q, pts + blocked[q], 8, cudaMemcpyDeviceToHost, e->stream));
+        e->sync();
+        for (size_t q = 0; q < empties.size(); ++q)
+            for (int i = 0; i < n; ++i) newc[size_t(empties[q]) * kMaxKnobs + i] = double(row_byte(h_rows[q], i));
+        auto* h_c = static_cast<double*>(e->staging("km.newc", size_t(kMaxClusters) * kMaxKnobs * 8));
+        std::copy(newc.begin(), newc.end(), h_c);
+        KT_CUDA(cudaMemcpyAsync(cent, h_c, newc.size() * 8, cudaMemcpyHostToDevice, e->stream));
+    }
+
+    LloydArgs last_args{};
+};
+
+// Batches of consecutive ks run speculatively in one Lloyd launch.
+static std::vector<int> next_batch(int k0, int upper, int round) {
+    static const int widths[] = {2, 2, 4, 8};
+    int want = round < 4 ? widths[round] : 8;
+    std::vector<int> ks;
+    int total = 0;
+    for (int k = k0; k <= upper && int(ks.size()) < want; ++k) {
+        if (total + k > kMaxClusters) break;
+        ks.push_back(k);
+        total += k;
+    }
+    return ks;
+}
+
+struct KneeResult {
+    std::vector<int> ks;
+    std::vector<double> losses;
+    int chosen_k = 0;
+    int passes = 0;
+    std::vector<double> centroids;  // chosen_k * n
+    const uint8_t* assign_dev = nullptr;  // chosen run's assignment (device), valid until next engine call
+};
+
+static KneeResult knee_scan(kt_engine* e, const uint64_t* pts, int64_t m, int n, uint64_t seed, double knee_c,
+                            int k_max) {
+    const int upper = int(std::min<int64_t>(k_max, m));
+    if (upper < 8) fail(KT_ERR_VALUE, "knee scan needs at least 8 distinct points");
+    KmeansSession ses(e, pts, m, n, seed);
+    KneeResult res;
+    double previous = INFINITY;
+    int k0 = 8;
+    for (int round = 0; k0 <= upper; ++round) {
+        std::vector<int> ks = next_batch(k0, upper, round);
+        auto out = ses.run(ks, nullptr);
+        int stop = -1;
+        for (size_t r = 0; r < out.size(); ++r) {
+            res.ks.push_back(out[r].k);
+            res.losses.push_back(out[r].loss);
+            res.passes += out[r].passes;
+            if (knee_c * out[r].loss > previous) {
+                stop = int(r);
+                break;
+            }
+            previous = out[r].loss;
+        }
+        const int pick = stop >= 0 ? stop : int(out.size()) - 1;
+        const bool done = stop >= 0 || ks.back() >= upper;
+        if (done) {
+            res.chosen_k = ks[pick];
+            const LloydArgs& a = ses.last_args;
+            std::vector<double> c(size_t(ks[pick]) * kMaxKnobs);
+            KT_CUDA(cudaMemcpyAsync(c.data(), a.cent + size_t(a.coff[pick]) * kMaxKnobs, c.size() * 8,
+                                    cudaMemcpyDeviceToHost, e->stream));
+            e->sync();
+            res.centroids.resize(size_t(ks[pick]) * n);
+            for (int j = 0; j < ks[pick]; ++j)
+                for (int i = 0; i < n; ++i) res.centroids[size_t(j) * n + i] = c[size_t(j) * kMaxKnobs + i];
+            res.assign_dev = a.assign + size_t(pick) * m;
+            return res;
+        }
+        k0 = ks.back() + 1;
+    }
+    fail(KT_ERR_INTERNAL, "knee scan ended without a result");
+}
+
+}  // namespace kt
+
+using namespace kt;
+
+extern "C" {
+
+int kt_dedup(kt_engine* e, const uint64_t* rows_dev, int64_t count, uint64_t* distinct_dev, int64_t* n_distinct) {
+    KT_API_BEGIN
+    *n_distinct = dedup(e, rows_dev, count, distinct_dev);
+    KT_API_END
+}
+
+int kt_mode_vote(kt_engine* e, const uint64_t* rows_dev, int64_t count, int n_knobs, int32_t* mode_out) {
+    KT_API_BEGIN
+    if (n_knobs < 1 || n_knobs > kMaxKnobs) fail(KT_ERR_UNSUPPORTED, "1..8 knobs supported");
+    mode_vote(e, rows_dev, count, n_knobs, mode_out);
+    KT_API_END
+}
+
+int kt_kmeans(kt_engine* e, const uint64_t* points_dev, int64_t m, int n_knobs, int k, uint64_t seed,
+              double* centroids_out, int64_t* assignment_out, double* loss_out, double* history_out,
+              int32_t* n_passes) {
+    KT_API_BEGIN
+    if (m < 1) fail(KT_ERR_VALUE, "kmeans needs at least one point");
+    if (n_knobs < 1 || n_knobs > kMaxKnobs) fail(KT_ERR_UNSUPPORTED, "1..8 knobs supported");
+    if (k < 1 || k > 63) fail(KT_ERR_UNSUPPORTED, "engine k-means supports 1 <= k <= 63");
+    // n_distinct check (sampler.py:84-87) is done by the caller with kt_dedup.
+    KmeansSession ses(e, points_dev, m, n_knobs, seed);
+    std::vector<double> hist;
+    auto out = ses.run({k}, history_out ? &hist : nullptr);
+    const LloydArgs& a = ses.last_args;
+    std::vector<double> c(size_t(k) * kMaxKnobs);
+    KT_CUDA(cudaMemcpyAsync(c.data(), a.cent, c.size() * 8, cudaMemcpyDeviceToHost, e->stream));
+    std::vector<uint8_t> asg;
+    if (assignment_out) {
+        asg.resize(size_t(m));
+        KT_CUDA(cudaMemcpyAsync(asg.data(), a.assign, size_t(m), cudaMemcpyDeviceToHost, e->stream));
+    }
+    e->sync();
+    for (int j = 0; j < k; ++j)
+        for (int i = 0; i < n_knobs; ++i) centroids_out[size_t(j) * n_knobs + i] = c[size_t(j) * kMaxKnobs + i];
+    if (assignment_out)
+        for (int64_t p = 0; p < m; ++p) assignment_out[p] = asg[size_t(p)];
+    *loss_out = out[0].loss;
+    *n_passes = out[0].passes;
+    if (history_out) {
+        if (int(hist.size()) != out[0].passes) fail(KT_ERR_INTERNAL, "history length mismatch");
+        std::copy(hist.begin(), hist.end(), history_out);
+    }
+    KT_API_END
+}
+
+int kt_knee_scan(kt_engine* e, const uint64_t* points_dev, int64_t m, int n_knobs, uint64_t seed,
+                 double knee_constant, int k_max, int32_t* scanned_k, double* scanned_loss, int32_t* n_scanned,
+                 double* centroids_out, int64_t* assignment_out) {
+    KT_API_BEGIN
+    if (n_knobs < 1 || n_knobs > kMaxKnobs) fail(KT_ERR_UNSUPPORTED, "1..8 knobs supported");
+    if (k_max > 63) fail(KT_ERR_UNSUPPORTED, "engine knee scan supports k_max <= 63");
+    KneeResult r = knee_scan(e, points_dev, m, n_knobs, seed, knee_constant, k_max);
+    *n_scanned = int32_t(r.ks.size());
+    for (size_t i = 0; i < r.ks.size(); ++i) {
+        scanned_k[i] = r.ks[i];
+        scanned_loss[i] = r.losses[i];
+    }
+    std::copy(r.centroids.begin(), r.centroids.end(), centroids_out);
+    if (assignment_out) {
+        std::vector<uint8_t> asg(static_cast<size_t>(m));
+        KT_CUDA(cudaMemcpyAsync(asg.data(), r.assign_dev, size_t(m), cudaMemcpyDeviceToHost, e->stream));
+        e->sync();
+        for (int64_t p = 0; p < m; ++p) assignment_out[p] = asg[size_t(p)];
+    }
+    KT_API_END
+}
+
+int kt_adaptive_sample(kt_engine* e, const uint64_t* rows_dev, int64_t count, int n_knobs, const int32_t* cards,
+                       const uint64_t* visited_rows, int64_t n_visited, uint64_t seed, double knee_constant,
+                       uint64_t* batch_out, int32_t* batch_len, kt_sample_info* info) {
+    KT_API_BEGIN
+    if (count < 1) fail(KT_ERR_VALUE, "trajectory is empty");
+    if (n_knobs < 1 || n_knobs > kMaxKnobs) fail(KT_ERR_UNSUPPORTED, "1..8 knobs supported");
+    kt_sample_info local{};
+    kt_sample_info& inf = info ? *info : local;
+    std::memset(&inf, 0, sizeof(inf));
+    std::unordered_set<uint64_t> visited(visited_rows, visited_rows + n_visited);
+    auto* distinct = static_cast<uint64_t*>(e->scratch("as.distinct", size_t(count) * 8));
+    const int64_t m = dedup(e, rows_dev, count, distinct);
+    inf.n_distinct = m;
+    int len = 0;
+    if (m <= 8) {  // sampler.py:194-195
+        uint64_t h[8];
+        KT_CUDA(cudaMemcpyAsync(h, distinct, size_t(m) * 8, cudaMemcpyDeviceToHost, e->stream));
+        e->sync();
+        for (int64_t i = 0; i < m; ++i)
+            if (!visited.count(h[i])) batch_out[len++] = h[i];
+        *batch_len = len;
+        return KT_OK;
+    }
+    KneeResult r = knee_scan(e, distinct, m, n_knobs, seed, knee_constant, 63);
+    inf.chosen_k = r.chosen_k;
+    inf.n_scanned = int32_t(r.ks.size());
+    for (size_t i = 0; i < r.ks.size() && i < 56; ++i) {
+        inf.scanned_k[i] = r.ks[i];
+        inf.scanned_loss[i] = r.losses[i];
+    }
+    inf.lloyd_passes = r.passes;
+    // batch assembly (sampler.py:200-215)
+    bool have_mode = false;
+    uint64_t mode_row = 0;
+    std::unordered_set<uint64_t> taken;
+    for (int j = 0; j < r.chosen_k; ++j) {
+        uint64_t row = 0;
+        for (int i = 0; i < n_knobs; ++i) {
+            const double x = r.centroids[size_t(j) * n_knobs + i];
+            const double f = std::floor(x + 0.5);
+            long long idx = f < 0.0 ? 0 : (f > double(cards[i] - 1) ? cards[i] - 1 : (long long)f);
+            row |= uint64_t(idx) << (8 * i);
+        }
+        if (visited.count(row)) {
+            if (!have_mode) {
+                int32_t md[kMaxKnobs];
+                mode_vote(e, rows_dev, count, n_knobs, md);
+                mode_row = 0;
+                for (int i = 0; i < n_knobs; ++i) mode_row |= uint64_t(md[i]) << (8 * i);
+                have_mode = true;
+            }
+            inf.used_mode = 1;
+            row = mode_row;
+            if (visited.count(row)) continue;
+        }
+        if (taken.count(row)) continue;
+        taken.insert(row);
+        batch_out[len++] = row;
+    }
+    *batch_len = len;
+    KT_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,128 @@
+"""CPU-side checks of the engine boundary: the C ABI library, host RNG, packing, scope rules."""
+
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_1905_12799_b200 as kt
+from paper_1905_12799_b200 import _lib, space as sp
+from paper_1905_12799_b200.sa import seed_words
+from paper_1905_12799_b200.workloads import RESNET18_S2, RESNET18_TASKS, VGG16_TASKS
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1905_12799_b200 import build
+
+    build.build()
+    return _lib.load()
+
+
+def test_library_exports_every_header_symbol(lib):
+    declared = _lib.header_symbols()
+    assert declared, "header declares no kt_ functions"
+    missing = [s for s in declared if not hasattr(lib, s)]
+    assert not missing, f"libknobtuner_b200.so lacks {missing}"
+    # every ctypes signature names a declared function, and vice versa
+    assert sorted(_lib.SIGNATURES) == declared
+
+
+def test_library_is_sm100a_only(lib):
+    import subprocess
+
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
+    archs = set(re.findall(r"sm_(\d+a?)", out))
+    assert archs == {"100a"}, archs
+
+
+def _draw(entropy: int, spawn: tuple, kind: int, bound: int, count: int):
+    ew = seed_words(entropy) if entropy < 2**64 else None
+    sw = np.array(spawn, dtype=np.uint32) if spawn else np.zeros(1, dtype=np.uint32)
+    out = np.zeros(count, dtype=np.float64 if kind == 0 else np.int64)
+    _lib.call("kt_pcg64_draw", _lib.as_ptr(ew, _lib.C.c_uint32), int(ew.size), _lib.as_ptr(sw, _lib.C.c_uint32),
+              len(spawn), kind, bound, count, _lib.ptr(out))
+    return out
+
+
+@pytest.mark.parametrize("entropy", [0, 1, 7, 123456789, 2**32 + 5, 2**63 + 11, 2**64 - 1])
+@pytest.mark.parametrize("spawn", [(), (0,), (3,), (5, 17), (0, 0, 0, 0, 9)])
+def test_seed_sequence_pcg64_matches_numpy(lib, entropy, spawn):
+    g = np.random.default_rng(np.random.SeedSequence(entropy, spawn_key=spawn))
+    assert np.array_equal(_draw(entropy, spawn, 0, 0, 50), g.random(50))
+    for bound in (1, 2, 3, 7, 8, 84, 1000, 65536, 999_999_937, 2**32):
+        g = np.random.default_rng(np.random.SeedSequence(entropy, spawn_key=spawn))
+        want = np.array([g.integers(0, bound) for _ in range(40)])
+        assert np.array_equal(_draw(entropy, spawn, 1, bound, 40), want), bound
+
+
+def test_interleaved_draw_order_matches_numpy():
+    """integers(0, n) takes the low half of a word and caches the high half; random() takes a fresh word."""
+    from paper_1905_12799_b200 import _lib
+
+    _lib.load()
+    g = np.random.default_rng(np.random.SeedSequence(42))
+    seq = [g.integers(0, 8), g.integers(0, 2), g.random(), g.integers(0, 8), g.random(), g.integers(0, 2)]
+    # reproduce with raw words: word0 -> lo/hi halves, word1 -> random, word2 -> lo, word3 -> random, hi of word2
+    raw = np.random.default_rng(np.random.SeedSequence(42)).bit_generator.random_raw(4)
+    lo = lambda w: int(w) & 0xFFFFFFFF
+    hi = lambda w: int(w) >> 32
+    assert seq[0] == (lo(raw[0]) * 8) >> 32 and seq[1] == (hi(raw[0]) * 2) >> 32
+    assert seq[2] == (int(raw[1]) >> 11) * 2.0**-53
+    assert seq[3] == (lo(raw[2]) * 8) >> 32 and seq[4] == (int(raw[3]) >> 11) * 2.0**-53
+    assert seq[5] == (hi(raw[2]) * 2) >> 32
+
+
+def test_pack_roundtrip_and_layout():
+    rng = np.random.default_rng(0)
+    idx = rng.integers(0, 255, size=(1000, 8))
+    rows = sp.pack(idx)
+    assert rows.dtype == np.uint64
+    assert np.array_equal(sp.unpack(rows, 8), idx)
+    assert int(sp.pack([[1, 2, 3]])[0]) == 1 | (2 << 8) | (3 << 16)
+
+
+def test_validation_messages_match_reference():
+    space = sp.grid(4, 3)
+    with pytest.raises(kt.errors.DimensionMismatchError, match="configuration has 3 indices, space 'grid' has 2 knobs"):
+        sp.index_matrix(space, [kt.Configuration((0, 0, 0))])
+    with pytest.raises(kt.errors.SpaceValidationError, match=r"knob 'k1': index 3 out of range \[0, 3\)"):
+        sp.index_matrix(space, [kt.Configuration((0, 3))])
+
+
+def test_engine_space_limits():
+    with pytest.raises(NotImplementedError):
+        sp.check_engine_space(sp.grid(*([2] * 9)))
+    with pytest.raises(NotImplementedError):
+        sp.check_engine_space(sp.grid(256))
+
+
+def test_workload_spaces():
+    cards = [len(v) for _, v in RESNET18_S2.knobs()]
+    assert cards == [84, 80, 80, 7, 2, 2, 3, 2]
+    assert int(np.prod(cards)) == 90_316_800
+    for t in RESNET18_TASKS + VGG16_TASKS:
+        sp.check_engine_space(sp.space_from_dict(t.space_dict()))
+
+
+def test_product_never_imports_the_oracle():
+    pkg = ROOT / "paper_1905_12799_b200"
+    for f in list(pkg.rglob("*.py")) + list(pkg.rglob("*.cu")) + list(pkg.rglob("*.cuh")):
+        text = f.read_text()
+        assert not re.search(r"^\s*(from|import)\s+oracle", text, re.M), f"{f} imports the oracle"
+        assert "reference/pkg" not in text, f"{f} reads the reference at run time"
+
+
+def test_engine_calls_fail_loudly_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(kt.EngineUnavailable):
+        kt.engine()
+    space = sp.grid(3, 3)
+    with pytest.raises(kt.EngineUnavailable):
+        kt.predict(kt.CostModel.sentinel(2), space, [kt.Configuration((0, 0))])
