@@ -1,0 +1,339 @@
+#!/usr/bin/env python
+"""Benchmark: candidate configs scored + clustered per second per tuning step (BASELINE.json metric).
+
+Step = one pass of the search-step hot path over one batch of candidates of
+the ResNet-18 3x3 64->64 56x56 conv space (S2, 90.3M configs):
+    K2 surrogate scoring (50 depth-4 boosted trees)  ->  K6 first-occurrence dedup
+    ->  K7/K8 knee k-means (k = 8, 9, ... until the knee)  ->  K9 mode / batch assembly
+exactly as predict() + adaptive_sample() compute it in the reference.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--candidates 1048576]
+
+N>1 runs under torchrun: one process per GPU, each rank tunes its own task
+(weak scaling, no data-path collective); time = max over ranks.
+Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "candidate configs scored+clustered/sec per tuning step"
+UNIT = "candidates/s"
+WORKLOAD = ("resnet18.c2_3x3_64x64_56 space (S2: 84x80x80x7x2x2x3x2 = 90,316,800 configs); per step {n} "
+            "uniform candidates -> K2 boosted-tree scores (50 trees, depth 4) + K6 dedup + K7/K8 knee k-means "
+            "(k=8..knee, seeded) + K9 mode + batch (predict + adaptive_sample)")
+
+
+def load_model():
+    doc = json.loads((ROOT / "data" / "models" / "s2_resnet18.json").read_text())
+    return doc
+
+
+def candidates(n: int, seed: int, cards: np.ndarray) -> np.ndarray:
+    rng = np.random.default_rng(seed)
+    return rng.integers(0, cards, size=(n, cards.size))
+
+
+def peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": float(d["hbm_gbs"]), "bf16_tflops": float(d["bf16_tflops"]), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------- CPU side
+def cpu_step(doc, idx: np.ndarray, seed: int):
+    from oracle import sampler as osamp
+    from oracle import trees as otrees
+
+    scores = otrees.predict_features(doc["model"], otrees.featurize_rows(doc["values"], idx))
+    batch = osamp.adaptive_sample(idx, set(), [len(v) for v in doc["values"]], seed)
+    return scores, batch
+
+
+def cpu_baseline(doc, cards, n_sample: int, reps: int = 1) -> dict:
+    idx = candidates(n_sample, 12345, cards)
+    t0 = time.perf_counter()
+    for r in range(reps):
+        cpu_step(doc, idx, 7 + r)
+    dt = (time.perf_counter() - t0) / reps
+    return {"value": n_sample / dt, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{n_sample} uniform S2 candidates per step (oracle/ numpy restatement of "
+                      f"predict_features + adaptive_sample, single-threaded), {reps} step(s), {dt:.2f} s/step"}
+
+
+def _ref_job(job):
+    n, cand_seed, seed = job
+    doc = load_model()
+    cards = np.array([len(v) for v in doc["values"]])
+    cpu_step(doc, candidates(n, cand_seed, cards), seed)
+
+
+def run_reference(args, rank: int, world: int) -> None:
+    """--impl reference: the reference's CPU algorithm (oracle port; the reference itself is pure Python
+    and /root/reference does not exist on the GPU box) on the host cores, rank 0 only."""
+    if rank != 0:
+        return
+    import multiprocessing as mp
+
+    doc = load_model()
+    cards = np.array([len(v) for v in doc["values"]])
+    n = args.ref_sample
+    procs = args.ref_procs or len(os.sched_getaffinity(0))
+    cpu_step(doc, candidates(n, 1, cards), 100)  # warm caches / imports in the parent
+    ctx = mp.get_context("fork")
+    with ctx.Pool(procs) as pool:
+        pool.map(_ref_job, [(n, 100 + w, 100 + w) for w in range(max(args.warmup, 1) * procs)][:procs])
+        t0 = time.perf_counter()
+        pool.map(_ref_job, [(n, 1000 + s, 200 + s) for s in range(args.steps * procs)])
+        wall = time.perf_counter() - t0
+    dt = wall / args.steps  # wall time per round of `procs` concurrent steps
+    value = n * procs / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD.format(n=n), "candidates_per_step": n,
+                   "parallelism": f"{procs} host processes, one independent task each"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port",
+                         "sample": f"{n} uniform S2 candidates per step per process, oracle numpy port "
+                                   f"(predict_features + adaptive_sample), {procs} processes x {args.steps} steps"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------- GPU side
+def run_ours(args, rank: int, world: int, local_rank: int) -> None:
+    import torch
+
+    import paper_1905_12799_b200 as kt
+    from paper_1905_12799_b200 import space as sp
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    eng = kt.engine(local_rank)
+    doc = load_model()
+    space = kt.space_from_dict({"name": doc["space"], "knobs": [{"name": f"k{i}", "values": v}
+                                                                  for i, v in enumerate(doc["values"])]})
+    model = kt.CostModel.from_dict(doc["model"])
+    cards = np.array(space.cardinalities)
+    N = args.candidates
+    no_visited = np.zeros(0, dtype=np.uint64)
+
+    # inputs: one distinct candidate set per step (and per rank), pinned on the host and resident on the device
+    n_sets = max(2, min(args.steps, 4))
+    host_sets = []
+    for s in range(n_sets):
+        rows = sp.pack(candidates(N, 10_000 * rank + s, cards)).view(np.int64)
+        host_sets.append(torch.from_numpy(rows).pin_memory())
+    dev = f"cuda:{local_rank}"
+    dev_sets = [h.to(dev) for h in host_sets]
+    scores_buf = torch.empty(N, dtype=torch.float64, device=dev)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+
+    def step(rows_dev, seed, info=None):
+        kt.predict_rows(model, space, rows_dev, out=scores_buf, engine=eng)
+        return kt.adaptive_sample_rows(rows_dev, no_visited, space, seed, engine=eng, info=info)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+
+    for w in range(args.warmup):
+        step(dev_sets[w % n_sets], 50 + w)
+    barrier()
+
+    # ---- timed region 1: device-resident inputs (value)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = eng.launches
+    infos = []
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        for s in range(args.steps):
+            flush.fill_(float(s))  # L2 flush, outside the timed events
+            with eng.scope():
+                ev[s][0].record(eng.stream)
+            info = kt._lib.SampleInfo()
+            step(dev_sets[s % n_sets], 1000 + s, info)
+            with eng.scope():
+                ev[s][1].record(eng.stream)
+            infos.append(info)
+        barrier()
+    launches = eng.launches - launches0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    t_total = sum(step_ms) / 1e3
+
+    # ---- timed region 2: end to end through the public API with host buffers
+    e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    d2h = 0
+    barrier()
+    for s in range(args.steps):
+        flush.fill_(float(s))
+        with eng.scope():
+            e2e_ev[s][0].record(eng.stream)
+            rows_dev = host_sets[s % n_sets].to(dev, non_blocking=True)
+        batch = step(rows_dev, 2000 + s)
+        with eng.scope():
+            e2e_ev[s][1].record(eng.stream)
+        d2h += batch.nbytes
+    barrier()
+    t_e2e = sum(a.elapsed_time(b) for a, b in e2e_ev) / 1e3
+
+    # ---- instrumented pass: per-kernel CUDA-event durations (roofline)
+    eng.set_timing(True)
+    eng.kernel_stats(reset=True)
+    kinfo = []
+    for s in range(args.steps):
+        flush.fill_(float(s))
+        info = kt._lib.SampleInfo()
+        step(dev_sets[s % n_sets], 1000 + s, info)
+        kinfo.append(info)
+    stats = eng.kernel_stats(reset=True)
+    eng.set_timing(False)
+
+    times = torch.tensor([t_total, t_e2e], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(times, op=dist.ReduceOp.MAX)
+    t_total, t_e2e = float(times[0]), float(times[1])
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    K = args.steps
+    value = world * N * K / t_total
+    e2e_value = world * N * K / t_e2e
+    pk = peaks()
+    # dominant kernel and its algorithmic bytes per launch
+    dom = max(stats.items(), key=lambda kv: kv[1][1])
+    dom_name, (dom_count, dom_ms) = dom
+    if dom_name == "lloyd":
+        alg_bytes = sum(i.lloyd_bytes for i in kinfo)
+        note = "per Lloyd pass: m*8 B point rows + 2*m B assignment (read+write) per active k"
+    elif dom_name == "score_trees":
+        alg_bytes = K * N * 16
+        note = "8 B row read + 8 B float64 score written per candidate"
+    else:
+        alg_bytes = None
+        note = "no byte model"
+    achieved = (alg_bytes / dom_count) / (dom_ms / dom_count / 1e3) / 1e9 if alg_bytes else None
+    kernel_table = {k: {"launches": c, "ms_total": round(ms, 4), "ms_per_step": round(ms / K, 4)}
+                    for k, (c, ms) in sorted(stats.items(), key=lambda kv: -kv[1][1])}
+    base = cpu_baseline(doc, cards, args.cpu_sample) if not args.no_cpu_baseline else None
+    chosen = sorted({i.chosen_k for i in infos})
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+        "ms_per_step": t_total / K * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD.format(n=N), "candidates_per_step": N, "parallelism": f"tasks x{world} (1 per GPU)",
+                   "l2": "flushed between steps (512 MiB write, outside the timed events)",
+                   "distinct_per_step": int(np.mean([i.n_distinct for i in infos])), "knee_k": chosen,
+                   "lloyd_passes_per_step": float(np.mean([i.lloyd_passes for i in infos]))},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": N * 8, "d2h_bytes_per_step": d2h // K},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": (achieved / pk["hbm_gbs"]) if achieved else None, "traffic": None,
+                     "peak_source": pk["source"], "bytes_model": note,
+                     "kernel_share_of_step": dom_ms / sum(ms for _, ms in stats.values())},
+        "kernels": kernel_table,
+        "clocks": clk.summary(),
+        "cpu_baseline": base,
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--candidates", type=int, default=1 << 20)
+    ap.add_argument("--cpu-sample", type=int, default=32768)
+    ap.add_argument("--ref-sample", type=int, default=16384)
+    ap.add_argument("--ref-procs", type=int, default=0, help="host processes for --impl reference (0: all cores)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

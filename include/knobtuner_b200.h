@@ -55,6 +55,11 @@ int kt_engine_set_stream(kt_engine* e, void* cuda_stream);
 int kt_engine_synchronize(kt_engine* e);
 /* Number of engine kernels launched since creation (evidence counter for the bench). */
 int64_t kt_engine_launch_count(const kt_engine* e);
+/* Per-kernel CUDA-event timing on the engine stream (off by default). */
+int kt_engine_set_timing(kt_engine* e, int enabled);
+/* Accumulated per-kernel stats: names is capacity x 32 chars; reset != 0 clears them. */
+int kt_engine_kernel_stats(kt_engine* e, int capacity, char* names, int64_t* counts, double* total_ms,
+                           int32_t* n_kernels, int reset);
 
 /* ------------------------------------------------------- host RNG streams */
 /* numpy SeedSequence(entropy, spawn_key) -> PCG64 -> random()/integers(0, n)
@@ -135,6 +140,9 @@ typedef struct kt_sample_info {
     double scanned_loss[56];
     int32_t lloyd_passes;   /* sum over scanned k */
     int32_t used_mode;      /* 1 if a visited centroid was replaced by the mode */
+    int32_t lloyd_launches; /* fused multi-k Lloyd launches */
+    int64_t lloyd_bytes;    /* algorithmic bytes of all Lloyd passes: per pass m*n point
+                               bytes + 2*m assignment bytes per active k */
 } kt_sample_info;
 
 /* The whole adaptive_sample (sampler.py:173-215): dedup -> knee k-means ->

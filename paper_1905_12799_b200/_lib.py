@@ -38,6 +38,8 @@ class SampleInfo(C.Structure):
         ("scanned_loss", C.c_double * 56),
         ("lloyd_passes", C.c_int32),
         ("used_mode", C.c_int32),
+        ("lloyd_launches", C.c_int32),
+        ("lloyd_bytes", C.c_int64),
     ]
 
 
@@ -50,6 +52,8 @@ SIGNATURES = {
     "kt_engine_set_stream": (C.c_int, [P, P]),
     "kt_engine_synchronize": (C.c_int, [P]),
     "kt_engine_launch_count": (C.c_int64, [P]),
+    "kt_engine_set_timing": (C.c_int, [P, C.c_int]),
+    "kt_engine_kernel_stats": (C.c_int, [P, C.c_int, C.c_char_p, pi64, pf64, pi32, C.c_int]),
     "kt_pcg64_draw": (C.c_int, [pu32, C.c_int, pu32, C.c_int, C.c_int, u64, i64, P]),
     "kt_forest_create": (C.c_int, [P, C.c_int, pi32, pf64, C.c_int, C.c_int, pi32, pi32, pf64, pi32, pi32, pf64,
                                    f64, C.POINTER(P)]),
@@ -151,6 +155,23 @@ class Engine:
 
     def synchronize(self) -> None:
         call("kt_engine_synchronize", self.handle)
+
+    def set_timing(self, enabled: bool) -> None:
+        call("kt_engine_set_timing", self.handle, int(bool(enabled)))
+
+    def kernel_stats(self, reset: bool = True) -> dict[str, tuple[int, float]]:
+        """{kernel name: (launches, total ms)} recorded while timing was on."""
+        cap = 64
+        names = C.create_string_buffer(cap * 32)
+        counts = (C.c_int64 * cap)()
+        ms = (C.c_double * cap)()
+        n = C.c_int32(0)
+        call("kt_engine_kernel_stats", self.handle, cap, names, counts, ms, C.byref(n), int(reset))
+        out = {}
+        for i in range(n.value):
+            name = names.raw[i * 32:(i + 1) * 32].split(b"\0", 1)[0].decode()
+            out[name] = (int(counts[i]), float(ms[i]))
+        return out
 
     def set_stream(self, stream_ptr: int | None) -> None:
         call("kt_engine_set_stream", self.handle, P(stream_ptr) if stream_ptr else None)

@@ -4,8 +4,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
 #include <string>
 #include <unordered_map>
+#include <vector>
 
 #include "../../include/knobtuner_b200.h"
 
@@ -121,12 +123,30 @@ struct kt_engine {
     std::unordered_map<std::string, Buf> dev;
     std::unordered_map<std::string, Buf> pinned;
 
+    // Optional per-kernel CUDA-event timing (kt_engine_set_timing).
+    bool timing = false;
+    cudaEvent_t open_start = nullptr;
+    struct Pending {
+        const char* name;
+        cudaEvent_t start, stop;
+    };
+    std::vector<Pending> pending;
+    std::vector<cudaEvent_t> event_pool;
+    struct Stat {
+        int64_t count = 0;
+        double ms = 0.0;
+    };
+    std::map<std::string, Stat> stats;
+
     // Named, growable device scratch (contents undefined after growth).
     void* scratch(const std::string& name, size_t bytes);
     // Named, growable pinned host staging buffer.
     void* staging(const std::string& name, size_t bytes);
     void note_launch(int n = 1) { launches += n; }
-    void check_launch(const char* what);
+    void pre_launch(const char* what);    // call right before a kernel launch
+    void check_launch(const char* what);  // call right after it
+    void flush_timing();
+    cudaEvent_t take_event();
     void sync();
 };
 

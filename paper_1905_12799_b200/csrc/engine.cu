@@ -49,10 +49,49 @@ void* kt_engine::staging(const std::string& name, size_t bytes) {
     return b.ptr;
 }
 
+cudaEvent_t kt_engine::take_event() {
+    if (!event_pool.empty()) {
+        cudaEvent_t ev = event_pool.back();
+        event_pool.pop_back();
+        return ev;
+    }
+    cudaEvent_t ev;
+    KT_CUDA(cudaEventCreate(&ev));
+    return ev;
+}
+
+void kt_engine::pre_launch(const char* what) {
+    (void)what;
+    if (!timing) return;
+    open_start = take_event();
+    KT_CUDA(cudaEventRecord(open_start, stream));
+}
+
 void kt_engine::check_launch(const char* what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) kt::fail(KT_ERR_CUDA, std::string("launch of ") + what + ": " + cudaGetErrorString(e));
     note_launch();
+    if (timing && open_start) {
+        cudaEvent_t stop = take_event();
+        KT_CUDA(cudaEventRecord(stop, stream));
+        pending.push_back({what, open_start, stop});
+        open_start = nullptr;
+    }
+}
+
+void kt_engine::flush_timing() {
+    if (pending.empty()) return;
+    KT_CUDA(cudaStreamSynchronize(stream));
+    for (auto& p : pending) {
+        float ms = 0.f;
+        KT_CUDA(cudaEventElapsedTime(&ms, p.start, p.stop));
+        Stat& s = stats[p.name];
+        s.count += 1;
+        s.ms += ms;
+        event_pool.push_back(p.start);
+        event_pool.push_back(p.stop);
+    }
+    pending.clear();
 }
 
 void kt_engine::sync() { KT_CUDA(cudaStreamSynchronize(stream)); }
@@ -110,6 +149,31 @@ int kt_engine_synchronize(kt_engine* e) {
 }
 
 int64_t kt_engine_launch_count(const kt_engine* e) { return e ? e->launches : 0; }
+
+int kt_engine_set_timing(kt_engine* e, int enabled) {
+    KT_API_BEGIN
+    e->flush_timing();
+    e->timing = enabled != 0;
+    KT_API_END
+}
+
+int kt_engine_kernel_stats(kt_engine* e, int capacity, char* names, int64_t* counts, double* total_ms,
+                           int32_t* n_kernels, int reset) {
+    KT_API_BEGIN
+    e->flush_timing();
+    int i = 0;
+    for (auto& kv : e->stats) {
+        if (i >= capacity) break;
+        std::strncpy(names + size_t(i) * 32, kv.first.c_str(), 31);
+        names[size_t(i) * 32 + 31] = '\0';
+        counts[i] = kv.second.count;
+        total_ms[i] = kv.second.ms;
+        ++i;
+    }
+    *n_kernels = i;
+    if (reset) e->stats.clear();
+    KT_API_END
+}
 
 int kt_pcg64_draw(const uint32_t* entropy, int ne, const uint32_t* spawn, int ns, int kind,
                   uint64_t bound, int64_t count, void* out) {

@@ -182,6 +182,7 @@ int kt_score_landscape(kt_engine* e, const kt_landscape* l, const uint64_t* rows
         a.r2[j] = l->radii[j] * l->radii[j];
     }
     const int grid = int(std::min<int64_t>(ceil_div(count, 256), int64_t(e->num_sms) * 8));
+    e->pre_launch("score_landscape");
     landscape_kernel<<<grid, 256, 0, e->stream>>>(a, rows_dev, count, runtime_dev);
     e->check_launch("score_landscape");
     KT_API_END

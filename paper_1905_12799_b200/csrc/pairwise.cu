@@ -137,9 +137,11 @@ void pairwise_loss(kt_engine* e, const uint64_t* pts, int64_t m, int n, const ui
     auto* vals = static_cast<double*>(e->scratch("loss.vals", size_t(L + I) * 8));
     auto* lvl = static_cast<int32_t*>(e->scratch("loss.levels", t.level_start.size() * 4));
     KT_CUDA(cudaMemcpyAsync(lvl, t.level_start.data(), t.level_start.size() * 4, cudaMemcpyHostToDevice, e->stream));
+    e->pre_launch("loss_leaf");
     loss_leaf_kernel<<<int(ceil_div(L, 128)), 128, 0, e->stream>>>(pts, assign, cent, n, t.d_leaf_start, t.d_leaf_len,
                                                                     L, vals);
     e->check_launch("loss_leaf");
+    e->pre_launch("loss_combine");
     loss_combine_kernel<<<1, 1024, 0, e->stream>>>(vals, L, t.d_left, t.d_right, lvl, t.n_levels, t.root, out_dev);
     e->check_launch("loss_combine");
 }
@@ -186,8 +188,10 @@ void pairwise_sum(kt_engine* e, const double* x, int64_t m, const double* center
     auto* vals = static_cast<double*>(e->scratch("psum.vals", size_t(L + I) * 8));
     auto* lvl = static_cast<int32_t*>(e->scratch("psum.levels", t.level_start.size() * 4));
     KT_CUDA(cudaMemcpyAsync(lvl, t.level_start.data(), t.level_start.size() * 4, cudaMemcpyHostToDevice, e->stream));
+    e->pre_launch("psum_leaf");
     array_leaf_kernel<<<int(ceil_div(L, 128)), 128, 0, e->stream>>>(x, center, t.d_leaf_start, t.d_leaf_len, L, vals);
     e->check_launch("psum_leaf");
+    e->pre_launch("psum_combine");
     loss_combine_kernel<<<1, 1024, 0, e->stream>>>(vals, L, t.d_left, t.d_right, lvl, t.n_levels, t.root, out_dev);
     e->check_launch("psum_combine");
 }

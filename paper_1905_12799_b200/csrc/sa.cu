@@ -127,6 +127,7 @@ static void launch_chains(kt_engine* e, const kt_forest* f, const SAArgs& a) {
     if (smem > 200 * 1024) fail(KT_ERR_UNSUPPORTED, "forest too large for the in-kernel SA walk");
     auto kern = sa_chain_kernel<D>;
     KT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    e->pre_launch("sa_chains");
     kern<<<int(ceil_div(a.chains, 128)), 128, smem, e->stream>>>(a);
     e->check_launch("sa_chains");
 }
@@ -166,10 +167,12 @@ extern "C" int kt_sa_chains(kt_engine* e, const kt_forest* f, const uint64_t* st
     auto* scal = static_cast<double*>(e->scratch("sa.scalars", 4 * 8));  // sum, mean, sumsq, temperature
     if (!has_initial_temperature) {
         pairwise_sum(e, start_scores, chains, nullptr, scal + 0);
+        e->pre_launch("sa_mean");
         sa_temperature_kernel<<<1, 1, 0, e->stream>>>(scal + 0, nullptr, chains, 0, 0.0, scal + 1, nullptr, 0);
         e->check_launch("sa_mean");
         pairwise_sum(e, start_scores, chains, scal + 1, scal + 2);
     }
+    e->pre_launch("sa_temperature");
     sa_temperature_kernel<<<1, 1, 0, e->stream>>>(nullptr, scal + 2, chains, has_initial_temperature,
                                                   initial_temperature, nullptr, scal + 3, 1);
     e->check_launch("sa_temperature");
@@ -208,6 +211,7 @@ extern "C" int kt_sa_chains(kt_engine* e, const kt_forest* f, const uint64_t* st
     }
     auto* offsets = static_cast<int64_t*>(e->scratch("sa.offsets", size_t(chains + 1) * 8));
     exclusive_scan(e, a.counts, offsets, chains);
+    e->pre_launch("sa_compact");
     sa_compact_kernel<<<int(ceil_div(int64_t(chains) * 32, 256)), 256, 0, e->stream>>>(
         a.slot_rows, a.slot_scores, a.slot_steps, a.counts, offsets, chains, steps, rows_out_dev, scores_out_dev,
         steps_out_dev);

@@ -147,6 +147,7 @@ __global__ void __launch_bounds__(256) dedup_scatter_kernel(const uint64_t* __re
 }
 
 void exclusive_scan(kt_engine* e, const int64_t* in, int64_t* out, int n) {
+    e->pre_launch("exclusive_scan");
     exclusive_scan_kernel<<<1, 1024, 0, e->stream>>>(in, out, n);
     e->check_launch("exclusive_scan");
 }
@@ -170,11 +171,14 @@ int64_t dedup(kt_engine* e, const uint64_t* rows, int64_t count, uint64_t* out) 
     auto* counts = static_cast<int64_t*>(e->scratch("dedup.counts", size_t(nb) * 8));
     auto* offsets = static_cast<int64_t*>(e->scratch("dedup.offsets", size_t(nb + 1) * 8));
     int grid = int(std::min<int64_t>(ceil_div(count, 256), int64_t(e->num_sms) * 8));
+    e->pre_launch("dedup_insert");
     dedup_insert_kernel<<<grid, 256, 0, e->stream>>>(rows, count, keys, first, cap - 1);
     e->check_launch("dedup_insert");
+    e->pre_launch("dedup_flag");
     dedup_flag_kernel<<<nb, 256, 0, e->stream>>>(rows, count, keys, first, cap - 1, bits, counts);
     e->check_launch("dedup_flag");
     exclusive_scan(e, counts, offsets, nb);
+    e->pre_launch("dedup_scatter");
     dedup_scatter_kernel<<<nb, 256, 0, e->stream>>>(rows, count, bits, offsets, out);
     e->check_launch("dedup_scatter");
     auto* h_total = static_cast<int64_t*>(e->staging("dedup.total", 8));
@@ -215,6 +219,7 @@ void mode_vote(kt_engine* e, const uint64_t* rows, int64_t count, int n, int32_t
     auto* hist = static_cast<unsigned int*>(e->scratch("mode.hist", kMaxKnobs * 256 * 4));
     KT_CUDA(cudaMemsetAsync(hist, 0, kMaxKnobs * 256 * 4, e->stream));
     int grid = int(std::min<int64_t>(ceil_div(count, 256), int64_t(e->num_sms) * 4));
+    e->pre_launch("mode_hist");
     mode_hist_kernel<<<grid, 256, 0, e->stream>>>(rows, count, n, hist);
     e->check_launch("mode_hist");
     auto* h = static_cast<unsigned int*>(e->staging("mode.hist", kMaxKnobs * 256 * 4));
@@ -651,10 +656,12 @@ struct KmeansSession {
         while (chosen < k) {
             const int j = chosen;
             if (j > 0) {
+                e->pre_launch("init_select");
                 init_select_kernel<<<1, 1024, 0, e->stream>>>(pts, m, d2, chunk_sums, nchunks, d_uniforms, j, cent_rows);
                 e->check_launch("init_select");
             }
             if (j + 1 < 64) {  // d2 update needed only if another centroid follows
+                e->pre_launch("init_update");
                 init_update_kernel<<<nchunks, 256, 0, e->stream>>>(pts, m, n, cent_rows, j, first_idx, d2, chunk_sums);
                 e->check_launch("init_update");
             }
@@ -699,6 +706,7 @@ struct KmeansSession {
         KT_CUDA(cudaMemsetAsync(a.assign, 0xff, size_t(R) * m, e->stream));
         KT_CUDA(cudaMemsetAsync(a.S, 0, size_t(K) * kSumW * 8, e->stream));
         for (int r = 0; r < R; ++r) {
+            e->pre_launch("rows_to_centroids");
             rows_to_centroids_kernel<<<int(ceil_div(ks[r] * kMaxKnobs, 256)), 256, 0, e->stream>>>(
                 cent_rows, ks[r], n, a.cent + size_t(a.coff[r]) * kMaxKnobs);
             e->check_launch("rows_to_centroids");
@@ -722,8 +730,10 @@ struct KmeansSession {
             a.it0 = it;
             a.it_end = history ? it + 1 : a.max_iters;
             void* params[] = {&a};
+            e->pre_launch("lloyd");
             KT_CUDA(cudaLaunchCooperativeKernel((const void*)lloyd_kernel, grid, 256, params, smem, e->stream));
             e->check_launch("lloyd");
+            ++lloyd_launches;
             KT_CUDA(cudaMemcpyAsync(h_ctrl, a.ctrl, 4, cudaMemcpyDeviceToHost, e->stream));
             KT_CUDA(cudaMemcpyAsync(h_state, a.run_state, R * 4, cudaMemcpyDeviceToHost, e->stream));
             if (history) {
@@ -756,7 +766,16 @@ struct KmeansSession {
         KT_CUDA(cudaMemcpyAsync(h_loss, d_loss, R * 8, cudaMemcpyDeviceToHost, e->stream));
         KT_CUDA(cudaMemcpyAsync(h_iter, a.run_iter, R * 4, cudaMemcpyDeviceToHost, e->stream));
         e->sync();
-        for (int r = 0; r < R; ++r) out[r] = {ks[r], h_iter[r] + 1, h_loss[r]};
+        int max_passes = 0;
+        for (int r = 0; r < R; ++r) {
+            out[r] = {ks[r], h_iter[r] + 1, h_loss[r]};
+            max_passes = std::max(max_passes, h_iter[r] + 1);
+        }
+        for (int it = 0; it < max_passes; ++it) {  // algorithmic bytes of the fused passes
+            int active = 0;
+            for (int r = 0; r < R; ++r) active += out[r].passes > it;
+            lloyd_bytes += m * n + 2 * m * active;
+        }
         last_args = a;
         return out;
     }
@@ -769,6 +788,7 @@ struct KmeansSession {
         double* cent = a.cent + size_t(co) * kMaxKnobs;  // centroids used by the pass
         auto* pd2 = static_cast<double*>(e->scratch("km.pd2", size_t(m) * 8));
         const int grid = int(std::min<int64_t>(ceil_div(m, 256), int64_t(e->num_sms) * 4));
+        e->pre_launch("point_d2");
         point_d2_kernel<<<grid, 256, 0, e->stream>>>(pts, m, n, asg, cent, pd2);
         e->check_launch("point_d2");
         std::vector<int64_t> blocked;
@@ -791,6 +811,7 @@ struct KmeansSession {
         for (size_t q = 0; q < empties.size(); ++q) {
             if (!blocked.empty())
                 KT_CUDA(cudaMemcpyAsync(d_blocked, blocked.data(), blocked.size() * 8, cudaMemcpyHostToDevice, e->stream));
+            e->pre_launch("argmax");
             argmax_kernel<<<grid, 256, 0, e->stream>>>(pd2, m, d_blocked, int(blocked.size()), pv, pi);
             e->check_launch("argmax");
             KT_CUDA(cudaMemcpyAsync(h_pv, pv, size_t(grid) * 8, cudaMemcpyDeviceToHost, e->stream));
@@ -818,6 +839,8 @@ struct KmeansSession {
     }
 
     LloydArgs last_args{};
+    int64_t lloyd_bytes = 0;
+    int lloyd_launches = 0;
 };
 
 // Batches of consecutive ks run speculatively in one Lloyd launch.
@@ -839,6 +862,8 @@ struct KneeResult {
     std::vector<double> losses;
     int chosen_k = 0;
     int passes = 0;
+    int64_t lloyd_bytes = 0;
+    int lloyd_launches = 0;
     std::vector<double> centroids;  // chosen_k * n
     const uint8_t* assign_dev = nullptr;  // chosen run's assignment (device), valid until next engine call
 };
@@ -878,6 +903,8 @@ static KneeResult knee_scan(kt_engine* e, const uint64_t* pts, int64_t m, int n,
             for (int j = 0; j < ks[pick]; ++j)
                 for (int i = 0; i < n; ++i) res.centroids[size_t(j) * n + i] = c[size_t(j) * kMaxKnobs + i];
             res.assign_dev = a.assign + size_t(pick) * m;
+            res.lloyd_bytes = ses.lloyd_bytes;
+            res.lloyd_launches = ses.lloyd_launches;
             return res;
         }
         k0 = ks.back() + 1;
@@ -990,6 +1017,8 @@ int kt_adaptive_sample(kt_engine* e, const uint64_t* rows_dev, int64_t count, in
         inf.scanned_loss[i] = r.losses[i];
     }
     inf.lloyd_passes = r.passes;
+    inf.lloyd_bytes = r.lloyd_bytes;
+    inf.lloyd_launches = r.lloyd_launches;
     // batch assembly (sampler.py:200-215)
     bool have_mode = false;
     uint64_t mode_row = 0;

@@ -148,6 +148,7 @@ static void launch_score(kt_engine* e, const kt_forest* f, const uint64_t* rows,
     int grid = int(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(e->num_sms) * std::max(occ, 1))));
     for (int t0 = 0; t0 < f->n_trees; t0 += per_chunk) {
         int t1 = std::min(f->n_trees, t0 + per_chunk);
+        e->pre_launch("score_trees");
         kern<<<grid, threads, size_t(t1 - t0) * bytes_per_tree, e->stream>>>(
             f->dev, f->words_per_tree, t0, t1, f->n_trees, f->base, rows, count, out);
         e->check_launch("score_trees");
@@ -158,6 +159,7 @@ void score_trees(kt_engine* e, const kt_forest* f, const uint64_t* rows, int64_t
     if (count <= 0) return;
     if (f->n_trees == 0) {
         int grid = int(std::min<int64_t>(ceil_div(count, 256), int64_t(e->num_sms) * 8));
+        e->pre_launch("fill");
         fill_kernel<<<grid, 256, 0, e->stream>>>(out, count, f->base);
         e->check_launch("fill");
         return;
