@@ -66,6 +66,8 @@ std::shared_ptr<PairwiseTree> make_tree(int64_t m) {
     KT_CUDA(cudaMalloc(&t->d_leaf_len, std::max<size_t>(1, L) * 4));
     KT_CUDA(cudaMalloc(&t->d_left, std::max<size_t>(1, I) * 4));
     KT_CUDA(cudaMalloc(&t->d_right, std::max<size_t>(1, I) * 4));
+    KT_CUDA(cudaMalloc(&t->d_level, t->level_start.size() * 4));
+    KT_CUDA(cudaMemcpy(t->d_level, t->level_start.data(), t->level_start.size() * 4, cudaMemcpyHostToDevice));
     KT_CUDA(cudaMemcpy(t->d_leaf_start, t->leaf_start.data(), L * 8, cudaMemcpyHostToDevice));
     KT_CUDA(cudaMemcpy(t->d_leaf_len, t->leaf_len.data(), L * 4, cudaMemcpyHostToDevice));
     if (I) {
@@ -87,39 +89,78 @@ const PairwiseTree& pairwise_tree(int device, int64_t m) {
     return *t;
 }
 
-// One thread per leaf: the squared distance of each point to its assigned
-// centroid, summed numpy-style (n<8: sequential from 0; else 8 accumulators).
-__global__ void loss_leaf_kernel(const uint64_t* __restrict__ pts, const uint8_t* __restrict__ assign,
-                                 const double* __restrict__ cent, int n, const int64_t* leaf_start,
-                                 const int32_t* leaf_len, int L, double* vals) {
-    const int l = blockIdx.x * blockDim.x + threadIdx.x;
-    if (l >= L) return;
+// ---------------------------------------------------------------- kernels
+// One warp per leaf (<= 128 values): lanes evaluate the values into shared
+// memory, lanes 0..7 run numpy's 8 strided accumulators in order, lane 0
+// folds them as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) and adds the tail.
+constexpr int kLeafWarps = 4;
+
+template <class Value>
+__device__ __forceinline__ void warp_leaf(int l, const int64_t* leaf_start, const int32_t* leaf_len, double* vals,
+                                          double* buf, Value value) {
+    const int lane = threadIdx.x & 31;
     const int64_t s = leaf_start[l];
     const int len = leaf_len[l];
-    auto v = [&](int i) { return np_sq_dist(pts[s + i], cent + int(assign[s + i]) * kMaxKnobs, n); };
-    double res;
-    if (len < 8) {
-        res = 0.0;
-        for (int i = 0; i < len; ++i) res = __dadd_rn(res, v(i));
-    } else {
-        double r[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) r[j] = v(j);
-        int i = 8;
-        for (; i < len - (len % 8); i += 8) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], v(i + j));
-        }
-        res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                        __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-        for (; i < len; ++i) res = __dadd_rn(res, v(i));
+    for (int i = lane; i < len; i += 32) buf[i] = value(s + i);
+    __syncwarp();
+    double r = 0.0;
+    const int body = len - (len % 8);
+    if (len >= 8 && lane < 8) {
+        r = buf[lane];
+        for (int i = 8 + lane; i < body; i += 8) r = __dadd_rn(r, buf[i]);
     }
-    vals[l] = res;
+    double r0 = __shfl_sync(0xffffffffu, r, 0), r1 = __shfl_sync(0xffffffffu, r, 1);
+    double r2 = __shfl_sync(0xffffffffu, r, 2), r3 = __shfl_sync(0xffffffffu, r, 3);
+    double r4 = __shfl_sync(0xffffffffu, r, 4), r5 = __shfl_sync(0xffffffffu, r, 5);
+    double r6 = __shfl_sync(0xffffffffu, r, 6), r7 = __shfl_sync(0xffffffffu, r, 7);
+    if (lane == 0) {
+        double res;
+        int i;
+        if (len < 8) {
+            res = 0.0;
+            i = 0;
+        } else {
+            res = __dadd_rn(__dadd_rn(__dadd_rn(r0, r1), __dadd_rn(r2, r3)), __dadd_rn(__dadd_rn(r4, r5), __dadd_rn(r6, r7)));
+            i = body;
+        }
+        for (; i < len; ++i) res = __dadd_rn(res, buf[i]);
+        vals[l] = res;
+    }
 }
 
-__global__ void __launch_bounds__(1024) loss_combine_kernel(double* vals, int L, const int32_t* left,
-                                                            const int32_t* right, const int32_t* level_start,
-                                                            int n_levels, int root, double* out) {
+__global__ void __launch_bounds__(kLeafWarps * 32) loss_leaf_kernel(const uint64_t* __restrict__ pts,
+                                                                    const uint8_t* __restrict__ assign,
+                                                                    const double* __restrict__ cent, int n,
+                                                                    const int64_t* leaf_start, const int32_t* leaf_len,
+                                                                    int L, double* vals) {
+    __shared__ double s_buf[kLeafWarps][128];
+    const int w = threadIdx.x >> 5;
+    const int l = blockIdx.x * kLeafWarps + w;
+    if (l >= L) return;
+    warp_leaf(l, leaf_start, leaf_len, vals, s_buf[w],
+              [&](int64_t p) { return np_sq_dist(pts[p], cent + int(assign[p]) * kMaxKnobs, n); });
+}
+
+__global__ void __launch_bounds__(kLeafWarps * 32) array_leaf_kernel(const double* __restrict__ x,
+                                                                     const double* center, const int64_t* leaf_start,
+                                                                     const int32_t* leaf_len, int L, double* vals) {
+    __shared__ double s_buf[kLeafWarps][128];
+    const int w = threadIdx.x >> 5;
+    const int l = blockIdx.x * kLeafWarps + w;
+    if (l >= L) return;
+    const double c = center ? *center : 0.0;
+    const bool sq = center != nullptr;
+    warp_leaf(l, leaf_start, leaf_len, vals, s_buf[w], [&](int64_t p) {
+        const double a = x[p];
+        if (!sq) return a;
+        const double d = __dsub_rn(a, c);
+        return __dmul_rn(d, d);
+    });
+}
+
+__global__ void __launch_bounds__(1024) combine_kernel(double* vals, int L, const int32_t* left, const int32_t* right,
+                                                       const int32_t* level_start, int n_levels, int root,
+                                                       double* out) {
     for (int lv = 0; lv < n_levels; ++lv) {
         const int a = level_start[lv], b = level_start[lv + 1];
         for (int i = a + threadIdx.x; i < b; i += blockDim.x) vals[L + i] = __dadd_rn(vals[left[i]], vals[right[i]]);
@@ -128,72 +169,35 @@ __global__ void __launch_bounds__(1024) loss_combine_kernel(double* vals, int L,
     if (threadIdx.x == 0) *out = vals[root];
 }
 
-// loss of one run (centroids cent[k][8], assignment assign[m]) -> *out_dev
-void pairwise_loss(kt_engine* e, const uint64_t* pts, int64_t m, int n, const uint8_t* assign,
-                          const double* cent, double* out_dev) {
-    const PairwiseTree& t = pairwise_tree(e->device, m);
+static void combine(kt_engine* e, const PairwiseTree& t, double* vals, double* out_dev) {
     const int L = int(t.leaf_start.size());
-    const int I = int(t.node_left.size());
-    auto* vals = static_cast<double*>(e->scratch("loss.vals", size_t(L + I) * 8));
-    auto* lvl = static_cast<int32_t*>(e->scratch("loss.levels", t.level_start.size() * 4));
-    KT_CUDA(cudaMemcpyAsync(lvl, t.level_start.data(), t.level_start.size() * 4, cudaMemcpyHostToDevice, e->stream));
-    e->pre_launch("loss_leaf");
-    loss_leaf_kernel<<<int(ceil_div(L, 128)), 128, 0, e->stream>>>(pts, assign, cent, n, t.d_leaf_start, t.d_leaf_len,
-                                                                    L, vals);
-    e->check_launch("loss_leaf");
-    e->pre_launch("loss_combine");
-    loss_combine_kernel<<<1, 1024, 0, e->stream>>>(vals, L, t.d_left, t.d_right, lvl, t.n_levels, t.root, out_dev);
-    e->check_launch("loss_combine");
+    e->pre_launch("pairwise_combine");
+    combine_kernel<<<1, 1024, 0, e->stream>>>(vals, L, t.d_left, t.d_right, t.d_level, t.n_levels, t.root, out_dev);
+    e->check_launch("pairwise_combine");
 }
 
-
-// ---------------------------------------------------------- plain arrays
-__global__ void array_leaf_kernel(const double* __restrict__ x, const double* center, const int64_t* leaf_start,
-                                  const int32_t* leaf_len, int L, double* vals) {
-    const int l = blockIdx.x * blockDim.x + threadIdx.x;
-    if (l >= L) return;
-    const int64_t s = leaf_start[l];
-    const int len = leaf_len[l];
-    const double c = center ? *center : 0.0;
-    auto v = [&](int i) {
-        const double a = x[s + i];
-        if (!center) return a;
-        const double d = __dsub_rn(a, c);
-        return __dmul_rn(d, d);
-    };
-    double res;
-    if (len < 8) {
-        res = 0.0;
-        for (int i = 0; i < len; ++i) res = __dadd_rn(res, v(i));
-    } else {
-        double r[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) r[j] = v(j);
-        int i = 8;
-        for (; i < len - (len % 8); i += 8) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], v(i + j));
-        }
-        res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                        __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-        for (; i < len; ++i) res = __dadd_rn(res, v(i));
-    }
-    vals[l] = res;
+void pairwise_loss(kt_engine* e, const uint64_t* pts, int64_t m, int n, const uint8_t* assign, const double* cent,
+                   double* out_dev) {
+    const PairwiseTree& t = pairwise_tree(e->device, m);
+    const int L = int(t.leaf_start.size());
+    auto* vals = static_cast<double*>(e->scratch("loss.vals", size_t(L + t.node_left.size()) * 8));
+    e->pre_launch("loss_leaf");
+    loss_leaf_kernel<<<int(ceil_div(L, kLeafWarps)), kLeafWarps * 32, 0, e->stream>>>(pts, assign, cent, n,
+                                                                                    t.d_leaf_start, t.d_leaf_len, L,
+                                                                                    vals);
+    e->check_launch("loss_leaf");
+    combine(e, t, vals, out_dev);
 }
 
 void pairwise_sum(kt_engine* e, const double* x, int64_t m, const double* center, double* out_dev) {
     const PairwiseTree& t = pairwise_tree(e->device, m);
     const int L = int(t.leaf_start.size());
-    const int I = int(t.node_left.size());
-    auto* vals = static_cast<double*>(e->scratch("psum.vals", size_t(L + I) * 8));
-    auto* lvl = static_cast<int32_t*>(e->scratch("psum.levels", t.level_start.size() * 4));
-    KT_CUDA(cudaMemcpyAsync(lvl, t.level_start.data(), t.level_start.size() * 4, cudaMemcpyHostToDevice, e->stream));
+    auto* vals = static_cast<double*>(e->scratch("psum.vals", size_t(L + t.node_left.size()) * 8));
     e->pre_launch("psum_leaf");
-    array_leaf_kernel<<<int(ceil_div(L, 128)), 128, 0, e->stream>>>(x, center, t.d_leaf_start, t.d_leaf_len, L, vals);
+    array_leaf_kernel<<<int(ceil_div(L, kLeafWarps)), kLeafWarps * 32, 0, e->stream>>>(x, center, t.d_leaf_start,
+                                                                                     t.d_leaf_len, L, vals);
     e->check_launch("psum_leaf");
-    e->pre_launch("psum_combine");
-    loss_combine_kernel<<<1, 1024, 0, e->stream>>>(vals, L, t.d_left, t.d_right, lvl, t.n_levels, t.root, out_dev);
-    e->check_launch("psum_combine");
+    combine(e, t, vals, out_dev);
 }
 
 }  // namespace kt

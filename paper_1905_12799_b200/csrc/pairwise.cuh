@@ -26,6 +26,7 @@ struct PairwiseTree {
     int32_t* d_leaf_len = nullptr;
     int32_t* d_left = nullptr;
     int32_t* d_right = nullptr;
+    int32_t* d_level = nullptr;
     int root = 0;
     int n_levels = 0;
     ~PairwiseTree() {
@@ -33,6 +34,7 @@ struct PairwiseTree {
         cudaFree(d_leaf_len);
         cudaFree(d_left);
         cudaFree(d_right);
+        cudaFree(d_level);
     }
 };
 

@@ -234,131 +234,182 @@ void mode_vote(kt_engine* e, const uint64_t* rows, int64_t count, int n, int32_t
 }
 
 // ====================================================== k-means++ init (K7)
-constexpr int kInitChunk = 4096;  // points per init block (256 threads x 16)
+// One cooperative launch produces centroids j0..j1-1.  Per centroid: every
+// block redundantly selects it (scan of the per-chunk weight sums, then of
+// the chosen chunk's weights), then all blocks update their chunks'
+// weights d2[p] = min(d2[p], |p - c_j|^2) and chunk sums.  Weights and sums
+// are double-buffered by centroid parity, so one grid barrier per centroid
+// suffices.  Everything is exact int64 except u * total (IEEE double, as numpy).
+constexpr int kInitChunk = 4096;  // points per chunk (one block-scan of 256 threads x 16)
+constexpr int kInitThreads = 256;
 
-// d2[p] = min(d2[p], |p - c_j|^2) (exact int) and per-chunk int64 sums.
-__global__ void __launch_bounds__(256) init_update_kernel(const uint64_t* __restrict__ pts, int64_t m, int n,
-                                                          uint64_t* cent_rows, int j, int64_t first_idx,
-                                                          int* __restrict__ d2, long long* __restrict__ chunk_sums) {
-    uint64_t c;
-    if (j == 0) {
-        c = pts[first_idx];
-        if (blockIdx.x == 0 && threadIdx.x == 0) cent_rows[0] = c;
-    } else {
-        c = cent_rows[j];
+struct InitArgs {
+    const uint64_t* pts;
+    int64_t m;
+    int n;
+    int j0, j1;
+    int64_t first_idx;
+    const double* uniforms;  // u_1, u_2, ... (random() draws after integers(0, m))
+    uint64_t* cent_rows;
+    int* d2[2];
+    long long* sums[2];
+    int nchunks;
+};
+
+// Block-wide exclusive scan of one int64 per thread; returns the block total.
+__device__ __forceinline__ long long block_exclusive_scan(long long v, long long& excl, long long* s_warp) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    long long incl = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const long long t = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += t;
     }
-    const int64_t base = int64_t(blockIdx.x) * kInitChunk;
-    long long s = 0;
-    for (int t = threadIdx.x; t < kInitChunk; t += blockDim.x) {
-        const int64_t p = base + t;
-        if (p >= m) break;
-        int v = int_sq_dist(pts[p], c, n);
-        if (j > 0) v = min(v, d2[p]);
-        d2[p] = v;
-        s += v;
-    }
-    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    __shared__ long long s_w[8];
-    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = s;
+    if (lane == 31) s_warp[warp] = incl;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        long long t = 0;
-        for (int w = 0; w < 8; ++w) t += s_w[w];
-        chunk_sums[blockIdx.x] = t;
+    if (warp == 0) {
+        long long w = lane < kInitThreads / 32 ? s_warp[lane] : 0;
+        long long wi = w;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const long long t = __shfl_up_sync(0xffffffffu, wi, off);
+            if (lane >= off) wi += t;
+        }
+        if (lane < kInitThreads / 32) s_warp[lane] = wi - w;
+        if (lane == kInitThreads / 32 - 1) s_warp[32] = wi;
     }
+    __syncthreads();
+    excl = s_warp[warp] + incl - v;
+    const long long total = s_warp[32];
+    __syncthreads();
+    return total;
 }
 
-// Pick centroid j: first index whose inclusive prefix of d2 exceeds
-// floor(u_j * total) — numpy's searchsorted(cumsum(d2), u * total, 'right').
-__global__ void __launch_bounds__(1024) init_select_kernel(const uint64_t* __restrict__ pts, int64_t m,
-                                                           const int* __restrict__ d2,
-                                                           const long long* __restrict__ chunk_sums, int nchunks,
-                                                           const double* __restrict__ uniforms, int j,
-                                                           uint64_t* cent_rows) {
-    __shared__ long long s_scan[1024];
-    __shared__ long long s_thresh;
+__global__ void __launch_bounds__(kInitThreads) init_kernel(InitArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ long long s_warp[33];
+    __shared__ long long s_T, s_before;
     __shared__ int s_chunk;
-    __shared__ long long s_before;
     __shared__ unsigned long long s_found;
+    __shared__ uint64_t s_c;
     const int tid = threadIdx.x;
-    // 1) inclusive scan of chunk sums (each thread owns a contiguous slice)
-    const int per = (nchunks + 1023) / 1024;
-    const int lo = min(nchunks, tid * per), hi = min(nchunks, lo + per);
-    long long mine = 0;
-    for (int i = lo; i < hi; ++i) mine += chunk_sums[i];
-    s_scan[tid] = mine;
-    if (tid == 0) {
-        s_chunk = -1;
-        s_found = ~0ull;
-    }
-    __syncthreads();
-    for (int off = 1; off < 1024; off <<= 1) {
-        long long v = tid >= off ? s_scan[tid - off] : 0;
-        __syncthreads();
-        s_scan[tid] += v;
-        __syncthreads();
-    }
-    if (tid == 1023) {
-        const long long total = s_scan[1023];
-        const double u = __dmul_rn(uniforms[j - 1], double(total));
-        s_thresh = (long long)floor(u);
-    }
-    __syncthreads();
-    const long long T = s_thresh;
-    // 2) the chunk where the running total first exceeds T
-    long long run = s_scan[tid] - mine;
-    for (int i = lo; i < hi; ++i) {
-        const long long next = run + chunk_sums[i];
-        if (run <= T && next > T) {
-            s_chunk = i;
-            s_before = run;
-        }
-        run = next;
-    }
-    __syncthreads();
-    const int ch = s_chunk;
-    if (ch >= 0) {
-        // 3) inside the chunk: 4 consecutive points per thread
-        const int64_t p0 = int64_t(ch) * kInitChunk + tid * 4;
-        long long v[4];
-        long long tsum = 0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            v[q] = (p0 + q < m) ? d2[p0 + q] : 0;
-            tsum += v[q];
-        }
-        __syncthreads();
-        s_scan[tid] = tsum;
-        __syncthreads();
-        for (int off = 1; off < 1024; off <<= 1) {
-            long long x = tid >= off ? s_scan[tid - off] : 0;
+    constexpr int per = kInitChunk / kInitThreads;  // 16
+    for (int j = a.j0; j < a.j1; ++j) {
+        // ---- centroid j (every block computes the same choice)
+        if (j == 0) {
+            if (tid == 0) s_c = a.pts[a.first_idx];
+        } else {
+            const long long* cs = a.sums[(j - 1) & 1];
+            const int* w = a.d2[(j - 1) & 1];
+            // total and chunk prefix: each thread owns a contiguous slice of chunk sums
+            const int cper = (a.nchunks + kInitThreads - 1) / kInitThreads;
+            const int lo = min(a.nchunks, tid * cper), hi = min(a.nchunks, lo + cper);
+            long long mine = 0;
+            for (int i = lo; i < hi; ++i) mine += __ldcg(cs + i);
+            long long excl;
+            const long long total = block_exclusive_scan(mine, excl, s_warp);
+            if (tid == 0) {
+                s_T = (long long)floor(__dmul_rn(a.uniforms[j - 1], double(total)));
+                s_chunk = -1;
+                s_found = ~0ull;
+            }
             __syncthreads();
-            s_scan[tid] += x;
+            const long long T = s_T;
+            long long run = excl;
+            for (int i = lo; i < hi; ++i) {
+                const long long next = run + __ldcg(cs + i);
+                if (run <= T && next > T) {
+                    s_chunk = i;
+                    s_before = run;
+                }
+                run = next;
+            }
             __syncthreads();
-        }
-        long long acc = s_before + s_scan[tid] - tsum;
+            const int ch = s_chunk;
+            if (ch >= 0) {
+                const int64_t p0 = int64_t(ch) * kInitChunk + tid * per;
+                long long v[per];
+                long long tsum = 0;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            acc += v[q];
-            if (acc > T && p0 + q < m) {
-                atomicMin(&s_found, (unsigned long long)(p0 + q));
-                break;
+                for (int q = 0; q < per; ++q) {
+                    v[q] = (p0 + q < a.m) ? __ldcg(w + p0 + q) : 0;
+                    tsum += v[q];
+                }
+                long long ex;
+                block_exclusive_scan(tsum, ex, s_warp);
+                long long acc = s_before + ex;
+#pragma unroll
+                for (int q = 0; q < per; ++q) {
+                    acc += v[q];
+                    if (acc > T && p0 + q < a.m) {
+                        atomicMin(&s_found, (unsigned long long)(p0 + q));
+                        break;
+                    }
+                }
+            }
+            __syncthreads();
+            if (tid == 0) {
+                int64_t idx = s_found == ~0ull ? a.m - 1 : int64_t(s_found);
+                if (idx > a.m - 1) idx = a.m - 1;
+                s_c = a.pts[idx];
             }
         }
-    }
-    __syncthreads();
-    if (tid == 0) {
-        int64_t idx = s_found == ~0ull ? m - 1 : int64_t(s_found);
-        if (idx > m - 1) idx = m - 1;
-        cent_rows[j] = pts[idx];
+        __syncthreads();
+        const uint64_t c = s_c;
+        if (blockIdx.x == 0 && tid == 0) a.cent_rows[j] = c;
+        // ---- weights for the next centroid
+        const int* wold = a.d2[(j - 1) & 1];
+        int* wnew = a.d2[j & 1];
+        long long* snew = a.sums[j & 1];
+        for (int ch = blockIdx.x; ch < a.nchunks; ch += gridDim.x) {
+            const int64_t base = int64_t(ch) * kInitChunk;
+            long long s = 0;
+#pragma unroll 4
+            for (int q = 0; q < per; ++q) {
+                const int64_t p = base + q * kInitThreads + tid;
+                if (p < a.m) {
+                    int v = int_sq_dist(a.pts[p], c, a.n);
+                    if (j > 0) v = min(v, __ldcg(wold + p));
+                    wnew[p] = v;
+                    s += v;
+                }
+            }
+            long long ex;
+            const long long tot = block_exclusive_scan(s, ex, s_warp);
+            if (tid == 0) snew[ch] = tot;
+        }
+        grid.sync();
     }
 }
 
 // ================================================================= Lloyd (K8)
+// One cooperative launch runs Lloyd iterations for up to 8 values of k at once
+// (speculative knee scan): every pass reads each point once and assigns it
+// under every active k.  Per point and k the kernel keeps Hamerly bounds —
+// u >= |p - c_a|, l <= min_{j != a} |p - c_j| — maintained with directed
+// rounding and widened by each centroid's drift; a point whose bounds prove
+// its assignment cannot change is skipped (no distance work).  Points that are
+// re-evaluated use fp32 distances with a proven error bound, and the
+// reference's float64 expression whenever the bound cannot separate the two
+// nearest centroids, so assignments equal numpy's argmin bit for bit.
+// Cluster sums are exact integers, updated by the deltas of points that
+// changed cluster; every block keeps an identical copy and derives the next
+// centroids itself, so an iteration needs one grid barrier.
 constexpr int kMaxRuns = 8;
 constexpr int kMaxClusters = 256;  // sum of k over the runs of one launch
 constexpr int kSumW = 9;           // 8 coordinate sums + count
-enum RunState : int { kActiveFromSums = 0, kActiveGiven = 1, kConverged = 2, kMaxed = 3, kNeedsReseed = 4 };
+enum RunState : int {
+    kActiveFromSums = 0,  // centroids = sums / counts of the previous pass (bounds valid)
+    kActiveGiven = 1,     // centroids given in LloydArgs::cent (after a reseed)
+    kConverged = 2,
+    kMaxed = 3,
+    kNeedsReseed = 4,
+    kActiveFromRows = 5  // first pass: centroids = the k-means++ rows
+};
+
+__host__ __device__ __forceinline__ bool run_active(int st) {
+    return st == kActiveFromSums || st == kActiveGiven || st == kActiveFromRows;
+}
 
 struct LloydArgs {
     const uint64_t* pts;
@@ -369,14 +420,45 @@ struct LloydArgs {
     int coff[kMaxRuns];
     int K;  // total clusters
     int it0, it_end, max_iters;
-    uint8_t* assign;         // [R][m], 255 = unassigned
-    double* cent;            // [K][8]
-    long long* S;            // [K][9]
-    unsigned long long* D;   // [3][K][9]
-    unsigned int* chg;       // [3][kMaxRuns]
-    int* run_state;          // [R]
-    int* run_iter;           // [R]
-    int* ctrl;               // [0] next iteration
+    uint8_t* assign;           // [R][m], 255 = unassigned
+    float2* bounds;            // [R][m] (u, l)
+    double* cent;              // [K][8] centroids of the latest pass
+    const uint64_t* init_rows; // k-means++ rows (prefix shared by all runs)
+    long long* S;              // [K][9] running sums
+    unsigned long long* D;     // [3][K][9] per-pass deltas
+    unsigned int* chg;         // [3][kMaxRuns]
+    int* run_state;            // [R]
+    int* run_iter;             // [R]
+    int* ctrl;                 // [0] next iteration
+};
+
+struct LloydLayout {
+    size_t S, c64, c32, delta, drift, total;
+};
+
+__host__ __device__ inline LloydLayout lloyd_layout(int K) {
+    LloydLayout L;
+    size_t o = 0;
+    L.c64 = o;
+    o += size_t(K) * kMaxKnobs * 8;
+    L.S = o;
+    o += size_t(K) * kSumW * 8;
+    L.c32 = o;
+    o += size_t(K) * kMaxKnobs * 4;
+    L.delta = o;
+    o += size_t(K) * kSumW * 4;
+    L.drift = o;
+    o += size_t(K) * 4;
+    L.total = (o + 15) & ~size_t(15);
+    return L;
+}
+
+struct RunShared {
+    int state[kMaxRuns];
+    int changed[kMaxRuns];
+    float m1[kMaxRuns], m2[kMaxRuns];  // largest / second largest drift
+    int amax[kMaxRuns];
+    int exit_flag, n_active;
 };
 
 // Conservative |fp32 - exact| bound for sum_i (p_i - c_i)^2 with p_i, |c_i| <= 255
@@ -384,17 +466,13 @@ struct LloydArgs {
 __device__ __forceinline__ float d2_bound(float d) {
     return 6.5e-5f * sqrtf(8.0f * d + 8.0f) + 5.5e-7f * d + 1e-6f;
 }
-
-struct LloydSmem {
-    long long S[kMaxClusters][kSumW];
-    double c64[kMaxClusters][kMaxKnobs];
-    float c32[kMaxClusters][kMaxKnobs];
-    int delta[kMaxClusters][kSumW];
-    int state[kMaxRuns];
-    int changed[kMaxRuns];
-    int exit_flag;
-    int n_active;
-};
+__device__ __forceinline__ float dist_up(float d2) { return __fsqrt_ru(__fadd_ru(d2, d2_bound(d2))); }
+__device__ __forceinline__ float dist_dn(float d2) {
+    const float lo = __fsub_rd(d2, d2_bound(d2));
+    return lo > 0.0f ? __fsqrt_rd(lo) : 0.0f;
+}
+// u < l with a margin far above float64 rounding of the reference's distances
+__device__ __forceinline__ bool surely_less(float u, float l) { return __fadd_ru(u, 1e-6f * (u + 1.0f)) < l; }
 
 __device__ __forceinline__ void unpack_row(uint64_t row, float p[kMaxKnobs]) {
     const uint32_t lo = uint32_t(row), hi = uint32_t(row >> 32);
@@ -408,22 +486,28 @@ __device__ __forceinline__ void unpack_row(uint64_t row, float p[kMaxKnobs]) {
     p[7] = float(hi >> 24);
 }
 
-__device__ __forceinline__ int assign_point(const LloydSmem& sm, uint64_t row, const float p[kMaxKnobs], int coff,
-                                            int k, int n) {
+__device__ __forceinline__ float f32_d2(const float p[kMaxKnobs], const float* c) {
+    const float4 c0 = *reinterpret_cast<const float4*>(c);
+    const float4 c1 = *reinterpret_cast<const float4*>(c + 4);
+    float t, d = 0.0f;
+    t = p[0] - c0.x; d = fmaf(t, t, d);
+    t = p[1] - c0.y; d = fmaf(t, t, d);
+    t = p[2] - c0.z; d = fmaf(t, t, d);
+    t = p[3] - c0.w; d = fmaf(t, t, d);
+    t = p[4] - c1.x; d = fmaf(t, t, d);
+    t = p[5] - c1.y; d = fmaf(t, t, d);
+    t = p[6] - c1.z; d = fmaf(t, t, d);
+    t = p[7] - c1.w; d = fmaf(t, t, d);
+    return d;
+}
+
+// Full assignment of one point under one k; returns the cluster and fresh bounds.
+__device__ __forceinline__ int full_assign(const float* c32, const double* c64, uint64_t row, const float p[kMaxKnobs],
+                                           int k, int n, float& u, float& l) {
     float best = INFINITY, second = INFINITY;
     int bj = 0;
     for (int j = 0; j < k; ++j) {
-        const float4 c0 = *reinterpret_cast<const float4*>(&sm.c32[coff + j][0]);
-        const float4 c1 = *reinterpret_cast<const float4*>(&sm.c32[coff + j][4]);
-        float t, d = 0.0f;
-        t = p[0] - c0.x; d = fmaf(t, t, d);
-        t = p[1] - c0.y; d = fmaf(t, t, d);
-        t = p[2] - c0.z; d = fmaf(t, t, d);
-        t = p[3] - c0.w; d = fmaf(t, t, d);
-        t = p[4] - c1.x; d = fmaf(t, t, d);
-        t = p[5] - c1.y; d = fmaf(t, t, d);
-        t = p[6] - c1.z; d = fmaf(t, t, d);
-        t = p[7] - c1.w; d = fmaf(t, t, d);
+        const float d = f32_d2(p, c32 + j * kMaxKnobs);
         if (d < best) {
             second = best;
             best = d;
@@ -436,68 +520,134 @@ __device__ __forceinline__ int assign_point(const LloydSmem& sm, uint64_t row, c
         // ambiguous: the reference's own float64 expression decides (ties -> lowest j)
         double bd = INFINITY;
         for (int j = 0; j < k; ++j) {
-            const double d = np_sq_dist(row, sm.c64[coff + j], n);
+            const double d = np_sq_dist(row, c64 + j * kMaxKnobs, n);
             if (d < bd) {
                 bd = d;
                 bj = j;
             }
         }
+        best = f32_d2(p, c32 + bj * kMaxKnobs);
+        second = INFINITY;
+        for (int j = 0; j < k; ++j)
+            if (j != bj) second = fminf(second, f32_d2(p, c32 + j * kMaxKnobs));
     }
+    u = dist_up(best);
+    l = k > 1 ? dist_dn(second) : INFINITY;
     return bj;
 }
 
-__global__ void __launch_bounds__(256) lloyd_kernel(LloydArgs a) {
+__global__ void __launch_bounds__(256, 4) lloyd_kernel(LloydArgs a) {
     extern __shared__ __align__(16) unsigned char s_raw[];
-    LloydSmem& sm = *reinterpret_cast<LloydSmem*>(s_raw);
+    __shared__ RunShared rs;
+    const LloydLayout L = lloyd_layout(a.K);
+    double* c64 = reinterpret_cast<double*>(s_raw + L.c64);
+    long long* S = reinterpret_cast<long long*>(s_raw + L.S);
+    float* c32 = reinterpret_cast<float*>(s_raw + L.c32);
+    int* delta = reinterpret_cast<int*>(s_raw + L.delta);
+    float* drift = reinterpret_cast<float*>(s_raw + L.drift);
     cg::grid_group grid = cg::this_grid();
     const int tid = threadIdx.x;
     const int K = a.K, R = a.R, n = a.n;
+    const int64_t m = a.m;
 
-    for (int i = tid; i < K * kSumW; i += blockDim.x) sm.S[i / kSumW][i % kSumW] = a.S[i];
-    if (tid < R) sm.state[tid] = a.run_state[tid];
-    __syncthreads();
+    for (int i = tid; i < K * kSumW; i += blockDim.x) S[i] = a.S[i];
+    for (int i = tid; i < K * kMaxKnobs; i += blockDim.x) c64[i] = a.cent[i];  // centroids of the previous pass
+    if (tid < R) rs.state[tid] = a.run_state[tid];
+    grid.sync();  // every block has read a.cent before block 0 overwrites it
 
     int it = a.it0;
     while (it < a.it_end) {
-        // ---- centroids used by this pass
+        // ---- this pass's centroids and each centroid's drift from the previous pass
         for (int r = 0; r < R; ++r) {
-            const int st = sm.state[r];
-            if (st != kActiveFromSums && st != kActiveGiven) continue;
-            for (int x = tid; x < a.k[r] * kMaxKnobs; x += blockDim.x) {
-                const int j = a.coff[r] + x / kMaxKnobs, i = x % kMaxKnobs;
-                double c;
-                if (i >= n) c = 0.0;
-                else if (st == kActiveFromSums) c = __ddiv_rn(double(sm.S[j][i]), double(sm.S[j][8]));
-                else c = a.cent[j * kMaxKnobs + i];
-                sm.c64[j][i] = c;
-                sm.c32[j][i] = float(c);
-                if (blockIdx.x == 0) a.cent[j * kMaxKnobs + i] = c;
+            const int st = rs.state[r];
+            if (!run_active(st)) continue;
+            for (int j = tid; j < a.k[r]; j += blockDim.x) {
+                const int g = a.coff[r] + j;
+                double moved = 0.0;
+                for (int i = 0; i < kMaxKnobs; ++i) {
+                    double c;
+                    if (i >= n) c = 0.0;
+                    else if (st == kActiveFromSums) c = __ddiv_rn(double(S[g * kSumW + i]), double(S[g * kSumW + 8]));
+                    else if (st == kActiveGiven) c = a.cent[g * kMaxKnobs + i];
+                    else c = double(row_byte(a.init_rows[j], i));
+                    const double dlt = c - c64[g * kMaxKnobs + i];
+                    moved += dlt * dlt;
+                    c64[g * kMaxKnobs + i] = c;
+                    c32[g * kMaxKnobs + i] = float(c);
+                    if (blockIdx.x == 0) a.cent[g * kMaxKnobs + i] = c;
+                }
+                drift[g] = __double2float_ru(sqrt(moved) * (1.0 + 1e-9) + 1e-30);
             }
         }
-        for (int i = tid; i < K * kSumW; i += blockDim.x) sm.delta[i / kSumW][i % kSumW] = 0;
-        if (tid < kMaxRuns) sm.changed[tid] = 0;
+        for (int i = tid; i < K * kSumW; i += blockDim.x) delta[i] = 0;
+        if (tid < kMaxRuns) rs.changed[tid] = 0;
+        __syncthreads();
+        if (tid < R && run_active(rs.state[tid])) {
+            float m1 = 0.0f, m2 = 0.0f;
+            int am = -1;
+            for (int j = 0; j < a.k[tid]; ++j) {
+                const float d = drift[a.coff[tid] + j];
+                if (d > m1) {
+                    m2 = m1;
+                    m1 = d;
+                    am = j;
+                } else if (d > m2) {
+                    m2 = d;
+                }
+            }
+            rs.m1[tid] = m1;
+            rs.m2[tid] = m2;
+            rs.amax[tid] = am;
+        }
         __syncthreads();
 
-        // ---- assignment pass (phase A)
+        // ---- assignment pass
         const int64_t gstride = int64_t(gridDim.x) * blockDim.x;
-        for (int64_t pidx = int64_t(blockIdx.x) * blockDim.x + tid; pidx < a.m; pidx += gstride) {
-            const uint64_t row = a.pts[pidx];
+        for (int64_t pidx = int64_t(blockIdx.x) * blockDim.x + tid; pidx < m; pidx += gstride) {
+            uint64_t row = 0;
+            bool have_row = false;
             float p[kMaxKnobs];
-            unpack_row(row, p);
             for (int r = 0; r < R; ++r) {
-                const int st = sm.state[r];
-                if (st != kActiveFromSums && st != kActiveGiven) continue;
-                const int j = assign_point(sm, row, p, a.coff[r], a.k[r], n);
-                uint8_t* as = a.assign + int64_t(r) * a.m + pidx;
-                const int old = *as;
-                if (old != j) {
-                    *as = uint8_t(j);
-                    sm.changed[r] = 1;
-                    int* dn = sm.delta[a.coff[r] + j];
+                const int st = rs.state[r];
+                if (!run_active(st)) continue;
+                const int64_t slot = int64_t(r) * m + pidx;
+                const int old = a.assign[slot];
+                const int co = a.coff[r];
+                float u, l;
+                int j = -1;
+                if (st == kActiveFromSums && old != 255) {
+                    const float2 b = a.bounds[slot];
+                    u = __fadd_ru(b.x, drift[co + old]);
+                    l = __fsub_rd(b.y, old == rs.amax[r] ? rs.m2[r] : rs.m1[r]);
+                    if (surely_less(u, l)) {
+                        j = old;
+                    } else {
+                        if (!have_row) {
+                            row = a.pts[pidx];
+                            unpack_row(row, p);
+                            have_row = true;
+                        }
+                        u = dist_up(f32_d2(p, c32 + (co + old) * kMaxKnobs));
+                        if (surely_less(u, l)) j = old;
+                    }
+                }
+                if (j < 0) {
+                    if (!have_row) {
+                        row = a.pts[pidx];
+                        unpack_row(row, p);
+                        have_row = true;
+                    }
+                    j = full_assign(c32 + co * kMaxKnobs, c64 + co * kMaxKnobs, row, p, a.k[r], n, u, l);
+                }
+                a.bounds[slot] = make_float2(u, l);
+                if (j != old) {
+                    a.assign[slot] = uint8_t(j);
+                    rs.changed[r] = 1;
+                    int* dn = delta + (co + j) * kSumW;
                     for (int i = 0; i < n; ++i) atomicAdd(dn + i, row_byte(row, i));
                     atomicAdd(dn + 8, 1);
                     if (old != 255) {
-                        int* dold = sm.delta[a.coff[r] + old];
+                        int* dold = delta + (co + old) * kSumW;
                         for (int i = 0; i < n; ++i) atomicSub(dold + i, row_byte(row, i));
                         atomicSub(dold + 8, 1);
                     }
@@ -508,10 +658,10 @@ __global__ void __launch_bounds__(256) lloyd_kernel(LloydArgs a) {
         const int buf = it % 3;
         unsigned long long* Dcur = a.D + size_t(buf) * K * kSumW;
         for (int i = tid; i < K * kSumW; i += blockDim.x) {
-            const int v = sm.delta[i / kSumW][i % kSumW];
+            const int v = delta[i];
             if (v) atomicAdd(Dcur + i, (unsigned long long)(long long)v);
         }
-        if (tid < R && sm.changed[tid]) atomicOr(a.chg + buf * kMaxRuns + tid, 1u);
+        if (tid < R && rs.changed[tid]) atomicOr(a.chg + buf * kMaxRuns + tid, 1u);
         if (blockIdx.x == 0) {
             const int nb = (it + 1) % 3;
             for (int i = tid; i < K * kSumW; i += blockDim.x) a.D[size_t(nb) * K * kSumW + i] = 0ull;
@@ -522,15 +672,15 @@ __global__ void __launch_bounds__(256) lloyd_kernel(LloydArgs a) {
         // ---- decisions (identical in every block)
         for (int i = tid; i < K * kSumW; i += blockDim.x) {
             const long long v = (long long)__ldcg(Dcur + i);
-            if (v) sm.S[i / kSumW][i % kSumW] += v;
+            if (v) S[i] += v;
         }
         __syncthreads();
         if (tid == 0) {
-            sm.exit_flag = 0;
-            sm.n_active = 0;
+            rs.exit_flag = 0;
+            rs.n_active = 0;
             for (int r = 0; r < R; ++r) {
-                int st = sm.state[r];
-                if (st != kActiveFromSums && st != kActiveGiven) continue;
+                int st = rs.state[r];
+                if (!run_active(st)) continue;
                 const unsigned changed = __ldcg(a.chg + buf * kMaxRuns + r);
                 if (!changed) {
                     st = kConverged;
@@ -538,26 +688,26 @@ __global__ void __launch_bounds__(256) lloyd_kernel(LloydArgs a) {
                     st = kMaxed;
                 } else {
                     bool empty = false;
-                    for (int j = 0; j < a.k[r]; ++j) empty |= sm.S[a.coff[r] + j][8] == 0;
+                    for (int j = 0; j < a.k[r]; ++j) empty |= S[(a.coff[r] + j) * kSumW + 8] == 0;
                     if (empty) {
                         st = kNeedsReseed;
-                        sm.exit_flag = 1;
+                        rs.exit_flag = 1;
                     } else {
                         st = kActiveFromSums;
-                        ++sm.n_active;
+                        ++rs.n_active;
                     }
                 }
                 if (st != kActiveFromSums && blockIdx.x == 0) a.run_iter[r] = it;
-                sm.state[r] = st;
+                rs.state[r] = st;
             }
         }
         __syncthreads();
         ++it;
-        if (sm.exit_flag || sm.n_active == 0) break;
+        if (rs.exit_flag || rs.n_active == 0) break;
     }
     if (blockIdx.x == 0) {
-        for (int i = tid; i < K * kSumW; i += blockDim.x) a.S[i] = sm.S[i / kSumW][i % kSumW];
-        if (tid < R) a.run_state[tid] = sm.state[tid];
+        for (int i = tid; i < K * kSumW; i += blockDim.x) a.S[i] = S[i];
+        if (tid < R) a.run_state[tid] = rs.state[tid];
         if (tid == 0) a.ctrl[0] = it;
     }
 }
@@ -609,12 +759,6 @@ __global__ void __launch_bounds__(256) argmax_kernel(const double* __restrict__ 
     }
 }
 
-__global__ void rows_to_centroids_kernel(const uint64_t* rows, int count, int n, double* cent) {
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    if (x >= count * kMaxKnobs) return;
-    const int j = x / kMaxKnobs, i = x % kMaxKnobs;
-    cent[x] = i < n ? double(row_byte(rows[j], i)) : 0.0;
-}
 
 // ============================================================ orchestration
 struct KmeansSession {
@@ -642,9 +786,9 @@ struct KmeansSession {
         uniforms.resize(64);
         for (auto& u : uniforms) u = g.random();
         cent_rows = static_cast<uint64_t*>(e->scratch("km.cent_rows", 64 * 8));
-        d2 = static_cast<int*>(e->scratch("km.d2", size_t(m) * 4));
+        d2 = static_cast<int*>(e->scratch("km.d2", size_t(m) * 8));  // two buffers
         nchunks = int(ceil_div(m, kInitChunk));
-        chunk_sums = static_cast<long long*>(e->scratch("km.chunk_sums", size_t(nchunks) * 8));
+        chunk_sums = static_cast<long long*>(e->scratch("km.chunk_sums", size_t(nchunks) * 16));
         d_uniforms = static_cast<double*>(e->scratch("km.uniforms", 64 * 8));
         auto* h = static_cast<double*>(e->staging("km.uniforms", 64 * 8));
         std::copy(uniforms.begin(), uniforms.end(), h);
@@ -652,21 +796,29 @@ struct KmeansSession {
     }
 
     void ensure_init(int k) {
-        if (nchunks > 1024 * 16) fail(KT_ERR_UNSUPPORTED, "k-means++ init supports < 64M points");
-        while (chosen < k) {
-            const int j = chosen;
-            if (j > 0) {
-                e->pre_launch("init_select");
-                init_select_kernel<<<1, 1024, 0, e->stream>>>(pts, m, d2, chunk_sums, nchunks, d_uniforms, j, cent_rows);
-                e->check_launch("init_select");
-            }
-            if (j + 1 < 64) {  // d2 update needed only if another centroid follows
-                e->pre_launch("init_update");
-                init_update_kernel<<<nchunks, 256, 0, e->stream>>>(pts, m, n, cent_rows, j, first_idx, d2, chunk_sums);
-                e->check_launch("init_update");
-            }
-            ++chosen;
-        }
+        k = std::min<int64_t>(std::max(k, 1), 63);
+        if (chosen >= k) return;
+        InitArgs ia{};
+        ia.pts = pts;
+        ia.m = m;
+        ia.n = n;
+        ia.j0 = chosen;
+        ia.j1 = k;
+        ia.first_idx = first_idx;
+        ia.uniforms = d_uniforms;
+        ia.cent_rows = cent_rows;
+        ia.d2[0] = d2;
+        ia.d2[1] = d2 + m;
+        ia.sums[0] = chunk_sums;
+        ia.sums[1] = chunk_sums + nchunks;
+        ia.nchunks = nchunks;
+        const int occ = std::max(1, occupancy_blocks((const void*)init_kernel, kInitThreads, 0));
+        const int grid = int(std::max<int64_t>(1, std::min<int64_t>(int64_t(occ) * e->num_sms, nchunks)));
+        void* params[] = {&ia};
+        e->pre_launch("kmeanspp_init");
+        KT_CUDA(cudaLaunchCooperativeKernel((const void*)init_kernel, grid, kInitThreads, params, 0, e->stream));
+        e->check_launch("kmeanspp_init");
+        chosen = k;
     }
 
     struct RunResult {
@@ -703,19 +855,16 @@ struct KmeansSession {
         a.run_iter = static_cast<int*>(e->scratch("km.iter", kMaxRuns * 4));
         a.ctrl = static_cast<int*>(e->scratch("km.ctrl", 16));
         double* d_loss = static_cast<double*>(e->scratch("km.loss", kMaxRuns * 8));
+        a.bounds = static_cast<float2*>(e->scratch("km.bounds", size_t(R) * m * sizeof(float2)));
+        a.init_rows = cent_rows;
         KT_CUDA(cudaMemsetAsync(a.assign, 0xff, size_t(R) * m, e->stream));
         KT_CUDA(cudaMemsetAsync(a.S, 0, size_t(K) * kSumW * 8, e->stream));
-        for (int r = 0; r < R; ++r) {
-            e->pre_launch("rows_to_centroids");
-            rows_to_centroids_kernel<<<int(ceil_div(ks[r] * kMaxKnobs, 256)), 256, 0, e->stream>>>(
-                cent_rows, ks[r], n, a.cent + size_t(a.coff[r]) * kMaxKnobs);
-            e->check_launch("rows_to_centroids");
-        }
+        KT_CUDA(cudaMemsetAsync(a.cent, 0, size_t(K) * kMaxKnobs * 8, e->stream));
         auto* h_state = static_cast<int*>(e->staging("km.state", 64));
-        for (int r = 0; r < R; ++r) h_state[r] = kActiveGiven;
+        for (int r = 0; r < R; ++r) h_state[r] = kActiveFromRows;
         KT_CUDA(cudaMemcpyAsync(a.run_state, h_state, R * 4, cudaMemcpyHostToDevice, e->stream));
 
-        const size_t smem = sizeof(LloydSmem);
+        const size_t smem = lloyd_layout(K).total;
         KT_CUDA(cudaFuncSetAttribute(lloyd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         const int occ = std::max(1, occupancy_blocks((const void*)lloyd_kernel, 256, smem));
         const int grid = int(std::max<int64_t>(1, std::min<int64_t>(int64_t(occ) * e->num_sms, ceil_div(m, 256))));
@@ -746,7 +895,7 @@ struct KmeansSession {
             bool reseed = false, active = false;
             for (int r = 0; r < R; ++r) {
                 reseed |= h_state[r] == kNeedsReseed;
-                active |= h_state[r] == kActiveFromSums || h_state[r] == kActiveGiven;
+                active |= run_active(h_state[r]);
             }
             if (reseed) {
                 KT_CUDA(cudaMemcpyAsync(h_S, a.S, size_t(K) * kSumW * 8, cudaMemcpyDeviceToHost, e->stream));
