@@ -439,12 +439,12 @@ struct LloydLayout {
 __host__ __device__ inline LloydLayout lloyd_layout(int K) {
     LloydLayout L;
     size_t o = 0;
-    L.c64 = o;
+    L.c64 = o;  // 64 B per cluster: keeps c32 16-byte aligned for float4 loads
     o += size_t(K) * kMaxKnobs * 8;
-    L.S = o;
-    o += size_t(K) * kSumW * 8;
     L.c32 = o;
     o += size_t(K) * kMaxKnobs * 4;
+    L.S = o;
+    o += size_t(K) * kSumW * 8;
     L.delta = o;
     o += size_t(K) * kSumW * 4;
     L.drift = o;
