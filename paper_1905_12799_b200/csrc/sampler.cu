@@ -537,8 +537,11 @@ __device__ __forceinline__ int full_assign(const float* c32, const double* c64, 
 }
 
 __global__ void __launch_bounds__(256, 4) lloyd_kernel(LloydArgs a) {
-    extern __shared__ __align__(16) unsigned char s_raw[];
+    extern __shared__ __align__(16) unsigned char s_dyn[];
     __shared__ RunShared rs;
+    // the dynamic window is only guaranteed 8-byte aligned after static smem (tools add their
+    // own static smem): align explicitly for the float4 centroid loads (16 spare bytes allocated)
+    unsigned char* s_raw = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(s_dyn) + 15) & ~uintptr_t(15));
     const LloydLayout L = lloyd_layout(a.K);
     double* c64 = reinterpret_cast<double*>(s_raw + L.c64);
     long long* S = reinterpret_cast<long long*>(s_raw + L.S);
@@ -864,7 +867,7 @@ struct KmeansSession {
         for (int r = 0; r < R; ++r) h_state[r] = kActiveFromRows;
         KT_CUDA(cudaMemcpyAsync(a.run_state, h_state, R * 4, cudaMemcpyHostToDevice, e->stream));
 
-        const size_t smem = lloyd_layout(K).total;
+        const size_t smem = lloyd_layout(K).total + 16;
         KT_CUDA(cudaFuncSetAttribute(lloyd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         const int occ = std::max(1, occupancy_blocks((const void*)lloyd_kernel, 256, smem));
         const int grid = int(std::max<int64_t>(1, std::min<int64_t>(int64_t(occ) * e->num_sms, ceil_div(m, 256))));
