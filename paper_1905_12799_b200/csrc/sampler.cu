@@ -20,6 +20,8 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <cmath>
 #include <map>
@@ -430,6 +432,7 @@ struct LloydArgs {
     int* run_state;            // [R]
     int* run_iter;             // [R]
     int* ctrl;                 // [0] next iteration
+    unsigned long long* stats; // optional [R][3]: bound-skips, tightened skips, full evaluations
 };
 
 struct LloydLayout {
@@ -454,6 +457,7 @@ __host__ __device__ inline LloydLayout lloyd_layout(int K) {
 }
 
 struct RunShared {
+    unsigned int cnt[kMaxRuns][3];
     int state[kMaxRuns];
     int changed[kMaxRuns];
     float m1[kMaxRuns], m2[kMaxRuns];  // largest / second largest drift
@@ -556,6 +560,7 @@ __global__ void __launch_bounds__(256, 4) lloyd_kernel(LloydArgs a) {
     for (int i = tid; i < K * kSumW; i += blockDim.x) S[i] = a.S[i];
     for (int i = tid; i < K * kMaxKnobs; i += blockDim.x) c64[i] = a.cent[i];  // centroids of the previous pass
     if (tid < R) rs.state[tid] = a.run_state[tid];
+    if (tid < kMaxRuns * 3) rs.cnt[tid / 3][tid % 3] = 0;
     grid.sync();  // every block has read a.cent before block 0 overwrites it
 
     int it = a.it0;
@@ -624,6 +629,7 @@ __global__ void __launch_bounds__(256, 4) lloyd_kernel(LloydArgs a) {
                     l = __fsub_rd(b.y, old == rs.amax[r] ? rs.m2[r] : rs.m1[r]);
                     if (surely_less(u, l)) {
                         j = old;
+                        if (a.stats) atomicAdd(&rs.cnt[r][0], 1u);
                     } else {
                         if (!have_row) {
                             row = a.pts[pidx];
@@ -631,7 +637,10 @@ __global__ void __launch_bounds__(256, 4) lloyd_kernel(LloydArgs a) {
                             have_row = true;
                         }
                         u = dist_up(f32_d2(p, c32 + (co + old) * kMaxKnobs));
-                        if (surely_less(u, l)) j = old;
+                        if (surely_less(u, l)) {
+                            j = old;
+                            if (a.stats) atomicAdd(&rs.cnt[r][1], 1u);
+                        }
                     }
                 }
                 if (j < 0) {
@@ -641,6 +650,7 @@ __global__ void __launch_bounds__(256, 4) lloyd_kernel(LloydArgs a) {
                         have_row = true;
                     }
                     j = full_assign(c32 + co * kMaxKnobs, c64 + co * kMaxKnobs, row, p, a.k[r], n, u, l);
+                    if (a.stats) atomicAdd(&rs.cnt[r][2], 1u);
                 }
                 a.bounds[slot] = make_float2(u, l);
                 if (j != old) {
@@ -708,6 +718,7 @@ __global__ void __launch_bounds__(256, 4) lloyd_kernel(LloydArgs a) {
         ++it;
         if (rs.exit_flag || rs.n_active == 0) break;
     }
+    if (a.stats && tid < R * 3) atomicAdd(a.stats + tid, (unsigned long long)rs.cnt[tid / 3][tid % 3]);
     if (blockIdx.x == 0) {
         for (int i = tid; i < K * kSumW; i += blockDim.x) a.S[i] = S[i];
         if (tid < R) a.run_state[tid] = rs.state[tid];
@@ -857,6 +868,12 @@ struct KmeansSession {
         a.run_state = static_cast<int*>(e->scratch("km.state", kMaxRuns * 4));
         a.run_iter = static_cast<int*>(e->scratch("km.iter", kMaxRuns * 4));
         a.ctrl = static_cast<int*>(e->scratch("km.ctrl", 16));
+        static const bool want_stats = std::getenv("KT_LLOYD_STATS") != nullptr;
+        a.stats = nullptr;
+        if (want_stats) {
+            a.stats = static_cast<unsigned long long*>(e->scratch("km.stats", kMaxRuns * 3 * 8));
+            KT_CUDA(cudaMemsetAsync(a.stats, 0, kMaxRuns * 3 * 8, e->stream));
+        }
         double* d_loss = static_cast<double*>(e->scratch("km.loss", kMaxRuns * 8));
         a.bounds = static_cast<float2*>(e->scratch("km.bounds", size_t(R) * m * sizeof(float2)));
         a.init_rows = cent_rows;
@@ -918,6 +935,13 @@ struct KmeansSession {
         KT_CUDA(cudaMemcpyAsync(h_loss, d_loss, R * 8, cudaMemcpyDeviceToHost, e->stream));
         KT_CUDA(cudaMemcpyAsync(h_iter, a.run_iter, R * 4, cudaMemcpyDeviceToHost, e->stream));
         e->sync();
+        if (a.stats) {
+            unsigned long long hs[kMaxRuns * 3];
+            KT_CUDA(cudaMemcpy(hs, a.stats, R * 3 * 8, cudaMemcpyDeviceToHost));
+            for (int r = 0; r < R; ++r)
+                std::fprintf(stderr, "[lloyd] k=%d passes=%d skip=%llu tightened=%llu full=%llu\n", ks[r], h_iter[r] + 1,
+                             hs[r * 3], hs[r * 3 + 1], hs[r * 3 + 2]);
+        }
         int max_passes = 0;
         for (int r = 0; r < R; ++r) {
             out[r] = {ks[r], h_iter[r] + 1, h_loss[r]};
