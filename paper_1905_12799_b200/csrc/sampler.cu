@@ -422,8 +422,9 @@ struct LloydArgs {
     int coff[kMaxRuns];
     int K;  // total clusters
     int it0, it_end, max_iters;
-    uint8_t* assign;           // [R][m], 255 = unassigned
-    float2* bounds;            // [R][m] (u, l)
+    int64_t stride;            // per-run row stride of assign/bounds (m rounded up to 16)
+    uint8_t* assign;           // [R][stride], 255 = unassigned
+    float2* bounds;            // [R][stride] (u, l)
     double* cent;              // [K][8] centroids of the latest pass
     const uint64_t* init_rows; // k-means++ rows (prefix shared by all runs)
     long long* S;              // [K][9] running sums
@@ -433,6 +434,7 @@ struct LloydArgs {
     int* run_iter;             // [R]
     int* ctrl;                 // [0] next iteration
     unsigned long long* stats; // optional [R][3]: bound-skips, tightened skips, full evaluations
+    long long* timeline;       // optional [100][4] globaltimer stamps of block 0 per pass
 };
 
 struct LloydLayout {
@@ -455,6 +457,13 @@ __host__ __device__ inline LloydLayout lloyd_layout(int K) {
     L.total = (o + 15) & ~size_t(15);
     return L;
 }
+
+struct LloydQueueEntry {
+    uint32_t point;
+    int32_t old;
+    float u, l;
+};
+constexpr int kLloydThreads = 256;
 
 struct RunShared {
     unsigned int cnt[kMaxRuns][3];
@@ -540,9 +549,11 @@ __device__ __forceinline__ int full_assign(const float* c32, const double* c64, 
     return bj;
 }
 
-__global__ void __launch_bounds__(256, 4) lloyd_kernel(LloydArgs a) {
+__global__ void __launch_bounds__(256, 3) lloyd_kernel(LloydArgs a) {
     extern __shared__ __align__(16) unsigned char s_dyn[];
     __shared__ RunShared rs;
+    __shared__ uint8_t run_of[kMaxClusters];
+    __shared__ LloydQueueEntry wqueue[kLloydThreads / 32 * 128];
     // the dynamic window is only guaranteed 8-byte aligned after static smem (tools add their
     // own static smem): align explicitly for the float4 centroid loads (16 spare bytes allocated)
     unsigned char* s_raw = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(s_dyn) + 15) & ~uintptr_t(15));
@@ -561,31 +572,45 @@ __global__ void __launch_bounds__(256, 4) lloyd_kernel(LloydArgs a) {
     for (int i = tid; i < K * kMaxKnobs; i += blockDim.x) c64[i] = a.cent[i];  // centroids of the previous pass
     if (tid < R) rs.state[tid] = a.run_state[tid];
     if (tid < kMaxRuns * 3) rs.cnt[tid / 3][tid % 3] = 0;
+    for (int r = 0; r < R; ++r)
+        for (int j = tid; j < a.k[r]; j += blockDim.x) run_of[a.coff[r] + j] = uint8_t(r);
     grid.sync();  // every block has read a.cent before block 0 overwrites it
 
     int it = a.it0;
+    auto stamp = [&](int phase) {
+        if (a.timeline && blockIdx.x == 0 && tid == 0 && it < 100) {
+            long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            a.timeline[it * 4 + phase] = t;
+        }
+    };
     while (it < a.it_end) {
-        // ---- this pass's centroids and each centroid's drift from the previous pass
-        for (int r = 0; r < R; ++r) {
+        stamp(0);
+        // ---- this pass's centroids and each centroid's drift from the previous pass:
+        // one thread per (cluster, coordinate); 8 consecutive lanes reduce a drift
+        for (int x0 = 0; x0 < K * kMaxKnobs; x0 += blockDim.x) {
+            const int x = x0 + tid;
+            const int g = x >> 3, i = x & 7;
+            const int r = x < K * kMaxKnobs ? run_of[g] : 0;
             const int st = rs.state[r];
-            if (!run_active(st)) continue;
-            for (int j = tid; j < a.k[r]; j += blockDim.x) {
-                const int g = a.coff[r] + j;
-                double moved = 0.0;
-                for (int i = 0; i < kMaxKnobs; ++i) {
-                    double c;
-                    if (i >= n) c = 0.0;
-                    else if (st == kActiveFromSums) c = __ddiv_rn(double(S[g * kSumW + i]), double(S[g * kSumW + 8]));
-                    else if (st == kActiveGiven) c = a.cent[g * kMaxKnobs + i];
-                    else c = double(row_byte(a.init_rows[j], i));
-                    const double dlt = c - c64[g * kMaxKnobs + i];
-                    moved += dlt * dlt;
-                    c64[g * kMaxKnobs + i] = c;
-                    c32[g * kMaxKnobs + i] = float(c);
-                    if (blockIdx.x == 0) a.cent[g * kMaxKnobs + i] = c;
-                }
-                drift[g] = __double2float_ru(sqrt(moved) * (1.0 + 1e-9) + 1e-30);
+            const bool live = x < K * kMaxKnobs && run_active(st);
+            double dlt2 = 0.0;
+            if (live) {
+                double c;
+                if (i >= n) c = 0.0;
+                else if (st == kActiveFromSums) c = __ddiv_rn(double(S[g * kSumW + i]), double(S[g * kSumW + 8]));
+                else if (st == kActiveGiven) c = a.cent[g * kMaxKnobs + i];
+                else c = double(row_byte(a.init_rows[g - a.coff[r]], i));
+                const double dlt = c - c64[g * kMaxKnobs + i];
+                dlt2 = dlt * dlt;
+                c64[g * kMaxKnobs + i] = c;
+                c32[g * kMaxKnobs + i] = float(c);
+                if (blockIdx.x == 0) a.cent[g * kMaxKnobs + i] = c;
             }
+            dlt2 += __shfl_xor_sync(0xffffffffu, dlt2, 1);
+            dlt2 += __shfl_xor_sync(0xffffffffu, dlt2, 2);
+            dlt2 += __shfl_xor_sync(0xffffffffu, dlt2, 4);
+            if (live && i == 0) drift[g] = __double2float_ru(sqrt(dlt2) * (1.0 + 1e-9) + 1e-30);
         }
         for (int i = tid; i < K * kSumW; i += blockDim.x) delta[i] = 0;
         if (tid < kMaxRuns) rs.changed[tid] = 0;
@@ -609,62 +634,105 @@ __global__ void __launch_bounds__(256, 4) lloyd_kernel(LloydArgs a) {
         }
         __syncthreads();
 
-        // ---- assignment pass
+        stamp(1);
+        // ---- assignment pass.  Per warp and round: each lane filters 4 consecutive
+        // points with its Hamerly bounds; the points the bounds cannot settle are
+        // queued in shared memory and then evaluated by all 32 lanes together.
+        const int64_t nq = (m + 3) >> 2;
         const int64_t gstride = int64_t(gridDim.x) * blockDim.x;
-        for (int64_t pidx = int64_t(blockIdx.x) * blockDim.x + tid; pidx < m; pidx += gstride) {
-            uint64_t row = 0;
-            bool have_row = false;
-            float p[kMaxKnobs];
+        const int64_t q_end = (nq + gstride - 1) / gstride * gstride;  // warp-uniform trip count
+        const int lane = tid & 31;
+        LloydQueueEntry* queue = wqueue + (tid >> 5) * 128;
+        for (int64_t q = int64_t(blockIdx.x) * blockDim.x + tid; q < q_end; q += gstride) {
+            const int64_t p0 = q << 2;
+            const int cnt = q < nq ? int(m - p0 < 4 ? m - p0 : 4) : 0;
             for (int r = 0; r < R; ++r) {
                 const int st = rs.state[r];
                 if (!run_active(st)) continue;
-                const int64_t slot = int64_t(r) * m + pidx;
-                const int old = a.assign[slot];
                 const int co = a.coff[r];
-                float u, l;
-                int j = -1;
-                if (st == kActiveFromSums && old != 255) {
-                    const float2 b = a.bounds[slot];
-                    u = __fadd_ru(b.x, drift[co + old]);
-                    l = __fsub_rd(b.y, old == rs.amax[r] ? rs.m2[r] : rs.m1[r]);
-                    if (surely_less(u, l)) {
-                        j = old;
-                        if (a.stats) atomicAdd(&rs.cnt[r][0], 1u);
+                uint8_t* as_r = a.assign + int64_t(r) * a.stride;
+                float2* bd_r = a.bounds + int64_t(r) * a.stride;
+                unsigned todo = 0;  // bit e: point e needs distance work
+                uint32_t as4 = 0xffffffffu;
+                float bu[4] = {0.f, 0.f, 0.f, 0.f}, bl[4] = {0.f, 0.f, 0.f, 0.f};
+                if (cnt > 0) {
+                    as4 = *reinterpret_cast<const uint32_t*>(as_r + p0);
+                    if (st == kActiveFromSums) {
+                        const float4 b01 = reinterpret_cast<const float4*>(bd_r)[q * 2];
+                        const float4 b23 = reinterpret_cast<const float4*>(bd_r)[q * 2 + 1];
+                        bu[0] = b01.x, bl[0] = b01.y, bu[1] = b01.z, bl[1] = b01.w;
+                        bu[2] = b23.x, bl[2] = b23.y, bu[3] = b23.z, bl[3] = b23.w;
+                        const float m1 = rs.m1[r], m2 = rs.m2[r];
+                        const int am = rs.amax[r];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int old = (as4 >> (8 * e)) & 0xff;
+                            if (e >= cnt) continue;
+                            if (old == 255) {
+                                todo |= 1u << e;
+                                continue;
+                            }
+                            bu[e] = __fadd_ru(bu[e], drift[co + old]);
+                            bl[e] = __fsub_rd(bl[e], old == am ? m2 : m1);
+                            if (!surely_less(bu[e], bl[e])) todo |= 1u << e;
+                        }
+                        // settled points keep their widened bounds (queued ones are rewritten below)
+                        reinterpret_cast<float4*>(bd_r)[q * 2] = make_float4(bu[0], bl[0], bu[1], bl[1]);
+                        reinterpret_cast<float4*>(bd_r)[q * 2 + 1] = make_float4(bu[2], bl[2], bu[3], bl[3]);
                     } else {
-                        if (!have_row) {
-                            row = a.pts[pidx];
-                            unpack_row(row, p);
-                            have_row = true;
-                        }
+                        todo = (1u << cnt) - 1u;
+                    }
+                }
+                // warp-level compaction of the unsettled points
+                int base = 0;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const bool mine = (todo >> e) & 1u;
+                    const unsigned bal = __ballot_sync(0xffffffffu, mine);
+                    if (mine) {
+                        LloydQueueEntry& qe = queue[base + __popc(bal & ((1u << lane) - 1u))];
+                        qe.point = uint32_t(p0 + e);
+                        qe.old = (as4 >> (8 * e)) & 0xff;
+                        qe.u = bu[e];
+                        qe.l = bl[e];
+                    }
+                    base += __popc(bal);
+                }
+                __syncwarp();
+                const bool bounded = st == kActiveFromSums;
+                for (int i = lane; i < base; i += 32) {
+                    const LloydQueueEntry qe = queue[i];
+                    const uint64_t row = __ldg(a.pts + qe.point);
+                    float p[kMaxKnobs];
+                    unpack_row(row, p);
+                    const int old = qe.old;
+                    float u = qe.u, l = qe.l;
+                    int j = -1;
+                    if (bounded && old != 255) {
                         u = dist_up(f32_d2(p, c32 + (co + old) * kMaxKnobs));
-                        if (surely_less(u, l)) {
-                            j = old;
-                            if (a.stats) atomicAdd(&rs.cnt[r][1], 1u);
+                        if (surely_less(u, l)) j = old;
+                    }
+                    if (a.stats) atomicAdd(&rs.cnt[r][j < 0 ? 2 : 1], 1u);
+                    if (j < 0) j = full_assign(c32 + co * kMaxKnobs, c64 + co * kMaxKnobs, row, p, a.k[r], n, u, l);
+                    bd_r[qe.point] = make_float2(u, l);
+                    if (j != old) {
+                        as_r[qe.point] = uint8_t(j);
+                        rs.changed[r] = 1;
+                        int* dn = delta + (co + j) * kSumW;
+                        for (int c = 0; c < n; ++c) atomicAdd(dn + c, row_byte(row, c));
+                        atomicAdd(dn + 8, 1);
+                        if (old != 255) {
+                            int* dold = delta + (co + old) * kSumW;
+                            for (int c = 0; c < n; ++c) atomicSub(dold + c, row_byte(row, c));
+                            atomicSub(dold + 8, 1);
                         }
                     }
                 }
-                if (j < 0) {
-                    if (!have_row) {
-                        row = a.pts[pidx];
-                        unpack_row(row, p);
-                        have_row = true;
-                    }
-                    j = full_assign(c32 + co * kMaxKnobs, c64 + co * kMaxKnobs, row, p, a.k[r], n, u, l);
-                    if (a.stats) atomicAdd(&rs.cnt[r][2], 1u);
+                if (a.stats) {
+                    const unsigned valid = __reduce_add_sync(0xffffffffu, unsigned(cnt));
+                    if (lane == 0) atomicAdd(&rs.cnt[r][0], valid - unsigned(base));
                 }
-                a.bounds[slot] = make_float2(u, l);
-                if (j != old) {
-                    a.assign[slot] = uint8_t(j);
-                    rs.changed[r] = 1;
-                    int* dn = delta + (co + j) * kSumW;
-                    for (int i = 0; i < n; ++i) atomicAdd(dn + i, row_byte(row, i));
-                    atomicAdd(dn + 8, 1);
-                    if (old != 255) {
-                        int* dold = delta + (co + old) * kSumW;
-                        for (int i = 0; i < n; ++i) atomicSub(dold + i, row_byte(row, i));
-                        atomicSub(dold + 8, 1);
-                    }
-                }
+                __syncwarp();
             }
         }
         __syncthreads();
@@ -680,7 +748,9 @@ __global__ void __launch_bounds__(256, 4) lloyd_kernel(LloydArgs a) {
             for (int i = tid; i < K * kSumW; i += blockDim.x) a.D[size_t(nb) * K * kSumW + i] = 0ull;
             if (tid < kMaxRuns) a.chg[nb * kMaxRuns + tid] = 0u;
         }
+        stamp(2);
         grid.sync();
+        stamp(3);
 
         // ---- decisions (identical in every block)
         for (int i = tid; i < K * kSumW; i += blockDim.x) {
@@ -860,7 +930,8 @@ struct KmeansSession {
         a.K = K;
         a.max_iters = 100;
         ensure_init(ks.back());
-        a.assign = static_cast<uint8_t*>(e->scratch("km.assign", size_t(R) * m));
+        a.stride = (m + 15) & ~int64_t(15);
+        a.assign = static_cast<uint8_t*>(e->scratch("km.assign", size_t(R) * a.stride));
         a.cent = static_cast<double*>(e->scratch("km.cent", size_t(K) * kMaxKnobs * 8));
         a.S = static_cast<long long*>(e->scratch("km.S", size_t(K) * kSumW * 8));
         a.D = static_cast<unsigned long long*>(e->scratch("km.D", size_t(3) * K * kSumW * 8));
@@ -874,10 +945,12 @@ struct KmeansSession {
             a.stats = static_cast<unsigned long long*>(e->scratch("km.stats", kMaxRuns * 3 * 8));
             KT_CUDA(cudaMemsetAsync(a.stats, 0, kMaxRuns * 3 * 8, e->stream));
         }
+        static const bool want_timeline = std::getenv("KT_LLOYD_TIMELINE") != nullptr;
+        a.timeline = want_timeline ? static_cast<long long*>(e->scratch("km.timeline", 400 * 8)) : nullptr;
         double* d_loss = static_cast<double*>(e->scratch("km.loss", kMaxRuns * 8));
-        a.bounds = static_cast<float2*>(e->scratch("km.bounds", size_t(R) * m * sizeof(float2)));
+        a.bounds = static_cast<float2*>(e->scratch("km.bounds", size_t(R) * a.stride * sizeof(float2)));
         a.init_rows = cent_rows;
-        KT_CUDA(cudaMemsetAsync(a.assign, 0xff, size_t(R) * m, e->stream));
+        KT_CUDA(cudaMemsetAsync(a.assign, 0xff, size_t(R) * a.stride, e->stream));
         KT_CUDA(cudaMemsetAsync(a.S, 0, size_t(K) * kSumW * 8, e->stream));
         KT_CUDA(cudaMemsetAsync(a.cent, 0, size_t(K) * kMaxKnobs * 8, e->stream));
         auto* h_state = static_cast<int*>(e->staging("km.state", 64));
@@ -931,7 +1004,7 @@ struct KmeansSession {
         }
         std::vector<RunResult> out(R);
         for (int r = 0; r < R; ++r)
-            pairwise_loss(e, pts, m, n, a.assign + size_t(r) * m, a.cent + size_t(a.coff[r]) * kMaxKnobs, d_loss + r);
+            pairwise_loss(e, pts, m, n, a.assign + size_t(r) * a.stride, a.cent + size_t(a.coff[r]) * kMaxKnobs, d_loss + r);
         KT_CUDA(cudaMemcpyAsync(h_loss, d_loss, R * 8, cudaMemcpyDeviceToHost, e->stream));
         KT_CUDA(cudaMemcpyAsync(h_iter, a.run_iter, R * 4, cudaMemcpyDeviceToHost, e->stream));
         e->sync();
@@ -941,6 +1014,16 @@ struct KmeansSession {
             for (int r = 0; r < R; ++r)
                 std::fprintf(stderr, "[lloyd] k=%d passes=%d skip=%llu tightened=%llu full=%llu\n", ks[r], h_iter[r] + 1,
                              hs[r * 3], hs[r * 3 + 1], hs[r * 3 + 2]);
+        }
+        if (a.timeline) {
+            long long tl[400];
+            KT_CUDA(cudaMemcpy(tl, a.timeline, sizeof(tl), cudaMemcpyDeviceToHost));
+            int mp = 0;
+            for (int r = 0; r < R; ++r) mp = std::max(mp, h_iter[r] + 1);
+            for (int it = 0; it + 1 < std::min(100, mp); ++it)
+                std::fprintf(stderr, "[lloyd] pass %d: centroids %.1f us, points %.1f us, barrier %.1f us, rest %.1f us\n",
+                             it, (tl[it * 4 + 1] - tl[it * 4]) * 1e-3, (tl[it * 4 + 2] - tl[it * 4 + 1]) * 1e-3,
+                             (tl[it * 4 + 3] - tl[it * 4 + 2]) * 1e-3, (tl[it * 4 + 4] - tl[it * 4 + 3]) * 1e-3);
         }
         int max_passes = 0;
         for (int r = 0; r < R; ++r) {
@@ -960,7 +1043,7 @@ struct KmeansSession {
     // unblocked points by the pass's own point distances (sampler.py:104-115).
     void reseed_run(LloydArgs& a, int r, const long long* h_S) {
         const int k = a.k[r], co = a.coff[r];
-        const uint8_t* asg = a.assign + size_t(r) * m;
+        const uint8_t* asg = a.assign + size_t(r) * a.stride;
         double* cent = a.cent + size_t(co) * kMaxKnobs;  // centroids used by the pass
         auto* pd2 = static_cast<double*>(e->scratch("km.pd2", size_t(m) * 8));
         const int grid = int(std::min<int64_t>(ceil_div(m, 256), int64_t(e->num_sms) * 4));
@@ -1078,7 +1161,7 @@ static KneeResult knee_scan(kt_engine* e, const uint64_t* pts, int64_t m, int n,
             res.centroids.resize(size_t(ks[pick]) * n);
             for (int j = 0; j < ks[pick]; ++j)
                 for (int i = 0; i < n; ++i) res.centroids[size_t(j) * n + i] = c[size_t(j) * kMaxKnobs + i];
-            res.assign_dev = a.assign + size_t(pick) * m;
+            res.assign_dev = a.assign + size_t(pick) * a.stride;
             res.lloyd_bytes = ses.lloyd_bytes;
             res.lloyd_launches = ses.lloyd_launches;
             return res;
