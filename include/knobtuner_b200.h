@@ -170,6 +170,41 @@ int kt_sa_chains(kt_engine* e, const kt_forest* f, const uint64_t* starts_dev, i
                  uint64_t* rows_out_dev, double* scores_out_dev, int32_t* steps_out_dev,
                  int64_t* n_out);
 
+/* -------------------------------------------- PPO search agents (K1, K4, K5) */
+/* Device-resident actor-critic (nets.py:8-10 layout, PARAM_KEYS order) with
+ * float64 master weights and Adam moments (Agent, agent.py:130-176).        */
+typedef struct kt_agent kt_agent;
+
+typedef struct kt_ppo_hyper {
+    double adam_step_size, discount, gae_parameter, clip, value_coef, entropy_coef;
+    int32_t epochs, max_steps;
+} kt_ppo_hyper;
+
+typedef struct kt_round_info {
+    int64_t steps;    /* T: PPO rows (agent steps) */
+    int64_t entries;  /* N = T + episodes: trajectory entries */
+    int64_t guarded;  /* agent-steps whose sampling was re-decided in float64 */
+    double policy_loss, value_loss, entropy, total;  /* final-epoch LossReport */
+    double guard_tau;
+} kt_round_info;
+
+int kt_agent_create(kt_engine* e, int n_knobs, int shared_width, int head_width, const double* params,
+                    const double* adam_m, const double* adam_v, int64_t adam_t, kt_agent** out);
+int kt_agent_destroy(kt_agent* a);
+/* Copy the device state back (params / Adam moments in PARAM_KEYS order). */
+int kt_agent_get_state(kt_engine* e, const kt_agent* a, double* params, double* adam_m, double* adam_v,
+                       int64_t* adam_t);
+/* One search round (run_search_round, agent.py:267-366) for max_steps >= 1:
+ * rollout of E episodes (episode e's uniforms from
+ * SeedSequence(seed, spawn_key=(round_index, e))), surrogate scores of every
+ * visited configuration, reward / GAE / advantage normalisation and `epochs`
+ * PPO+Adam updates.  Outputs the episode-major trajectory: rows, scores and
+ * step indices (capacity E * (max_steps + 1)), *n_out entries.            */
+int kt_search_round(kt_engine* e, kt_agent* a, const kt_forest* f, const uint64_t* starts_dev, int32_t E,
+                    const int32_t* cards, int n_knobs, const uint32_t* seed_words, int n_seed_words,
+                    int64_t round_index, const kt_ppo_hyper* hyper, uint64_t* rows_out_dev,
+                    double* scores_out_dev, int32_t* steps_out_dev, int64_t* n_out, kt_round_info* info);
+
 #ifdef __cplusplus
 }
 #endif

@@ -43,6 +43,18 @@ class SampleInfo(C.Structure):
     ]
 
 
+class RoundInfo(C.Structure):
+    _fields_ = [("steps", C.c_int64), ("entries", C.c_int64), ("guarded", C.c_int64),
+                ("policy_loss", C.c_double), ("value_loss", C.c_double), ("entropy", C.c_double),
+                ("total", C.c_double), ("guard_tau", C.c_double)]
+
+
+class PPOHyper(C.Structure):
+    _fields_ = [("adam_step_size", C.c_double), ("discount", C.c_double), ("gae_parameter", C.c_double),
+                ("clip", C.c_double), ("value_coef", C.c_double), ("entropy_coef", C.c_double),
+                ("epochs", C.c_int32), ("max_steps", C.c_int32)]
+
+
 # name -> (restype, argtypes); every entry must exist in the header and the .so
 SIGNATURES = {
     "kt_last_error": (C.c_char_p, []),
@@ -69,6 +81,11 @@ SIGNATURES = {
     "kt_knee_scan": (C.c_int, [P, P, i64, C.c_int, u64, f64, C.c_int, pi32, pf64, pi32, pf64, pi64]),
     "kt_adaptive_sample": (C.c_int, [P, P, i64, C.c_int, pi32, pu64, i64, u64, f64, pu64, pi32,
                                      C.POINTER(SampleInfo)]),
+    "kt_agent_create": (C.c_int, [P, C.c_int, C.c_int, C.c_int, pf64, pf64, pf64, i64, C.POINTER(P)]),
+    "kt_agent_destroy": (C.c_int, [P]),
+    "kt_agent_get_state": (C.c_int, [P, P, pf64, pf64, pf64, pi64]),
+    "kt_search_round": (C.c_int, [P, P, P, P, i32, pi32, C.c_int, pu32, C.c_int, i64, C.POINTER(PPOHyper), P, P, P,
+                                  pi64, C.POINTER(RoundInfo)]),
     "kt_sa_chains": (C.c_int, [P, P, P, i32, i32, i32, pi32, C.c_int, pu32, C.c_int, C.c_int, f64, f64, P, P, P,
                                pi64]),
 }

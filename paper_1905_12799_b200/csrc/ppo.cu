@@ -1,0 +1,701 @@
+// ppo.cu — K4 rewards / GAE / normalisation and K5 PPO update, plus the
+// run_search_round orchestration (agent.py:267-366) around K1 (rollout.cu).
+//
+// Reference: run_search_round reward shaping (agent.py:331-349), compute_gae
+// (agent.py:191-210), ppo_update (agent.py:218-258), ppo_loss_and_grads and
+// _backward (nets.py:94-171), adam_step (nets.py:189-200).
+//
+// Numerics.  Statistics that gate control flow or normalise data (reward and
+// advantage mean / std) use numpy's pairwise float64 order (pairwise.cu); GAE
+// runs in float64, one thread per episode, in the reference's reverse order;
+// the master parameters and Adam moments are float64 with the reference's
+// update expression.  The PPO forward/backward GEMMs run in fp32 with float64
+// split-K reduction of the weight gradients in a fixed order, so results are
+// deterministic run to run and within the north star's 1e-5 relative fp32
+// tolerance of the float64 reference.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "agent.cuh"
+#include "forest.cuh"
+#include "pairwise.cuh"
+#include "rng.cuh"
+
+namespace kt {
+
+// ============================================================ generic fp32 GEMM
+// C[m][n] = epi( sum_k A(m,k) * B(k,n) ), row-major storage with leading dims.
+//   A(m,k) = TA ? A[k*lda + m] : A[m*lda + k]
+//   B(k,n) = TB ? B[n*ldb + k] : B[k*ldb + n]
+// Split-K over `splits`: each z-slice accumulates k in [z*kc, (z+1)*kc) into
+// Cpart[z][m][n] (no epilogue); reduce_splits sums the slices in order.
+enum Epi : int { kEpiNone = 0, kEpiBiasTanh = 1, kEpiTanhDeriv = 2, kEpiBias = 3 };
+
+constexpr int kGemmTile = 64, kGemmK = 16, kGemmThreads = 256;
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(kGemmThreads) gemm_kernel(int M, int N, int K, const float* __restrict__ A, int lda,
+                                                             const float* __restrict__ B, int ldb, float* C, int ldc,
+                                                             int epi, const float* __restrict__ bias,
+                                                             const float* __restrict__ aux, int ldaux, int kchunk) {
+    __shared__ float As[kGemmK][kGemmTile + 4];
+    __shared__ float Bs[kGemmK][kGemmTile + 4];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int m0 = blockIdx.y * kGemmTile, n0 = blockIdx.x * kGemmTile;
+    const int kbeg = blockIdx.z * kchunk, kend = min(K, kbeg + kchunk);
+    float acc[4][4] = {};
+    for (int k0 = kbeg; k0 < kend; k0 += kGemmK) {
+        for (int i = threadIdx.x; i < kGemmK * kGemmTile; i += kGemmThreads) {
+            const int kk = i / kGemmTile, mm = i % kGemmTile;
+            const int gk = k0 + kk, gm = m0 + mm, gn = n0 + mm;
+            float av = 0.f, bv = 0.f;
+            if (gk < kend && gm < M) av = TA ? A[size_t(gk) * lda + gm] : A[size_t(gm) * lda + gk];
+            if (gk < kend && gn < N) bv = TB ? B[size_t(gn) * ldb + gk] : B[size_t(gk) * ldb + gn];
+            As[kk][mm] = av;
+            Bs[kk][mm] = bv;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < kGemmK; ++kk) {
+            float a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+    float* Cz = C + size_t(blockIdx.z) * size_t(M) * ldc;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int m = m0 + ty * 4 + i;
+        if (m >= M) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int nn = n0 + tx * 4 + j;
+            if (nn >= N) continue;
+            float v = acc[i][j];
+            if (epi == kEpiBiasTanh) v = tanhf(v + bias[nn]);
+            else if (epi == kEpiBias) v = v + bias[nn];
+            else if (epi == kEpiTanhDeriv) {
+                const float h = aux[size_t(m) * ldaux + nn];
+                v = v * (1.0f - h * h);
+            }
+            Cz[size_t(m) * ldc + nn] = v;
+        }
+    }
+}
+
+template <bool TA, bool TB>
+static void gemm(kt_engine* e, int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C,
+                 int ldc, int epi = kEpiNone, const float* bias = nullptr, const float* aux = nullptr, int ldaux = 0,
+                 int splits = 1) {
+    const int kchunk = int(ceil_div(ceil_div(K, splits), kGemmK) * kGemmK);
+    dim3 grid(unsigned(ceil_div(N, kGemmTile)), unsigned(ceil_div(M, kGemmTile)), unsigned(splits));
+    e->pre_launch("ppo_gemm");
+    gemm_kernel<TA, TB><<<grid, kGemmThreads, 0, e->stream>>>(M, N, K, A, lda, B, ldb, C, ldc, epi, bias, aux, ldaux,
+                                                               kchunk);
+    e->check_launch("ppo_gemm");
+}
+
+// out[i] (float64) = sum_z part[z][i] in z order
+__global__ void reduce_splits_kernel(const float* part, int splits, int64_t count, double* out) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x) {
+        double s = 0.0;
+        for (int z = 0; z < splits; ++z) s += double(part[size_t(z) * count + i]);
+        out[i] = s;
+    }
+}
+
+// column sums of X[rows][cols] (fp32) -> out (float64): fixed row blocks, then fixed-order combine
+template <class Tv>
+__global__ void colsum_partial_kernel(const Tv* X, int64_t rows, int cols, int ld, int64_t rows_per_block,
+                                      double* part) {
+    const int64_t r0 = int64_t(blockIdx.x) * rows_per_block, r1 = min(rows, r0 + rows_per_block);
+    for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+        double s = 0.0;
+        for (int64_t r = r0; r < r1; ++r) s += double(X[size_t(r) * ld + c]);
+        part[size_t(blockIdx.x) * cols + c] = s;
+    }
+}
+
+__global__ void colsum_final_kernel(const double* part, int blocks, int cols, double* out) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= cols) return;
+    double s = 0.0;
+    for (int b = 0; b < blocks; ++b) s += part[size_t(b) * cols + c];
+    out[c] = s;
+}
+
+// ============================================================ weights
+__global__ void pad_weights_kernel(const double* p, int n, int h, int g, PaddedWeights* w) {
+    const ParamLayout L = param_layout(n, h, g);
+    float* flat = reinterpret_cast<float*>(w);
+    for (int i = threadIdx.x; i < int(sizeof(PaddedWeights) / 4); i += blockDim.x) flat[i] = 0.f;
+    __syncthreads();
+    for (int i = threadIdx.x; i < h * n; i += blockDim.x) w->w1t[i % n][i / n] = float(p[L.w1 + i]);
+    for (int i = threadIdx.x; i < h; i += blockDim.x) w->b1[i] = float(p[L.b1 + i]);
+    for (int i = threadIdx.x; i < g * h; i += blockDim.x) {
+        w->w2pt[i % h][i / h] = float(p[L.w2p + i]);
+        w->w2vt[i % h][i / h] = float(p[L.w2v + i]);
+    }
+    for (int i = threadIdx.x; i < g; i += blockDim.x) {
+        w->b2p[i] = float(p[L.b2p + i]);
+        w->b2v[i] = float(p[L.b2v + i]);
+        w->w3v[i] = float(p[L.w3v + i]);
+    }
+    for (int i = threadIdx.x; i < 3 * n * g; i += blockDim.x) w->w3pt[i % g][i / g] = float(p[L.w3p + i]);
+    for (int i = threadIdx.x; i < 3 * n; i += blockDim.x) w->b3p[i] = float(p[L.b3p + i]);
+    if (threadIdx.x == 0) w->b3v = float(p[L.b3v]);
+}
+
+// Dense fp32 matrices for the PPO GEMMs (row-major [out][in]), from float64 params.
+struct DenseWeights {
+    float* w1;   // [h][n]
+    float* b1;   // [h]
+    float* w2;   // [2g][h]  rows 0..g-1 = w2p, g..2g-1 = w2v
+    float* b2;   // [2g]
+    float* w3;   // [3n+1][2g] block diagonal: logits from hp, value from hv
+    float* b3;   // [3n+1]
+};
+
+__global__ void dense_weights_kernel(const double* p, int n, int h, int g, DenseWeights d) {
+    const ParamLayout L = param_layout(n, h, g);
+    const int t = blockIdx.x * blockDim.x + threadIdx.x, T = gridDim.x * blockDim.x;
+    for (int i = t; i < h * n; i += T) d.w1[i] = float(p[L.w1 + i]);
+    for (int i = t; i < h; i += T) d.b1[i] = float(p[L.b1 + i]);
+    for (int i = t; i < g * h; i += T) {
+        d.w2[i] = float(p[L.w2p + i]);
+        d.w2[g * h + i] = float(p[L.w2v + i]);
+    }
+    for (int i = t; i < g; i += T) {
+        d.b2[i] = float(p[L.b2p + i]);
+        d.b2[g + i] = float(p[L.b2v + i]);
+    }
+    const int n3 = 3 * n;
+    for (int i = t; i < (n3 + 1) * 2 * g; i += T) {
+        const int o = i / (2 * g), k = i % (2 * g);
+        float v = 0.f;
+        if (o < n3 && k < g) v = float(p[L.w3p + o * g + k]);
+        if (o == n3 && k >= g) v = float(p[L.w3v + k - g]);
+        d.w3[i] = v;
+    }
+    for (int i = t; i < n3; i += T) d.b3[i] = float(p[L.b3p + i]);
+    if (t == 0) d.b3[n3] = float(p[L.b3v]);
+}
+
+// ============================================================ reward shaping / GAE
+// rewards[t] = score of the configuration step t landed on (agent.py:339-342)
+__global__ void gather_rewards_kernel(const double* scores, const int32_t* lengths, const int64_t* step_off,
+                                      const int64_t* visit_off, int E, double* rewards) {
+    const int ep = blockIdx.x;
+    if (ep >= E) return;
+    const int len = lengths[ep];
+    for (int s = threadIdx.x; s < len; s += blockDim.x) rewards[step_off[ep] + s] = scores[visit_off[ep] + 1 + s];
+}
+
+__global__ void normalize_kernel(double* x, int64_t count, const double* sum, const double* sumsq, double floor_std,
+                                 int center_only_returns, double* returns, const double* values) {
+    const double mean = __ddiv_rn(*sum, double(count));
+    const double sd = __dsqrt_rn(__ddiv_rn(*sumsq, double(count)));
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x) {
+        const double v = x[i];
+        if (sd < floor_std) {
+            x[i] = 0.0;
+            if (returns) returns[i] = values[i];
+        } else {
+            if (returns) returns[i] = v + values[i];
+            x[i] = center_only_returns ? v : __ddiv_rn(__dsub_rn(v, mean), sd);
+        }
+    }
+}
+
+__global__ void mean_kernel(const double* sum, int64_t count, double* mean) { *mean = __ddiv_rn(*sum, double(count)); }
+
+// per-episode GAE, terminal value 0 (agent.py:191-210, :230-233)
+__global__ void gae_kernel(const double* rewards, const double* values, const int32_t* lengths, const int64_t* step_off,
+                           int E, double gamma, double lam, double* adv) {
+    const int ep = blockIdx.x * blockDim.x + threadIdx.x;
+    if (ep >= E) return;
+    const int64_t o = step_off[ep];
+    const int len = lengths[ep];
+    double acc = 0.0;
+    const double gl = gamma * lam;
+    for (int t = len - 1; t >= 0; --t) {
+        const double next = t + 1 < len ? values[o + t + 1] : 0.0;
+        const double delta = __dsub_rn(__dadd_rn(rewards[o + t], __dmul_rn(gamma, next)), values[o + t]);
+        acc = __dadd_rn(delta, __dmul_rn(gl, acc));
+        adv[o + t] = acc;
+    }
+}
+
+// ============================================================ PPO row-wise part
+// Inputs per row: logits+value z[row][3n+1], actions, old logp, advantages, returns.
+// Outputs: dz[row][3n+1] (d total / d logits, d values) and per-row loss terms.
+__global__ void ppo_rows_kernel(const float* z, int ldz, int n, int64_t T, const uint16_t* actions,
+                                const double* old_logp, const double* adv, const double* ret, double clip,
+                                double value_coef, double entropy_coef, float* dz, double* terms /* [T][3] */) {
+    for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < T; r += int64_t(gridDim.x) * blockDim.x) {
+        const float* zr = z + size_t(r) * ldz;
+        const uint32_t act = actions[r];
+        double lp[kMaxKnobs][3], pr[kMaxKnobs][3], H[kMaxKnobs];
+        double newlp = 0.0, ent = 0.0;
+        for (int k = 0; k < n; ++k) {
+            const double z0 = zr[3 * k], z1 = zr[3 * k + 1], z2 = zr[3 * k + 2];
+            const double m = fmax(z0, fmax(z1, z2));
+            const double lse = log(exp(z0 - m) + exp(z1 - m) + exp(z2 - m));
+            lp[k][0] = z0 - m - lse, lp[k][1] = z1 - m - lse, lp[k][2] = z2 - m - lse;
+            H[k] = 0.0;
+            for (int j = 0; j < 3; ++j) {
+                pr[k][j] = exp(lp[k][j]);
+                H[k] -= pr[k][j] * lp[k][j];
+            }
+            newlp += lp[k][(act >> (2 * k)) & 3];
+            ent += H[k];
+        }
+        const double ratio = exp(newlp - old_logp[r]);
+        const double A = adv[r];
+        const double clipped = fmin(fmax(ratio, 1.0 - clip), 1.0 + clip);
+        const double raw = ratio * A, cl = clipped * A;
+        const double objective = fmin(raw, cl);
+        const double v = zr[3 * n];
+        const double err = v - ret[r];
+        const double invB = 1.0 / double(T);
+        const double coeff = raw <= cl ? A * ratio * invB : 0.0;
+        float* d = dz + size_t(r) * ldz;
+        for (int k = 0; k < n; ++k) {
+            const int ak = (act >> (2 * k)) & 3;
+            for (int j = 0; j < 3; ++j) {
+                const double onehot = j == ak ? 1.0 : 0.0;
+                const double g = -coeff * (onehot - pr[k][j]) + entropy_coef * invB * pr[k][j] * (lp[k][j] + H[k]);
+                d[3 * k + j] = float(g);
+            }
+        }
+        d[3 * n] = float(value_coef * 2.0 * err * invB);
+        terms[r * 3 + 0] = objective;
+        terms[r * 3 + 1] = err * err;
+        terms[r * 3 + 2] = ent;
+    }
+}
+
+// states (rows) -> X[T][n] fp32, encode_state (space.py:181-188)
+__global__ void encode_kernel(const uint64_t* rows, int64_t T, int n, const int32_t* cards_dev, float* X) {
+    for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < T; r += int64_t(gridDim.x) * blockDim.x) {
+        const uint64_t row = rows[r];
+        for (int k = 0; k < n; ++k)
+            X[size_t(r) * n + k] = float(double(row_byte(row, k)) / double(max(1, cards_dev[k] - 1)));
+    }
+}
+
+// Adam (nets.py:189-200), float64; grads come as the concatenation in PARAM_KEYS order.
+__global__ void adam_kernel(double* p, double* m, double* v, const double* g, int count, double lr, double bias1,
+                            double bias2) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
+        // exact reference expression order, no FMA contraction
+        const double gi = g[i];
+        const double mi = __dadd_rn(__dmul_rn(0.9, m[i]), __dmul_rn(1.0 - 0.9, gi));
+        const double vi = __dadd_rn(__dmul_rn(0.999, v[i]), __dmul_rn(1.0 - 0.999, __dmul_rn(gi, gi)));
+        m[i] = mi;
+        v[i] = vi;
+        const double mh = __ddiv_rn(mi, bias1), vh = __ddiv_rn(vi, bias2);
+        p[i] = __dsub_rn(p[i], __ddiv_rn(__dmul_rn(lr, mh), __dadd_rn(__dsqrt_rn(vh), 1e-8)));
+    }
+}
+
+// Gather the dense-layout gradients back into PARAM_KEYS order.
+__global__ void gather_grads_kernel(int n, int h, int g, const double* gw1, const double* gb1, const double* gw2,
+                                    const double* gb2, const double* gw3, const double* gb3, double* out) {
+    const ParamLayout L = param_layout(n, h, g);
+    const int t = blockIdx.x * blockDim.x + threadIdx.x, T = gridDim.x * blockDim.x;
+    const int n3 = 3 * n;
+    for (int i = t; i < h * n; i += T) out[L.w1 + i] = gw1[i];
+    for (int i = t; i < h; i += T) out[L.b1 + i] = gb1[i];
+    for (int i = t; i < g * h; i += T) {
+        out[L.w2p + i] = gw2[i];
+        out[L.w2v + i] = gw2[g * h + i];
+    }
+    for (int i = t; i < g; i += T) {
+        out[L.b2p + i] = gb2[i];
+        out[L.b2v + i] = gb2[g + i];
+        out[L.w3v + i] = gw3[n3 * 2 * g + g + i];
+    }
+    for (int i = t; i < n3 * g; i += T) out[L.w3p + i] = gw3[(i / g) * 2 * g + (i % g)];
+    for (int i = t; i < n3; i += T) out[L.b3p + i] = gb3[i];
+    if (t == 0) out[L.b3v] = gb3[n3];
+}
+
+}  // namespace kt
+
+// ============================================================ orchestration
+struct kt_agent {
+    int n = 0, h = 0, g = 0, P = 0;
+    double* p64 = nullptr;
+    double* m64 = nullptr;
+    double* v64 = nullptr;
+    int64_t t = 0;
+    kt::PaddedWeights* w32 = nullptr;
+    float* dense = nullptr;
+    kt::DenseWeights dw{};
+    std::vector<double> host_p;
+    int device = 0;
+};
+
+namespace kt {
+
+__global__ void lengths_kernel(const int32_t* len, int E, int64_t* steps, int64_t* visits) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+        steps[e] = len[e];
+        visits[e] = int64_t(len[e]) + 1;
+    }
+}
+
+__global__ void compact_round_kernel(int E, int S, const int32_t* len, const int64_t* step_off,
+                                     const int64_t* visit_off, const uint64_t* visited, const uint64_t* states,
+                                     const uint16_t* actions, const double* logp, const double* values,
+                                     uint64_t* rows_out, int32_t* steps_out, uint64_t* st_c, uint16_t* ac_c,
+                                     double* lp_c, double* v_c) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= E) return;
+    const int L = len[warp];
+    const int64_t vo = visit_off[warp], so = step_off[warp];
+    for (int s = lane; s <= L; s += 32) {
+        rows_out[vo + s] = visited[int64_t(warp) * (S + 1) + s];
+        steps_out[vo + s] = s;
+    }
+    for (int s = lane; s < L; s += 32) {
+        const int64_t src = int64_t(warp) * S + s;
+        st_c[so + s] = states[src];
+        ac_c[so + s] = actions[src];
+        lp_c[so + s] = logp[src];
+        v_c[so + s] = values[src];
+    }
+}
+
+__global__ void loss_report_kernel(const double* sums, int64_t T, double value_coef, double entropy_coef,
+                                   double* out) {
+    const double pol = -__ddiv_rn(sums[0], double(T));
+    const double vl = __ddiv_rn(sums[1], double(T));
+    const double ent = __ddiv_rn(sums[2], double(T));
+    out[0] = pol;
+    out[1] = vl;
+    out[2] = ent;
+    out[3] = pol + value_coef * vl - entropy_coef * ent;
+}
+
+// a-priori bound on |fp32 cdf - exact cdf| of the rollout's forward pass
+static double rollout_guard_tau(const kt_agent& ag) {
+    const ParamLayout L = param_layout(ag.n, ag.h, ag.g);
+    const std::vector<double>& p = ag.host_p;
+    const double eps = std::ldexp(1.0, -24);
+    auto gam = [&](int k) { return k * eps / (1.0 - k * eps); };
+    const double tanh_err = 3.0e-7;
+    double e_h1 = 0.0;
+    for (int o = 0; o < L.h; ++o) {
+        double sa = std::fabs(p[L.b1 + o]), sw = 0.0;
+        for (int k = 0; k < L.n; ++k) sw += std::fabs(p[L.w1 + o * L.n + k]);
+        e_h1 = std::max(e_h1, gam(L.n + 1) * (sa + sw) + 2 * eps * sw);
+    }
+    e_h1 += tanh_err;
+    double e_h2 = 0.0;
+    for (int o = 0; o < 2 * L.g; ++o) {
+        const int w = o < L.g ? L.w2p + o * L.h : L.w2v + (o - L.g) * L.h;
+        const double b = std::fabs(p[o < L.g ? L.b2p + o : L.b2v + o - L.g]);
+        double sw = 0.0;
+        for (int k = 0; k < L.h; ++k) sw += std::fabs(p[w + k]);
+        e_h2 = std::max(e_h2, gam(L.h + 1) * (sw + b) + e_h1 * sw);
+    }
+    e_h2 += tanh_err;
+    double e_z = 0.0;
+    for (int o = 0; o < 3 * L.n; ++o) {
+        double sw = 0.0;
+        for (int k = 0; k < L.g; ++k) sw += std::fabs(p[L.w3p + o * L.g + k]);
+        e_z = std::max(e_z, gam(L.g + 1) * (sw + std::fabs(p[L.b3p + o])) + e_h2 * sw);
+    }
+    // softmax / cumsum in fp32: |d log p| <= 2 e_z + rounding, |d cdf| <= 2 * max |d p|
+    return 2.0 * (2.2 * e_z + 2.0e-6) + 1.0e-6;
+}
+
+static void refresh_weights(kt_engine* e, kt_agent* ag) {
+    e->pre_launch("pad_weights");
+    pad_weights_kernel<<<1, 1024, 0, e->stream>>>(ag->p64, ag->n, ag->h, ag->g, ag->w32);
+    e->check_launch("pad_weights");
+    e->pre_launch("dense_weights");
+    dense_weights_kernel<<<32, 256, 0, e->stream>>>(ag->p64, ag->n, ag->h, ag->g, ag->dw);
+    e->check_launch("dense_weights");
+}
+
+template <class Tv>
+static void colsum(kt_engine* e, const Tv* X, int64_t rows, int cols, int ld, double* out) {
+    const int64_t per = 2048;
+    const int blocks = int(std::max<int64_t>(1, ceil_div(rows, per)));
+    auto* part = static_cast<double*>(e->scratch("ppo.colsum", size_t(blocks) * cols * 8));
+    e->pre_launch("colsum");
+    colsum_partial_kernel<Tv><<<blocks, 128, 0, e->stream>>>(X, rows, cols, ld, per, part);
+    e->check_launch("colsum");
+    e->pre_launch("colsum_final");
+    colsum_final_kernel<<<int(ceil_div(cols, 128)), 128, 0, e->stream>>>(part, blocks, cols, out);
+    e->check_launch("colsum_final");
+}
+
+// weight gradient out[M][N] (float64) = A^T B over T rows, deterministic split-K
+static void wgrad(kt_engine* e, int M, int N, int64_t T, const float* A, int lda, const float* B, int ldb,
+                  double* out) {
+    const int splits = int(std::min<int64_t>(4096, std::max<int64_t>(1, ceil_div(T, 1024))));
+    auto* part = static_cast<float*>(e->scratch("ppo.wgrad", size_t(splits) * M * N * 4));
+    gemm<true, false>(e, M, N, int(T), A, lda, B, ldb, part, N, kEpiNone, nullptr, nullptr, 0, splits);
+    const int64_t count = int64_t(M) * N;
+    e->pre_launch("reduce_splits");
+    reduce_splits_kernel<<<int(std::min<int64_t>(1024, ceil_div(count, 256))), 256, 0, e->stream>>>(part, splits,
+                                                                                                     count, out);
+    e->check_launch("reduce_splits");
+}
+
+}  // namespace kt
+
+extern "C" {
+
+int kt_agent_create(kt_engine* e, int n, int h, int g, const double* params, const double* adam_m,
+                    const double* adam_v, int64_t adam_t, kt_agent** out) {
+    KT_API_BEGIN
+    using namespace kt;
+    if (n < 1 || n > kMaxKnobs) fail(KT_ERR_UNSUPPORTED, "engine agents support 1..8 knobs");
+    if (h < 1 || h > kH || g < 1 || g > kG)
+        fail(KT_ERR_UNSUPPORTED, "engine agents support shared_width <= 128 and head_width <= 64");
+    auto* ag = new kt_agent();
+    ag->n = n, ag->h = h, ag->g = g;
+    ag->P = param_layout(n, h, g).total;
+    ag->t = adam_t;
+    ag->device = e->device;
+    ag->host_p.assign(params, params + ag->P);
+    const size_t pb = size_t(ag->P) * 8;
+    KT_CUDA(cudaMalloc(&ag->p64, pb));
+    KT_CUDA(cudaMalloc(&ag->m64, pb));
+    KT_CUDA(cudaMalloc(&ag->v64, pb));
+    KT_CUDA(cudaMemcpy(ag->p64, params, pb, cudaMemcpyHostToDevice));
+    KT_CUDA(cudaMemcpy(ag->m64, adam_m, pb, cudaMemcpyHostToDevice));
+    KT_CUDA(cudaMemcpy(ag->v64, adam_v, pb, cudaMemcpyHostToDevice));
+    KT_CUDA(cudaMalloc(&ag->w32, sizeof(PaddedWeights)));
+    const int n3 = 3 * n + 1;
+    const size_t dense = size_t(h) * n + h + size_t(2 * g) * h + 2 * g + size_t(n3) * 2 * g + n3;
+    KT_CUDA(cudaMalloc(&ag->dense, dense * 4));
+    float* d = ag->dense;
+    ag->dw.w1 = d, d += size_t(h) * n;
+    ag->dw.b1 = d, d += h;
+    ag->dw.w2 = d, d += size_t(2 * g) * h;
+    ag->dw.b2 = d, d += 2 * g;
+    ag->dw.w3 = d, d += size_t(n3) * 2 * g;
+    ag->dw.b3 = d;
+    *out = ag;
+    KT_API_END
+}
+
+int kt_agent_destroy(kt_agent* ag) {
+    KT_API_BEGIN
+    if (!ag) return KT_OK;
+    cudaFree(ag->p64);
+    cudaFree(ag->m64);
+    cudaFree(ag->v64);
+    cudaFree(ag->w32);
+    cudaFree(ag->dense);
+    delete ag;
+    KT_API_END
+}
+
+int kt_agent_get_state(kt_engine* e, const kt_agent* ag, double* params, double* adam_m, double* adam_v,
+                       int64_t* adam_t) {
+    KT_API_BEGIN
+    const size_t pb = size_t(ag->P) * 8;
+    KT_CUDA(cudaMemcpyAsync(params, ag->p64, pb, cudaMemcpyDeviceToHost, e->stream));
+    KT_CUDA(cudaMemcpyAsync(adam_m, ag->m64, pb, cudaMemcpyDeviceToHost, e->stream));
+    KT_CUDA(cudaMemcpyAsync(adam_v, ag->v64, pb, cudaMemcpyDeviceToHost, e->stream));
+    e->sync();
+    *adam_t = ag->t;
+    KT_API_END
+}
+
+int kt_search_round(kt_engine* e, kt_agent* ag, const kt_forest* f, const uint64_t* starts_dev, int32_t E,
+                    const int32_t* cards, int n_knobs, const uint32_t* seed_words, int n_seed_words,
+                    int64_t round_index, const kt_ppo_hyper* hp, uint64_t* rows_out_dev, double* scores_out_dev,
+                    int32_t* steps_out_dev, int64_t* n_out, kt_round_info* info) {
+    KT_API_BEGIN
+    using namespace kt;
+    if (E < 1) fail(KT_ERR_VALUE, "run_search_round needs at least one start configuration");
+    if (n_knobs != ag->n) fail(KT_ERR_DIMENSION, "agent and space disagree on the knob count");
+    if (f->n_knobs != n_knobs) fail(KT_ERR_DIMENSION, "model and space disagree on the knob count");
+    const int S = hp->max_steps;
+    if (S < 1) fail(KT_ERR_VALUE, "max_steps_per_episode == 0 is handled by the host");
+    if (n_seed_words < 1 || n_seed_words > 4) fail(KT_ERR_VALUE, "seed must fit in 128 bits");
+    const int n = n_knobs;
+    const ParamLayout L = param_layout(ag->n, ag->h, ag->g);
+    refresh_weights(e, ag);
+
+    // ---- K1 rollout
+    RolloutArgs ra{};
+    ra.w32 = ag->w32;
+    ra.p64 = ag->p64;
+    ra.n = n, ra.h = ag->h, ra.g = ag->g, ra.S = S, ra.E = E;
+    for (int k = 0; k < n; ++k) ra.cards[k] = cards[k];
+    for (int i = 0; i < n_seed_words; ++i) ra.seed_words[i] = seed_words[i];
+    ra.n_seed_words = n_seed_words;
+    ra.n_round_words = u64_words(uint64_t(round_index), ra.round_words);
+    ra.tau = float(rollout_guard_tau(*ag));
+    ra.starts = starts_dev;
+    const size_t slots = size_t(E) * S;
+    ra.visited = static_cast<uint64_t*>(e->scratch("rl.visited", size_t(E) * (S + 1) * 8));
+    ra.states = static_cast<uint64_t*>(e->scratch("rl.states", slots * 8));
+    ra.actions = static_cast<uint16_t*>(e->scratch("rl.actions", slots * 2));
+    ra.logp = static_cast<double*>(e->scratch("rl.logp", slots * 8));
+    ra.values = static_cast<double*>(e->scratch("rl.values", slots * 8));
+    ra.lengths = static_cast<int32_t*>(e->scratch("rl.lengths", size_t(E) * 4));
+    ra.n_guarded = static_cast<unsigned long long*>(e->scratch("rl.guarded", 8));
+    KT_CUDA(cudaMemsetAsync(ra.n_guarded, 0, 8, e->stream));
+    launch_rollout(e, ra);
+
+    // ---- episode-major compaction (agent.py:331-363)
+    auto* lens_s = static_cast<int64_t*>(e->scratch("rl.lens_s", size_t(E) * 8));
+    auto* lens_v = static_cast<int64_t*>(e->scratch("rl.lens_v", size_t(E) * 8));
+    auto* off_s = static_cast<int64_t*>(e->scratch("rl.off_s", size_t(E + 1) * 8));
+    auto* off_v = static_cast<int64_t*>(e->scratch("rl.off_v", size_t(E + 1) * 8));
+    e->pre_launch("round_lengths");
+    lengths_kernel<<<int(std::min<int64_t>(1024, ceil_div(E, 256))), 256, 0, e->stream>>>(ra.lengths, E, lens_s,
+                                                                                          lens_v);
+    e->check_launch("round_lengths");
+    exclusive_scan(e, lens_s, off_s, E);
+    exclusive_scan(e, lens_v, off_v, E);
+    int64_t totals[2];
+    KT_CUDA(cudaMemcpyAsync(&totals[0], off_s + E, 8, cudaMemcpyDeviceToHost, e->stream));
+    KT_CUDA(cudaMemcpyAsync(&totals[1], off_v + E, 8, cudaMemcpyDeviceToHost, e->stream));
+    e->sync();
+    const int64_t T = totals[0], N = totals[1];
+    auto* st_c = static_cast<uint64_t*>(e->scratch("rl.st_c", size_t(T) * 8));
+    auto* ac_c = static_cast<uint16_t*>(e->scratch("rl.ac_c", size_t(T) * 2));
+    auto* lp_c = static_cast<double*>(e->scratch("rl.lp_c", size_t(T) * 8));
+    auto* v_c = static_cast<double*>(e->scratch("rl.v_c", size_t(T) * 8));
+    e->pre_launch("compact_round");
+    compact_round_kernel<<<int(ceil_div(int64_t(E) * 32, 256)), 256, 0, e->stream>>>(
+        E, S, ra.lengths, off_s, off_v, ra.visited, ra.states, ra.actions, ra.logp, ra.values, rows_out_dev,
+        steps_out_dev, st_c, ac_c, lp_c, v_c);
+    e->check_launch("compact_round");
+
+    // ---- K2 scores of every visited configuration, rewards = landing scores
+    score_trees(e, f, rows_out_dev, N, scores_out_dev);
+    auto* rew = static_cast<double*>(e->scratch("rl.rewards", size_t(T) * 8));
+    e->pre_launch("gather_rewards");
+    gather_rewards_kernel<<<E, 64, 0, e->stream>>>(scores_out_dev, ra.lengths, off_s, off_v, E, rew);
+    e->check_launch("gather_rewards");
+    auto* sc = static_cast<double*>(e->scratch("rl.scalars", 16 * 8));  // sum, mean, sumsq per statistic
+    const int nb = int(std::min<int64_t>(2048, ceil_div(T, 256)));
+    pairwise_sum(e, rew, T, nullptr, sc + 0);
+    e->pre_launch("mean");
+    mean_kernel<<<1, 1, 0, e->stream>>>(sc + 0, T, sc + 1);
+    e->check_launch("mean");
+    pairwise_sum(e, rew, T, sc + 1, sc + 2);
+    e->pre_launch("normalize");
+    normalize_kernel<<<nb, 256, 0, e->stream>>>(rew, T, sc + 0, sc + 2, 1e-8, 0, nullptr, nullptr);
+    e->check_launch("normalize");
+
+    // ---- K4 GAE + advantage normalisation (agent.py:229-242)
+    auto* adv = static_cast<double*>(e->scratch("rl.adv", size_t(T) * 8));
+    auto* ret = static_cast<double*>(e->scratch("rl.ret", size_t(T) * 8));
+    e->pre_launch("gae");
+    gae_kernel<<<int(ceil_div(E, 128)), 128, 0, e->stream>>>(rew, v_c, ra.lengths, off_s, E, hp->discount,
+                                                              hp->gae_parameter, adv);
+    e->check_launch("gae");
+    pairwise_sum(e, adv, T, nullptr, sc + 4);
+    e->pre_launch("mean");
+    mean_kernel<<<1, 1, 0, e->stream>>>(sc + 4, T, sc + 5);
+    e->check_launch("mean");
+    pairwise_sum(e, adv, T, sc + 5, sc + 6);
+    e->pre_launch("normalize");
+    normalize_kernel<<<nb, 256, 0, e->stream>>>(adv, T, sc + 4, sc + 6, 1e-8, 0, ret, v_c);
+    e->check_launch("normalize");
+
+    // ---- K5 PPO epochs (nets.py:94-200)
+    const int h = ag->h, g2 = 2 * ag->g, n3 = 3 * n + 1;
+    auto* X = static_cast<float*>(e->scratch("ppo.X", size_t(T) * n * 4));
+    auto* H1 = static_cast<float*>(e->scratch("ppo.H1", size_t(T) * h * 4));
+    auto* H2 = static_cast<float*>(e->scratch("ppo.H2", size_t(T) * g2 * 4));
+    auto* Z = static_cast<float*>(e->scratch("ppo.Z", size_t(T) * n3 * 4));
+    auto* dZ = static_cast<float*>(e->scratch("ppo.dZ", size_t(T) * n3 * 4));
+    auto* dP2 = static_cast<float*>(e->scratch("ppo.dP2", size_t(T) * g2 * 4));
+    auto* dP1 = static_cast<float*>(e->scratch("ppo.dP1", size_t(T) * h * 4));
+    auto* terms = static_cast<double*>(e->scratch("ppo.terms", size_t(T) * 3 * 8));
+    auto* gbuf = static_cast<double*>(e->scratch("ppo.grads", size_t(h * n + h + g2 * h + g2 + n3 * g2 + n3) * 8));
+    double* gw1 = gbuf;
+    double* gb1 = gw1 + h * n;
+    double* gw2 = gb1 + h;
+    double* gb2 = gw2 + g2 * h;
+    double* gw3 = gb2 + g2;
+    double* gb3 = gw3 + n3 * g2;
+    auto* gflat = static_cast<double*>(e->scratch("ppo.gflat", size_t(ag->P) * 8));
+    auto* cards_dev = static_cast<int32_t*>(e->scratch("ppo.cards", 64));
+    KT_CUDA(cudaMemcpyAsync(cards_dev, cards, size_t(n) * 4, cudaMemcpyHostToDevice, e->stream));
+    e->pre_launch("encode_states");
+    encode_kernel<<<nb, 256, 0, e->stream>>>(st_c, T, n, cards_dev, X);
+    e->check_launch("encode_states");
+    auto* report = static_cast<double*>(e->scratch("ppo.report", 8 * 8));
+    for (int ep = 0; ep < hp->epochs; ++ep) {
+        if (ep > 0) refresh_weights(e, ag);
+        const DenseWeights& w = ag->dw;
+        gemm<false, true>(e, int(T), h, n, X, n, w.w1, n, H1, h, kEpiBiasTanh, w.b1);
+        gemm<false, true>(e, int(T), g2, h, H1, h, w.w2, h, H2, g2, kEpiBiasTanh, w.b2);
+        gemm<false, true>(e, int(T), n3, g2, H2, g2, w.w3, g2, Z, n3, kEpiBias, w.b3);
+        e->pre_launch("ppo_rows");
+        ppo_rows_kernel<<<nb, 256, 0, e->stream>>>(Z, n3, n, T, ac_c, lp_c, adv, ret, hp->clip, hp->value_coef,
+                                                    hp->entropy_coef, dZ, terms);
+        e->check_launch("ppo_rows");
+        wgrad(e, n3, g2, T, dZ, n3, H2, g2, gw3);
+        colsum(e, dZ, T, n3, n3, gb3);
+        gemm<false, false>(e, int(T), g2, n3, dZ, n3, w.w3, g2, dP2, g2, kEpiTanhDeriv, nullptr, H2, g2);
+        wgrad(e, g2, h, T, dP2, g2, H1, h, gw2);
+        colsum(e, dP2, T, g2, g2, gb2);
+        gemm<false, false>(e, int(T), h, g2, dP2, g2, w.w2, h, dP1, h, kEpiTanhDeriv, nullptr, H1, h);
+        wgrad(e, h, n, T, dP1, h, X, n, gw1);
+        colsum(e, dP1, T, h, h, gb1);
+        e->pre_launch("gather_grads");
+        gather_grads_kernel<<<32, 256, 0, e->stream>>>(n, ag->h, ag->g, gw1, gb1, gw2, gb2, gw3, gb3, gflat);
+        e->check_launch("gather_grads");
+        ag->t += 1;
+        const double bias1 = 1.0 - std::pow(0.9, double(ag->t));
+        const double bias2 = 1.0 - std::pow(0.999, double(ag->t));
+        e->pre_launch("adam");
+        adam_kernel<<<int(ceil_div(ag->P, 256)), 256, 0, e->stream>>>(ag->p64, ag->m64, ag->v64, gflat, ag->P,
+                                                                      hp->adam_step_size, bias1, bias2);
+        e->check_launch("adam");
+        if (ep == hp->epochs - 1) {
+            auto* tsum = static_cast<double*>(e->scratch("ppo.tsum", 3 * 8));
+            colsum(e, terms, T, 3, 3, tsum);
+            e->pre_launch("loss_report");
+            loss_report_kernel<<<1, 1, 0, e->stream>>>(tsum, T, hp->value_coef, hp->entropy_coef, report);
+            e->check_launch("loss_report");
+        }
+    }
+    // host mirror of the parameters (guard bound of the next round, checkpoints)
+    KT_CUDA(cudaMemcpyAsync(ag->host_p.data(), ag->p64, size_t(ag->P) * 8, cudaMemcpyDeviceToHost, e->stream));
+    double rep[4];
+    unsigned long long guarded = 0;
+    KT_CUDA(cudaMemcpyAsync(rep, report, 4 * 8, cudaMemcpyDeviceToHost, e->stream));
+    KT_CUDA(cudaMemcpyAsync(&guarded, ra.n_guarded, 8, cudaMemcpyDeviceToHost, e->stream));
+    e->sync();
+    (void)L;
+    *n_out = N;
+    if (info) {
+        info->steps = T;
+        info->entries = N;
+        info->guarded = int64_t(guarded);
+        info->policy_loss = rep[0];
+        info->value_loss = rep[1];
+        info->entropy = rep[2];
+        info->total = rep[3];
+        info->guard_tau = ra.tau;
+    }
+    KT_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,149 @@
+"""Parity of the B200 PPO search round (K1 rollout, K4 GAE, K5 PPO) with the reference.
+
+* Rollout decisions are exact: for identical parameters and uniforms the
+  trajectory (configs, scores, step indices) must be bit-identical (float64
+  re-decision inside the a-priori fp32 error band; measure-zero caveat).
+* The PPO update runs its GEMMs in fp32 (north star: 1e-5 relative for fp32
+  paths): the parameter *update* of a round is compared with the reference's.
+* Later rounds are compared per call (survey §7 hard part 2): the oracle is
+  seeded with the engine's own post-update state, then both run one round.
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1905_12799_b200 as kt  # noqa: E402
+from golden_io import GOLDEN, meta, npz  # noqa: E402
+from oracle import agent as oagent  # noqa: E402
+from paper_1905_12799_b200.agent import PARAM_KEYS, _flat  # noqa: E402
+
+MODELS = json.loads((GOLDEN / "models.json").read_text())
+LR = 1e-3
+
+
+def space_of(values):
+    return kt.DesignSpace("grid", tuple(kt.KnobDef(f"k{i}", tuple(v)) for i, v in enumerate(values)))
+
+
+def oracle_from(agent):
+    return {"params": {k: v.copy() for k, v in agent.params.items()},
+            "m": {k: v.copy() for k, v in agent.adam.m.items()}, "v": {k: v.copy() for k, v in agent.adam.v.items()},
+            "t": agent.adam.t, "seed": agent.seed, "rounds": agent.rounds_completed}
+
+
+def assert_update_close(before, after, want_after, rel=1e-5):
+    """|update - reference update| <= rel * |reference update| + rel * lr (Adam steps are ~lr)."""
+    got, want = after - before, want_after - before
+    err = np.abs(got - want)
+    bound = rel * np.abs(want) + rel * LR
+    frac_bad = float(np.mean(err > bound))
+    assert frac_bad < 2e-3, f"{frac_bad:.2%} of parameters outside tolerance, max err {err.max():.3e}"
+
+
+@pytest.mark.parametrize("name", sorted(meta("rl")))
+def test_first_round_matches_reference(name):
+    g = npz("rl")
+    md = meta("rl")[name]
+    mm = MODELS[md["model"]]
+    space = space_of(mm["values"])
+    model = kt.CostModel.from_dict(mm["model"])
+    hyper = kt.AgentHyperparams.from_dict(md["hyper"])
+    agent = kt.init_agent(space, hyper, seed=md["seed"])
+    assert np.array_equal(_flat(agent.params), g[f"{name}/params0"])
+    starts = [kt.Configuration(tuple(r)) for r in g[f"{name}/r0/starts"].tolist()]
+    before = _flat(agent.params)
+    tr = kt.run_search_round(agent, model, space, starts)
+    assert np.array_equal(tr.index_matrix(), g[f"{name}/r0/idx"])
+    assert np.array_equal(tr.scores(), g[f"{name}/r0/scores"])
+    assert tr.step_indices == tuple(g[f"{name}/r0/steps"].tolist())
+    assert agent.rounds_completed == 1
+    if hyper.max_steps_per_episode:
+        assert_update_close(before, _flat(agent.params), g[f"{name}/r0/params"])
+
+
+@pytest.mark.parametrize("name", ["bowl_default_2r", "bowl_tiny"])
+def test_later_rounds_per_call_parity(name):
+    g = npz("rl")
+    md = meta("rl")[name]
+    mm = MODELS[md["model"]]
+    space = space_of(mm["values"])
+    model = kt.CostModel.from_dict(mm["model"])
+    hyper = kt.AgentHyperparams.from_dict(md["hyper"])
+    agent = kt.init_agent(space, hyper, seed=md["seed"])
+    rng = np.random.default_rng(77)
+    for _ in range(3):
+        ref = oracle_from(agent)
+        starts = rng.integers(0, np.array(space.cardinalities), size=(md["E"], len(space.knobs)))
+        before = _flat(agent.params)
+        tr = kt.run_search_round(agent, model, space, [kt.Configuration(tuple(r)) for r in starts.tolist()])
+        o_idx, o_sc, o_st = oagent.search_round(ref, mm["model"], mm["values"], starts, md["hyper"])
+        assert np.array_equal(tr.index_matrix(), o_idx)
+        assert np.array_equal(tr.scores(), o_sc)
+        assert np.array_equal(np.array(tr.step_indices), o_st)
+        want = np.concatenate([ref["params"][k].ravel() for k in PARAM_KEYS])
+        assert_update_close(before, _flat(agent.params), want)
+        assert agent.adam.t == ref["t"] and agent.rounds_completed == ref["rounds"]
+
+
+def test_large_round_vs_oracle():
+    """4096 episodes of 32 steps on the Table-1 conv space: exact trajectory, update within tolerance."""
+    mm = MODELS["table1"]
+    space = space_of(mm["values"])
+    model = kt.CostModel.from_dict(mm["model"])
+    hyper = kt.AgentHyperparams(episodes_per_round=4096)
+    agent = kt.init_agent(space, hyper, seed=21)
+    ref = oracle_from(agent)
+    starts = np.random.default_rng(4).integers(0, np.array(space.cardinalities), size=(4096, 8))
+    before = _flat(agent.params)
+    info = kt._lib.RoundInfo()
+    rows = torch.from_numpy(kt.pack(starts).view(np.int64)).cuda()
+    r_rows, r_sc, r_st = kt.run_search_rows(agent, model, space, rows, info=info)
+    o_idx, o_sc, o_st = oagent.search_round(ref, mm["model"], mm["values"], starts, hyper.to_dict())
+    assert np.array_equal(kt.unpack(r_rows.cpu().numpy().view(np.uint64), 8), o_idx)
+    assert np.array_equal(r_sc.cpu().numpy(), o_sc)
+    assert np.array_equal(r_st.cpu().numpy(), o_st)
+    want = np.concatenate([ref["params"][k].ravel() for k in PARAM_KEYS])
+    assert_update_close(before, _flat(agent.params), want)
+    assert info.steps == len(o_idx) - 4096
+
+
+def test_zero_steps_and_errors():
+    space = kt.grid(4, 4)
+    agent = kt.init_agent(space, kt.AgentHyperparams(max_steps_per_episode=0, shared_width=4, head_width=4), seed=0)
+    starts = [kt.Configuration((0, 0)), kt.Configuration((3, 2))]
+    tr = kt.run_search_round(agent, kt.CostModel.sentinel(2), space, starts)
+    assert [c.indices for c in tr.configs()] == [(0, 0), (3, 2)] and agent.rounds_completed == 1
+    with pytest.raises(ValueError):
+        kt.run_search_round(agent, kt.CostModel.sentinel(2), space, [])
+    with pytest.raises(kt.errors.DimensionMismatchError):
+        kt.run_search_round(agent, kt.CostModel.sentinel(3), kt.grid(3, 3, 3), [kt.Configuration((0, 0, 0))])
+
+
+def test_cardinality_one_space():
+    space = kt.DesignSpace("one", (kt.KnobDef("k", (1,)),))
+    hyper = kt.AgentHyperparams(shared_width=4, head_width=4, episodes_per_round=4, max_steps_per_episode=8)
+    agent = kt.init_agent(space, hyper, seed=0)
+    model = kt.CostModel.from_dict(MODELS["bowl_g10"]["model"]) if False else None
+    tr = kt.run_search_round(agent, kt.CostModel.sentinel(1, base_score=1.0), space, [kt.Configuration((0,))])
+    assert {c.indices for c in tr.configs()} == {(0,)}
+
+
+def test_checkpoint_roundtrip_after_device_round():
+    space = kt.grid(6, 6)
+    hyper = kt.AgentHyperparams(shared_width=4, head_width=4, episodes_per_round=4, max_steps_per_episode=8)
+    model = kt.CostModel.sentinel(2, base_score=1.0)
+    starts = [kt.Configuration((0, 0)), kt.Configuration((5, 5))]
+    a = kt.init_agent(space, hyper, seed=2)
+    kt.run_search_round(a, model, space, starts)
+    resumed = kt.Agent.from_json(a.to_json())
+    t1 = kt.run_search_round(a, model, space, starts)
+    t2 = kt.run_search_round(resumed, model, space, starts)
+    assert t1.entries == t2.entries
