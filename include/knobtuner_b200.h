@@ -203,7 +203,8 @@ int kt_agent_get_state(kt_engine* e, const kt_agent* a, double* params, double* 
 int kt_search_round(kt_engine* e, kt_agent* a, const kt_forest* f, const uint64_t* starts_dev, int32_t E,
                     const int32_t* cards, int n_knobs, const uint32_t* seed_words, int n_seed_words,
                     int64_t round_index, const kt_ppo_hyper* hyper, uint64_t* rows_out_dev,
-                    double* scores_out_dev, int32_t* steps_out_dev, int64_t* n_out, kt_round_info* info);
+                    double* scores_out_dev, int32_t* steps_out_dev, int64_t* n_out, kt_round_info* info,
+                    double* logp_out_dev /* T or NULL */, double* values_out_dev /* T or NULL */);
 
 #ifdef __cplusplus
 }

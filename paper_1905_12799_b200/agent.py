@@ -205,8 +205,13 @@ RoundInfo = _lib.RoundInfo
 PPOHyper = _lib.PPOHyper
 
 
-def run_search_rows(agent, model, space, start_rows, engine=None, info: RoundInfo | None = None):
-    """Array path: CUDA int64 start rows -> (rows, scores, step indices) CUDA tensors; mutates ``agent``."""
+def run_search_rows(agent, model, space, start_rows, engine=None, info: RoundInfo | None = None,
+                    rollout_out: dict | None = None):
+    """Array path: CUDA int64 start rows -> (rows, scores, step indices) CUDA tensors; mutates ``agent``.
+
+    ``rollout_out`` (optional dict) receives the rollout's per-step log-probs and
+    values (Rollout.log_probs / values, agent.py:351-363) as CUDA float64 tensors.
+    """
     import torch
 
     engine = engine or _lib.engine()
@@ -229,10 +234,18 @@ def run_search_rows(agent, model, space, start_rows, engine=None, info: RoundInf
         rows = torch.empty(cap, dtype=torch.int64, device=start_rows.device)
         scores = torch.empty(cap, dtype=torch.float64, device=start_rows.device)
         steps = torch.empty(cap, dtype=torch.int32, device=start_rows.device)
+        lp = vals = None
+        if rollout_out is not None:
+            lp = torch.empty(E * S, dtype=torch.float64, device=start_rows.device)
+            vals = torch.empty(E * S, dtype=torch.float64, device=start_rows.device)
         _lib.call("kt_search_round", engine.handle, dev_agent.handle, f.handle, _lib.ptr(start_rows), E,
                   _lib.as_ptr(cards, _lib.C.c_int32), int(cards.size), _lib.as_ptr(words, _lib.C.c_uint32),
                   int(words.size), int(agent.rounds_completed), _lib.C.byref(hp), _lib.ptr(rows), _lib.ptr(scores),
-                  _lib.ptr(steps), _lib.C.byref(total), _lib.C.byref(info))
+                  _lib.ptr(steps), _lib.C.byref(total), _lib.C.byref(info),
+                  _lib.ptr(lp) if lp is not None else None, _lib.ptr(vals) if vals is not None else None)
+        if rollout_out is not None:
+            rollout_out["log_probs"] = lp[: info.steps]
+            rollout_out["values"] = vals[: info.steps]
     dev_agent.pull_into(agent, engine)
     agent.rounds_completed += 1
     n = int(total.value)

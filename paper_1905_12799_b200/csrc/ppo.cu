@@ -522,7 +522,8 @@ int kt_agent_get_state(kt_engine* e, const kt_agent* ag, double* params, double*
 int kt_search_round(kt_engine* e, kt_agent* ag, const kt_forest* f, const uint64_t* starts_dev, int32_t E,
                     const int32_t* cards, int n_knobs, const uint32_t* seed_words, int n_seed_words,
                     int64_t round_index, const kt_ppo_hyper* hp, uint64_t* rows_out_dev, double* scores_out_dev,
-                    int32_t* steps_out_dev, int64_t* n_out, kt_round_info* info) {
+                    int32_t* steps_out_dev, int64_t* n_out, kt_round_info* info, double* logp_out_dev,
+                    double* values_out_dev) {
     KT_API_BEGIN
     using namespace kt;
     if (E < 1) fail(KT_ERR_VALUE, "run_search_round needs at least one start configuration");
@@ -582,6 +583,9 @@ int kt_search_round(kt_engine* e, kt_agent* ag, const kt_forest* f, const uint64
         E, S, ra.lengths, off_s, off_v, ra.visited, ra.states, ra.actions, ra.logp, ra.values, rows_out_dev,
         steps_out_dev, st_c, ac_c, lp_c, v_c);
     e->check_launch("compact_round");
+    if (logp_out_dev) KT_CUDA(cudaMemcpyAsync(logp_out_dev, lp_c, size_t(T) * 8, cudaMemcpyDeviceToDevice, e->stream));
+    if (values_out_dev)
+        KT_CUDA(cudaMemcpyAsync(values_out_dev, v_c, size_t(T) * 8, cudaMemcpyDeviceToDevice, e->stream));
 
     // ---- K2 scores of every visited configuration, rewards = landing scores
     score_trees(e, f, rows_out_dev, N, scores_out_dev);
