@@ -206,6 +206,14 @@ int kt_search_round(kt_engine* e, kt_agent* a, const kt_forest* f, const uint64_
                     double* scores_out_dev, int32_t* steps_out_dev, int64_t* n_out, kt_round_info* info,
                     double* logp_out_dev /* T or NULL */, double* values_out_dev /* T or NULL */);
 
+/* ------------------------------------------------------------ utilities */
+/* fp32 GEMM on the tensor cores (tcgen05 kind::tf32, 3xTF32 split, fp32 accumulate
+ * in TMEM): C[m][n] = sum_k A(m,k) B(k,n), row-major device arrays;
+ * A(m,k) = trans_a ? A[k*lda+m] : A[m*lda+k], B(k,n) = trans_b ? B[n*ldb+k] : B[k*ldb+n].
+ * Used by the PPO update; exported for verification.                        */
+int kt_gemm_f32(kt_engine* e, int trans_a, int trans_b, int M, int N, int K, const float* A, int lda,
+                const float* B, int ldb, float* C, int ldc);
+
 #ifdef __cplusplus
 }
 #endif

@@ -86,6 +86,7 @@ SIGNATURES = {
     "kt_agent_get_state": (C.c_int, [P, P, pf64, pf64, pf64, pi64]),
     "kt_search_round": (C.c_int, [P, P, P, P, i32, pi32, C.c_int, pu32, C.c_int, i64, C.POINTER(PPOHyper), P, P, P,
                                   pi64, C.POINTER(RoundInfo), P, P]),
+    "kt_gemm_f32": (C.c_int, [P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P, C.c_int, P, C.c_int, P, C.c_int]),
     "kt_sa_chains": (C.c_int, [P, P, P, i32, i32, i32, pi32, C.c_int, pu32, C.c_int, C.c_int, f64, f64, P, P, P,
                                pi64]),
 }

@@ -80,4 +80,8 @@ struct RolloutArgs {
 
 void launch_rollout(kt_engine* e, const RolloutArgs& a);
 
+// fp32 GEMM on tcgen05 (gemm_tc.cu): C = epi(A(m,k) B(k,n)), TA: A MN-major, TB: B K-major.
+void tc_gemm(kt_engine* e, bool TA, bool TB, int M, int N, int K, const float* A, int lda, const float* B, int ldb,
+             float* C, int ldc, int epi, const float* bias, const float* aux, int ldaux, int splits);
+
 }  // namespace kt

@@ -1,0 +1,233 @@
+// gemm_tc.cu — fp32 GEMMs on the 5th-generation tensor cores (tcgen05, kind::tf32, "3xTF32").
+//
+// C[m][n] = epi( sum_k A(m,k) * B(k,n) ) with the same operand conventions as
+// the CUDA-core gemm in ppo.cu:
+//   A(m,k) = TA ? A[k*lda + m] (MN-major) : A[m*lda + k] (K-major)
+//   B(k,n) = TB ? B[n*ldb + k] (K-major)  : B[k*ldb + n] (MN-major)
+// One CTA (128 threads) owns a 128 x BN output tile whose fp32 accumulator
+// lives in TMEM.  K is consumed in chunks of 32: all threads stage the chunk
+// into shared memory in the canonical no-swizzle UMMA layout (umma.cuh), split
+// into tf32 hi and lo parts; one thread issues hi*hi + hi*lo + lo*hi for each
+// of the 4 k-groups (12 tcgen05.mma), committing to an mbarrier.  Two stage
+// buffers let the next chunk's loads overlap the tensor core.  The dropped
+// lo*lo term is 2^-22 relative, so products are fp32-accurate; accumulation is
+// fp32 in TMEM.  The epilogue (bias + tanh, tanh derivative, or split-K
+// partial store) reads TMEM with tcgen05.ld, one row per thread.
+#include <algorithm>
+
+#include "common.cuh"
+#include "umma.cuh"
+
+namespace kt {
+
+constexpr int kTcBM = 128, kTcBK = 32, kTcThreads = 128;
+
+struct TcGemmArgs {
+    int M, N, K;
+    const float* A;
+    int lda;
+    const float* B;
+    int ldb;
+    float* C;
+    int ldc;
+    int epi;  // 0 none, 1 bias+tanh, 2 * (1 - aux^2), 3 bias
+    const float* bias;
+    const float* aux;
+    int ldaux;
+    int kchunk;  // K range per blockIdx.z (multiple of 32)
+    int BN;      // tile N (multiple of 16, <= 128)
+};
+
+template <bool MN_MAJOR>
+__device__ __forceinline__ void stage_tile(float* hi, float* lo, const float* G, int ld, int rows, int r0, int rlimit,
+                                           int k0, int klimit, bool vec_ok) {
+    // rows x 32 tile; element (r, k) -> hi/lo at the canonical address (in floats)
+    if (!MN_MAJOR) {
+        // K-major: global G[(r0 + r) * ld + k0 + k]
+        const int nvec = rows * (kTcBK / 4);
+        for (int f = threadIdx.x; f < nvec; f += kTcThreads) {
+            const int r = f / (kTcBK / 4), kq = f % (kTcBK / 4);
+            const int gr = r0 + r, gk = k0 + 4 * kq;
+            float v[4] = {0.f, 0.f, 0.f, 0.f};
+            if (gr < rlimit) {
+                const float* src = G + size_t(gr) * ld + gk;
+                if (vec_ok && gk + 3 < klimit) {
+                    const float4 q = *reinterpret_cast<const float4*>(src);
+                    v[0] = q.x, v[1] = q.y, v[2] = q.z, v[3] = q.w;
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        if (gk + e < klimit) v[e] = src[e];
+                }
+            }
+            const int off = kq * rows * 4 + (r >> 3) * 32 + (r & 7) * 4;
+            float4 h, l;
+            umma::split_tf32(v[0], h.x, l.x);
+            umma::split_tf32(v[1], h.y, l.y);
+            umma::split_tf32(v[2], h.z, l.z);
+            umma::split_tf32(v[3], h.w, l.w);
+            *reinterpret_cast<float4*>(hi + off) = h;
+            *reinterpret_cast<float4*>(lo + off) = l;
+        }
+    } else {
+        // MN-major: global G[(k0 + k) * ld + r0 + r]
+        const int nvec = (rows / 4) * kTcBK;
+        for (int f = threadIdx.x; f < nvec; f += kTcThreads) {
+            const int k = f / (rows / 4), rq = f % (rows / 4);
+            const int gk = k0 + k, gr = r0 + 4 * rq;
+            float v[4] = {0.f, 0.f, 0.f, 0.f};
+            if (gk < klimit) {
+                const float* src = G + size_t(gk) * ld + gr;
+                if (vec_ok && gr + 3 < rlimit) {
+                    const float4 q = *reinterpret_cast<const float4*>(src);
+                    v[0] = q.x, v[1] = q.y, v[2] = q.z, v[3] = q.w;
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        if (gr + e < rlimit) v[e] = src[e];
+                }
+            }
+            const int off = (k >> 3) * (rows / 4) * 32 + rq * 32 + (k & 7) * 4;
+            float4 h, l;
+            umma::split_tf32(v[0], h.x, l.x);
+            umma::split_tf32(v[1], h.y, l.y);
+            umma::split_tf32(v[2], h.z, l.z);
+            umma::split_tf32(v[3], h.w, l.w);
+            *reinterpret_cast<float4*>(hi + off) = h;
+            *reinterpret_cast<float4*>(lo + off) = l;
+        }
+    }
+}
+
+template <bool MN_MAJOR>
+__device__ __forceinline__ uint64_t tile_desc(uint32_t base, int rows, int j) {
+    if (!MN_MAJOR) return umma::smem_desc(base + uint32_t(2 * j * rows * 16), uint32_t(rows * 16), 128u);
+    return umma::smem_desc(base + uint32_t(j * (rows / 4) * 128), uint32_t((rows / 4) * 128), 128u);
+}
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(TcGemmArgs g) {
+    extern __shared__ __align__(1024) unsigned char s_dyn[];
+    __shared__ uint64_t mma_bar[2];
+    __shared__ uint32_t tmem_slot;
+    constexpr bool A_MN = TA, B_MN = !TB;
+    const int BN = g.BN;
+    float* base = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(s_dyn) + 1023) & ~uintptr_t(1023));
+    const int a_floats = kTcBM * kTcBK, b_floats = BN * kTcBK;
+    const int stage_floats = 2 * a_floats + 2 * b_floats;  // A hi, A lo, B hi, B lo
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int m0 = blockIdx.y * kTcBM, n0 = blockIdx.x * BN;
+    const int kbeg = blockIdx.z * g.kchunk, kend = min(g.K, kbeg + g.kchunk);
+    const int nchunks = kend > kbeg ? (kend - kbeg + kTcBK - 1) / kTcBK : 0;
+    const uint32_t ncols = BN <= 32 ? 32u : (BN <= 64 ? 64u : 128u);
+
+    if (tid == 0) {
+        umma::mbar_init(umma::smem_addr(&mma_bar[0]), 1);
+        umma::mbar_init(umma::smem_addr(&mma_bar[1]), 1);
+        umma::mbar_fence_init();
+    }
+    if (warp == 0) umma::tmem_alloc(umma::smem_addr(&tmem_slot), ncols);
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+    const uint32_t tmem = tmem_slot;
+    const uint32_t idesc = umma::idesc_tf32(BN, A_MN, B_MN);
+    const bool a_vec = (g.lda % 4) == 0 && (reinterpret_cast<uintptr_t>(g.A) % 16) == 0;
+    const bool b_vec = (g.ldb % 4) == 0 && (reinterpret_cast<uintptr_t>(g.B) % 16) == 0;
+
+    for (int c = 0; c < nchunks; ++c) {
+        const int s = c & 1;
+        if (c >= 2) umma::mbar_wait(umma::smem_addr(&mma_bar[s]), uint32_t((c - 2) >> 1) & 1u);
+        float* st = base + s * stage_floats;
+        float *a_hi = st, *a_lo = st + a_floats, *b_hi = st + 2 * a_floats, *b_lo = b_hi + b_floats;
+        const int k0 = kbeg + c * kTcBK;
+        stage_tile<A_MN>(a_hi, a_lo, g.A, g.lda, kTcBM, m0, g.M, k0, kend, a_vec);
+        stage_tile<B_MN>(b_hi, b_lo, g.B, g.ldb, BN, n0, g.N, k0, kend, b_vec);
+        umma::fence_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+            umma::fence_after();
+            const uint32_t ah = umma::smem_addr(a_hi), al = umma::smem_addr(a_lo);
+            const uint32_t bh = umma::smem_addr(b_hi), bl = umma::smem_addr(b_lo);
+#pragma unroll
+            for (int j = 0; j < kTcBK / 8; ++j) {
+                const uint64_t dah = tile_desc<A_MN>(ah, kTcBM, j), dal = tile_desc<A_MN>(al, kTcBM, j);
+                const uint64_t dbh = tile_desc<B_MN>(bh, BN, j), dbl = tile_desc<B_MN>(bl, BN, j);
+                umma::mma_tf32(tmem, dah, dbh, idesc, (c | j) != 0);
+                umma::mma_tf32(tmem, dah, dbl, idesc, 1u);
+                umma::mma_tf32(tmem, dal, dbh, idesc, 1u);
+            }
+            umma::commit(umma::smem_addr(&mma_bar[s]));
+        }
+        __syncwarp();
+    }
+    if (nchunks > 0) umma::mbar_wait(umma::smem_addr(&mma_bar[(nchunks - 1) & 1]), uint32_t((nchunks - 1) >> 1) & 1u);
+    umma::fence_after();
+
+    // ---- epilogue: thread (warp w, lane l) owns output row m0 + 32w + l
+    const int m = m0 + warp * 32 + (tid & 31);
+    float* Cz = g.C + size_t(blockIdx.z) * size_t(g.M) * g.ldc;
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+        float v[32];
+        if (nchunks > 0) {
+            umma::tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + uint32_t(c0), v);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0.f;
+        }
+        if (m < g.M) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const int n = n0 + c0 + i;
+                if (c0 + i >= BN || n >= g.N) continue;
+                float x = v[i];
+                if (g.epi == 1) x = tanhf(x + g.bias[n]);
+                else if (g.epi == 3) x = x + g.bias[n];
+                else if (g.epi == 2) {
+                    const float h = g.aux[size_t(m) * g.ldaux + n];
+                    x = x * (1.0f - h * h);
+                }
+                Cz[size_t(m) * g.ldc + n] = x;
+            }
+        }
+    }
+    umma::fence_before();
+    __syncthreads();
+    if (warp == 0) umma::tmem_dealloc(tmem, ncols);
+}
+
+template <bool TA, bool TB>
+static void launch_tc(kt_engine* e, const TcGemmArgs& a, dim3 grid, size_t smem) {
+    auto kern = tc_gemm_kernel<TA, TB>;
+    KT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    e->pre_launch("tc_gemm");
+    kern<<<grid, kTcThreads, smem, e->stream>>>(a);
+    e->check_launch("tc_gemm");
+}
+
+// Public helper used by ppo.cu and kt_gemm_f32.
+void tc_gemm(kt_engine* e, bool TA, bool TB, int M, int N, int K, const float* A, int lda, const float* B, int ldb,
+             float* C, int ldc, int epi, const float* bias, const float* aux, int ldaux, int splits) {
+    TcGemmArgs a{M, N, K, A, lda, B, ldb, C, ldc, epi, bias, aux, ldaux, 0, 0};
+    const int n_tiles = int(ceil_div(N, 128));
+    int bn = int(ceil_div(ceil_div(N, n_tiles), 16) * 16);
+    bn = std::max(16, std::min(128, bn));
+    a.BN = bn;
+    a.kchunk = int(ceil_div(ceil_div(K, splits), kTcBK) * kTcBK);
+    dim3 grid(unsigned(ceil_div(N, bn)), unsigned(ceil_div(M, kTcBM)), unsigned(splits));
+    const size_t smem = size_t(2) * (2 * kTcBM * kTcBK + 2 * bn * kTcBK) * 4 + 1024;
+    if (TA && TB) launch_tc<true, true>(e, a, grid, smem);
+    else if (TA) launch_tc<true, false>(e, a, grid, smem);
+    else if (TB) launch_tc<false, true>(e, a, grid, smem);
+    else launch_tc<false, false>(e, a, grid, smem);
+}
+
+}  // namespace kt
+
+extern "C" int kt_gemm_f32(kt_engine* e, int trans_a, int trans_b, int M, int N, int K, const float* A, int lda,
+                           const float* B, int ldb, float* C, int ldc) {
+    KT_API_BEGIN
+    if (M < 1 || N < 1 || K < 0) kt::fail(KT_ERR_VALUE, "bad GEMM shape");
+    kt::tc_gemm(e, trans_a != 0, trans_b != 0, M, N, K, A, lda, B, ldb, C, ldc, 0, nullptr, nullptr, 0, 1);
+    KT_API_END
+}

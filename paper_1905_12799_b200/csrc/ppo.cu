@@ -9,10 +9,11 @@
 // advantage mean / std) use numpy's pairwise float64 order (pairwise.cu); GAE
 // runs in float64, one thread per episode, in the reference's reverse order;
 // the master parameters and Adam moments are float64 with the reference's
-// update expression.  The PPO forward/backward GEMMs run in fp32 with float64
-// split-K reduction of the weight gradients in a fixed order, so results are
-// deterministic run to run and within the north star's 1e-5 relative fp32
-// tolerance of the float64 reference.
+// update expression.  The PPO forward/backward GEMMs run on the tensor cores
+// (tcgen05 kind::tf32 with a 3xTF32 hi/lo split = fp32-accurate products, fp32
+// accumulation in TMEM) with float64 split-K reduction of the weight gradients
+// in a fixed order, so results are deterministic run to run and within the
+// north star's fp32 tolerance of the float64 reference.
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -25,84 +26,8 @@
 
 namespace kt {
 
-// ============================================================ generic fp32 GEMM
-// C[m][n] = epi( sum_k A(m,k) * B(k,n) ), row-major storage with leading dims.
-//   A(m,k) = TA ? A[k*lda + m] : A[m*lda + k]
-//   B(k,n) = TB ? B[n*ldb + k] : B[k*ldb + n]
-// Split-K over `splits`: each z-slice accumulates k in [z*kc, (z+1)*kc) into
-// Cpart[z][m][n] (no epilogue); reduce_splits sums the slices in order.
+// GEMMs run on the tensor cores (gemm_tc.cu, 3xTF32 tcgen05); epilogue codes:
 enum Epi : int { kEpiNone = 0, kEpiBiasTanh = 1, kEpiTanhDeriv = 2, kEpiBias = 3 };
-
-constexpr int kGemmTile = 64, kGemmK = 16, kGemmThreads = 256;
-
-template <bool TA, bool TB>
-__global__ void __launch_bounds__(kGemmThreads) gemm_kernel(int M, int N, int K, const float* __restrict__ A, int lda,
-                                                             const float* __restrict__ B, int ldb, float* C, int ldc,
-                                                             int epi, const float* __restrict__ bias,
-                                                             const float* __restrict__ aux, int ldaux, int kchunk) {
-    __shared__ float As[kGemmK][kGemmTile + 4];
-    __shared__ float Bs[kGemmK][kGemmTile + 4];
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    const int m0 = blockIdx.y * kGemmTile, n0 = blockIdx.x * kGemmTile;
-    const int kbeg = blockIdx.z * kchunk, kend = min(K, kbeg + kchunk);
-    float acc[4][4] = {};
-    for (int k0 = kbeg; k0 < kend; k0 += kGemmK) {
-        for (int i = threadIdx.x; i < kGemmK * kGemmTile; i += kGemmThreads) {
-            const int kk = i / kGemmTile, mm = i % kGemmTile;
-            const int gk = k0 + kk, gm = m0 + mm, gn = n0 + mm;
-            float av = 0.f, bv = 0.f;
-            if (gk < kend && gm < M) av = TA ? A[size_t(gk) * lda + gm] : A[size_t(gm) * lda + gk];
-            if (gk < kend && gn < N) bv = TB ? B[size_t(gn) * ldb + gk] : B[size_t(gk) * ldb + gn];
-            As[kk][mm] = av;
-            Bs[kk][mm] = bv;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int kk = 0; kk < kGemmK; ++kk) {
-            float a[4], b[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
-        }
-        __syncthreads();
-    }
-    float* Cz = C + size_t(blockIdx.z) * size_t(M) * ldc;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int m = m0 + ty * 4 + i;
-        if (m >= M) continue;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int nn = n0 + tx * 4 + j;
-            if (nn >= N) continue;
-            float v = acc[i][j];
-            if (epi == kEpiBiasTanh) v = tanhf(v + bias[nn]);
-            else if (epi == kEpiBias) v = v + bias[nn];
-            else if (epi == kEpiTanhDeriv) {
-                const float h = aux[size_t(m) * ldaux + nn];
-                v = v * (1.0f - h * h);
-            }
-            Cz[size_t(m) * ldc + nn] = v;
-        }
-    }
-}
-
-template <bool TA, bool TB>
-static void gemm(kt_engine* e, int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C,
-                 int ldc, int epi = kEpiNone, const float* bias = nullptr, const float* aux = nullptr, int ldaux = 0,
-                 int splits = 1) {
-    const int kchunk = int(ceil_div(ceil_div(K, splits), kGemmK) * kGemmK);
-    dim3 grid(unsigned(ceil_div(N, kGemmTile)), unsigned(ceil_div(M, kGemmTile)), unsigned(splits));
-    e->pre_launch("ppo_gemm");
-    gemm_kernel<TA, TB><<<grid, kGemmThreads, 0, e->stream>>>(M, N, K, A, lda, B, ldb, C, ldc, epi, bias, aux, ldaux,
-                                                               kchunk);
-    e->check_launch("ppo_gemm");
-}
 
 // out[i] (float64) = sum_z part[z][i] in z order
 __global__ void reduce_splits_kernel(const float* part, int splits, int64_t count, double* out) {
@@ -448,7 +373,7 @@ static void wgrad(kt_engine* e, int M, int N, int64_t T, const float* A, int lda
                   double* out) {
     const int splits = int(std::min<int64_t>(4096, std::max<int64_t>(1, ceil_div(T, 1024))));
     auto* part = static_cast<float*>(e->scratch("ppo.wgrad", size_t(splits) * M * N * 4));
-    gemm<true, false>(e, M, N, int(T), A, lda, B, ldb, part, N, kEpiNone, nullptr, nullptr, 0, splits);
+    tc_gemm(e, true, false, M, N, int(T), A, lda, B, ldb, part, N, kEpiNone, nullptr, nullptr, 0, splits);
     const int64_t count = int64_t(M) * N;
     e->pre_launch("reduce_splits");
     reduce_splits_kernel<<<int(std::min<int64_t>(1024, ceil_div(count, 256))), 256, 0, e->stream>>>(part, splits,
@@ -647,19 +572,19 @@ int kt_search_round(kt_engine* e, kt_agent* ag, const kt_forest* f, const uint64
     for (int ep = 0; ep < hp->epochs; ++ep) {
         if (ep > 0) refresh_weights(e, ag);
         const DenseWeights& w = ag->dw;
-        gemm<false, true>(e, int(T), h, n, X, n, w.w1, n, H1, h, kEpiBiasTanh, w.b1);
-        gemm<false, true>(e, int(T), g2, h, H1, h, w.w2, h, H2, g2, kEpiBiasTanh, w.b2);
-        gemm<false, true>(e, int(T), n3, g2, H2, g2, w.w3, g2, Z, n3, kEpiBias, w.b3);
+        tc_gemm(e, false, true, int(T), h, n, X, n, w.w1, n, H1, h, kEpiBiasTanh, w.b1, nullptr, 0, 1);
+        tc_gemm(e, false, true, int(T), g2, h, H1, h, w.w2, h, H2, g2, kEpiBiasTanh, w.b2, nullptr, 0, 1);
+        tc_gemm(e, false, true, int(T), n3, g2, H2, g2, w.w3, g2, Z, n3, kEpiBias, w.b3, nullptr, 0, 1);
         e->pre_launch("ppo_rows");
         ppo_rows_kernel<<<nb, 256, 0, e->stream>>>(Z, n3, n, T, ac_c, lp_c, adv, ret, hp->clip, hp->value_coef,
                                                     hp->entropy_coef, dZ, terms);
         e->check_launch("ppo_rows");
         wgrad(e, n3, g2, T, dZ, n3, H2, g2, gw3);
         colsum(e, dZ, T, n3, n3, gb3);
-        gemm<false, false>(e, int(T), g2, n3, dZ, n3, w.w3, g2, dP2, g2, kEpiTanhDeriv, nullptr, H2, g2);
+        tc_gemm(e, false, false, int(T), g2, n3, dZ, n3, w.w3, g2, dP2, g2, kEpiTanhDeriv, nullptr, H2, g2, 1);
         wgrad(e, g2, h, T, dP2, g2, H1, h, gw2);
         colsum(e, dP2, T, g2, g2, gb2);
-        gemm<false, false>(e, int(T), h, g2, dP2, g2, w.w2, h, dP1, h, kEpiTanhDeriv, nullptr, H1, h);
+        tc_gemm(e, false, false, int(T), h, g2, dP2, g2, w.w2, h, dP1, h, kEpiTanhDeriv, nullptr, H1, h, 1);
         wgrad(e, h, n, T, dP1, h, X, n, gw1);
         colsum(e, dP1, T, h, h, gb1);
         e->pre_launch("gather_grads");
