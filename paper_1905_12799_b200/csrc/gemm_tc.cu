@@ -7,7 +7,8 @@
 // One CTA (128 threads) owns a 128 x BN output tile whose fp32 accumulator
 // lives in TMEM.  K is consumed in chunks of 32: all threads stage the chunk
 // into shared memory in the canonical no-swizzle UMMA layout (umma.cuh), split
-// into tf32 hi and lo parts; one thread issues hi*hi + hi*lo + lo*hi for each
+// into tf32 hi and lo parts (MN-major global operands are transposed while
+// staging, so the tensor core always reads K-major tiles); one thread issues hi*hi + hi*lo + lo*hi for each
 // of the 4 k-groups (12 tcgen05.mma), committing to an mbarrier.  Two stage
 // buffers let the next chunk's loads overlap the tensor core.  The dropped
 // lo*lo term is 2^-22 relative, so products are fp32-accurate; accumulation is
@@ -70,24 +71,20 @@ __device__ __forceinline__ void stage_tile(float* hi, float* lo, const float* G,
             *reinterpret_cast<float4*>(lo + off) = l;
         }
     } else {
-        // MN-major: global G[(k0 + k) * ld + r0 + r]
-        const int nvec = (rows / 4) * kTcBK;
+        // MN-major in global memory (G[(k0 + k) * ld + r0 + r]): transposed while staging.
+        // Lanes walk r (coalesced 4-byte loads), each thread gathers 4 consecutive k
+        // and writes one 16-byte K-major chunk (conflict-free across the warp).
+        const int nvec = rows * (kTcBK / 4);
         for (int f = threadIdx.x; f < nvec; f += kTcThreads) {
-            const int k = f / (rows / 4), rq = f % (rows / 4);
-            const int gk = k0 + k, gr = r0 + 4 * rq;
+            const int r = f % rows, kq = f / rows;
+            const int gr = r0 + r, gk = k0 + 4 * kq;
             float v[4] = {0.f, 0.f, 0.f, 0.f};
-            if (gk < klimit) {
-                const float* src = G + size_t(gk) * ld + gr;
-                if (vec_ok && gr + 3 < rlimit) {
-                    const float4 q = *reinterpret_cast<const float4*>(src);
-                    v[0] = q.x, v[1] = q.y, v[2] = q.z, v[3] = q.w;
-                } else {
+            if (gr < rlimit) {
 #pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        if (gr + e < rlimit) v[e] = src[e];
-                }
+                for (int e = 0; e < 4; ++e)
+                    if (gk + e < klimit) v[e] = G[size_t(gk + e) * ld + gr];
             }
-            const int off = (k >> 3) * (rows / 4) * 32 + rq * 32 + (k & 7) * 4;
+            const int off = kq * rows * 4 + (r >> 3) * 32 + (r & 7) * 4;
             float4 h, l;
             umma::split_tf32(v[0], h.x, l.x);
             umma::split_tf32(v[1], h.y, l.y);
@@ -99,10 +96,9 @@ __device__ __forceinline__ void stage_tile(float* hi, float* lo, const float* G,
     }
 }
 
-template <bool MN_MAJOR>
+// Shared tiles are always K-major (canonical no-swizzle layout, umma.cuh).
 __device__ __forceinline__ uint64_t tile_desc(uint32_t base, int rows, int j) {
-    if (!MN_MAJOR) return umma::smem_desc(base + uint32_t(2 * j * rows * 16), uint32_t(rows * 16), 128u);
-    return umma::smem_desc(base + uint32_t(j * (rows / 4) * 128), uint32_t((rows / 4) * 128), 128u);
+    return umma::smem_desc(base + uint32_t(2 * j * rows * 16), uint32_t(rows * 16), 128u);
 }
 
 template <bool TA, bool TB>
@@ -110,7 +106,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(TcGemmArgs g) {
     extern __shared__ __align__(1024) unsigned char s_dyn[];
     __shared__ uint64_t mma_bar[2];
     __shared__ uint32_t tmem_slot;
-    constexpr bool A_MN = TA, B_MN = !TB;
+    constexpr bool A_MN = TA, B_MN = !TB;  // global-memory majorness (staging transposes MN-major)
     const int BN = g.BN;
     float* base = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(s_dyn) + 1023) & ~uintptr_t(1023));
     const int a_floats = kTcBM * kTcBK, b_floats = BN * kTcBK;
@@ -131,7 +127,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(TcGemmArgs g) {
     __syncthreads();
     umma::fence_after();
     const uint32_t tmem = tmem_slot;
-    const uint32_t idesc = umma::idesc_tf32(BN, A_MN, B_MN);
+    const uint32_t idesc = umma::idesc_tf32(BN, false, false);
     const bool a_vec = (g.lda % 4) == 0 && (reinterpret_cast<uintptr_t>(g.A) % 16) == 0;
     const bool b_vec = (g.ldb % 4) == 0 && (reinterpret_cast<uintptr_t>(g.B) % 16) == 0;
 
@@ -151,8 +147,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(TcGemmArgs g) {
             const uint32_t bh = umma::smem_addr(b_hi), bl = umma::smem_addr(b_lo);
 #pragma unroll
             for (int j = 0; j < kTcBK / 8; ++j) {
-                const uint64_t dah = tile_desc<A_MN>(ah, kTcBM, j), dal = tile_desc<A_MN>(al, kTcBM, j);
-                const uint64_t dbh = tile_desc<B_MN>(bh, BN, j), dbl = tile_desc<B_MN>(bl, BN, j);
+                const uint64_t dah = tile_desc(ah, kTcBM, j), dal = tile_desc(al, kTcBM, j);
+                const uint64_t dbh = tile_desc(bh, BN, j), dbl = tile_desc(bl, BN, j);
                 umma::mma_tf32(tmem, dah, dbh, idesc, (c | j) != 0);
                 umma::mma_tf32(tmem, dah, dbl, idesc, 1u);
                 umma::mma_tf32(tmem, dal, dbh, idesc, 1u);

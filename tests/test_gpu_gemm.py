@@ -34,4 +34,5 @@ def test_gemm_layouts(ta, tb, shape):
     want = A.astype(np.float64) @ B.astype(np.float64)
     scale = np.abs(A).astype(np.float64) @ np.abs(B).astype(np.float64)
     err = np.abs(C - want) / np.maximum(scale, 1e-30)
-    assert err.max() < 2e-6, err.max()  # fp32-accurate (plain TF32 would be ~1e-3)
+    # fp32-accurate products (plain TF32 would be ~1e-3); fp32 accumulation error grows ~sqrt(K)
+    assert err.max() < 1e-6 + 1e-7 * np.sqrt(K), err.max()
