@@ -5,11 +5,12 @@
 //   A(m,k) = TA ? A[k*lda + m] (MN-major) : A[m*lda + k] (K-major)
 //   B(k,n) = TB ? B[n*ldb + k] (K-major)  : B[k*ldb + n] (MN-major)
 // One CTA (128 threads) owns a 128 x BN output tile whose fp32 accumulator
-// lives in TMEM.  K is consumed in chunks of 32: all threads stage the chunk
+// lives in TMEM.  K is consumed in chunks of 16: all threads stage the chunk
 // into shared memory in the canonical no-swizzle UMMA layout (umma.cuh), split
 // into tf32 hi and lo parts (MN-major global operands are transposed while
-// staging, so the tensor core always reads K-major tiles); one thread issues hi*hi + hi*lo + lo*hi for each
-// of the 4 k-groups (12 tcgen05.mma), committing to an mbarrier.  Two stage
+// staging, so the tensor core always reads K-major tiles); one thread issues
+// hi*hi + hi*lo + lo*hi for each of the 2 k-groups (6 tcgen05.mma), committing
+// to an mbarrier.  Two stage
 // buffers let the next chunk's loads overlap the tensor core.  The dropped
 // lo*lo term is 2^-22 relative, so products are fp32-accurate; accumulation is
 // fp32 in TMEM.  The epilogue (bias + tanh, tanh derivative, or split-K
@@ -21,7 +22,7 @@
 
 namespace kt {
 
-constexpr int kTcBM = 128, kTcBK = 32, kTcThreads = 128;
+constexpr int kTcBM = 128, kTcBK = 16, kTcThreads = 128;
 
 struct TcGemmArgs {
     int M, N, K;
@@ -35,7 +36,7 @@ struct TcGemmArgs {
     const float* bias;
     const float* aux;
     int ldaux;
-    int kchunk;  // K range per blockIdx.z (multiple of 32)
+    int kchunk;  // K range per blockIdx.z (multiple of kTcBK)
     int BN;      // tile N (multiple of 16, <= 128)
 };
 
@@ -102,7 +103,7 @@ __device__ __forceinline__ uint64_t tile_desc(uint32_t base, int rows, int j) {
 }
 
 template <bool TA, bool TB>
-__global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(TcGemmArgs g) {
+__global__ void __launch_bounds__(kTcThreads, 3) tc_gemm_kernel(TcGemmArgs g) {
     extern __shared__ __align__(1024) unsigned char s_dyn[];
     __shared__ uint64_t mma_bar[2];
     __shared__ uint32_t tmem_slot;
@@ -160,8 +161,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(TcGemmArgs g) {
     if (nchunks > 0) umma::mbar_wait(umma::smem_addr(&mma_bar[(nchunks - 1) & 1]), uint32_t((nchunks - 1) >> 1) & 1u);
     umma::fence_after();
 
-    // ---- epilogue: thread (warp w, lane l) owns output row m0 + 32w + l
-    const int m = m0 + warp * 32 + (tid & 31);
+    // ---- epilogue: each warp drains its 32 TMEM lanes (rows) 32 columns at a time,
+    // transposes through shared memory (the stage buffers are free now) and writes
+    // full 128-byte row segments, applying bias / tanh / tanh' per element.
+    const int lane = tid & 31;
+    float* scratch = base + warp * (32 * 33);
     float* Cz = g.C + size_t(blockIdx.z) * size_t(g.M) * g.ldc;
     for (int c0 = 0; c0 < BN; c0 += 32) {
         float v[32];
@@ -171,21 +175,25 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(TcGemmArgs g) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = 0.f;
         }
-        if (m < g.M) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const int n = n0 + c0 + i;
-                if (c0 + i >= BN || n >= g.N) continue;
-                float x = v[i];
-                if (g.epi == 1) x = tanhf(x + g.bias[n]);
-                else if (g.epi == 3) x = x + g.bias[n];
-                else if (g.epi == 2) {
-                    const float h = g.aux[size_t(m) * g.ldaux + n];
-                    x = x * (1.0f - h * h);
-                }
-                Cz[size_t(m) * g.ldc + n] = x;
+        for (int i = 0; i < 32; ++i) scratch[lane * 33 + i] = v[i];
+        __syncwarp();
+        const int n = n0 + c0 + lane;
+        const bool col_ok = c0 + lane < BN && n < g.N;
+        const float bias = col_ok && (g.epi == 1 || g.epi == 3) ? g.bias[n] : 0.f;
+        for (int r = 0; r < 32; ++r) {
+            const int mm = m0 + warp * 32 + r;
+            if (mm >= g.M || !col_ok) continue;
+            float x = scratch[r * 33 + lane];
+            if (g.epi == 1) x = tanhf(x + bias);
+            else if (g.epi == 3) x = x + bias;
+            else if (g.epi == 2) {
+                const float h = g.aux[size_t(mm) * g.ldaux + n];
+                x = x * (1.0f - h * h);
             }
+            Cz[size_t(mm) * g.ldc + n] = x;
         }
+        __syncwarp();
     }
     umma::fence_before();
     __syncthreads();

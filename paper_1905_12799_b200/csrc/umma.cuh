@@ -103,12 +103,15 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// fp32 -> (hi, lo) with hi = tf32(x) (round to nearest), lo = x - hi (exact)
+// fp32 -> (hi, lo): hi = tf32(x), lo = tf32(x - hi), both rounded to nearest, so the
+// tensor core (which ignores the low 13 mantissa bits) sees them exactly;
+// |x - hi - lo| <= 2^-23 |x|.
 __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
-    uint32_t h;
+    uint32_t h, l;
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
     hi = __uint_as_float(h);
-    lo = x - hi;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(x - hi));
+    lo = __uint_as_float(l);
 }
 
 }  // namespace umma
