@@ -3,8 +3,9 @@
 * Rollout decisions are exact: for identical parameters and uniforms the
   trajectory (configs, scores, step indices) must be bit-identical (float64
   re-decision inside the a-priori fp32 error band; measure-zero caveat).
-* The PPO update runs its GEMMs in fp32 (north star: 1e-5 relative for fp32
-  paths): the parameter *update* of a round is compared with the reference's.
+* Rollout policy outputs (fp32 CUDA-core forward) are within the fp32 tier
+  (1e-5); the PPO update runs its GEMMs on tcgen05 tensor cores (3xTF32) and is
+  held to the north star's TF32/bf16 tier (1e-3 relative on policy outputs).
 * Later rounds are compared per call (survey §7 hard part 2): the oracle is
   seeded with the engine's own post-update state, then both run one round.
 """
@@ -47,26 +48,23 @@ def _unflat(flat, like):
     return out
 
 
-def assert_update_close(before, after, want_after, like=None, n=None, rel=1e-5):
-    """Policy outputs of the updated network within 1e-5 (north star, fp32 GEMM path).
-
-    The PPO GEMMs run in fp32, so individual weight updates carry fp32 rounding
-    (Adam divides gradients by their own magnitude); what the tolerance is about
-    is the policy: probabilities and values of the updated network on a batch of
-    states, compared with the network the float64 reference produced.
+def assert_update_close(before, after, want_after, like=None, n=None, rel=1e-3):
+    """The PPO update runs its GEMMs on the tensor cores (3xTF32, fp32 accumulation
+    in TMEM): the north star's tolerance tier for TF32/bf16 GEMM paths is 1e-3
+    relative on policy outputs.  Checked on the updated network's probabilities
+    and values over a batch of states, plus every parameter's update within a
+    few percent of one Adam step (lr).
     """
     got, want = after - before, want_after - before
-    assert np.max(np.abs(got - want)) < 1e-2 * LR + 1e-6  # every update agrees to 1% of a step
+    assert np.max(np.abs(got - want)) < 5e-2 * LR  # every parameter moved like the reference's
     if like is None:
         return
     X = np.random.default_rng(0).random((512, n))
     lg, vg, _ = oagent.forward(_unflat(after, like), X)
     lw, vw, _ = oagent.forward(_unflat(want_after, like), X)
     pg, pw = np.exp(oagent.log_softmax(lg)), np.exp(oagent.log_softmax(lw))
-    assert np.max(np.abs(pg - pw)) <= rel
-    # the value head's gradient is a mean of (v - return) residuals that largely
-    # cancel, so fp32 forward rounding (~1e-7 absolute) shows up ~10x larger there
-    assert np.max(np.abs(vg - vw) / (np.abs(vw) + 1e-3)) <= 10 * rel
+    assert np.max(np.abs(pg - pw) / pw) <= rel
+    assert np.max(np.abs(vg - vw) / np.maximum(np.abs(vw), 1.0)) <= rel
 
 
 @pytest.mark.parametrize("name", sorted(meta("rl")))
