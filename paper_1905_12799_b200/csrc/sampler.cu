@@ -424,11 +424,7 @@ struct LloydArgs {
     int it0, it_end, max_iters;
     int64_t stride;            // per-run row stride of assign/bounds (m rounded up to 16)
     uint8_t* assign;           // [R][stride], 255 = unassigned
-    float2* bounds;            // [R][stride] (u, l) when last refreshed
-    uint8_t* t0;               // [R][stride] pass of that refresh
-    float* tile_exp;           // [R][tstride] per 32-point tile: budget G up to which it is settled
-    int64_t tstride;
-    double* hist;              // [(2K + R)][kHist] cumulative drifts per pass: own (K), max-other (K), budget (R)
+    float2* bounds;            // [R][stride] (u, l)
     double* cent;              // [K][8] centroids of the latest pass
     const uint64_t* init_rows; // k-means++ rows (prefix shared by all runs)
     long long* S;              // [K][9] running sums
@@ -442,7 +438,7 @@ struct LloydArgs {
 };
 
 struct LloydLayout {
-    size_t S, c64, c32, delta, drift, cum, total;
+    size_t S, c64, c32, delta, drift, total;
 };
 
 __host__ __device__ inline LloydLayout lloyd_layout(int K) {
@@ -458,14 +454,16 @@ __host__ __device__ inline LloydLayout lloyd_layout(int K) {
     o += size_t(K) * kSumW * 4;
     L.drift = o;
     o += size_t(K) * 4;
-    o = (o + 7) & ~size_t(7);
-    L.cum = o;  // cur_d[K], cur_m[K], cur_g[kMaxRuns] (double)
-    o += (size_t(2) * K + kMaxRuns) * 8;
     L.total = (o + 15) & ~size_t(15);
     return L;
 }
 
-constexpr int kHist = 101;  // passes 0..99 (+1 spare)
+struct LloydQueueEntry {
+    uint32_t point;
+    int32_t old;
+    float u, l;
+};
+constexpr int kLloydThreads = 256;
 
 struct RunShared {
     unsigned int cnt[kMaxRuns][3];
@@ -555,6 +553,7 @@ __global__ void __launch_bounds__(256, 3) lloyd_kernel(LloydArgs a) {
     extern __shared__ __align__(16) unsigned char s_dyn[];
     __shared__ RunShared rs;
     __shared__ uint8_t run_of[kMaxClusters];
+    __shared__ LloydQueueEntry wqueue[kLloydThreads / 32 * 128];
     // the dynamic window is only guaranteed 8-byte aligned after static smem (tools add their
     // own static smem): align explicitly for the float4 centroid loads (16 spare bytes allocated)
     unsigned char* s_raw = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(s_dyn) + 15) & ~uintptr_t(15));
@@ -564,9 +563,6 @@ __global__ void __launch_bounds__(256, 3) lloyd_kernel(LloydArgs a) {
     float* c32 = reinterpret_cast<float*>(s_raw + L.c32);
     int* delta = reinterpret_cast<int*>(s_raw + L.delta);
     float* drift = reinterpret_cast<float*>(s_raw + L.drift);
-    double* cur_d = reinterpret_cast<double*>(s_raw + L.cum);
-    double* cur_m = cur_d + a.K;
-    double* cur_g = cur_m + a.K;
     cg::grid_group grid = cg::this_grid();
     const int tid = threadIdx.x;
     const int K = a.K, R = a.R, n = a.n;
@@ -574,8 +570,6 @@ __global__ void __launch_bounds__(256, 3) lloyd_kernel(LloydArgs a) {
 
     for (int i = tid; i < K * kSumW; i += blockDim.x) S[i] = a.S[i];
     for (int i = tid; i < K * kMaxKnobs; i += blockDim.x) c64[i] = a.cent[i];  // centroids of the previous pass
-    for (int i = tid; i < 2 * K + R; i += blockDim.x)  // running drift sums up to the previous pass
-        (i < 2 * K ? cur_d[i] : cur_g[i - 2 * K]) = a.it0 > 0 ? a.hist[size_t(i) * kHist + a.it0 - 1] : 0.0;
     if (tid < R) rs.state[tid] = a.run_state[tid];
     if (tid < kMaxRuns * 3) rs.cnt[tid / 3][tid % 3] = 0;
     for (int r = 0; r < R; ++r)
@@ -639,109 +633,106 @@ __global__ void __launch_bounds__(256, 3) lloyd_kernel(LloydArgs a) {
             rs.amax[tid] = am;
         }
         __syncthreads();
-        // running drift sums through this pass (identical in every block; block 0 records them)
-        for (int g = tid; g < K; g += blockDim.x) {
-            const int r = run_of[g];
-            if (!run_active(rs.state[r])) continue;
-            cur_d[g] += double(drift[g]);
-            cur_m[g] += double(g - a.coff[r] == rs.amax[r] ? rs.m2[r] : rs.m1[r]);
-            if (blockIdx.x == 0) {
-                a.hist[size_t(g) * kHist + it] = cur_d[g];
-                a.hist[size_t(K + g) * kHist + it] = cur_m[g];
-            }
-        }
-        if (tid < R && run_active(rs.state[tid])) {
-            cur_g[tid] += 2.0 * double(rs.m1[tid]);
-            if (blockIdx.x == 0) a.hist[size_t(2 * K + tid) * kHist + it] = cur_g[tid];
-        }
-        __syncthreads();
 
         stamp(1);
-        // ---- assignment pass over warp tiles of 32 points.  A tile whose stored
-        // slack (min over its points of l - u when last refreshed at budget G0)
-        // exceeds the global drift budget accumulated since (G - G0, with
-        // G = 2 * sum of per-pass max drift) is skipped without touching its
-        // points.  Otherwise each lane re-checks its point with per-cluster
-        // cumulative drifts (Hamerly), tightens the upper bound or re-evaluates
-        // in full, and the tile's bounds and slack are refreshed.
-        {
-            const int lane = tid & 31;
-            const int64_t ntiles = (m + 31) >> 5;
-            const int64_t wstride = int64_t(gridDim.x) * (blockDim.x >> 5);
-            for (int64_t tile = int64_t(blockIdx.x) * (blockDim.x >> 5) + (tid >> 5); tile < ntiles; tile += wstride) {
-                const int64_t p = (tile << 5) + lane;
-                const bool valid = p < m;
-                uint64_t row = 0;
-                bool have_row = false;
-                float p32[kMaxKnobs];
-                for (int r = 0; r < R; ++r) {
-                    const int st = rs.state[r];
-                    if (!run_active(st)) continue;
-                    const bool bounded = st == kActiveFromSums;
-                    const double gnow = cur_g[r];
-                    if (bounded && gnow < double(a.tile_exp[int64_t(r) * a.tstride + tile])) {
-                        if (a.stats && lane == 0) atomicAdd(&rs.cnt[r][0], 32u);
-                        continue;  // every point of the tile provably keeps its cluster
-                    }
-                    const int co = a.coff[r];
-                    const int64_t slot = int64_t(r) * a.stride + p;
-                    const int old = valid ? int(a.assign[slot]) : 255;
-                    float u = 0.f, l = INFINITY;
-                    int j = old;
-                    bool work = valid;
-                    if (valid && bounded && old != 255) {
-                        const float2 b = a.bounds[slot];
-                        const int t0 = a.t0[slot];
-                        const int g = co + old;
-                        const double du = cur_d[g] - a.hist[size_t(g) * kHist + t0];
-                        const double dm = cur_m[g] - a.hist[size_t(K + g) * kHist + t0];
-                        u = __double2float_ru(double(b.x) + du * (1.0 + 1e-12));
-                        l = __double2float_rd(double(b.y) - dm * (1.0 + 1e-12));
-                        if (surely_less(u, l)) {
-                            work = false;
-                            if (a.stats) atomicAdd(&rs.cnt[r][0], 1u);
-                        }
-                    }
-                    if (work) {
-                        if (!have_row) {
-                            row = a.pts[p];
-                            unpack_row(row, p32);
-                            have_row = true;
-                        }
-                        bool done = false;
-                        if (bounded && old != 255) {
-                            u = dist_up(f32_d2(p32, c32 + (co + old) * kMaxKnobs));
-                            if (surely_less(u, l)) {
-                                done = true;
-                                if (a.stats) atomicAdd(&rs.cnt[r][1], 1u);
-                            }
-                        }
-                        if (!done) {
-                            j = full_assign(c32 + co * kMaxKnobs, c64 + co * kMaxKnobs, row, p32, a.k[r], n, u, l);
-                            if (a.stats) atomicAdd(&rs.cnt[r][2], 1u);
-                        }
-                    }
-                    if (valid) {
-                        a.bounds[slot] = make_float2(u, l);
-                        a.t0[slot] = uint8_t(it);
-                        if (j != old) {
-                            a.assign[slot] = uint8_t(j);
-                            rs.changed[r] = 1;
-                            int* dn = delta + (co + j) * kSumW;
-                            for (int i = 0; i < n; ++i) atomicAdd(dn + i, row_byte(row, i));
-                            atomicAdd(dn + 8, 1);
-                            if (old != 255) {
-                                int* dold = delta + (co + old) * kSumW;
-                                for (int i = 0; i < n; ++i) atomicSub(dold + i, row_byte(row, i));
-                                atomicSub(dold + 8, 1);
-                            }
-                        }
-                    }
-                    float slack = valid ? __fsub_rd(l, __fadd_ru(u, 1e-6f * (u + 1.0f))) : INFINITY;
+        // ---- assignment pass.  Per warp and round: each lane filters 4 consecutive
+        // points with its Hamerly bounds; the points the bounds cannot settle are
+        // queued in shared memory and then evaluated by all 32 lanes together.
+        const int64_t nq = (m + 3) >> 2;
+        const int64_t gstride = int64_t(gridDim.x) * blockDim.x;
+        const int64_t q_end = (nq + gstride - 1) / gstride * gstride;  // warp-uniform trip count
+        const int lane = tid & 31;
+        LloydQueueEntry* queue = wqueue + (tid >> 5) * 128;
+        for (int64_t q = int64_t(blockIdx.x) * blockDim.x + tid; q < q_end; q += gstride) {
+            const int64_t p0 = q << 2;
+            const int cnt = q < nq ? int(m - p0 < 4 ? m - p0 : 4) : 0;
+            for (int r = 0; r < R; ++r) {
+                const int st = rs.state[r];
+                if (!run_active(st)) continue;
+                const int co = a.coff[r];
+                uint8_t* as_r = a.assign + int64_t(r) * a.stride;
+                float2* bd_r = a.bounds + int64_t(r) * a.stride;
+                unsigned todo = 0;  // bit e: point e needs distance work
+                uint32_t as4 = 0xffffffffu;
+                float bu[4] = {0.f, 0.f, 0.f, 0.f}, bl[4] = {0.f, 0.f, 0.f, 0.f};
+                if (cnt > 0) {
+                    as4 = *reinterpret_cast<const uint32_t*>(as_r + p0);
+                    if (st == kActiveFromSums) {
+                        const float4 b01 = reinterpret_cast<const float4*>(bd_r)[q * 2];
+                        const float4 b23 = reinterpret_cast<const float4*>(bd_r)[q * 2 + 1];
+                        bu[0] = b01.x, bl[0] = b01.y, bu[1] = b01.z, bl[1] = b01.w;
+                        bu[2] = b23.x, bl[2] = b23.y, bu[3] = b23.z, bl[3] = b23.w;
+                        const float m1 = rs.m1[r], m2 = rs.m2[r];
+                        const int am = rs.amax[r];
 #pragma unroll
-                    for (int off = 16; off; off >>= 1) slack = fminf(slack, __shfl_xor_sync(0xffffffffu, slack, off));
-                    if (lane == 0) a.tile_exp[int64_t(r) * a.tstride + tile] = __double2float_rd(gnow + double(slack));
+                        for (int e = 0; e < 4; ++e) {
+                            const int old = (as4 >> (8 * e)) & 0xff;
+                            if (e >= cnt) continue;
+                            if (old == 255) {
+                                todo |= 1u << e;
+                                continue;
+                            }
+                            bu[e] = __fadd_ru(bu[e], drift[co + old]);
+                            bl[e] = __fsub_rd(bl[e], old == am ? m2 : m1);
+                            if (!surely_less(bu[e], bl[e])) todo |= 1u << e;
+                        }
+                        // settled points keep their widened bounds (queued ones are rewritten below)
+                        reinterpret_cast<float4*>(bd_r)[q * 2] = make_float4(bu[0], bl[0], bu[1], bl[1]);
+                        reinterpret_cast<float4*>(bd_r)[q * 2 + 1] = make_float4(bu[2], bl[2], bu[3], bl[3]);
+                    } else {
+                        todo = (1u << cnt) - 1u;
+                    }
                 }
+                // warp-level compaction of the unsettled points
+                int base = 0;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const bool mine = (todo >> e) & 1u;
+                    const unsigned bal = __ballot_sync(0xffffffffu, mine);
+                    if (mine) {
+                        LloydQueueEntry& qe = queue[base + __popc(bal & ((1u << lane) - 1u))];
+                        qe.point = uint32_t(p0 + e);
+                        qe.old = (as4 >> (8 * e)) & 0xff;
+                        qe.u = bu[e];
+                        qe.l = bl[e];
+                    }
+                    base += __popc(bal);
+                }
+                __syncwarp();
+                const bool bounded = st == kActiveFromSums;
+                for (int i = lane; i < base; i += 32) {
+                    const LloydQueueEntry qe = queue[i];
+                    const uint64_t row = __ldg(a.pts + qe.point);
+                    float p[kMaxKnobs];
+                    unpack_row(row, p);
+                    const int old = qe.old;
+                    float u = qe.u, l = qe.l;
+                    int j = -1;
+                    if (bounded && old != 255) {
+                        u = dist_up(f32_d2(p, c32 + (co + old) * kMaxKnobs));
+                        if (surely_less(u, l)) j = old;
+                    }
+                    if (a.stats) atomicAdd(&rs.cnt[r][j < 0 ? 2 : 1], 1u);
+                    if (j < 0) j = full_assign(c32 + co * kMaxKnobs, c64 + co * kMaxKnobs, row, p, a.k[r], n, u, l);
+                    bd_r[qe.point] = make_float2(u, l);
+                    if (j != old) {
+                        as_r[qe.point] = uint8_t(j);
+                        rs.changed[r] = 1;
+                        int* dn = delta + (co + j) * kSumW;
+                        for (int c = 0; c < n; ++c) atomicAdd(dn + c, row_byte(row, c));
+                        atomicAdd(dn + 8, 1);
+                        if (old != 255) {
+                            int* dold = delta + (co + old) * kSumW;
+                            for (int c = 0; c < n; ++c) atomicSub(dold + c, row_byte(row, c));
+                            atomicSub(dold + 8, 1);
+                        }
+                    }
+                }
+                if (a.stats) {
+                    const unsigned valid = __reduce_add_sync(0xffffffffu, unsigned(cnt));
+                    if (lane == 0) atomicAdd(&rs.cnt[r][0], valid - unsigned(base));
+                }
+                __syncwarp();
             }
         }
         __syncthreads();
@@ -958,10 +949,6 @@ struct KmeansSession {
         a.timeline = want_timeline ? static_cast<long long*>(e->scratch("km.timeline", 400 * 8)) : nullptr;
         double* d_loss = static_cast<double*>(e->scratch("km.loss", kMaxRuns * 8));
         a.bounds = static_cast<float2*>(e->scratch("km.bounds", size_t(R) * a.stride * sizeof(float2)));
-        a.t0 = static_cast<uint8_t*>(e->scratch("km.t0", size_t(R) * a.stride));
-        a.tstride = ceil_div(m, 32);
-        a.tile_exp = static_cast<float*>(e->scratch("km.tile_exp", size_t(R) * a.tstride * 4));
-        a.hist = static_cast<double*>(e->scratch("km.hist", (size_t(2) * K + R) * kHist * 8));
         a.init_rows = cent_rows;
         KT_CUDA(cudaMemsetAsync(a.assign, 0xff, size_t(R) * a.stride, e->stream));
         KT_CUDA(cudaMemsetAsync(a.S, 0, size_t(K) * kSumW * 8, e->stream));
