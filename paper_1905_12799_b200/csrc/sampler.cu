@@ -459,6 +459,7 @@ __host__ __device__ inline LloydLayout lloyd_layout(int K) {
 }
 
 struct LloydQueueEntry {
+    uint64_t row;
     uint32_t point;
     int32_t old;
     float u, l;
@@ -646,6 +647,17 @@ __global__ void __launch_bounds__(256, 3) lloyd_kernel(LloydArgs a) {
         for (int64_t q = int64_t(blockIdx.x) * blockDim.x + tid; q < q_end; q += gstride) {
             const int64_t p0 = q << 2;
             const int cnt = q < nq ? int(m - p0 < 4 ? m - p0 : 4) : 0;
+            // the quad's rows are fetched with its state (one round trip) and ride in the queue
+            uint64_t rw[4] = {0, 0, 0, 0};
+            if (cnt == 4) {
+                const ulonglong2 v0 = __ldg(reinterpret_cast<const ulonglong2*>(a.pts + p0));
+                const ulonglong2 v1 = __ldg(reinterpret_cast<const ulonglong2*>(a.pts + p0 + 2));
+                rw[0] = v0.x, rw[1] = v0.y, rw[2] = v1.x, rw[3] = v1.y;
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if (e < cnt) rw[e] = a.pts[p0 + e];
+            }
             for (int r = 0; r < R; ++r) {
                 const int st = rs.state[r];
                 if (!run_active(st)) continue;
@@ -691,6 +703,7 @@ __global__ void __launch_bounds__(256, 3) lloyd_kernel(LloydArgs a) {
                     const unsigned bal = __ballot_sync(0xffffffffu, mine);
                     if (mine) {
                         LloydQueueEntry& qe = queue[base + __popc(bal & ((1u << lane) - 1u))];
+                        qe.row = rw[e];
                         qe.point = uint32_t(p0 + e);
                         qe.old = (as4 >> (8 * e)) & 0xff;
                         qe.u = bu[e];
@@ -702,7 +715,7 @@ __global__ void __launch_bounds__(256, 3) lloyd_kernel(LloydArgs a) {
                 const bool bounded = st == kActiveFromSums;
                 for (int i = lane; i < base; i += 32) {
                     const LloydQueueEntry qe = queue[i];
-                    const uint64_t row = __ldg(a.pts + qe.point);
+                    const uint64_t row = qe.row;
                     float p[kMaxKnobs];
                     unpack_row(row, p);
                     const int old = qe.old;
