@@ -430,6 +430,7 @@ struct LloydArgs {
     long long* S;              // [K][9] running sums
     unsigned long long* D;     // [3][K][9] per-pass deltas
     unsigned int* chg;         // [3][kMaxRuns]
+    unsigned int* work;        // [3] per-pass chunk counters
     int* run_state;            // [R]
     int* run_iter;             // [R]
     int* ctrl;                 // [0] next iteration
@@ -640,11 +641,16 @@ __global__ void __launch_bounds__(256, 3) lloyd_kernel(LloydArgs a) {
         // points with its Hamerly bounds; the points the bounds cannot settle are
         // queued in shared memory and then evaluated by all 32 lanes together.
         const int64_t nq = (m + 3) >> 2;
-        const int64_t gstride = int64_t(gridDim.x) * blockDim.x;
-        const int64_t q_end = (nq + gstride - 1) / gstride * gstride;  // warp-uniform trip count
         const int lane = tid & 31;
         LloydQueueEntry* queue = wqueue + (tid >> 5) * 128;
-        for (int64_t q = int64_t(blockIdx.x) * blockDim.x + tid; q < q_end; q += gstride) {
+        // warps grab 32-quad chunks from a per-pass counter: work-balanced passes
+        unsigned int* work = a.work + (it % 3);
+        while (true) {
+            unsigned int chunk = 0;
+            if (lane == 0) chunk = atomicAdd(work, 32u);
+            chunk = __shfl_sync(0xffffffffu, chunk, 0);
+            if (int64_t(chunk) >= nq) break;
+            const int64_t q = int64_t(chunk) + lane;
             const int64_t p0 = q << 2;
             const int cnt = q < nq ? int(m - p0 < 4 ? m - p0 : 4) : 0;
             // the quad's rows are fetched with its state (one round trip) and ride in the queue
@@ -760,6 +766,7 @@ __global__ void __launch_bounds__(256, 3) lloyd_kernel(LloydArgs a) {
             const int nb = (it + 1) % 3;
             for (int i = tid; i < K * kSumW; i += blockDim.x) a.D[size_t(nb) * K * kSumW + i] = 0ull;
             if (tid < kMaxRuns) a.chg[nb * kMaxRuns + tid] = 0u;
+            if (tid == 0) a.work[nb] = 0u;
         }
         stamp(2);
         grid.sync();
@@ -949,6 +956,7 @@ struct KmeansSession {
         a.S = static_cast<long long*>(e->scratch("km.S", size_t(K) * kSumW * 8));
         a.D = static_cast<unsigned long long*>(e->scratch("km.D", size_t(3) * K * kSumW * 8));
         a.chg = static_cast<unsigned int*>(e->scratch("km.chg", 3 * kMaxRuns * 4));
+        a.work = static_cast<unsigned int*>(e->scratch("km.work", 16));
         a.run_state = static_cast<int*>(e->scratch("km.state", kMaxRuns * 4));
         a.run_iter = static_cast<int*>(e->scratch("km.iter", kMaxRuns * 4));
         a.ctrl = static_cast<int*>(e->scratch("km.ctrl", 16));
@@ -982,6 +990,7 @@ struct KmeansSession {
         while (true) {
             KT_CUDA(cudaMemsetAsync(a.D, 0, size_t(3) * K * kSumW * 8, e->stream));
             KT_CUDA(cudaMemsetAsync(a.chg, 0, 3 * kMaxRuns * 4, e->stream));
+            KT_CUDA(cudaMemsetAsync(a.work, 0, 16, e->stream));
             a.it0 = it;
             a.it_end = history ? it + 1 : a.max_iters;
             void* params[] = {&a};
