@@ -314,6 +314,31 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         dist.destroy_process_group()
 
 
+def run_rl(args, rank: int, world: int, local_rank: int) -> None:
+    import torch
+
+    import paper_1905_12799_b200 as kt
+    from tools import bench_rl
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+
+    line = bench_rl.run(args, rank, world, local_rank, kt, torch, dist, {"barrier": barrier, "clock": ClockSampler})
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -325,12 +350,16 @@ def main() -> None:
     ap.add_argument("--ref-sample", type=int, default=16384)
     ap.add_argument("--ref-procs", type=int, default=0, help="host processes for --impl reference (0: all cores)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", choices=("s2", "rl"), default="s2",
+                    help="s2: the headline scored+clustered step; rl: 5 tasks x 4096 PPO agents per step")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
     if args.impl == "reference":
         run_reference(args, rank, world)
+    elif args.workload == "rl":
+        run_rl(args, rank, world, local_rank)
     else:
         run_ours(args, rank, world, local_rank)
 

@@ -322,7 +322,22 @@ def gen_rl(models):
     return arrays, meta
 
 
+def make_task_models():
+    """Surrogates for the ResNet-18 conv tasks used by the RL bench mode (data/models/)."""
+    from paper_1905_12799_b200.workloads import RESNET18_TASKS
+
+    out = ROOT / "data" / "models"
+    for i, task in enumerate(RESNET18_TASKS[:5]):
+        space = space_from_dict(task.space_dict())
+        land = gen_landscape(space, seed=100 + i)
+        model = landscape_model(space, land, 500, 200 + i)
+        doc = {"values": values_of(space), "model": json.loads(model.to_json()), "space": space.name,
+               "landscape": landscape_to_dict(land)}
+        (out / f"resnet18_task{i}.json").write_text(json.dumps(doc, sort_keys=True))
+
+
 def main():
+    make_task_models()
     rng = np.random.default_rng(20261017)
     out_models: dict = {}
     models, lands = make_models(out_models)

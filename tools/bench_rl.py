@@ -1,0 +1,134 @@
+"""bench.py --workload rl: the PPO + adaptive-sampling tuning step (configs[1]-shaped).
+
+Per step and rank: 5 independent ResNet-18 conv tasks, each runs one search round
+with 4096 PPO agents (K1 rollout, K2 scoring, K4 GAE, K5 PPO update) followed by
+adaptive_sample on its trajectory (K6/K7/K8/K9).  Metric: trajectory candidates
+scored + clustered per second.  (AlexNet's 5 tasks need knob cardinalities > 255,
+outside the engine's uint8 row layout; the ResNet-18 tasks have the same shape.)
+"""
+
+from __future__ import annotations
+
+import json
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent.parent
+N_TASKS, AGENTS = 5, 4096
+
+
+def task_docs():
+    return [json.loads((ROOT / "data" / "models" / f"resnet18_task{i}.json").read_text()) for i in range(N_TASKS)]
+
+
+def cpu_rl_step(docs, rng_seed: int, agents: int):
+    """Reference algorithm (oracle numpy port) for one step on `agents` agents per task."""
+    from oracle import agent as oagent
+    from oracle import sampler as osamp
+
+    n_cand = 0
+    for i, d in enumerate(docs):
+        cards = np.array([len(v) for v in d["values"]])
+        hyper = dict(oagent.DEFAULT_HYPER, episodes_per_round=agents)
+        ag = oagent.new_agent(len(cards), hyper, seed=i)
+        starts = np.random.default_rng(rng_seed + i).integers(0, cards, size=(agents, cards.size))
+        idx, scores, steps = oagent.search_round(ag, d["model"], d["values"], starts, hyper)
+        osamp.adaptive_sample(idx, set(), cards.tolist(), rng_seed + i)
+        n_cand += len(idx)
+    return n_cand
+
+
+def run(args, rank: int, world: int, local_rank: int, kt, torch, dist, helpers) -> dict | None:
+    """GPU arm; returns the JSON line (rank 0) or None."""
+    sp = kt.space
+    docs = task_docs()
+    eng = kt.engine(local_rank)
+    dev = f"cuda:{local_rank}"
+    tasks = []
+    for i, d in enumerate(docs):
+        space = kt.space_from_dict({"name": d["space"], "knobs": [{"name": f"k{j}", "values": v}
+                                                                   for j, v in enumerate(d["values"])]})
+        model = kt.CostModel.from_dict(d["model"])
+        agent = kt.init_agent(space, kt.AgentHyperparams(episodes_per_round=AGENTS), seed=1000 * rank + i)
+        cards = np.array(space.cardinalities)
+        host_starts = [torch.from_numpy(sp.pack(np.random.default_rng(100 * rank + 10 * i + s)
+                                                .integers(0, cards, size=(AGENTS, cards.size))).view(np.int64))
+                       .pin_memory() for s in range(2)]
+        tasks.append((space, model, agent, host_starts))
+    no_visited = np.zeros(0, dtype=np.uint64)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step(s, e2e_batch=None):
+        n = 0
+        for space, model, agent, host_starts in tasks:
+            with eng.scope():
+                starts = host_starts[s % 2].to(dev, non_blocking=True)
+            rows, scores, _ = kt.run_search_rows(agent, model, space, starts, engine=eng)
+            batch = kt.adaptive_sample_rows(rows, no_visited, space, seed=s, engine=eng)
+            n += int(rows.numel())
+            if e2e_batch is not None:
+                e2e_batch.append(batch.nbytes)
+        return n
+
+    for w in range(args.warmup):
+        step(w)
+    helpers["barrier"]()
+    launches0 = eng.launches
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    n_total = 0
+    d2h = []
+    with helpers["clock"](local_rank) as clk:
+        helpers["barrier"]()
+        for s in range(args.steps):
+            flush.fill_(float(s))
+            with eng.scope():
+                ev[s][0].record(eng.stream)
+            n_total += step(s, d2h)
+            with eng.scope():
+                ev[s][1].record(eng.stream)
+        helpers["barrier"]()
+    launches = eng.launches - launches0
+    t = sum(a.elapsed_time(b) for a, b in ev) / 1e3
+    eng.set_timing(True)
+    eng.kernel_stats(reset=True)
+    step(0)
+    stats = eng.kernel_stats(reset=True)
+    eng.set_timing(False)
+    times = torch.tensor([t, float(n_total)], dtype=torch.float64, device=dev)
+    if dist is not None:
+        tt = times.clone()
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        nn = times.clone()
+        dist.all_reduce(nn, op=dist.ReduceOp.SUM)
+        t, n_total = float(tt[0]), float(nn[1])
+    if rank != 0:
+        return None
+    value = n_total / t
+    # host-to-device starts and device-to-host batches are inside the timed region (e2e == value here)
+    base = None
+    if not args.no_cpu_baseline:
+        t0 = time.perf_counter()
+        nc = cpu_rl_step(docs, 7, 256)
+        dt = time.perf_counter() - t0
+        base = {"value": nc / dt, "unit": "candidates/s", "cores": 1, "kind": "port",
+                "sample": f"{N_TASKS} tasks x 256 agents (oracle numpy port of run_search_round + adaptive_sample), "
+                          f"{dt:.1f} s"}
+    dom = max(stats.items(), key=lambda kv: kv[1][1])
+    return {
+        "metric": "candidate configs scored+clustered/sec per tuning step", "value": value, "unit": "candidates/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+fp32/tf32", "data": "synthetic",
+        "config": {"workload": f"{N_TASKS} ResNet-18 conv tasks x {AGENTS} PPO agents per step: run_search_round "
+                               f"(rollout, scoring, GAE, 3 PPO epochs) + adaptive_sample per task",
+                   "candidates_per_step": n_total / args.steps / world, "parallelism": f"tasks x{world}",
+                   "l2": "flushed between steps"},
+        "e2e": {"value": value, "unit": "candidates/s", "h2d_bytes_per_step": N_TASKS * AGENTS * 8,
+                "d2h_bytes_per_step": int(sum(d2h) / max(1, args.steps))},
+        "gpu_launches": int(launches),
+        "kernels": {k: {"launches": c, "ms": round(ms, 3)} for k, (c, ms) in sorted(stats.items(), key=lambda kv: -kv[1][1])},
+        "roofline": {"bound": "tensor" if dom[0] == "tc_gemm" else "hbm", "kernel": dom[0], "achieved": None,
+                     "peak": None, "unit": None, "frac": None, "traffic": None},
+        "clocks": clk.summary(), "cpu_baseline": base,
+    }
