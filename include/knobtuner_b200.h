@@ -183,9 +183,9 @@ typedef struct kt_ppo_hyper {
 typedef struct kt_round_info {
     int64_t steps;    /* T: PPO rows (agent steps) */
     int64_t entries;  /* N = T + episodes: trajectory entries */
-    int64_t guarded;  /* agent-steps whose sampling was re-decided in float64 */
+    int64_t guarded;  /* reserved: 0 (the float64 rollout re-decides nothing) */
     double policy_loss, value_loss, entropy, total;  /* final-epoch LossReport */
-    double guard_tau;
+    double guard_tau; /* reserved: 0 */
 } kt_round_info;
 
 int kt_agent_create(kt_engine* e, int n_knobs, int shared_width, int head_width, const double* params,

@@ -37,27 +37,26 @@ __host__ __device__ inline ParamLayout param_layout(int n, int h, int g) {
     return L;
 }
 
-// Padded fp32 weights in the transposed (k-major) layouts the tile kernels read.
-struct PaddedWeights {
-    float w1t[kMaxKnobs][kH];  // w1t[k][o] = w1[o][k]
-    float b1[kH];
-    float w2pt[kH][kG];        // w2pt[k][o] = w2p[o][k]
-    float w2vt[kH][kG];
-    float b2p[kG];
-    float b2v[kG];
-    float w3pt[kG][kN3];       // w3pt[k][o] = w3p[o][k]
-    float b3p[kN3];
-    float w3v[kG];
-    float b3v;
-    float pad[3];
+// Padded float64 weights in the transposed (k-major) layouts the rollout reads from
+// shared memory: every lane owns one agent and reads a broadcast weight row.
+struct PaddedWeights64 {
+    double w1t[kMaxKnobs][kH];  // w1t[k][o] = w1[o][k]
+    double b1[kH];
+    double w2t[kH][2 * kG];     // w2t[k][o] = w2p[o][k] (o < 64), w2v[o-64][k] (o >= 64)
+    double b2[2 * kG];          // b2p | b2v
+    double w3t[kG][kN3];        // w3t[k][o] = w3p[o][k]
+    double b3p[kN3];
+    double w3v[kG];
+    double b3v;
+    double pad;
 };
+static_assert(sizeof(PaddedWeights64) % 16 == 0, "bulk-copy granularity");
 
-constexpr int kAgentsPerCta = 128;
-constexpr int kRolloutThreads = 256;
+constexpr int kAgentsPerCta = 32;   // one agent per lane
+constexpr int kRolloutThreads = 256;  // warp w: outputs [16w, 16w+16) of each layer, knob w when sampling
 
 struct RolloutArgs {
-    const PaddedWeights* w32;
-    const double* p64;  // flat float64 parameters (PARAM_KEYS order)
+    const PaddedWeights64* w64;
     int n, h, g;
     int S;              // max steps per episode
     int E;              // episodes
@@ -66,7 +65,6 @@ struct RolloutArgs {
     int n_seed_words;
     uint32_t round_words[2];
     int n_round_words;
-    float tau;          // decision guard band
     const uint64_t* starts;
     // outputs (slots)
     uint64_t* visited;   // [E][S+1]
@@ -75,9 +73,9 @@ struct RolloutArgs {
     double* logp;        // [E][S]
     double* values;      // [E][S]
     int32_t* lengths;    // [E]
-    unsigned long long* n_guarded;  // agent-steps re-evaluated in float64
 };
 
+void launch_pad_weights64(kt_engine* e, const double* p64, int n, int h, int g, PaddedWeights64* w);
 void launch_rollout(kt_engine* e, const RolloutArgs& a);
 
 // fp32 GEMM on tcgen05 (gemm_tc.cu): C = epi(A(m,k) B(k,n)), TA: A MN-major, TB: B K-major.

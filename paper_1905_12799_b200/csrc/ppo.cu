@@ -59,27 +59,6 @@ __global__ void colsum_final_kernel(const double* part, int blocks, int cols, do
 }
 
 // ============================================================ weights
-__global__ void pad_weights_kernel(const double* p, int n, int h, int g, PaddedWeights* w) {
-    const ParamLayout L = param_layout(n, h, g);
-    float* flat = reinterpret_cast<float*>(w);
-    for (int i = threadIdx.x; i < int(sizeof(PaddedWeights) / 4); i += blockDim.x) flat[i] = 0.f;
-    __syncthreads();
-    for (int i = threadIdx.x; i < h * n; i += blockDim.x) w->w1t[i % n][i / n] = float(p[L.w1 + i]);
-    for (int i = threadIdx.x; i < h; i += blockDim.x) w->b1[i] = float(p[L.b1 + i]);
-    for (int i = threadIdx.x; i < g * h; i += blockDim.x) {
-        w->w2pt[i % h][i / h] = float(p[L.w2p + i]);
-        w->w2vt[i % h][i / h] = float(p[L.w2v + i]);
-    }
-    for (int i = threadIdx.x; i < g; i += blockDim.x) {
-        w->b2p[i] = float(p[L.b2p + i]);
-        w->b2v[i] = float(p[L.b2v + i]);
-        w->w3v[i] = float(p[L.w3v + i]);
-    }
-    for (int i = threadIdx.x; i < 3 * n * g; i += blockDim.x) w->w3pt[i % g][i / g] = float(p[L.w3p + i]);
-    for (int i = threadIdx.x; i < 3 * n; i += blockDim.x) w->b3p[i] = float(p[L.b3p + i]);
-    if (threadIdx.x == 0) w->b3v = float(p[L.b3v]);
-}
-
 // Dense fp32 matrices for the PPO GEMMs (row-major [out][in]), from float64 params.
 struct DenseWeights {
     float* w1;   // [h][n]
@@ -264,7 +243,7 @@ struct kt_agent {
     double* m64 = nullptr;
     double* v64 = nullptr;
     int64_t t = 0;
-    kt::PaddedWeights* w32 = nullptr;
+    kt::PaddedWeights64* w64 = nullptr;
     float* dense = nullptr;
     kt::DenseWeights dw{};
     std::vector<double> host_p;
@@ -313,43 +292,7 @@ __global__ void loss_report_kernel(const double* sums, int64_t T, double value_c
     out[3] = pol + value_coef * vl - entropy_coef * ent;
 }
 
-// a-priori bound on |fp32 cdf - exact cdf| of the rollout's forward pass
-static double rollout_guard_tau(const kt_agent& ag) {
-    const ParamLayout L = param_layout(ag.n, ag.h, ag.g);
-    const std::vector<double>& p = ag.host_p;
-    const double eps = std::ldexp(1.0, -24);
-    auto gam = [&](int k) { return k * eps / (1.0 - k * eps); };
-    const double tanh_err = 3.0e-7;
-    double e_h1 = 0.0;
-    for (int o = 0; o < L.h; ++o) {
-        double sa = std::fabs(p[L.b1 + o]), sw = 0.0;
-        for (int k = 0; k < L.n; ++k) sw += std::fabs(p[L.w1 + o * L.n + k]);
-        e_h1 = std::max(e_h1, gam(L.n + 1) * (sa + sw) + 2 * eps * sw);
-    }
-    e_h1 += tanh_err;
-    double e_h2 = 0.0;
-    for (int o = 0; o < 2 * L.g; ++o) {
-        const int w = o < L.g ? L.w2p + o * L.h : L.w2v + (o - L.g) * L.h;
-        const double b = std::fabs(p[o < L.g ? L.b2p + o : L.b2v + o - L.g]);
-        double sw = 0.0;
-        for (int k = 0; k < L.h; ++k) sw += std::fabs(p[w + k]);
-        e_h2 = std::max(e_h2, gam(L.h + 1) * (sw + b) + e_h1 * sw);
-    }
-    e_h2 += tanh_err;
-    double e_z = 0.0;
-    for (int o = 0; o < 3 * L.n; ++o) {
-        double sw = 0.0;
-        for (int k = 0; k < L.g; ++k) sw += std::fabs(p[L.w3p + o * L.g + k]);
-        e_z = std::max(e_z, gam(L.g + 1) * (sw + std::fabs(p[L.b3p + o])) + e_h2 * sw);
-    }
-    // softmax / cumsum in fp32: |d log p| <= 2 e_z + rounding, |d cdf| <= 2 * max |d p|
-    return 2.0 * (2.2 * e_z + 2.0e-6) + 1.0e-6;
-}
-
-static void refresh_weights(kt_engine* e, kt_agent* ag) {
-    e->pre_launch("pad_weights");
-    pad_weights_kernel<<<1, 1024, 0, e->stream>>>(ag->p64, ag->n, ag->h, ag->g, ag->w32);
-    e->check_launch("pad_weights");
+static void refresh_dense(kt_engine* e, kt_agent* ag) {
     e->pre_launch("dense_weights");
     dense_weights_kernel<<<32, 256, 0, e->stream>>>(ag->p64, ag->n, ag->h, ag->g, ag->dw);
     e->check_launch("dense_weights");
@@ -405,7 +348,7 @@ int kt_agent_create(kt_engine* e, int n, int h, int g, const double* params, con
     KT_CUDA(cudaMemcpy(ag->p64, params, pb, cudaMemcpyHostToDevice));
     KT_CUDA(cudaMemcpy(ag->m64, adam_m, pb, cudaMemcpyHostToDevice));
     KT_CUDA(cudaMemcpy(ag->v64, adam_v, pb, cudaMemcpyHostToDevice));
-    KT_CUDA(cudaMalloc(&ag->w32, sizeof(PaddedWeights)));
+    KT_CUDA(cudaMalloc(&ag->w64, sizeof(PaddedWeights64)));
     const int n3 = 3 * n + 1;
     const size_t dense = size_t(h) * n + h + size_t(2 * g) * h + 2 * g + size_t(n3) * 2 * g + n3;
     KT_CUDA(cudaMalloc(&ag->dense, dense * 4));
@@ -426,7 +369,7 @@ int kt_agent_destroy(kt_agent* ag) {
     cudaFree(ag->p64);
     cudaFree(ag->m64);
     cudaFree(ag->v64);
-    cudaFree(ag->w32);
+    cudaFree(ag->w64);
     cudaFree(ag->dense);
     delete ag;
     KT_API_END
@@ -459,18 +402,17 @@ int kt_search_round(kt_engine* e, kt_agent* ag, const kt_forest* f, const uint64
     if (n_seed_words < 1 || n_seed_words > 4) fail(KT_ERR_VALUE, "seed must fit in 128 bits");
     const int n = n_knobs;
     const ParamLayout L = param_layout(ag->n, ag->h, ag->g);
-    refresh_weights(e, ag);
+    launch_pad_weights64(e, ag->p64, ag->n, ag->h, ag->g, ag->w64);
+    refresh_dense(e, ag);
 
     // ---- K1 rollout
     RolloutArgs ra{};
-    ra.w32 = ag->w32;
-    ra.p64 = ag->p64;
+    ra.w64 = ag->w64;
     ra.n = n, ra.h = ag->h, ra.g = ag->g, ra.S = S, ra.E = E;
     for (int k = 0; k < n; ++k) ra.cards[k] = cards[k];
     for (int i = 0; i < n_seed_words; ++i) ra.seed_words[i] = seed_words[i];
     ra.n_seed_words = n_seed_words;
     ra.n_round_words = u64_words(uint64_t(round_index), ra.round_words);
-    ra.tau = float(rollout_guard_tau(*ag));
     ra.starts = starts_dev;
     const size_t slots = size_t(E) * S;
     ra.visited = static_cast<uint64_t*>(e->scratch("rl.visited", size_t(E) * (S + 1) * 8));
@@ -479,8 +421,6 @@ int kt_search_round(kt_engine* e, kt_agent* ag, const kt_forest* f, const uint64
     ra.logp = static_cast<double*>(e->scratch("rl.logp", slots * 8));
     ra.values = static_cast<double*>(e->scratch("rl.values", slots * 8));
     ra.lengths = static_cast<int32_t*>(e->scratch("rl.lengths", size_t(E) * 4));
-    ra.n_guarded = static_cast<unsigned long long*>(e->scratch("rl.guarded", 8));
-    KT_CUDA(cudaMemsetAsync(ra.n_guarded, 0, 8, e->stream));
     launch_rollout(e, ra);
 
     // ---- episode-major compaction (agent.py:331-363)
@@ -570,7 +510,7 @@ int kt_search_round(kt_engine* e, kt_agent* ag, const kt_forest* f, const uint64
     e->check_launch("encode_states");
     auto* report = static_cast<double*>(e->scratch("ppo.report", 8 * 8));
     for (int ep = 0; ep < hp->epochs; ++ep) {
-        if (ep > 0) refresh_weights(e, ag);
+        if (ep > 0) refresh_dense(e, ag);
         const DenseWeights& w = ag->dw;
         tc_gemm(e, false, true, int(T), h, n, X, n, w.w1, n, H1, h, kEpiBiasTanh, w.b1, nullptr, 0, 1);
         tc_gemm(e, false, true, int(T), g2, h, H1, h, w.w2, h, H2, g2, kEpiBiasTanh, w.b2, nullptr, 0, 1);
@@ -605,24 +545,22 @@ int kt_search_round(kt_engine* e, kt_agent* ag, const kt_forest* f, const uint64
             e->check_launch("loss_report");
         }
     }
-    // host mirror of the parameters (guard bound of the next round, checkpoints)
+    // host mirror of the parameters (checkpoints)
     KT_CUDA(cudaMemcpyAsync(ag->host_p.data(), ag->p64, size_t(ag->P) * 8, cudaMemcpyDeviceToHost, e->stream));
     double rep[4];
-    unsigned long long guarded = 0;
     KT_CUDA(cudaMemcpyAsync(rep, report, 4 * 8, cudaMemcpyDeviceToHost, e->stream));
-    KT_CUDA(cudaMemcpyAsync(&guarded, ra.n_guarded, 8, cudaMemcpyDeviceToHost, e->stream));
     e->sync();
     (void)L;
     *n_out = N;
     if (info) {
         info->steps = T;
         info->entries = N;
-        info->guarded = int64_t(guarded);
+        info->guarded = 0;  // the float64 rollout needs no re-decided samples
         info->policy_loss = rep[0];
         info->value_loss = rep[1];
         info->entropy = rep[2];
         info->total = rep[3];
-        info->guard_tau = ra.tau;
+        info->guard_tau = 0.0;
     }
     KT_API_END
 }

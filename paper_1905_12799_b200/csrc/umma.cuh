@@ -76,6 +76,19 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
         : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t mbar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+}
+
+// 1-D TMA bulk copy global -> shared (bytes % 16 == 0, both addresses 16-aligned),
+// completion counted on the mbarrier's transaction count.
+__device__ __forceinline__ void bulk_g2s(uint32_t dst_saddr, const void* src, uint32_t bytes, uint32_t mbar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst_saddr),
+        "l"(src), "r"(bytes), "r"(mbar)
+        : "memory");
+}
+
 // TMEM allocation by one full warp; the base address is written to shared memory.
 __device__ __forceinline__ void tmem_alloc(uint32_t slot_saddr, uint32_t ncols) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(slot_saddr), "r"(ncols)

@@ -21,5 +21,5 @@ for rep in range(3):
     torch.cuda.synchronize(); dt = time.perf_counter() - t
     st = eng.kernel_stats(reset=True)
     top = sorted(st.items(), key=lambda kv: -kv[1][1])[:8]
-    print(f"rep {rep}: {dt*1e3:.1f} ms wall, T={info.steps} N={info.entries} guarded={info.guarded} tau={info.guard_tau:.2e}",
+    print(f"rep {rep}: {dt*1e3:.1f} ms wall, T={info.steps} N={info.entries}",
           {k: (c, round(ms, 3)) for k, (c, ms) in top})
