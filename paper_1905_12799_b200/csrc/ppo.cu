@@ -38,24 +38,57 @@ __global__ void reduce_splits_kernel(const float* part, int splits, int64_t coun
     }
 }
 
-// column sums of X[rows][cols] (fp32) -> out (float64): fixed row blocks, then fixed-order combine
+// Column sums of X[rows][cols] -> out (float64), deterministic two-level order:
+// block b sums rows [b*R, (b+1)*R) — warp w takes rows r = w (mod 8), lanes take
+// columns — then the 8 warp sums combine in warp order; the final kernel sums the
+// block partials of one column by a fixed strided split and a fixed smem tree.
+constexpr int kColsumRows = 512;
+
 template <class Tv>
-__global__ void colsum_partial_kernel(const Tv* X, int64_t rows, int cols, int ld, int64_t rows_per_block,
-                                      double* part) {
-    const int64_t r0 = int64_t(blockIdx.x) * rows_per_block, r1 = min(rows, r0 + rows_per_block);
-    for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+__global__ void __launch_bounds__(256) colsum_partial_kernel(const Tv* __restrict__ X, int64_t rows, int cols, int ld,
+                                                             double* __restrict__ part) {
+    __shared__ double red[8][33];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t r0 = int64_t(blockIdx.x) * kColsumRows, r1 = min(rows, r0 + kColsumRows);
+    for (int c0 = 0; c0 < cols; c0 += 32) {
+        const int c = c0 + lane;
         double s = 0.0;
-        for (int64_t r = r0; r < r1; ++r) s += double(X[size_t(r) * ld + c]);
-        part[size_t(blockIdx.x) * cols + c] = s;
+        if (c < cols) {
+            int64_t r = r0 + warp;
+            for (; r + 24 < r1; r += 32) {  // four independent loads in flight
+                const double x0 = double(X[size_t(r) * ld + c]), x1 = double(X[size_t(r + 8) * ld + c]);
+                const double x2 = double(X[size_t(r + 16) * ld + c]), x3 = double(X[size_t(r + 24) * ld + c]);
+                s += x0;
+                s += x1;
+                s += x2;
+                s += x3;
+            }
+            for (; r < r1; r += 8) s += double(X[size_t(r) * ld + c]);
+        }
+        red[warp][lane] = s;
+        __syncthreads();
+        if (warp == 0 && c < cols) {
+            double t = red[0][lane];
+            for (int w = 1; w < 8; ++w) t += red[w][lane];
+            part[size_t(blockIdx.x) * cols + c] = t;
+        }
+        __syncthreads();
     }
 }
 
-__global__ void colsum_final_kernel(const double* part, int blocks, int cols, double* out) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= cols) return;
+__global__ void __launch_bounds__(256) colsum_final_kernel(const double* __restrict__ part, int blocks, int cols,
+                                                           double* __restrict__ out) {
+    __shared__ double red[256];
+    const int c = blockIdx.x;
     double s = 0.0;
-    for (int b = 0; b < blocks; ++b) s += part[size_t(b) * cols + c];
-    out[c] = s;
+    for (int b = threadIdx.x; b < blocks; b += 256) s += part[size_t(b) * cols + c];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[c] = red[0];
 }
 
 // ============================================================ weights
@@ -300,14 +333,13 @@ static void refresh_dense(kt_engine* e, kt_agent* ag) {
 
 template <class Tv>
 static void colsum(kt_engine* e, const Tv* X, int64_t rows, int cols, int ld, double* out) {
-    const int64_t per = 2048;
-    const int blocks = int(std::max<int64_t>(1, ceil_div(rows, per)));
+    const int blocks = int(std::max<int64_t>(1, ceil_div(rows, kColsumRows)));
     auto* part = static_cast<double*>(e->scratch("ppo.colsum", size_t(blocks) * cols * 8));
     e->pre_launch("colsum");
-    colsum_partial_kernel<Tv><<<blocks, 128, 0, e->stream>>>(X, rows, cols, ld, per, part);
+    colsum_partial_kernel<Tv><<<blocks, 256, 0, e->stream>>>(X, rows, cols, ld, part);
     e->check_launch("colsum");
     e->pre_launch("colsum_final");
-    colsum_final_kernel<<<int(ceil_div(cols, 128)), 128, 0, e->stream>>>(part, blocks, cols, out);
+    colsum_final_kernel<<<cols, 256, 0, e->stream>>>(part, blocks, cols, out);
     e->check_launch("colsum_final");
 }
 

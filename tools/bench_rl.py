@@ -128,7 +128,7 @@ def run(args, rank: int, world: int, local_rank: int, kt, torch, dist, helpers) 
                 "d2h_bytes_per_step": int(sum(d2h) / max(1, args.steps))},
         "gpu_launches": int(launches),
         "kernels": {k: {"launches": c, "ms": round(ms, 3)} for k, (c, ms) in sorted(stats.items(), key=lambda kv: -kv[1][1])},
-        "roofline": {"bound": "tensor" if dom[0] == "tc_gemm" else "hbm", "kernel": dom[0], "achieved": None,
+        "roofline": {"bound": "tensor" if dom[0].startswith("tc_gemm") else "hbm", "kernel": dom[0], "achieved": None,
                      "peak": None, "unit": None, "frac": None, "traffic": None},
         "clocks": clk.summary(), "cpu_baseline": base,
     }
