@@ -48,6 +48,15 @@ constexpr int kMaxKnobs = 8;      // a row is one uint64: knob i in byte i
 constexpr int kMaxCard = 255;     // index 255 never occurs -> usable as a sentinel
 constexpr uint64_t kEmptyRow = ~0ull;
 
+// Align a pointer into dynamic shared memory by pointer arithmetic on the shared
+// array itself, so the compiler keeps the shared address space (LDS/STS).  Casting
+// through uintptr_t would turn every access into a generic LD/ST.
+template <unsigned ALIGN>
+__device__ __forceinline__ unsigned char* align_shared(unsigned char* p) {
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p));
+    return p + ((ALIGN - (a & (ALIGN - 1))) & (ALIGN - 1));
+}
+
 __host__ __device__ __forceinline__ int row_byte(uint64_t row, int i) {
     return int((row >> (8 * i)) & 0xffu);
 }

@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(kTcThreads, 3) tc_gemm_kernel(TcGemmArgs g) {
     __shared__ uint32_t tmem_slot;
     constexpr bool A_MN = TA, B_MN = !TB;  // global-memory majorness (staging transposes MN-major)
     const int BN = g.BN;
-    float* base = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(s_dyn) + 1023) & ~uintptr_t(1023));
+    float* base = reinterpret_cast<float*>(align_shared<1024>(s_dyn));
     const int a_floats = kTcBM * kTcBK, b_floats = BN * kTcBK;
     const int stage_floats = 2 * a_floats + 2 * b_floats;  // A hi, A lo, B hi, B lo
     const int tid = threadIdx.x, warp = tid >> 5;

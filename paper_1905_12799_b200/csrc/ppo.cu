@@ -30,11 +30,32 @@ namespace kt {
 enum Epi : int { kEpiNone = 0, kEpiBiasTanh = 1, kEpiTanhDeriv = 2, kEpiBias = 3 };
 
 // out[i] (float64) = sum_z part[z][i] in z order
-__global__ void reduce_splits_kernel(const float* part, int splits, int64_t count, double* out) {
-    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x) {
-        double s = 0.0;
-        for (int z = 0; z < splits; ++z) s += double(part[size_t(z) * count + i]);
-        out[i] = s;
+// out[i] = sum over split-K partials, fixed order: warp w sums splits z = w (mod 8)
+// for the block's 32 elements (lanes), then the 8 warp sums combine in warp order.
+__global__ void __launch_bounds__(256) reduce_splits_kernel(const float* __restrict__ part, int splits, int64_t count,
+                                                            double* __restrict__ out) {
+    __shared__ double red[8][33];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t i = int64_t(blockIdx.x) * 32 + lane;
+    double s = 0.0;
+    if (i < count) {
+        int z = warp;
+        for (; z + 24 < splits; z += 32) {
+            const double x0 = part[size_t(z) * count + i], x1 = part[size_t(z + 8) * count + i];
+            const double x2 = part[size_t(z + 16) * count + i], x3 = part[size_t(z + 24) * count + i];
+            s += x0;
+            s += x1;
+            s += x2;
+            s += x3;
+        }
+        for (; z < splits; z += 8) s += double(part[size_t(z) * count + i]);
+    }
+    red[warp][lane] = s;
+    __syncthreads();
+    if (warp == 0 && i < count) {
+        double t = red[0][lane];
+        for (int w = 1; w < 8; ++w) t += red[w][lane];
+        out[i] = t;
     }
 }
 
@@ -346,13 +367,14 @@ static void colsum(kt_engine* e, const Tv* X, int64_t rows, int cols, int ld, do
 // weight gradient out[M][N] (float64) = A^T B over T rows, deterministic split-K
 static void wgrad(kt_engine* e, int M, int N, int64_t T, const float* A, int lda, const float* B, int ldb,
                   double* out) {
-    const int splits = int(std::min<int64_t>(4096, std::max<int64_t>(1, ceil_div(T, 1024))));
+    // split-K so the grid fills ~6 CTAs per SM (148 SMs), each split >= 256 rows
+    const int tiles = int(ceil_div(M, 128) * ceil_div(N, 128));
+    const int splits = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(T, 256), 888 / tiles)));
     auto* part = static_cast<float*>(e->scratch("ppo.wgrad", size_t(splits) * M * N * 4));
     tc_gemm(e, true, false, M, N, int(T), A, lda, B, ldb, part, N, kEpiNone, nullptr, nullptr, 0, splits);
     const int64_t count = int64_t(M) * N;
     e->pre_launch("reduce_splits");
-    reduce_splits_kernel<<<int(std::min<int64_t>(1024, ceil_div(count, 256))), 256, 0, e->stream>>>(part, splits,
-                                                                                                     count, out);
+    reduce_splits_kernel<<<int(ceil_div(count, 32)), 256, 0, e->stream>>>(part, splits, count, out);
     e->check_launch("reduce_splits");
 }
 

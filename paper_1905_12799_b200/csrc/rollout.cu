@@ -44,7 +44,7 @@ struct RolloutSmem {
 
 __global__ void __launch_bounds__(kRolloutThreads, 1) rollout_kernel(RolloutArgs a) {
     extern __shared__ unsigned char s_raw[];
-    RolloutSmem& sm = *reinterpret_cast<RolloutSmem*>((reinterpret_cast<uintptr_t>(s_raw) + 127) & ~uintptr_t(127));
+    RolloutSmem& sm = *reinterpret_cast<RolloutSmem*>(align_shared<128>(s_raw));
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int n = a.n;
     const uint32_t mbar = umma::smem_addr(&sm.mbar);

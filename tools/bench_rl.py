@@ -60,13 +60,17 @@ def run(args, rank: int, world: int, local_rank: int, kt, torch, dist, helpers) 
     no_visited = np.zeros(0, dtype=np.uint64)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
-    def step(s, e2e_batch=None):
+    def step(s, e2e_batch=None, infos=None):
         n = 0
         for space, model, agent, host_starts in tasks:
             with eng.scope():
                 starts = host_starts[s % 2].to(dev, non_blocking=True)
             rows, scores, _ = kt.run_search_rows(agent, model, space, starts, engine=eng)
-            batch = kt.adaptive_sample_rows(rows, no_visited, space, seed=s, engine=eng)
+            info = kt._lib.SampleInfo() if infos is not None else None
+            batch = kt.adaptive_sample_rows(rows, no_visited, space, seed=s, engine=eng, info=info)
+            if infos is not None:
+                infos.append({"entries": int(rows.numel()), "distinct": int(info.n_distinct), "k": int(info.chosen_k),
+                              "lloyd_passes": int(info.lloyd_passes), "lloyd_launches": int(info.lloyd_launches)})
             n += int(rows.numel())
             if e2e_batch is not None:
                 e2e_batch.append(batch.nbytes)
@@ -93,7 +97,8 @@ def run(args, rank: int, world: int, local_rank: int, kt, torch, dist, helpers) 
     t = sum(a.elapsed_time(b) for a, b in ev) / 1e3
     eng.set_timing(True)
     eng.kernel_stats(reset=True)
-    step(0)
+    infos = []
+    step(0, infos=infos)
     stats = eng.kernel_stats(reset=True)
     eng.set_timing(False)
     times = torch.tensor([t, float(n_total)], dtype=torch.float64, device=dev)
@@ -127,6 +132,7 @@ def run(args, rank: int, world: int, local_rank: int, kt, torch, dist, helpers) 
         "e2e": {"value": value, "unit": "candidates/s", "h2d_bytes_per_step": N_TASKS * AGENTS * 8,
                 "d2h_bytes_per_step": int(sum(d2h) / max(1, args.steps))},
         "gpu_launches": int(launches),
+        "sample_info": infos,
         "kernels": {k: {"launches": c, "ms": round(ms, 3)} for k, (c, ms) in sorted(stats.items(), key=lambda kv: -kv[1][1])},
         "roofline": {"bound": "tensor" if dom[0].startswith("tc_gemm") else "hbm", "kernel": dom[0], "achieved": None,
                      "peak": None, "unit": None, "frac": None, "traffic": None},
