@@ -11,8 +11,13 @@
  * Conventions
  *   - Plain C types only: pointers + sizes.  "_dev" pointers are CUDA device
  *     memory on the engine's device; everything else is host memory.
- *   - A configuration is a "row": knob i's index in byte i of a uint64
- *     (n_knobs <= 8, every cardinality <= 255).  Unused high bytes are 0.
+ *   - A configuration is a "row": one uint64 holding the n_knobs (<= 8) knob
+ *     indices.  When every cardinality is <= 255 knob i's index is byte i
+ *     (unused high bytes 0); otherwise knob i occupies the bit field
+ *     [shift_i, shift_i + width_i) with width_i = max(1, bit_length(card_i - 1))
+ *     packed from bit 0 upwards, at most 63 bits in all (cards <= 65535).  Every
+ *     entry point that reads rows takes the cardinalities (directly or through
+ *     the forest / landscape handle) and derives the same layout.
  *   - Every call returns KT_OK or an error code; kt_last_error() gives the
  *     message.  Error codes map 1:1 onto the reference's exception types so
  *     the Python shim re-raises the same class with the same message
@@ -43,6 +48,10 @@ enum {
 
 const char* kt_last_error(void);
 const char* kt_version(void);
+
+/* Row layout of a space (host only, no device needed): per-knob bit shift and
+ * width, byte-per-knob when every cardinality is <= 255 (see Conventions).   */
+int kt_row_layout(const int32_t* cards, int n_knobs, int32_t* shift_out, int32_t* width_out);
 
 /* ------------------------------------------------------------------ engine */
 /* One engine per device: owns a CUDA stream and a growable device workspace. */
@@ -98,7 +107,7 @@ int kt_score_trees(kt_engine* e, const kt_forest* f, const uint64_t* rows_dev,
  * str(landscape.seed) (the blake2b payload prefix).                        */
 typedef struct kt_landscape kt_landscape;
 
-int kt_landscape_create(kt_engine* e, int n_knobs, int n_centers, const int32_t* centers,
+int kt_landscape_create(kt_engine* e, int n_knobs, const int32_t* cards, int n_centers, const int32_t* centers,
                         const double* depths, const double* radii, double base_runtime,
                         double noise_rel, const char* seed_text, kt_landscape** out);
 int kt_landscape_destroy(kt_landscape* l);
@@ -113,21 +122,21 @@ int kt_dedup(kt_engine* e, const uint64_t* rows_dev, int64_t count,
 
 /* Per-knob mode over all rows, ties -> smallest index (mode_config, sampler.py:151-158). */
 int kt_mode_vote(kt_engine* e, const uint64_t* rows_dev, int64_t count,
-                 int n_knobs, int32_t* mode_out);
+                 int n_knobs, const int32_t* cards, int32_t* mode_out);
 
 /* Seeded k-means on lattice points (kmeans, sampler.py:72-122).
  * assignment_out: host int64[m] (may be NULL); centroids_out: host double[k*n];
  * history_out: host double[100] (may be NULL: then only the final loss is
  * computed); returns the number of Lloyd passes in *n_passes.               */
 int kt_kmeans(kt_engine* e, const uint64_t* points_dev, int64_t m, int n_knobs,
-              int k, uint64_t seed, double* centroids_out, int64_t* assignment_out,
+              const int32_t* cards, int k, uint64_t seed, double* centroids_out, int64_t* assignment_out,
               double* loss_out, double* history_out, int32_t* n_passes);
 
 /* Knee scan (knee_scan, sampler.py:125-148): grows k from 8 until
  * knee_constant * L_k > L_{k-1}; returns the breaking k's clustering.
  * scanned_k/scanned_loss: host arrays of capacity 56.                       */
 int kt_knee_scan(kt_engine* e, const uint64_t* points_dev, int64_t m, int n_knobs,
-                 uint64_t seed, double knee_constant, int k_max,
+                 const int32_t* cards, uint64_t seed, double knee_constant, int k_max,
                  int32_t* scanned_k, double* scanned_loss, int32_t* n_scanned,
                  double* centroids_out /* k_max*n */, int64_t* assignment_out /* m or NULL */);
 

@@ -59,6 +59,7 @@ class PPOHyper(C.Structure):
 SIGNATURES = {
     "kt_last_error": (C.c_char_p, []),
     "kt_version": (C.c_char_p, []),
+    "kt_row_layout": (C.c_int, [pi32, C.c_int, pi32, pi32]),
     "kt_engine_create": (C.c_int, [C.c_int, C.POINTER(P)]),
     "kt_engine_destroy": (C.c_int, [P]),
     "kt_engine_set_stream": (C.c_int, [P, P]),
@@ -72,13 +73,13 @@ SIGNATURES = {
     "kt_forest_destroy": (C.c_int, [P]),
     "kt_forest_depth": (C.c_int, [P]),
     "kt_score_trees": (C.c_int, [P, P, P, i64, P]),
-    "kt_landscape_create": (C.c_int, [P, C.c_int, C.c_int, pi32, pf64, pf64, f64, f64, C.c_char_p, C.POINTER(P)]),
+    "kt_landscape_create": (C.c_int, [P, C.c_int, pi32, C.c_int, pi32, pf64, pf64, f64, f64, C.c_char_p, C.POINTER(P)]),
     "kt_landscape_destroy": (C.c_int, [P]),
     "kt_score_landscape": (C.c_int, [P, P, P, i64, P]),
     "kt_dedup": (C.c_int, [P, P, i64, P, pi64]),
-    "kt_mode_vote": (C.c_int, [P, P, i64, C.c_int, pi32]),
-    "kt_kmeans": (C.c_int, [P, P, i64, C.c_int, C.c_int, u64, pf64, pi64, pf64, pf64, pi32]),
-    "kt_knee_scan": (C.c_int, [P, P, i64, C.c_int, u64, f64, C.c_int, pi32, pf64, pi32, pf64, pi64]),
+    "kt_mode_vote": (C.c_int, [P, P, i64, C.c_int, pi32, pi32]),
+    "kt_kmeans": (C.c_int, [P, P, i64, C.c_int, pi32, C.c_int, u64, pf64, pi64, pf64, pf64, pi32]),
+    "kt_knee_scan": (C.c_int, [P, P, i64, C.c_int, pi32, u64, f64, C.c_int, pi32, pf64, pi32, pf64, pi64]),
     "kt_adaptive_sample": (C.c_int, [P, P, i64, C.c_int, pi32, pu64, i64, u64, f64, pu64, pi32,
                                      C.POINTER(SampleInfo)]),
     "kt_agent_create": (C.c_int, [P, C.c_int, C.c_int, C.c_int, pf64, pf64, pf64, i64, C.POINTER(P)]),

@@ -266,10 +266,11 @@ def run_search_round(agent, model, space, starts) -> Trajectory:
     if agent.hyper.max_steps_per_episode == 0:
         scores = predict(model, space, starts)
         agent.rounds_completed += 1
-        return Trajectory(sp.pack(idx), scores, np.zeros(len(starts), dtype=np.int64), n_knobs=len(space.knobs),
-                          config_cls=cls)
+        cards = sp.cardinalities(space)
+        return Trajectory(sp.pack(idx, cards), scores, np.zeros(len(starts), dtype=np.int64),
+                          n_knobs=len(space.knobs), config_cls=cls, cards=cards)
     engine = _lib.engine()
     with engine.scope():
-        start_rows = torch.from_numpy(sp.pack(idx).view(np.int64)).to(f"cuda:{engine.device}")
+        start_rows = torch.from_numpy(sp.pack(idx, sp.cardinalities(space)).view(np.int64)).to(f"cuda:{engine.device}")
     rows, scores, steps = run_search_rows(agent, model, space, start_rows, engine=engine)
-    return Trajectory(rows, scores, steps, n_knobs=len(space.knobs), config_cls=cls)
+    return Trajectory(rows, scores, steps, n_knobs=len(space.knobs), config_cls=cls, cards=sp.cardinalities(space))

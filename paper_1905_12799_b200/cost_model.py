@@ -195,5 +195,5 @@ def predict(model, space, configs) -> np.ndarray:
     f = device_forest(model, space, engine)
     if (idx < f.neg_prefix[None, :]).any():
         raise ValueError("featurize requires non-negative knob values")
-    rows = torch.from_numpy(sp.pack(idx).view(np.int64)).to(f"cuda:{engine.device}")
+    rows = torch.from_numpy(sp.pack(idx, sp.cardinalities(space)).view(np.int64)).to(f"cuda:{engine.device}")
     return predict_rows(model, space, rows, engine=engine).cpu().numpy()

@@ -61,6 +61,7 @@ struct RolloutArgs {
     int S;              // max steps per episode
     int E;              // episodes
     int32_t cards[kMaxKnobs];
+    RowFmt fmt;
     uint32_t seed_words[4];
     int n_seed_words;
     uint32_t round_words[2];

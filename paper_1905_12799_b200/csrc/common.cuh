@@ -44,7 +44,7 @@ void set_last_error(const std::string& msg);
     return KT_OK;
 
 // ---------------------------------------------------------------- layout
-constexpr int kMaxKnobs = 8;      // a row is one uint64: knob i in byte i
+constexpr int kMaxKnobs = 8;      // a row is one uint64 (see RowFmt)
 constexpr int kMaxCard = 255;     // index 255 never occurs -> usable as a sentinel
 constexpr uint64_t kEmptyRow = ~0ull;
 
@@ -57,9 +57,27 @@ __device__ __forceinline__ unsigned char* align_shared(unsigned char* p) {
     return p + ((ALIGN - (a & (ALIGN - 1))) & (ALIGN - 1));
 }
 
-__host__ __device__ __forceinline__ int row_byte(uint64_t row, int i) {
-    return int((row >> (8 * i)) & 0xffu);
-}
+
+// Row layout of a space: knob i occupies bits [shift[i], shift[i] + width[i]) of
+// the uint64 row.  Spaces whose cardinalities are all <= 255 use one byte per knob
+// (shift 8i, width 8: `bytes` = 1, the fast paths); wider spaces (AlexNet's
+// tile_f has 480 settings) pack minimal-width fields, sum of widths <= 64.
+struct RowFmt {
+    uint8_t shift[kMaxKnobs];
+    uint8_t width[kMaxKnobs];
+    int32_t cmax;   // largest index any knob can take (max cardinality - 1)
+    int32_t bytes;  // 1: the byte-per-knob layout
+    __host__ __device__ __forceinline__ int get(uint64_t row, int i) const {
+        return int((row >> shift[i]) & ((1ull << width[i]) - 1ull));
+    }
+    __host__ __device__ __forceinline__ uint64_t set(uint64_t row, int i, int v) const {
+        const uint64_t mask = ((1ull << width[i]) - 1ull) << shift[i];
+        return (row & ~mask) | ((uint64_t(v) << shift[i]) & mask);
+    }
+};
+
+// Same rule as paper_1905_12799_b200.space.row_layout (host side).
+RowFmt row_fmt(const int32_t* cards, int n);
 
 // ---------------------------------------------------------- numpy sums
 // numpy's pairwise_sum for a contiguous run of n <= 8 float64 values
@@ -80,24 +98,24 @@ __device__ __forceinline__ double np_sum_small(const double* t, int n) {
 }
 
 // ((p - c)**2).sum(axis=-1) for a lattice point p (row) and float64 centroid c.
-__device__ __forceinline__ double np_sq_dist(uint64_t row, const double* c, int n) {
+__device__ __forceinline__ double np_sq_dist(uint64_t row, const double* c, int n, const RowFmt& f) {
     double t[kMaxKnobs];
 #pragma unroll
     for (int i = 0; i < kMaxKnobs; ++i) {
         if (i < n) {
-            double d = __dsub_rn(double(row_byte(row, i)), c[i]);
+            double d = __dsub_rn(double(f.get(row, i)), c[i]);
             t[i] = __dmul_rn(d, d);
         }
     }
     return np_sum_small(t, n);
 }
 
-__device__ __forceinline__ int int_sq_dist(uint64_t a, uint64_t b, int n) {
-    int s = 0;
+__device__ __forceinline__ int64_t int_sq_dist(uint64_t a, uint64_t b, int n, const RowFmt& f) {
+    int64_t s = 0;
 #pragma unroll
     for (int i = 0; i < kMaxKnobs; ++i) {
         if (i < n) {
-            int d = row_byte(a, i) - row_byte(b, i);
+            const int64_t d = f.get(a, i) - f.get(b, i);
             s += d * d;
         }
     }

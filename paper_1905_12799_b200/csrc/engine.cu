@@ -1,4 +1,5 @@
 // engine.cu — engine lifetime, workspace, error plumbing, host RNG entry point.
+#include <algorithm>
 #include <cstring>
 #include <stdexcept>
 #include <vector>
@@ -18,6 +19,34 @@ int occupancy_blocks(const void* kernel, int threads, size_t smem) {
     int blocks = 0;
     KT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, threads, smem));
     return blocks;
+}
+
+RowFmt row_fmt(const int32_t* cards, int n) {
+    if (n < 1 || n > kMaxKnobs) fail(KT_ERR_UNSUPPORTED, "the engine supports spaces of 1..8 knobs");
+    RowFmt f{};
+    int maxc = 1;
+    for (int k = 0; k < n; ++k) {
+        if (cards[k] < 1) fail(KT_ERR_VALUE, "knob cardinalities must be >= 1");
+        maxc = std::max(maxc, int(cards[k]));
+    }
+    f.cmax = maxc - 1;
+    if (maxc <= kMaxCard) {  // one byte per knob
+        f.bytes = 1;
+        for (int k = 0; k < kMaxKnobs; ++k) f.shift[k] = uint8_t(8 * k), f.width[k] = 8;
+        return f;
+    }
+    if (maxc > 65535) fail(KT_ERR_UNSUPPORTED, "engine rows support knobs with at most 65535 settings");
+    int pos = 0;
+    for (int k = 0; k < n; ++k) {
+        int w = 1;
+        while ((1 << w) < cards[k]) ++w;
+        f.shift[k] = uint8_t(pos);
+        f.width[k] = uint8_t(w);
+        pos += w;
+    }
+    // bit 63 stays clear, so no row can equal the all-ones empty-slot sentinel
+    if (pos > 63) fail(KT_ERR_UNSUPPORTED, "the space's knob indices need more than 63 bits per row");
+    return f;
 }
 
 }  // namespace kt
@@ -101,6 +130,16 @@ extern "C" {
 const char* kt_last_error(void) { return kt::g_last_error.c_str(); }
 
 const char* kt_version(void) { return "knobtuner_b200 0.1 (sm_100a)"; }
+
+int kt_row_layout(const int32_t* cards, int n_knobs, int32_t* shift_out, int32_t* width_out) {
+    KT_API_BEGIN
+    const kt::RowFmt f = kt::row_fmt(cards, n_knobs);
+    for (int k = 0; k < n_knobs; ++k) {
+        shift_out[k] = f.shift[k];
+        width_out[k] = f.width[k];
+    }
+    KT_API_END
+}
 
 int kt_engine_create(int device, kt_engine** out) {
     KT_API_BEGIN

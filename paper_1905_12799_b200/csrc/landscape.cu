@@ -25,6 +25,7 @@ struct kt_landscape {
     double base = 1.0;
     double noise = 0.0;
     std::string prefix;  // str(seed) + ":"
+    kt::RowFmt fmt{};
     int32_t centers[kMaxCenters][8] = {};
     double depths[kMaxCenters] = {};
     double radii[kMaxCenters] = {};
@@ -34,6 +35,7 @@ namespace kt {
 
 struct LandscapeArgs {
     int n, n_centers, prefix_len;
+    RowFmt fmt;
     double base, noise;
     int32_t centers[kMaxCenters][8];
     double depths[kMaxCenters];
@@ -96,9 +98,9 @@ __global__ void __launch_bounds__(256) landscape_kernel(const LandscapeArgs a, c
         const uint64_t row = rows[i];
         double depth_term = 0.0;
         for (int j = 0; j < a.n_centers; ++j) {
-            int d2 = 0;
+            int64_t d2 = 0;  // exact: numpy's int64 ((x - c) ** 2).sum()
             for (int q = 0; q < a.n; ++q) {
-                const int d = row_byte(row, q) - a.centers[j][q];
+                const int64_t d = a.fmt.get(row, q) - a.centers[j][q];
                 d2 += d * d;
             }
             const double e = exp(__ddiv_rn(-double(d2), a.r2[j]));
@@ -113,8 +115,10 @@ __global__ void __launch_bounds__(256) landscape_kernel(const LandscapeArgs a, c
             for (; pos < a.prefix_len; ++pos) put_byte(m, pos, a.prefix[pos]);
             for (int q = 0; q < a.n; ++q) {
                 if (q) put_byte(m, pos++, ',');
-                const int v = row_byte(row, q);
-                if (v >= 100) put_byte(m, pos++, '0' + v / 100);
+                const int v = a.fmt.get(row, q);  // str(v): up to 5 digits
+                if (v >= 10000) put_byte(m, pos++, '0' + v / 10000);
+                if (v >= 1000) put_byte(m, pos++, '0' + (v / 1000) % 10);
+                if (v >= 100) put_byte(m, pos++, '0' + (v / 100) % 10);
                 if (v >= 10) put_byte(m, pos++, '0' + (v / 10) % 10);
                 put_byte(m, pos++, '0' + v % 10);
             }
@@ -132,7 +136,8 @@ __global__ void __launch_bounds__(256) landscape_kernel(const LandscapeArgs a, c
 
 extern "C" {
 
-int kt_landscape_create(kt_engine* e, int n_knobs, int n_centers, const int32_t* centers, const double* depths,
+int kt_landscape_create(kt_engine* e, int n_knobs, const int32_t* cards, int n_centers, const int32_t* centers,
+                        const double* depths,
                         const double* radii, double base_runtime, double noise_rel, const char* seed_text,
                         kt_landscape** out) {
     KT_API_BEGIN
@@ -140,13 +145,16 @@ int kt_landscape_create(kt_engine* e, int n_knobs, int n_centers, const int32_t*
     (void)e;
     if (n_knobs < 1 || n_knobs > kMaxKnobs) fail(KT_ERR_UNSUPPORTED, "1..8 knobs supported");
     if (n_centers < 1 || n_centers > kMaxCenters) fail(KT_ERR_UNSUPPORTED, "1..16 landscape centers supported");
+    const RowFmt fmt = row_fmt(cards, n_knobs);
     auto* l = new kt_landscape();
+    l->fmt = fmt;
     l->n = n_knobs;
     l->n_centers = n_centers;
     l->base = base_runtime;
     l->noise = noise_rel;
     l->prefix = std::string(seed_text ? seed_text : "") + ":";
-    if (l->prefix.size() + 4 * size_t(n_knobs) > 128 || l->prefix.size() > 64) {
+    const size_t digits = fmt.cmax >= 10000 ? 5 : (fmt.cmax >= 1000 ? 4 : 3);
+    if (l->prefix.size() + (digits + 1) * size_t(n_knobs) > 128 || l->prefix.size() > 64) {
         delete l;
         fail(KT_ERR_UNSUPPORTED, "landscape seed text too long for a one-block blake2b payload");
     }
@@ -171,6 +179,7 @@ int kt_score_landscape(kt_engine* e, const kt_landscape* l, const uint64_t* rows
     if (count <= 0) return KT_OK;
     LandscapeArgs a{};
     a.n = l->n;
+    a.fmt = l->fmt;
     a.n_centers = l->n_centers;
     a.base = l->base;
     a.noise = l->noise;

@@ -131,14 +131,14 @@ __device__ __forceinline__ void warp_leaf(int l, const int64_t* leaf_start, cons
 __global__ void __launch_bounds__(kLeafWarps * 32) loss_leaf_kernel(const uint64_t* __restrict__ pts,
                                                                     const uint8_t* __restrict__ assign,
                                                                     const double* __restrict__ cent, int n,
-                                                                    const int64_t* leaf_start, const int32_t* leaf_len,
+                                                                    const RowFmt fmt, const int64_t* leaf_start, const int32_t* leaf_len,
                                                                     int L, double* vals) {
     __shared__ double s_buf[kLeafWarps][128];
     const int w = threadIdx.x >> 5;
     const int l = blockIdx.x * kLeafWarps + w;
     if (l >= L) return;
     warp_leaf(l, leaf_start, leaf_len, vals, s_buf[w],
-              [&](int64_t p) { return np_sq_dist(pts[p], cent + int(assign[p]) * kMaxKnobs, n); });
+              [&](int64_t p) { return np_sq_dist(pts[p], cent + int(assign[p]) * kMaxKnobs, n, fmt); });
 }
 
 __global__ void __launch_bounds__(kLeafWarps * 32) array_leaf_kernel(const double* __restrict__ x,
@@ -176,13 +176,13 @@ static void combine(kt_engine* e, const PairwiseTree& t, double* vals, double* o
     e->check_launch("pairwise_combine");
 }
 
-void pairwise_loss(kt_engine* e, const uint64_t* pts, int64_t m, int n, const uint8_t* assign, const double* cent,
-                   double* out_dev) {
+void pairwise_loss(kt_engine* e, const uint64_t* pts, int64_t m, int n, const RowFmt& fmt, const uint8_t* assign,
+                   const double* cent, double* out_dev) {
     const PairwiseTree& t = pairwise_tree(e->device, m);
     const int L = int(t.leaf_start.size());
     auto* vals = static_cast<double*>(e->scratch("loss.vals", size_t(L + t.node_left.size()) * 8));
     e->pre_launch("loss_leaf");
-    loss_leaf_kernel<<<int(ceil_div(L, kLeafWarps)), kLeafWarps * 32, 0, e->stream>>>(pts, assign, cent, n,
+    loss_leaf_kernel<<<int(ceil_div(L, kLeafWarps)), kLeafWarps * 32, 0, e->stream>>>(pts, assign, cent, n, fmt,
                                                                                     t.d_leaf_start, t.d_leaf_len, L,
                                                                                     vals);
     e->check_launch("loss_leaf");

@@ -41,7 +41,8 @@ struct PairwiseTree {
 const PairwiseTree& pairwise_tree(int device, int64_t m);
 
 // k-means loss: sum over points of the float64 squared distance to the assigned centroid.
-void pairwise_loss(kt_engine* e, const uint64_t* pts, int64_t m, int n, const uint8_t* assign, const double* cent,
+void pairwise_loss(kt_engine* e, const uint64_t* pts, int64_t m, int n, const RowFmt& fmt, const uint8_t* assign,
+                   const double* cent,
                    double* out_dev);
 
 // numpy sum of x[0..m) (center == nullptr) or of (x - *center)^2 (center: device scalar).

@@ -243,11 +243,12 @@ __global__ void ppo_rows_kernel(const float* z, int ldz, int n, int64_t T, const
 }
 
 // states (rows) -> X[T][n] fp32, encode_state (space.py:181-188)
-__global__ void encode_kernel(const uint64_t* rows, int64_t T, int n, const int32_t* cards_dev, float* X) {
+__global__ void encode_kernel(const uint64_t* rows, int64_t T, int n, const RowFmt fmt, const int32_t* cards_dev,
+                              float* X) {
     for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < T; r += int64_t(gridDim.x) * blockDim.x) {
         const uint64_t row = rows[r];
         for (int k = 0; k < n; ++k)
-            X[size_t(r) * n + k] = float(double(row_byte(row, k)) / double(max(1, cards_dev[k] - 1)));
+            X[size_t(r) * n + k] = float(double(fmt.get(row, k)) / double(max(1, cards_dev[k] - 1)));
     }
 }
 
@@ -464,6 +465,8 @@ int kt_search_round(kt_engine* e, kt_agent* ag, const kt_forest* f, const uint64
     ra.w64 = ag->w64;
     ra.n = n, ra.h = ag->h, ra.g = ag->g, ra.S = S, ra.E = E;
     for (int k = 0; k < n; ++k) ra.cards[k] = cards[k];
+    ra.fmt = row_fmt(cards, n);
+    if (ra.fmt.bytes != f->fmt.bytes) fail(KT_ERR_DIMENSION, "model and space disagree on the row layout");
     for (int i = 0; i < n_seed_words; ++i) ra.seed_words[i] = seed_words[i];
     ra.n_seed_words = n_seed_words;
     ra.n_round_words = u64_words(uint64_t(round_index), ra.round_words);
@@ -560,7 +563,7 @@ int kt_search_round(kt_engine* e, kt_agent* ag, const kt_forest* f, const uint64
     auto* cards_dev = static_cast<int32_t*>(e->scratch("ppo.cards", 64));
     KT_CUDA(cudaMemcpyAsync(cards_dev, cards, size_t(n) * 4, cudaMemcpyHostToDevice, e->stream));
     e->pre_launch("encode_states");
-    encode_kernel<<<nb, 256, 0, e->stream>>>(st_c, T, n, cards_dev, X);
+    encode_kernel<<<nb, 256, 0, e->stream>>>(st_c, T, n, ra.fmt, cards_dev, X);
     e->check_launch("encode_states");
     auto* report = static_cast<double*>(e->scratch("ppo.report", 8 * 8));
     for (int ep = 0; ep < hp->epochs; ++ep) {

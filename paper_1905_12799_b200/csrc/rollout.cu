@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(kRolloutThreads, 1) rollout_kernel(RolloutArgs
         if (warp == 0) {
             const bool act_now = owner && active;
             for (int k = 0; k < kMaxKnobs; ++k)
-                sm.xt[k][lane] = (act_now && k < n) ? __ddiv_rn(double(row_byte(row, k)), double(max(1, a.cards[k] - 1)))
+                sm.xt[k][lane] = (act_now && k < n) ? __ddiv_rn(double(a.fmt.get(row, k)), double(max(1, a.cards[k] - 1)))
                                                     : 0.0;
             if (act_now)
                 for (int k = 0; k < n; ++k) sm.u[lane][k] = rng.random();
@@ -178,9 +178,9 @@ __global__ void __launch_bounds__(kRolloutThreads, 1) rollout_kernel(RolloutArgs
                 const int ak = sm.ak[lane][k];
                 act |= uint32_t(ak) << (2 * k);
                 stay &= ak == 1;
-                int v = row_byte(row, k) + ak - 1;
+                int v = a.fmt.get(row, k) + ak - 1;
                 v = v < 0 ? 0 : (v > a.cards[k] - 1 ? a.cards[k] - 1 : v);
-                nrow = (nrow & ~(0xffull << (8 * k))) | (uint64_t(v) << (8 * k));
+                nrow = a.fmt.set(nrow, k, v);
             }
             const int64_t slot = int64_t(e) * a.S + s;
             a.states[slot] = row;

@@ -47,6 +47,7 @@ struct SAArgs {
     const double* temperature;
     int chains, steps, n;
     int32_t cards[kMaxKnobs];
+    RowFmt fmt;
     uint32_t seed_words[4];
     int n_seed_words;
     double cooling;
@@ -58,10 +59,17 @@ struct SAArgs {
 
 template <int D>
 __device__ __forceinline__ double score_row(const uint64_t* forest, int words_per_tree, int n_trees, double base,
-                                            uint64_t row) {
-    const uint32_t lo = uint32_t(row), hi = uint32_t(row >> 32);
-    double acc = walk_tree<D>(forest, lo, hi);
-    for (int t = 1; t < n_trees; ++t) acc = __dadd_rn(acc, walk_tree<D>(forest + t * words_per_tree, lo, hi));
+                                            uint64_t row, bool wide, const RowFmt& fmt) {
+    double acc;
+    if (wide) {
+        const WideRow x = widen_row(row, fmt);
+        acc = walk_tree_wide<D>(forest, x);
+        for (int t = 1; t < n_trees; ++t) acc = __dadd_rn(acc, walk_tree_wide<D>(forest + t * words_per_tree, x));
+    } else {
+        const uint32_t lo = uint32_t(row), hi = uint32_t(row >> 32);
+        acc = walk_tree<D>(forest, lo, hi);
+        for (int t = 1; t < n_trees; ++t) acc = __dadd_rn(acc, walk_tree<D>(forest + t * words_per_tree, lo, hi));
+    }
     return __dadd_rn(base, acc);
 }
 
@@ -87,10 +95,10 @@ __global__ void __launch_bounds__(128) sa_chain_kernel(SAArgs a) {
     for (int s = 1; s <= a.steps; ++s) {
         const int knob = int(g.bounded32(uint32_t(a.n - 1)));
         const int sign = int(g.bounded32(1u)) * 2 - 1;
-        int v = row_byte(row, knob) + sign;
+        int v = a.fmt.get(row, knob) + sign;
         v = v < 0 ? 0 : (v > a.cards[knob] - 1 ? a.cards[knob] - 1 : v);
-        const uint64_t prop = (row & ~(0xffull << (8 * knob))) | (uint64_t(v) << (8 * knob));
-        const double ps = score_row<D>(s_forest, a.words_per_tree, a.n_trees, a.base, prop);
+        const uint64_t prop = a.fmt.set(row, knob, v);
+        const double ps = score_row<D>(s_forest, a.words_per_tree, a.n_trees, a.base, prop, !a.fmt.bytes, a.fmt);
         const double delta = __dsub_rn(ps, score);
         bool accept = delta >= 0.0;
         if (!accept) accept = g.random() < exp(__ddiv_rn(delta, temp));
@@ -147,6 +155,8 @@ extern "C" int kt_sa_chains(kt_engine* e, const kt_forest* f, const uint64_t* st
     if (n_knobs != f->n_knobs) fail(KT_ERR_DIMENSION, "forest and space disagree on the knob count");
     if (n_seed_words < 1 || n_seed_words > 4) fail(KT_ERR_VALUE, "seed must fit in 128 bits");
     if (chains > 64 * 1024 * 1024) fail(KT_ERR_UNSUPPORTED, "at most 2^26 chains per call");
+    const RowFmt fmt = row_fmt(cards, n_knobs);
+    if (fmt.bytes != f->fmt.bytes) fail(KT_ERR_DIMENSION, "forest and space disagree on the row layout");
     // starts: the first min(n_starts, chains) given, the rest padded from the parent stream
     // (sa.py:79-85: pad_rng = default_rng(seed_seq); random_config draws integers(0, card) per knob)
     auto* starts = static_cast<uint64_t*>(e->scratch("sa.starts", size_t(chains) * 8));
@@ -157,7 +167,7 @@ extern "C" int kt_sa_chains(kt_engine* e, const kt_forest* f, const uint64_t* st
         auto* h = static_cast<uint64_t*>(e->staging("sa.pad", size_t(chains - given) * 8));
         for (int c = 0; c < chains - given; ++c) {
             uint64_t row = 0;
-            for (int q = 0; q < n_knobs; ++q) row |= uint64_t(pad.bounded32(uint32_t(cards[q] - 1))) << (8 * q);
+            for (int q = 0; q < n_knobs; ++q) row = fmt.set(row, q, int(pad.bounded32(uint32_t(cards[q] - 1))));
             h[c] = row;
         }
         KT_CUDA(cudaMemcpyAsync(starts + given, h, size_t(chains - given) * 8, cudaMemcpyHostToDevice, e->stream));
@@ -189,6 +199,7 @@ extern "C" int kt_sa_chains(kt_engine* e, const kt_forest* f, const uint64_t* st
     a.steps = steps;
     a.n = n_knobs;
     for (int q = 0; q < n_knobs; ++q) a.cards[q] = cards[q];
+    a.fmt = fmt;
     for (int q = 0; q < n_seed_words; ++q) a.seed_words[q] = seed_words[q];
     a.n_seed_words = n_seed_words;
     a.cooling = cooling;

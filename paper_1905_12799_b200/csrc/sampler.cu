@@ -190,10 +190,18 @@ int64_t dedup(kt_engine* e, const uint64_t* rows, int64_t count, uint64_t* out) 
 }
 
 // ============================================================== mode vote (K9)
-__global__ void __launch_bounds__(256) mode_hist_kernel(const uint64_t* __restrict__ rows, int64_t count, int n,
-                                                        unsigned int* __restrict__ hist /* [8][256] */) {
-    __shared__ unsigned int s_hist[kMaxKnobs * 256];
-    for (int i = threadIdx.x; i < kMaxKnobs * 256; i += blockDim.x) s_hist[i] = 0;
+// Per-knob histograms back to back: knob d's bins start at off[d] (off[n] bins in all).
+struct ModeArgs {
+    RowFmt fmt;
+    int n;
+    int off[kMaxKnobs + 1];
+};
+
+__global__ void __launch_bounds__(256) mode_hist_kernel(const uint64_t* __restrict__ rows, int64_t count,
+                                                        const ModeArgs a, unsigned int* __restrict__ hist) {
+    extern __shared__ unsigned int s_hist[];
+    const int n = a.n, bins = a.off[a.n];
+    for (int i = threadIdx.x; i < bins; i += blockDim.x) s_hist[i] = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const int64_t warps_total = int64_t(gridDim.x) * (blockDim.x >> 5);
@@ -205,32 +213,42 @@ __global__ void __launch_bounds__(256) mode_hist_kernel(const uint64_t* __restri
         if (!valid) continue;
         const uint64_t row = rows[i];
         for (int d = 0; d < n; ++d) {
-            const int v = row_byte(row, d);
+            const int v = a.off[d] + a.fmt.get(row, d);
             const unsigned peers = __match_any_sync(active, v);
-            if (lane == __ffs(peers) - 1) atomicAdd(&s_hist[d * 256 + v], unsigned(__popc(peers)));
+            if (lane == __ffs(peers) - 1) atomicAdd(&s_hist[v], unsigned(__popc(peers)));
         }
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < n * 256; i += blockDim.x)
+    for (int i = threadIdx.x; i < bins; i += blockDim.x)
         if (s_hist[i]) atomicAdd(&hist[i], s_hist[i]);
 }
 
-void mode_vote(kt_engine* e, const uint64_t* rows, int64_t count, int n, int32_t* mode_out) {
+void mode_vote(kt_engine* e, const uint64_t* rows, int64_t count, int n, const RowFmt& fmt, const int32_t* cards,
+               int32_t* mode_out) {
     if (count <= 0) fail(KT_ERR_VALUE, "mode vote needs at least one row");
     if (count >= (int64_t(1) << 32)) fail(KT_ERR_UNSUPPORTED, "mode vote supports < 2^32 rows");
-    auto* hist = static_cast<unsigned int*>(e->scratch("mode.hist", kMaxKnobs * 256 * 4));
-    KT_CUDA(cudaMemsetAsync(hist, 0, kMaxKnobs * 256 * 4, e->stream));
+    ModeArgs a{};
+    a.fmt = fmt;
+    a.n = n;
+    for (int d = 0; d < n; ++d) a.off[d + 1] = a.off[d] + cards[d];
+    const int bins = a.off[n];
+    const size_t smem = size_t(bins) * 4;
+    if (smem > 200 * 1024) fail(KT_ERR_UNSUPPORTED, "mode vote supports at most 51200 knob settings in all");
+    auto* hist = static_cast<unsigned int*>(e->scratch("mode.hist", smem));
+    KT_CUDA(cudaMemsetAsync(hist, 0, smem, e->stream));
+    KT_CUDA(cudaFuncSetAttribute(mode_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int grid = int(std::min<int64_t>(ceil_div(count, 256), int64_t(e->num_sms) * 4));
     e->pre_launch("mode_hist");
-    mode_hist_kernel<<<grid, 256, 0, e->stream>>>(rows, count, n, hist);
+    mode_hist_kernel<<<grid, 256, smem, e->stream>>>(rows, count, a, hist);
     e->check_launch("mode_hist");
-    auto* h = static_cast<unsigned int*>(e->staging("mode.hist", kMaxKnobs * 256 * 4));
-    KT_CUDA(cudaMemcpyAsync(h, hist, kMaxKnobs * 256 * 4, cudaMemcpyDeviceToHost, e->stream));
+    auto* h = static_cast<unsigned int*>(e->staging("mode.hist", smem));
+    KT_CUDA(cudaMemcpyAsync(h, hist, smem, cudaMemcpyDeviceToHost, e->stream));
     e->sync();
     for (int d = 0; d < n; ++d) {
+        const unsigned int* hd = h + a.off[d];
         int best = 0;
-        for (int v = 1; v < 256; ++v)
-            if (h[d * 256 + v] > h[d * 256 + best]) best = v;  // ties -> smallest index
+        for (int v = 1; v < cards[d]; ++v)
+            if (hd[v] > hd[best]) best = v;  // ties -> smallest index
         mode_out[d] = best;
     }
 }
@@ -249,6 +267,7 @@ struct InitArgs {
     const uint64_t* pts;
     int64_t m;
     int n;
+    RowFmt fmt;
     int j0, j1;
     int64_t first_idx;
     const double* uniforms;  // u_1, u_2, ... (random() draws after integers(0, m))
@@ -370,7 +389,7 @@ __global__ void __launch_bounds__(kInitThreads) init_kernel(InitArgs a) {
             for (int q = 0; q < per; ++q) {
                 const int64_t p = base + q * kInitThreads + tid;
                 if (p < a.m) {
-                    int v = int_sq_dist(a.pts[p], c, a.n);
+                    int v = int(int_sq_dist(a.pts[p], c, a.n, a.fmt));  // < 2^31 (host check)
                     if (j > 0) v = min(v, __ldcg(wold + p));
                     wnew[p] = v;
                     s += v;
@@ -400,6 +419,10 @@ __global__ void __launch_bounds__(kInitThreads) init_kernel(InitArgs a) {
 constexpr int kMaxRuns = 8;
 constexpr int kMaxClusters = 256;  // sum of k over the runs of one launch
 constexpr int kSumW = 9;           // 8 coordinate sums + count
+// Per-block delta accumulators (int32 shared atomics): low bytes of the 8
+// coordinates, count, then high bytes (nonzero only in wide row layouts), so
+// every counter grows by at most 255 per point in any layout.
+constexpr int kDeltaW = 17;
 enum RunState : int {
     kActiveFromSums = 0,  // centroids = sums / counts of the previous pass (bounds valid)
     kActiveGiven = 1,     // centroids given in LloydArgs::cent (after a reseed)
@@ -417,6 +440,8 @@ struct LloydArgs {
     const uint64_t* pts;
     int64_t m;
     int n;
+    RowFmt fmt;
+    float bk1;  // centroid-rounding coefficient of d2_bound (scales with the largest coordinate)
     int R;
     int k[kMaxRuns];
     int coff[kMaxRuns];
@@ -452,7 +477,7 @@ __host__ __device__ inline LloydLayout lloyd_layout(int K) {
     L.S = o;
     o += size_t(K) * kSumW * 8;
     L.delta = o;
-    o += size_t(K) * kSumW * 4;
+    o += size_t(K) * kDeltaW * 4;
     L.drift = o;
     o += size_t(K) * 4;
     L.total = (o + 15) & ~size_t(15);
@@ -478,18 +503,24 @@ struct RunShared {
 
 // Conservative |fp32 - exact| bound for sum_i (p_i - c_i)^2 with p_i, |c_i| <= 255
 // (derivation in DESIGN.md §K8).
-__device__ __forceinline__ float d2_bound(float d) {
-    return 6.5e-5f * sqrtf(8.0f * d + 8.0f) + 5.5e-7f * d + 1e-6f;
+// k1 = 6.5e-5 for coordinates <= 255 and grows linearly with the largest coordinate.
+__device__ __forceinline__ float d2_bound(float d, float k1) {
+    return k1 * sqrtf(8.0f * d + 8.0f) + 5.5e-7f * d + 1e-6f;
 }
-__device__ __forceinline__ float dist_up(float d2) { return __fsqrt_ru(__fadd_ru(d2, d2_bound(d2))); }
-__device__ __forceinline__ float dist_dn(float d2) {
-    const float lo = __fsub_rd(d2, d2_bound(d2));
+__device__ __forceinline__ float dist_up(float d2, float k1) { return __fsqrt_ru(__fadd_ru(d2, d2_bound(d2, k1))); }
+__device__ __forceinline__ float dist_dn(float d2, float k1) {
+    const float lo = __fsub_rd(d2, d2_bound(d2, k1));
     return lo > 0.0f ? __fsqrt_rd(lo) : 0.0f;
 }
 // u < l with a margin far above float64 rounding of the reference's distances
 __device__ __forceinline__ bool surely_less(float u, float l) { return __fadd_ru(u, 1e-6f * (u + 1.0f)) < l; }
 
-__device__ __forceinline__ void unpack_row(uint64_t row, float p[kMaxKnobs]) {
+__device__ __forceinline__ void unpack_row(uint64_t row, float p[kMaxKnobs], const RowFmt& f) {
+    if (!f.bytes) {
+#pragma unroll
+        for (int i = 0; i < kMaxKnobs; ++i) p[i] = float(f.get(row, i));  // unused knobs: width 0 -> 0
+        return;
+    }
     const uint32_t lo = uint32_t(row), hi = uint32_t(row >> 32);
     p[0] = float(lo & 0xff);
     p[1] = float((lo >> 8) & 0xff);
@@ -518,7 +549,7 @@ __device__ __forceinline__ float f32_d2(const float p[kMaxKnobs], const float* c
 
 // Full assignment of one point under one k; returns the cluster and fresh bounds.
 __device__ __forceinline__ int full_assign(const float* c32, const double* c64, uint64_t row, const float p[kMaxKnobs],
-                                           int k, int n, float& u, float& l) {
+                                           int k, int n, const RowFmt& fmt, float k1, float& u, float& l) {
     float best = INFINITY, second = INFINITY;
     int bj = 0;
     for (int j = 0; j < k; ++j) {
@@ -531,11 +562,11 @@ __device__ __forceinline__ int full_assign(const float* c32, const double* c64, 
             second = d;
         }
     }
-    if (k > 1 && !(second - best > d2_bound(best) + d2_bound(second))) {
+    if (k > 1 && !(second - best > d2_bound(best, k1) + d2_bound(second, k1))) {
         // ambiguous: the reference's own float64 expression decides (ties -> lowest j)
         double bd = INFINITY;
         for (int j = 0; j < k; ++j) {
-            const double d = np_sq_dist(row, c64 + j * kMaxKnobs, n);
+            const double d = np_sq_dist(row, c64 + j * kMaxKnobs, n, fmt);
             if (d < bd) {
                 bd = d;
                 bj = j;
@@ -546,8 +577,8 @@ __device__ __forceinline__ int full_assign(const float* c32, const double* c64, 
         for (int j = 0; j < k; ++j)
             if (j != bj) second = fminf(second, f32_d2(p, c32 + j * kMaxKnobs));
     }
-    u = dist_up(best);
-    l = k > 1 ? dist_dn(second) : INFINITY;
+    u = dist_up(best, k1);
+    l = k > 1 ? dist_dn(second, k1) : INFINITY;
     return bj;
 }
 
@@ -602,7 +633,7 @@ __global__ void __launch_bounds__(256, 3) lloyd_kernel(LloydArgs a) {
                 if (i >= n) c = 0.0;
                 else if (st == kActiveFromSums) c = __ddiv_rn(double(S[g * kSumW + i]), double(S[g * kSumW + 8]));
                 else if (st == kActiveGiven) c = a.cent[g * kMaxKnobs + i];
-                else c = double(row_byte(a.init_rows[g - a.coff[r]], i));
+                else c = double(a.fmt.get(a.init_rows[g - a.coff[r]], i));
                 const double dlt = c - c64[g * kMaxKnobs + i];
                 dlt2 = dlt * dlt;
                 c64[g * kMaxKnobs + i] = c;
@@ -614,7 +645,7 @@ __global__ void __launch_bounds__(256, 3) lloyd_kernel(LloydArgs a) {
             dlt2 += __shfl_xor_sync(0xffffffffu, dlt2, 4);
             if (live && i == 0) drift[g] = __double2float_ru(sqrt(dlt2) * (1.0 + 1e-9) + 1e-30);
         }
-        for (int i = tid; i < K * kSumW; i += blockDim.x) delta[i] = 0;
+        for (int i = tid; i < K * kDeltaW; i += blockDim.x) delta[i] = 0;
         if (tid < kMaxRuns) rs.changed[tid] = 0;
         __syncthreads();
         if (tid < R && run_active(rs.state[tid])) {
@@ -723,26 +754,35 @@ __global__ void __launch_bounds__(256, 3) lloyd_kernel(LloydArgs a) {
                     const LloydQueueEntry qe = queue[i];
                     const uint64_t row = qe.row;
                     float p[kMaxKnobs];
-                    unpack_row(row, p);
+                    unpack_row(row, p, a.fmt);
                     const int old = qe.old;
                     float u = qe.u, l = qe.l;
                     int j = -1;
                     if (bounded && old != 255) {
-                        u = dist_up(f32_d2(p, c32 + (co + old) * kMaxKnobs));
+                        u = dist_up(f32_d2(p, c32 + (co + old) * kMaxKnobs), a.bk1);
                         if (surely_less(u, l)) j = old;
                     }
                     if (a.stats) atomicAdd(&rs.cnt[r][j < 0 ? 2 : 1], 1u);
-                    if (j < 0) j = full_assign(c32 + co * kMaxKnobs, c64 + co * kMaxKnobs, row, p, a.k[r], n, u, l);
+                    if (j < 0)
+                        j = full_assign(c32 + co * kMaxKnobs, c64 + co * kMaxKnobs, row, p, a.k[r], n, a.fmt, a.bk1, u, l);
                     bd_r[qe.point] = make_float2(u, l);
                     if (j != old) {
                         as_r[qe.point] = uint8_t(j);
                         rs.changed[r] = 1;
-                        int* dn = delta + (co + j) * kSumW;
-                        for (int c = 0; c < n; ++c) atomicAdd(dn + c, row_byte(row, c));
+                        int* dn = delta + (co + j) * kDeltaW;
+                        for (int c = 0; c < n; ++c) {
+                            const int v = a.fmt.get(row, c);
+                            atomicAdd(dn + c, v & 0xff);
+                            if (v >> 8) atomicAdd(dn + 9 + c, v >> 8);
+                        }
                         atomicAdd(dn + 8, 1);
                         if (old != 255) {
-                            int* dold = delta + (co + old) * kSumW;
-                            for (int c = 0; c < n; ++c) atomicSub(dold + c, row_byte(row, c));
+                            int* dold = delta + (co + old) * kDeltaW;
+                            for (int c = 0; c < n; ++c) {
+                                const int v = a.fmt.get(row, c);
+                                atomicSub(dold + c, v & 0xff);
+                                if (v >> 8) atomicSub(dold + 9 + c, v >> 8);
+                            }
                             atomicSub(dold + 8, 1);
                         }
                     }
@@ -758,8 +798,9 @@ __global__ void __launch_bounds__(256, 3) lloyd_kernel(LloydArgs a) {
         const int buf = it % 3;
         unsigned long long* Dcur = a.D + size_t(buf) * K * kSumW;
         for (int i = tid; i < K * kSumW; i += blockDim.x) {
-            const int v = delta[i];
-            if (v) atomicAdd(Dcur + i, (unsigned long long)(long long)v);
+            const int g = i / kSumW, c = i % kSumW;
+            const long long v = (long long)delta[g * kDeltaW + c] + (c < 8 ? 256ll * delta[g * kDeltaW + 9 + c] : 0ll);
+            if (v) atomicAdd(Dcur + i, (unsigned long long)v);
         }
         if (tid < R && rs.changed[tid]) atomicOr(a.chg + buf * kMaxRuns + tid, 1u);
         if (blockIdx.x == 0) {
@@ -817,10 +858,11 @@ __global__ void __launch_bounds__(256, 3) lloyd_kernel(LloydArgs a) {
 }
 
 // ============================================================ reseed helpers
-__global__ void point_d2_kernel(const uint64_t* __restrict__ pts, int64_t m, int n, const uint8_t* __restrict__ assign,
-                                const double* __restrict__ cent, double* __restrict__ out) {
+__global__ void point_d2_kernel(const uint64_t* __restrict__ pts, int64_t m, int n, const RowFmt fmt,
+                                const uint8_t* __restrict__ assign, const double* __restrict__ cent,
+                                double* __restrict__ out) {
     for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < m; p += int64_t(gridDim.x) * blockDim.x)
-        out[p] = np_sq_dist(pts[p], cent + int(assign[p]) * kMaxKnobs, n);
+        out[p] = np_sq_dist(pts[p], cent + int(assign[p]) * kMaxKnobs, n, fmt);
 }
 
 // argmax of d2 over points not in `blocked` (ties -> lowest index); per-block partials.
@@ -870,6 +912,7 @@ struct KmeansSession {
     const uint64_t* pts;
     int64_t m;
     int n;
+    RowFmt fmt;
     uint64_t seed;
     // incremental k-means++ state
     int chosen = 0;  // centroids chosen so far
@@ -881,7 +924,17 @@ struct KmeansSession {
     double* d_uniforms = nullptr;
     int nchunks = 0;
 
-    KmeansSession(kt_engine* e_, const uint64_t* p, int64_t m_, int n_, uint64_t s) : e(e_), pts(p), m(m_), n(n_), seed(s) {
+    KmeansSession(kt_engine* e_, const uint64_t* p, int64_t m_, int n_, const RowFmt& f, uint64_t s)
+        : e(e_), pts(p), m(m_), n(n_), fmt(f), seed(s) {
+        // k-means++ weights are exact integers: int32 per point, and every prefix
+        // sum below 2^53 so that numpy's float64 cumsum is exact too
+        double max_d2 = 0.0;
+        for (int i = 0; i < n; ++i) {
+            const double c = f.bytes ? 254.0 : double((1ll << f.width[i]) - 1);
+            max_d2 += c * c;
+        }
+        if (max_d2 >= 2147483648.0 || max_d2 * double(m) >= 9007199254740992.0)
+            fail(KT_ERR_UNSUPPORTED, "k-means++ weights of this space exceed the exact-integer range");
         uint32_t w[2];
         int nw = u64_words(seed, w);
         Pcg64 g = pcg64_from_seed_sequence(w, nw, nullptr, 0);
@@ -906,6 +959,7 @@ struct KmeansSession {
         ia.pts = pts;
         ia.m = m;
         ia.n = n;
+        ia.fmt = fmt;
         ia.j0 = chosen;
         ia.j1 = k;
         ia.first_idx = first_idx;
@@ -939,6 +993,8 @@ struct KmeansSession {
         a.pts = pts;
         a.m = m;
         a.n = n;
+        a.fmt = fmt;
+        a.bk1 = float(6.5e-5 * std::max(1.0, double(fmt.cmax) / 255.0));
         a.R = R;
         int K = 0;
         for (int r = 0; r < R; ++r) {
@@ -1005,7 +1061,7 @@ struct KmeansSession {
             KT_CUDA(cudaMemcpyAsync(h_ctrl, a.ctrl, 4, cudaMemcpyDeviceToHost, e->stream));
             KT_CUDA(cudaMemcpyAsync(h_state, a.run_state, R * 4, cudaMemcpyDeviceToHost, e->stream));
             if (history) {
-                pairwise_loss(e, pts, m, n, a.assign, a.cent, d_loss);
+                pairwise_loss(e, pts, m, n, fmt, a.assign, a.cent, d_loss);
                 KT_CUDA(cudaMemcpyAsync(h_loss, d_loss, 8, cudaMemcpyDeviceToHost, e->stream));
             }
             e->sync();
@@ -1030,7 +1086,8 @@ struct KmeansSession {
         }
         std::vector<RunResult> out(R);
         for (int r = 0; r < R; ++r)
-            pairwise_loss(e, pts, m, n, a.assign + size_t(r) * a.stride, a.cent + size_t(a.coff[r]) * kMaxKnobs, d_loss + r);
+            pairwise_loss(e, pts, m, n, fmt, a.assign + size_t(r) * a.stride, a.cent + size_t(a.coff[r]) * kMaxKnobs,
+                          d_loss + r);
         KT_CUDA(cudaMemcpyAsync(h_loss, d_loss, R * 8, cudaMemcpyDeviceToHost, e->stream));
         KT_CUDA(cudaMemcpyAsync(h_iter, a.run_iter, R * 4, cudaMemcpyDeviceToHost, e->stream));
         e->sync();
@@ -1074,7 +1131,7 @@ struct KmeansSession {
         auto* pd2 = static_cast<double*>(e->scratch("km.pd2", size_t(m) * 8));
         const int grid = int(std::min<int64_t>(ceil_div(m, 256), int64_t(e->num_sms) * 4));
         e->pre_launch("point_d2");
-        point_d2_kernel<<<grid, 256, 0, e->stream>>>(pts, m, n, asg, cent, pd2);
+        point_d2_kernel<<<grid, 256, 0, e->stream>>>(pts, m, n, fmt, asg, cent, pd2);
         e->check_launch("point_d2");
         std::vector<int64_t> blocked;
         auto* d_blocked = static_cast<int64_t*>(e->scratch("km.blocked", 64 * 8));
@@ -1117,7 +1174,7 @@ struct KmeansSession {
             KT_CUDA(cudaMemcpyAsync(h_rows + q, pts + blocked[q], 8, cudaMemcpyDeviceToHost, e->stream));
         e->sync();
         for (size_t q = 0; q < empties.size(); ++q)
-            for (int i = 0; i < n; ++i) newc[size_t(empties[q]) * kMaxKnobs + i] = double(row_byte(h_rows[q], i));
+            for (int i = 0; i < n; ++i) newc[size_t(empties[q]) * kMaxKnobs + i] = double(fmt.get(h_rows[q], i));
         auto* h_c = static_cast<double*>(e->staging("km.newc", size_t(kMaxClusters) * kMaxKnobs * 8));
         std::copy(newc.begin(), newc.end(), h_c);
         KT_CUDA(cudaMemcpyAsync(cent, h_c, newc.size() * 8, cudaMemcpyHostToDevice, e->stream));
@@ -1153,11 +1210,11 @@ struct KneeResult {
     const uint8_t* assign_dev = nullptr;  // chosen run's assignment (device), valid until next engine call
 };
 
-static KneeResult knee_scan(kt_engine* e, const uint64_t* pts, int64_t m, int n, uint64_t seed, double knee_c,
-                            int k_max) {
+static KneeResult knee_scan(kt_engine* e, const uint64_t* pts, int64_t m, int n, const RowFmt& fmt, uint64_t seed,
+                            double knee_c, int k_max) {
     const int upper = int(std::min<int64_t>(k_max, m));
     if (upper < 8) fail(KT_ERR_VALUE, "knee scan needs at least 8 distinct points");
-    KmeansSession ses(e, pts, m, n, seed);
+    KmeansSession ses(e, pts, m, n, fmt, seed);
     KneeResult res;
     double previous = INFINITY;
     int k0 = 8;
@@ -1209,14 +1266,16 @@ int kt_dedup(kt_engine* e, const uint64_t* rows_dev, int64_t count, uint64_t* di
     KT_API_END
 }
 
-int kt_mode_vote(kt_engine* e, const uint64_t* rows_dev, int64_t count, int n_knobs, int32_t* mode_out) {
+int kt_mode_vote(kt_engine* e, const uint64_t* rows_dev, int64_t count, int n_knobs, const int32_t* cards,
+                 int32_t* mode_out) {
     KT_API_BEGIN
-    if (n_knobs < 1 || n_knobs > kMaxKnobs) fail(KT_ERR_UNSUPPORTED, "1..8 knobs supported");
-    mode_vote(e, rows_dev, count, n_knobs, mode_out);
+    const RowFmt fmt = row_fmt(cards, n_knobs);
+    mode_vote(e, rows_dev, count, n_knobs, fmt, cards, mode_out);
     KT_API_END
 }
 
-int kt_kmeans(kt_engine* e, const uint64_t* points_dev, int64_t m, int n_knobs, int k, uint64_t seed,
+int kt_kmeans(kt_engine* e, const uint64_t* points_dev, int64_t m, int n_knobs, const int32_t* cards, int k,
+              uint64_t seed,
               double* centroids_out, int64_t* assignment_out, double* loss_out, double* history_out,
               int32_t* n_passes) {
     KT_API_BEGIN
@@ -1224,7 +1283,7 @@ int kt_kmeans(kt_engine* e, const uint64_t* points_dev, int64_t m, int n_knobs, 
     if (n_knobs < 1 || n_knobs > kMaxKnobs) fail(KT_ERR_UNSUPPORTED, "1..8 knobs supported");
     if (k < 1 || k > 63) fail(KT_ERR_UNSUPPORTED, "engine k-means supports 1 <= k <= 63");
     // n_distinct check (sampler.py:84-87) is done by the caller with kt_dedup.
-    KmeansSession ses(e, points_dev, m, n_knobs, seed);
+    KmeansSession ses(e, points_dev, m, n_knobs, row_fmt(cards, n_knobs), seed);
     std::vector<double> hist;
     auto out = ses.run({k}, history_out ? &hist : nullptr);
     const LloydArgs& a = ses.last_args;
@@ -1249,13 +1308,13 @@ int kt_kmeans(kt_engine* e, const uint64_t* points_dev, int64_t m, int n_knobs, 
     KT_API_END
 }
 
-int kt_knee_scan(kt_engine* e, const uint64_t* points_dev, int64_t m, int n_knobs, uint64_t seed,
+int kt_knee_scan(kt_engine* e, const uint64_t* points_dev, int64_t m, int n_knobs, const int32_t* cards, uint64_t seed,
                  double knee_constant, int k_max, int32_t* scanned_k, double* scanned_loss, int32_t* n_scanned,
                  double* centroids_out, int64_t* assignment_out) {
     KT_API_BEGIN
     if (n_knobs < 1 || n_knobs > kMaxKnobs) fail(KT_ERR_UNSUPPORTED, "1..8 knobs supported");
     if (k_max > 63) fail(KT_ERR_UNSUPPORTED, "engine knee scan supports k_max <= 63");
-    KneeResult r = knee_scan(e, points_dev, m, n_knobs, seed, knee_constant, k_max);
+    KneeResult r = knee_scan(e, points_dev, m, n_knobs, row_fmt(cards, n_knobs), seed, knee_constant, k_max);
     *n_scanned = int32_t(r.ks.size());
     for (size_t i = 0; i < r.ks.size(); ++i) {
         scanned_k[i] = r.ks[i];
@@ -1276,7 +1335,7 @@ int kt_adaptive_sample(kt_engine* e, const uint64_t* rows_dev, int64_t count, in
                        uint64_t* batch_out, int32_t* batch_len, kt_sample_info* info) {
     KT_API_BEGIN
     if (count < 1) fail(KT_ERR_VALUE, "trajectory is empty");
-    if (n_knobs < 1 || n_knobs > kMaxKnobs) fail(KT_ERR_UNSUPPORTED, "1..8 knobs supported");
+    const RowFmt fmt = row_fmt(cards, n_knobs);
     kt_sample_info local{};
     kt_sample_info& inf = info ? *info : local;
     std::memset(&inf, 0, sizeof(inf));
@@ -1294,7 +1353,7 @@ int kt_adaptive_sample(kt_engine* e, const uint64_t* rows_dev, int64_t count, in
         *batch_len = len;
         return KT_OK;
     }
-    KneeResult r = knee_scan(e, distinct, m, n_knobs, seed, knee_constant, 63);
+    KneeResult r = knee_scan(e, distinct, m, n_knobs, fmt, seed, knee_constant, 63);
     inf.chosen_k = r.chosen_k;
     inf.n_scanned = int32_t(r.ks.size());
     for (size_t i = 0; i < r.ks.size() && i < 56; ++i) {
@@ -1314,14 +1373,14 @@ int kt_adaptive_sample(kt_engine* e, const uint64_t* rows_dev, int64_t count, in
             const double x = r.centroids[size_t(j) * n_knobs + i];
             const double f = std::floor(x + 0.5);
             long long idx = f < 0.0 ? 0 : (f > double(cards[i] - 1) ? cards[i] - 1 : (long long)f);
-            row |= uint64_t(idx) << (8 * i);
+            row = fmt.set(row, i, int(idx));
         }
         if (visited.count(row)) {
             if (!have_mode) {
                 int32_t md[kMaxKnobs];
-                mode_vote(e, rows_dev, count, n_knobs, md);
+                mode_vote(e, rows_dev, count, n_knobs, fmt, cards, md);
                 mode_row = 0;
-                for (int i = 0; i < n_knobs; ++i) mode_row |= uint64_t(md[i]) << (8 * i);
+                for (int i = 0; i < n_knobs; ++i) mode_row = fmt.set(mode_row, i, md[i]);
                 have_mode = true;
             }
             inf.used_mode = 1;

@@ -49,6 +49,7 @@ struct Packer {
     const int32_t* cards;
     const double* table;
     int max_card;
+    bool wide;
     const int32_t *feat, *left, *right;
     const double *thr, *val;
     std::vector<uint16_t> heap;  // 2^D - 1 internal entries
@@ -62,7 +63,7 @@ struct Packer {
         const double* row = table + size_t(f) * max_card;
         int cut = 0;
         while (cut < card && row[cut] <= thr[node]) ++cut;  // table is non-decreasing
-        return uint16_t(f | (cut << 8));
+        return uint16_t(wide ? (f | (cut << 3)) : (f | (cut << 8)));
     }
     void fill(int node, int h, int depth) {
         if (depth == D) {
@@ -70,7 +71,7 @@ struct Packer {
             return;
         }
         if (feat[node] < 0) {
-            heap[h] = uint16_t(0 | (255 << 8));  // idx < 255 always: left
+            heap[h] = uint16_t(wide ? (8191 << 3) : (255 << 8));  // idx < cut always: left
             fill(node, 2 * h + 1, depth + 1);
             fill(node, 2 * h + 2, depth + 1);
         } else {
@@ -83,11 +84,11 @@ struct Packer {
 }  // namespace
 
 // Rows are processed two per thread for memory/LDS latency overlap.
-template <int D>
+template <int D, bool WIDE>
 __global__ void __launch_bounds__(256) score_trees_kernel(const uint64_t* __restrict__ forest, int words_per_tree,
                                                           int t0, int t1, int n_trees, double base,
                                                           const uint64_t* __restrict__ rows, int64_t count,
-                                                          double* __restrict__ out) {
+                                                          double* __restrict__ out, const RowFmt fmt) {
     extern __shared__ uint64_t s_forest[];
     const int nt = t1 - t0;
     const int total = nt * words_per_tree;
@@ -103,11 +104,20 @@ __global__ void __launch_bounds__(256) score_trees_kernel(const uint64_t* __rest
         uint64_t r1 = two ? rows[i + 1] : r0;
         uint32_t lo0 = uint32_t(r0), hi0 = uint32_t(r0 >> 32);
         uint32_t lo1 = uint32_t(r1), hi1 = uint32_t(r1 >> 32);
+        WideRow x0{}, x1{};
+        if constexpr (WIDE) {
+            x0 = widen_row(r0, fmt);
+            x1 = widen_row(r1, fmt);
+        }
+        auto walk = [&](const uint64_t* tr, int which) -> double {
+            if constexpr (WIDE) return walk_tree_wide<D>(tr, which ? x1 : x0);
+            else return walk_tree<D>(tr, which ? lo1 : lo0, which ? hi1 : hi0);
+        };
         double a0, a1;
         int t = 0;
         if (first_chunk) {
-            a0 = walk_tree<D>(s_forest, lo0, hi0);
-            a1 = walk_tree<D>(s_forest, lo1, hi1);
+            a0 = walk(s_forest, 0);
+            a1 = walk(s_forest, 1);
             t = 1;
         } else {
             a0 = out[i];
@@ -116,8 +126,8 @@ __global__ void __launch_bounds__(256) score_trees_kernel(const uint64_t* __rest
 #pragma unroll 2
         for (; t < nt; ++t) {
             const uint64_t* tr = s_forest + t * words_per_tree;
-            a0 = __dadd_rn(a0, walk_tree<D>(tr, lo0, hi0));
-            a1 = __dadd_rn(a1, walk_tree<D>(tr, lo1, hi1));
+            a0 = __dadd_rn(a0, walk(tr, 0));
+            a1 = __dadd_rn(a1, walk(tr, 1));
         }
         if (last_chunk) {
             a0 = __dadd_rn(base, a0);
@@ -133,15 +143,15 @@ __global__ void fill_kernel(double* out, int64_t count, double v) {
         out[i] = v;
 }
 
-template <int D>
-static void launch_score(kt_engine* e, const kt_forest* f, const uint64_t* rows, int64_t count, double* out) {
+template <int D, bool WIDE>
+static void launch_score_t(kt_engine* e, const kt_forest* f, const uint64_t* rows, int64_t count, double* out) {
     const int threads = 256;
     const size_t bytes_per_tree = size_t(f->words_per_tree) * 8;
     const size_t smem_cap = 96 * 1024;
     int per_chunk = int(std::max<size_t>(1, smem_cap / bytes_per_tree));
     per_chunk = std::min(per_chunk, f->n_trees);
     const size_t smem = size_t(per_chunk) * bytes_per_tree;
-    auto kern = score_trees_kernel<D>;
+    auto kern = score_trees_kernel<D, WIDE>;
     KT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int occ = occupancy_blocks((const void*)kern, threads, smem);
     int64_t want = ceil_div(count, threads * 2);
@@ -150,9 +160,15 @@ static void launch_score(kt_engine* e, const kt_forest* f, const uint64_t* rows,
         int t1 = std::min(f->n_trees, t0 + per_chunk);
         e->pre_launch("score_trees");
         kern<<<grid, threads, size_t(t1 - t0) * bytes_per_tree, e->stream>>>(
-            f->dev, f->words_per_tree, t0, t1, f->n_trees, f->base, rows, count, out);
+            f->dev, f->words_per_tree, t0, t1, f->n_trees, f->base, rows, count, out, f->fmt);
         e->check_launch("score_trees");
     }
+}
+
+template <int D>
+static void launch_score(kt_engine* e, const kt_forest* f, const uint64_t* rows, int64_t count, double* out) {
+    if (f->wide) launch_score_t<D, true>(e, f, rows, count, out);
+    else launch_score_t<D, false>(e, f, rows, count, out);
 }
 
 void score_trees(kt_engine* e, const kt_forest* f, const uint64_t* rows, int64_t count, double* out) {
@@ -189,10 +205,14 @@ int kt_forest_create(kt_engine* e, int n_knobs, const int32_t* cards, const doub
     using namespace kt;
     if (n_knobs < 1 || n_knobs > kMaxKnobs)
         fail(KT_ERR_UNSUPPORTED, "engine rows hold 1..8 knobs, got " + std::to_string(n_knobs));
-    for (int i = 0; i < n_knobs; ++i)
-        if (cards[i] < 1 || cards[i] > kMaxCard || cards[i] > max_card)
-            fail(KT_ERR_UNSUPPORTED, "knob cardinality must be in [1, 255]");
+    const RowFmt fmt = row_fmt(cards, n_knobs);
+    for (int i = 0; i < n_knobs; ++i) {
+        if (cards[i] > max_card) fail(KT_ERR_VALUE, "feature table narrower than a knob's cardinality");
+        if (!fmt.bytes && cards[i] > 8191) fail(KT_ERR_UNSUPPORTED, "tree cut points support at most 8191 settings");
+    }
     auto* f = new kt_forest();
+    f->fmt = fmt;
+    f->wide = !fmt.bytes;
     f->n_knobs = n_knobs;
     f->n_trees = n_trees;
     f->base = base_score;
@@ -210,7 +230,7 @@ int kt_forest_create(kt_engine* e, int n_knobs, const int32_t* cards, const doub
     f->host.assign(size_t(n_trees) * f->words_per_tree, 0);
     for (int t = 0; t < n_trees; ++t) {
         int lo = node_offset[t];
-        Packer p{D, n_knobs, cards, feature_table, max_card, feature + lo, child_left + lo, child_right + lo,
+        Packer p{D, n_knobs, cards, feature_table, max_card, !fmt.bytes, feature + lo, child_left + lo, child_right + lo,
                  threshold + lo, value + lo, std::vector<uint16_t>((1 << D) - 1, 0), std::vector<double>(1 << D, 0.0)};
         p.fill(0, 0, 0);
         uint64_t* dst = f->host.data() + size_t(t) * f->words_per_tree;

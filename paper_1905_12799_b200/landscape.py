@@ -62,12 +62,12 @@ def load_landscape(path, space) -> SyntheticLandscape:
 class DeviceLandscape:
     def __init__(self, landscape, engine: _lib.Engine):
         n = len(landscape.space.knobs)
-        sp.check_engine_space(landscape.space)
+        cards = sp.check_engine_space(landscape.space)
         centers = np.ascontiguousarray(np.asarray(landscape.centers, dtype=np.int32).reshape(-1, n))
         depths = np.ascontiguousarray(np.asarray(landscape.depths, dtype=np.float64))
         radii = np.ascontiguousarray(np.asarray(landscape.radii, dtype=np.float64))
         h = _lib.P()
-        _lib.call("kt_landscape_create", engine.handle, n, int(centers.shape[0]),
+        _lib.call("kt_landscape_create", engine.handle, n, _lib.as_ptr(cards, _lib.C.c_int32), int(centers.shape[0]),
                   _lib.as_ptr(centers, _lib.C.c_int32), _lib.as_ptr(depths, _lib.C.c_double),
                   _lib.as_ptr(radii, _lib.C.c_double), float(landscape.base_runtime), float(landscape.noise_rel),
                   str(landscape.seed).encode("ascii"), _lib.C.byref(h))

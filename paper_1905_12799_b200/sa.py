@@ -81,7 +81,7 @@ def run_sa_round(params, model, space, starts, seed: int):
     engine = _lib.engine()
     used = idx[: params.chains]
     with engine.scope():
-        start_rows = torch.from_numpy(sp.pack(used).view(np.int64)).to(f"cuda:{engine.device}")
+        start_rows = torch.from_numpy(sp.pack(used, sp.cardinalities(space)).view(np.int64)).to(f"cuda:{engine.device}")
     rows, scores, steps = run_sa_rows(params, model, space, start_rows, seed, engine=engine)
     cls = type(starts[0]) if hasattr(starts[0], "indices") else sp.Configuration
-    return Trajectory(rows, scores, steps, n_knobs=len(space.knobs), config_cls=cls)
+    return Trajectory(rows, scores, steps, n_knobs=len(space.knobs), config_cls=cls, cards=sp.cardinalities(space))

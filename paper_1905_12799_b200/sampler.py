@@ -48,14 +48,14 @@ class VisitedSet:
         return len(self._seen)
 
 
-def visited_rows(visited) -> np.ndarray:
+def visited_rows(visited, cards=None) -> np.ndarray:
     """Packed rows of a VisitedSet (ours or the reference's, whose set is ``_seen``)."""
     seen = getattr(visited, "_seen", None)
     if seen is None:
         raise TypeError("visited set must expose its index tuples (VisitedSet._seen)")
     if not seen:
         return np.zeros(0, dtype=np.uint64)
-    return sp.pack(np.array(sorted(seen), dtype=np.int64))
+    return sp.pack(np.array(sorted(seen), dtype=np.int64), cards)
 
 
 @dataclass(frozen=True)
@@ -66,13 +66,18 @@ class ClusteringResult:
     loss_history: tuple
 
 
-def _lattice_rows(points: np.ndarray) -> np.ndarray:
-    """Engine rows for lattice points; NotImplementedError for anything else."""
+def _lattice_rows(points: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """Engine rows (and the per-dimension extents that fix their layout) for lattice
+    points; NotImplementedError for anything else."""
     if points.shape[1] > sp.MAX_KNOBS:
         raise NotImplementedError("engine k-means supports at most 8 dimensions")
-    if not np.all(np.isfinite(points)) or np.any(points != np.round(points)) or points.min() < 0 or points.max() > 254:
-        raise NotImplementedError("engine k-means runs on lattice points (integer coordinates in [0, 254])")
-    return sp.pack(points.astype(np.int64))
+    if (not np.all(np.isfinite(points)) or np.any(points != np.round(points)) or points.min() < 0
+            or points.max() >= sp.MAX_WIDE_CARD):
+        raise NotImplementedError(f"engine k-means runs on lattice points (integer coordinates in "
+                                  f"[0, {sp.MAX_WIDE_CARD - 1}])")
+    idx = points.astype(np.int64)
+    cards = (idx.max(axis=0) + 1).astype(np.int32)
+    return sp.pack(idx, cards), cards
 
 
 def _device_points(points):
@@ -83,11 +88,11 @@ def _device_points(points):
         pts = pts[:, None]
     if pts.size == 0:
         raise ValueError("kmeans needs at least one point")
-    rows = _lattice_rows(pts)
+    rows, cards = _lattice_rows(pts)
     eng = _lib.engine()
     with eng.scope():
         d = torch.from_numpy(rows.view(np.int64)).to(f"cuda:{eng.device}")
-    return eng, pts, d
+    return eng, pts, d, cards
 
 
 def _n_distinct(eng, d) -> int:
@@ -103,7 +108,7 @@ def _n_distinct(eng, d) -> int:
 
 def kmeans(points, k: int, seed: int) -> ClusteringResult:
     """Lloyd's algorithm with seeded k-means++ starts (sampler.py:72-122), on the device."""
-    eng, pts, d = _device_points(points)
+    eng, pts, d, cards = _device_points(points)
     m, n = pts.shape
     nd = _n_distinct(eng, d)
     if not 1 <= k <= nd:
@@ -114,7 +119,8 @@ def kmeans(points, k: int, seed: int) -> ClusteringResult:
     loss = _lib.C.c_double(0.0)
     passes = _lib.C.c_int32(0)
     with eng.scope():
-        _lib.call("kt_kmeans", eng.handle, _lib.ptr(d), m, n, int(k), int(seed) & (2**64 - 1),
+        _lib.call("kt_kmeans", eng.handle, _lib.ptr(d), m, n, _lib.as_ptr(cards, _lib.C.c_int32), int(k),
+                  int(seed) & (2**64 - 1),
                   _lib.as_ptr(cent, _lib.C.c_double), _lib.as_ptr(asg, _lib.C.c_int64), _lib.C.byref(loss),
                   _lib.as_ptr(hist, _lib.C.c_double), _lib.C.byref(passes))
     return ClusteringResult(centroids=cent, assignment=asg, loss=float(loss.value),
@@ -123,7 +129,7 @@ def kmeans(points, k: int, seed: int) -> ClusteringResult:
 
 def knee_scan(points, seed: int, knee_constant: float = KNEE_CONSTANT, k_max: int = KNEE_K_MAX):
     """Grow k from 8 until knee_constant * Loss(k) > previous loss (sampler.py:125-148)."""
-    eng, pts, d = _device_points(points)
+    eng, pts, d, cards = _device_points(points)
     m, n = pts.shape
     ks = np.zeros(56, dtype=np.int32)
     ls = np.zeros(56, dtype=np.float64)
@@ -135,7 +141,8 @@ def knee_scan(points, seed: int, knee_constant: float = KNEE_CONSTANT, k_max: in
     # the scan itself runs on the distinct points in first-occurrence order only
     # when they are already distinct; duplicates are valid k-means input too
     with eng.scope():
-        _lib.call("kt_knee_scan", eng.handle, _lib.ptr(d), m, n, int(seed) & (2**64 - 1), float(knee_constant),
+        _lib.call("kt_knee_scan", eng.handle, _lib.ptr(d), m, n, _lib.as_ptr(cards, _lib.C.c_int32),
+                  int(seed) & (2**64 - 1), float(knee_constant),
                   int(min(k_max, nd)), _lib.as_ptr(ks, _lib.C.c_int32), _lib.as_ptr(ls, _lib.C.c_double),
                   _lib.C.byref(cnt), _lib.as_ptr(cent, _lib.C.c_double), None)
     scanned = [(int(ks[i]), float(ls[i])) for i in range(cnt.value)]
@@ -147,11 +154,12 @@ def knee_scan(points, seed: int, knee_constant: float = KNEE_CONSTANT, k_max: in
 def mode_config(trajectory, space):
     """Per-knob most frequent index over the trajectory; ties take the smallest (sampler.py:151-158)."""
     eng = _lib.engine()
-    sp.check_engine_space(space)
+    cards = sp.check_engine_space(space)
     rows = trajectory_rows(trajectory, space, eng.device)
     out = np.zeros(sp.MAX_KNOBS, dtype=np.int32)
     with eng.scope():
         _lib.call("kt_mode_vote", eng.handle, _lib.ptr(rows), int(rows.numel()), len(space.knobs),
+                  _lib.as_ptr(cards, _lib.C.c_int32),
                   _lib.as_ptr(out, _lib.C.c_int32))
     return config_class_of(trajectory)(tuple(int(v) for v in out[: len(space.knobs)]))
 
@@ -172,7 +180,7 @@ def adaptive_sample_rows(rows, visited, space, seed: int, knee_constant: float =
     """Array path: device rows (torch int64) -> batch rows (numpy uint64)."""
     eng = engine or _lib.engine()
     cards = sp.check_engine_space(space)
-    vis = visited if isinstance(visited, np.ndarray) else visited_rows(visited)
+    vis = visited if isinstance(visited, np.ndarray) else visited_rows(visited, cards)
     vis = np.ascontiguousarray(vis, dtype=np.uint64)
     batch = np.zeros(64, dtype=np.uint64)
     blen = _lib.C.c_int32(0)
@@ -191,4 +199,4 @@ def adaptive_sample(trajectory, visited, space, seed: int, knee_constant: float 
     rows = trajectory_rows(trajectory, space, eng.device)
     batch = adaptive_sample_rows(rows, visited, space, seed, knee_constant, engine=eng)
     cls = config_class_of(trajectory)
-    return [cls(tuple(r)) for r in sp.unpack(batch, len(space.knobs)).tolist()]
+    return [cls(tuple(r)) for r in sp.unpack(batch, len(space.knobs), sp.cardinalities(space)).tolist()]

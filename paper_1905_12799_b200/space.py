@@ -5,9 +5,11 @@ enough to be interchangeable: every public function here accepts either these
 classes or the reference's own objects (duck typing on ``.knobs``,
 ``.cardinalities``, ``.indices``).
 
-Engine layout: a configuration is one ``uint64`` *row* whose byte i is knob
-i's index (spaces of up to 8 knobs with at most 255 settings each — every
-space of the benchmark workloads; see workloads.py).
+Engine layout: a configuration is one ``uint64`` *row*.  Spaces of up to 8
+knobs with at most 255 settings each use byte i for knob i's index; spaces with
+wider knobs (AlexNet's tile_f has 480 settings) pack minimal-width bit fields,
+knob i in bits [shift_i, shift_i + width_i), at most 63 bits in all
+(``row_layout``; the C side's ``row_fmt`` applies the same rule).
 """
 
 from __future__ import annotations
@@ -20,7 +22,9 @@ import numpy as np
 from . import errors
 
 MAX_KNOBS = 8
-MAX_CARD = 255
+MAX_CARD = 255           # byte layout limit
+MAX_WIDE_CARD = 65535    # bit-field layout limit
+MAX_ROW_BITS = 63
 
 
 @dataclass(frozen=True)
@@ -92,34 +96,64 @@ def knob_names(space) -> list[str]:
     return [k.name for k in space.knobs]
 
 
+def row_layout(cards) -> tuple[np.ndarray, np.ndarray]:
+    """(shifts, widths) of each knob's field in a row; bytes when every card <= 255."""
+    cards = np.asarray(cards, dtype=np.int64).reshape(-1)
+    n = cards.size
+    if not 1 <= n <= MAX_KNOBS:
+        raise NotImplementedError(f"engine rows hold 1..{MAX_KNOBS} knobs; got {n}")
+    if cards.max() <= MAX_CARD:
+        return np.arange(n, dtype=np.int64) * 8, np.full(n, 8, dtype=np.int64)
+    if cards.max() > MAX_WIDE_CARD:
+        raise NotImplementedError(f"engine rows hold knob cardinalities <= {MAX_WIDE_CARD}; got {int(cards.max())}")
+    widths = np.array([max(1, int(c - 1).bit_length()) for c in cards], dtype=np.int64)
+    shifts = np.concatenate([[0], np.cumsum(widths)[:-1]]).astype(np.int64)
+    if int(widths.sum()) > MAX_ROW_BITS:
+        raise NotImplementedError(f"the space's knob indices need {int(widths.sum())} bits; rows hold {MAX_ROW_BITS}")
+    return shifts, widths
+
+
 def check_engine_space(space) -> np.ndarray:
     """Cardinalities as int32, or NotImplementedError if outside the row layout."""
     cards = cardinalities(space)
-    if not 1 <= cards.size <= MAX_KNOBS:
-        raise NotImplementedError(f"engine rows hold 1..{MAX_KNOBS} knobs; space {space.name!r} has {cards.size}")
-    if cards.max() > MAX_CARD:
-        raise NotImplementedError(f"engine rows hold knob cardinalities <= {MAX_CARD}; space {space.name!r} has {int(cards.max())}")
+    try:
+        row_layout(cards)
+    except NotImplementedError as ex:
+        raise NotImplementedError(f"space {space.name!r}: {ex}") from None
     return cards
 
 
 # ------------------------------------------------------------- packing
-def pack(idx) -> np.ndarray:
-    """(N, n) index matrix -> (N,) uint64 rows (byte i = knob i)."""
+def pack(idx, cards=None) -> np.ndarray:
+    """(N, n) index matrix -> (N,) uint64 rows (byte i = knob i, or the bit fields
+    of ``row_layout(cards)`` when a knob has more than 255 settings)."""
     idx = np.asarray(idx)
     if idx.ndim == 1:
         idx = idx[None, :]
     N, n = idx.shape
     if n > MAX_KNOBS:
         raise NotImplementedError(f"engine rows hold at most {MAX_KNOBS} knobs")
-    b = np.zeros((N, 8), dtype=np.uint8)
-    b[:, :n] = idx.astype(np.uint8)
-    return b.view("<u8").reshape(N)
+    if cards is None or int(np.max(cards)) <= MAX_CARD:
+        b = np.zeros((N, 8), dtype=np.uint8)
+        b[:, :n] = idx.astype(np.uint8)
+        return b.view("<u8").reshape(N)
+    shifts, _ = row_layout(cards)
+    rows = np.zeros(N, dtype=np.uint64)
+    for k in range(n):
+        rows |= idx[:, k].astype(np.uint64) << np.uint64(shifts[k])
+    return rows
 
 
-def unpack(rows, n: int) -> np.ndarray:
+def unpack(rows, n: int, cards=None) -> np.ndarray:
     """(N,) uint64 rows -> (N, n) int64 index matrix."""
     r = np.ascontiguousarray(np.asarray(rows).astype("<u8", copy=False).view(np.uint64))
-    return r.view(np.uint8).reshape(-1, 8)[:, :n].astype(np.int64)
+    if cards is None or int(np.max(cards)) <= MAX_CARD:
+        return r.view(np.uint8).reshape(-1, 8)[:, :n].astype(np.int64)
+    shifts, widths = row_layout(cards)
+    out = np.empty((r.size, n), dtype=np.int64)
+    for k in range(n):
+        out[:, k] = ((r >> np.uint64(shifts[k])) & np.uint64((1 << int(widths[k])) - 1)).astype(np.int64)
+    return out
 
 
 def validate_index_matrix(space, idx: np.ndarray) -> None:
@@ -156,8 +190,8 @@ def index_matrix(space, configs) -> np.ndarray:
 
 
 def rows_from_configs(space, configs) -> np.ndarray:
-    return pack(index_matrix(space, configs))
+    return pack(index_matrix(space, configs), cardinalities(space))
 
 
-def configs_from_rows(rows, n: int, cls=Configuration) -> list:
-    return [cls(tuple(r)) for r in unpack(rows, n).tolist()]
+def configs_from_rows(rows, n: int, cls=Configuration, cards=None) -> list:
+    return [cls(tuple(r)) for r in unpack(rows, n, cards).tolist()]

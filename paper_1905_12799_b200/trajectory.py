@@ -16,7 +16,7 @@ from . import space as sp
 
 
 class Trajectory:
-    def __init__(self, rows, scores, step_indices=None, n_knobs: int = 0, config_cls=sp.Configuration):
+    def __init__(self, rows, scores, step_indices=None, n_knobs: int = 0, config_cls=sp.Configuration, cards=None):
         if int(rows.shape[0]) == 0:
             raise ValueError("trajectory is empty")
         if int(scores.shape[0]) != int(rows.shape[0]):
@@ -28,6 +28,7 @@ class Trajectory:
         self._scores = scores
         self._steps = step_indices
         self.n_knobs = int(n_knobs)
+        self.cards = None if cards is None else np.asarray(cards, dtype=np.int64)  # row layout (space.row_layout)
         self.config_cls = config_cls
         self._entries = None
 
@@ -53,7 +54,7 @@ class Trajectory:
         return self._scores
 
     def index_matrix(self) -> np.ndarray:
-        return sp.unpack(self.rows_numpy(), self.n_knobs)
+        return sp.unpack(self.rows_numpy(), self.n_knobs, self.cards)
 
     # --------------------------------------------------- reference interface
     @property

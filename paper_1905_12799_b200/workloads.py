@@ -106,6 +106,16 @@ RESNET18_TASKS = (
     DenseLayer("resnet18.dense_512x1000", 512, 1000),
 )
 
+# AlexNet's 5 conv layers (configs[1]); conv3-conv5 have tile_f cardinality 480 / 165,
+# beyond one byte per knob, so their rows use the variable-width layout (space.row_layout).
+ALEXNET_TASKS = (
+    ConvLayer("alexnet.c1_11x11_3x96_55", 3, 96, 55, 11),
+    ConvLayer("alexnet.c2_5x5_96x256_27", 96, 256, 27, 5),
+    ConvLayer("alexnet.c3_3x3_256x384_13", 256, 384, 13, 3),
+    ConvLayer("alexnet.c4_3x3_384x384_13", 384, 384, 13, 3),
+    ConvLayer("alexnet.c5_3x3_384x256_13", 384, 256, 13, 3),
+)
+
 VGG16_TASKS = (
     ConvLayer("vgg16.c1_3x3_3x64_224", 3, 64, 224, 3),
     ConvLayer("vgg16.c2_3x3_64x64_224", 64, 64, 224, 3),

@@ -336,6 +336,95 @@ def make_task_models():
         (out / f"resnet18_task{i}.json").write_text(json.dumps(doc, sort_keys=True))
 
 
+def make_alexnet_models():
+    """Surrogates + landscapes for AlexNet's 5 conv tasks (configs[1]; bit-field rows)."""
+    from paper_1905_12799_b200.workloads import ALEXNET_TASKS
+
+    out = ROOT / "data" / "models"
+    models = {}
+    for i, task in enumerate(ALEXNET_TASKS):
+        space = space_from_dict(task.space_dict())
+        land = gen_landscape(space, seed=300 + i)
+        model = landscape_model(space, land, 500, 400 + i)
+        doc = {"values": values_of(space), "model": json.loads(model.to_json()), "space": space.name,
+               "landscape": landscape_to_dict(land)}
+        (out / f"alexnet_task{i}.json").write_text(json.dumps(doc, sort_keys=True))
+        models[f"alexnet{i}"] = (space, model, land)
+    return models
+
+
+def gen_wide():
+    """Golden vectors on spaces whose knobs exceed 255 settings (AlexNet conv3/conv4,
+    plus a synthetic 8-knob space near the 63-bit row limit): every path once."""
+    rng = np.random.default_rng(480)
+    alex = make_alexnet_models()
+    arrays, meta = {}, {"models": {}, "adaptive": {}, "sa": {}, "rl": {}}
+    wide8 = space_from_dict({"name": "wide8", "knobs": [{"name": f"k{i}", "values": list(range(c))}
+                                                        for i, c in enumerate((300, 257, 1000, 9, 2, 3, 70, 5))]})
+    land_w8 = gen_landscape(wide8, seed=5)
+    models = {"alexnet2": alex["alexnet2"][:2], "alexnet3": alex["alexnet3"][:2],
+              "wide8": (wide8, landscape_model(wide8, land_w8, 400, 6))}
+    for name, (space, model) in models.items():
+        meta["models"][name] = {"values": values_of(space), "model": json.loads(model.to_json()), "space": space.name}
+        cards = np.array(space.cardinalities)
+        idx = rng.integers(0, cards, size=(3000, len(cards)))
+        idx = np.vstack([idx, np.zeros(len(cards), dtype=np.int64), cards - 1])
+        arrays[f"predict/{name}/idx"] = idx
+        arrays[f"predict/{name}/scores"] = predict(model, space, [Configuration(tuple(r)) for r in idx.tolist()])
+    for name, space, land in (("alexnet3", alex["alexnet3"][0], alex["alexnet3"][2]), ("wide8", wide8, land_w8)):
+        cards = np.array(space.cardinalities)
+        idx = rng.integers(0, cards, size=(1500, len(cards)))
+        idx = np.vstack([idx] + [np.array(c, dtype=np.int64)[None, :] for c in land.centers])
+        arrays[f"landscape/{name}/idx"] = idx
+        arrays[f"landscape/{name}/runtime"] = np.array([synthetic_runtime(land, Configuration(tuple(r)))
+                                                        for r in idx.tolist()])
+        meta["models"][name]["landscape"] = landscape_to_dict(land)
+    # adaptive sampling (dedup, knee k-means, mode vote, batch) on wide points
+    a3, m3 = models["alexnet3"]
+    agent = init_agent(a3, AgentHyperparams(episodes_per_round=128), seed=8)
+    st = np.random.default_rng(9)
+    starts = [random_config(a3, st) for _ in range(128)]
+    tr = run_search_round(agent, m3, a3, starts)
+    cases = [("alexnet3_rl_round", a3, idx_of(tr.configs()), [tuple(r) for r in idx_of(starts).tolist()], 4242),
+             ("alexnet3_uniform", a3, rng.integers(0, np.array(a3.cardinalities), size=(4000, 8)), [], 7),
+             ("wide8_uniform", wide8, rng.integers(0, np.array(wide8.cardinalities), size=(3000, 8)), [], 8)]
+    for name, space, pts, vis, seed in cases:
+        batch = adaptive_sample(traj_of(np.asarray(pts)), VisitedSet([Configuration(v) for v in vis]), space, seed=seed)
+        arrays[f"adaptive/{name}/idx"] = np.asarray(pts, dtype=np.int64)
+        arrays[f"adaptive/{name}/visited"] = np.array(vis, dtype=np.int64).reshape(-1, space.n_knobs)
+        arrays[f"adaptive/{name}/batch"] = idx_of(batch).reshape(-1, space.n_knobs)
+        arrays[f"adaptive/{name}/mode"] = np.array(mode_config(traj_of(np.asarray(pts)), space).indices, dtype=np.int64)
+        meta["adaptive"][name] = {"cards": list(space.cardinalities), "seed": seed, "model": space.name}
+    # SA chains (default params) on the wide surrogate
+    for name, mname, params, n_starts, seed in (("alexnet3_64x128", "alexnet3", SAParams(), 64, 77),
+                                                ("wide8_32x64", "wide8", SAParams(chains=32, steps_per_round=64), 20, 5)):
+        space, model = models[mname]
+        r = np.random.default_rng(seed)
+        starts = [random_config(space, r) for _ in range(n_starts)]
+        tr = run_sa_round(params, model, space, starts, seed)
+        arrays[f"sa/{name}/starts"] = idx_of(starts)
+        arrays[f"sa/{name}/idx"] = idx_of(tr.configs())
+        arrays[f"sa/{name}/scores"] = tr.scores()
+        arrays[f"sa/{name}/steps"] = np.array(tr.step_indices, dtype=np.int64)
+        meta["sa"][name] = {"model": mname, "chains": params.chains, "steps": params.steps_per_round,
+                            "initial_temperature": params.initial_temperature, "cooling": params.cooling, "seed": seed}
+    # one PPO search round (trajectory bit-exact, update at the TF32 tier)
+    hyper = AgentHyperparams(episodes_per_round=256)
+    agent = init_agent(a3, hyper, seed=12)
+    st = np.random.default_rng(13)
+    starts = [random_config(a3, st) for _ in range(256)]
+    arrays["rl/alexnet3/params0"] = nets.flatten_params(agent.params)
+    tr = run_search_round(agent, m3, a3, starts)
+    arrays["rl/alexnet3/starts"] = idx_of(starts)
+    arrays["rl/alexnet3/idx"] = idx_of(tr.configs())
+    arrays["rl/alexnet3/scores"] = tr.scores()
+    arrays["rl/alexnet3/steps"] = np.array(tr.step_indices, dtype=np.int64)
+    arrays["rl/alexnet3/params"] = nets.flatten_params(agent.params)
+    meta["rl"]["alexnet3"] = {"model": "alexnet3", "hyper": hyper.to_dict(), "seed": 12}
+    np.savez_compressed(HERE / "wide.npz", **arrays)
+    (HERE / "wide.json").write_text(json.dumps(meta, sort_keys=True))
+
+
 def main():
     make_task_models()
     rng = np.random.default_rng(20261017)
@@ -362,8 +451,14 @@ def main():
     arrays, meta = gen_rl(models)
     np.savez_compressed(HERE / "rl.npz", **arrays)
     (HERE / "rl.json").write_text(json.dumps(meta, sort_keys=True))
+    gen_wide()
     print("golden vectors written to", HERE)
 
 
 if __name__ == "__main__":
-    main()
+    import sys
+
+    if sys.argv[1:] == ["wide"]:  # only the bit-field-layout fixtures (leaves the others untouched)
+        gen_wide()
+    else:
+        main()

@@ -9,7 +9,7 @@ import pytest
 import paper_1905_12799_b200 as kt
 from paper_1905_12799_b200 import _lib, space as sp
 from paper_1905_12799_b200.sa import seed_words
-from paper_1905_12799_b200.workloads import RESNET18_S2, RESNET18_TASKS, VGG16_TASKS
+from paper_1905_12799_b200.workloads import ALEXNET_TASKS, RESNET18_S2, RESNET18_TASKS, VGG16_TASKS
 
 ROOT = Path(__file__).resolve().parent.parent
 
@@ -97,14 +97,49 @@ def test_engine_space_limits():
     with pytest.raises(NotImplementedError):
         sp.check_engine_space(sp.grid(*([2] * 9)))
     with pytest.raises(NotImplementedError):
-        sp.check_engine_space(sp.grid(256))
+        sp.check_engine_space(sp.grid(65536))
+    with pytest.raises(NotImplementedError):  # 8 x 9 bits > 63
+        sp.check_engine_space(sp.grid(*([300] * 8)))
+    sp.check_engine_space(sp.grid(256))  # wide layout: one 8-bit field
+
+
+def test_row_layout_wide_spaces():
+    shifts, widths = sp.row_layout([480, 4, 4, 16, 2, 2, 3, 2])  # AlexNet conv4
+    assert widths.tolist() == [9, 2, 2, 4, 1, 1, 2, 1]
+    assert shifts.tolist() == [0, 9, 11, 13, 17, 18, 19, 21]
+    assert sp.row_layout([84, 80, 80, 7, 2, 2, 3, 2])[0].tolist() == [0, 8, 16, 24, 32, 40, 48, 56]
+    rng = np.random.default_rng(0)
+    for cards in ([480, 4, 4, 16, 2, 2, 3, 2], [256], [65535, 2, 3], [300, 300, 300, 300, 300, 300, 300]):
+        idx = rng.integers(0, np.array(cards), size=(1000, len(cards)))
+        rows = sp.pack(idx, cards)
+        assert np.array_equal(sp.unpack(rows, len(cards), cards), idx)
+        assert len(np.unique(rows)) == len(np.unique(idx, axis=0))  # injective
+        assert not np.any(rows == np.uint64(2**64 - 1))  # never the dedup sentinel
+
+
+def test_c_row_layout_matches_python():
+    lib = kt._lib.load()
+    C = kt._lib.C
+    for cards in ([84, 80, 80, 7, 2, 2, 3, 2], [480, 4, 4, 16, 2, 2, 3, 2], [165, 20, 20, 12, 2, 2, 3, 2], [1], [256],
+                  [65535, 7], [300] * 7):
+        c = np.array(cards, dtype=np.int32)
+        sh = np.zeros(len(cards), dtype=np.int32)
+        wd = np.zeros(len(cards), dtype=np.int32)
+        assert lib.kt_row_layout(c.ctypes.data_as(C.POINTER(C.c_int32)), len(cards),
+                                 sh.ctypes.data_as(C.POINTER(C.c_int32)), wd.ctypes.data_as(C.POINTER(C.c_int32))) == 0
+        ps, pw = sp.row_layout(cards)
+        assert sh.tolist() == ps.tolist() and wd.tolist() == pw.tolist()
+    bad = np.array([300] * 8, dtype=np.int32)
+    sh = np.zeros(8, dtype=np.int32)
+    assert lib.kt_row_layout(bad.ctypes.data_as(C.POINTER(C.c_int32)), 8, sh.ctypes.data_as(C.POINTER(C.c_int32)),
+                             sh.ctypes.data_as(C.POINTER(C.c_int32))) == kt._lib.KT_ERR_UNSUPPORTED
 
 
 def test_workload_spaces():
     cards = [len(v) for _, v in RESNET18_S2.knobs()]
     assert cards == [84, 80, 80, 7, 2, 2, 3, 2]
     assert int(np.prod(cards)) == 90_316_800
-    for t in RESNET18_TASKS + VGG16_TASKS:
+    for t in RESNET18_TASKS + VGG16_TASKS + ALEXNET_TASKS:
         sp.check_engine_space(sp.space_from_dict(t.space_dict()))
 
 

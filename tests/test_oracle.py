@@ -199,3 +199,60 @@ def test_ppo_gradient_finite_differences():
             an = grads[key].flat[i]
             worst = max(worst, abs(fd - an) / max(1e-6, abs(fd), abs(an)))
     assert worst < 1e-4
+
+
+# ------------------------------------------------ wide spaces (knobs > 255 settings)
+def _wide(kind):
+    return sorted(meta("wide")[kind])
+
+
+@pytest.mark.parametrize("name", ["alexnet2", "alexnet3", "wide8"])
+def test_wide_predict_matches_reference(name):
+    m = meta("wide")["models"][name]
+    g = npz("wide")
+    X = otrees.featurize_rows(m["values"], g[f"predict/{name}/idx"])
+    assert np.array_equal(otrees.predict_features(m["model"], X), g[f"predict/{name}/scores"])
+
+
+@pytest.mark.parametrize("name", ["alexnet3", "wide8"])
+def test_wide_landscape_matches_reference(name):
+    m = meta("wide")["models"][name]
+    g = npz("wide")
+    got = oland.synthetic_runtimes(m["landscape"], g[f"landscape/{name}/idx"])
+    assert np.array_equal(got, g[f"landscape/{name}/runtime"])
+
+
+@pytest.mark.parametrize("name", _wide("adaptive"))
+def test_wide_adaptive_sample_matches_reference(name):
+    g = npz("wide")
+    md = meta("wide")["adaptive"][name]
+    visited = {tuple(r) for r in g[f"adaptive/{name}/visited"].tolist()}
+    batch = osamp.adaptive_sample(g[f"adaptive/{name}/idx"], visited, md["cards"], md["seed"])
+    assert batch == [tuple(r) for r in g[f"adaptive/{name}/batch"].tolist()]
+    assert osamp.mode_vote(g[f"adaptive/{name}/idx"], md["cards"]) == tuple(g[f"adaptive/{name}/mode"].tolist())
+
+
+@pytest.mark.parametrize("name", _wide("sa"))
+def test_wide_sa_matches_reference(name):
+    g = npz("wide")
+    md = meta("wide")["sa"][name]
+    m = meta("wide")["models"][md["model"]]
+    idx, scores, steps = osa.run_sa_round(m["model"], m["values"], g[f"sa/{name}/starts"], md["seed"],
+                                          chains=md["chains"], steps=md["steps"],
+                                          initial_temperature=md["initial_temperature"], cooling=md["cooling"])
+    assert np.array_equal(idx, g[f"sa/{name}/idx"])
+    assert np.array_equal(scores, g[f"sa/{name}/scores"])
+    assert np.array_equal(steps, g[f"sa/{name}/steps"])
+
+
+def test_wide_search_round_matches_reference():
+    g = npz("wide")
+    md = meta("wide")["rl"]["alexnet3"]
+    m = meta("wide")["models"]["alexnet3"]
+    agent = oagent.new_agent(len(m["values"]), md["hyper"], md["seed"])
+    assert np.array_equal(_flat(agent["params"]), g["rl/alexnet3/params0"])
+    idx, scores, steps = oagent.search_round(agent, m["model"], m["values"], g["rl/alexnet3/starts"], md["hyper"])
+    assert np.array_equal(idx, g["rl/alexnet3/idx"])
+    assert np.array_equal(scores, g["rl/alexnet3/scores"])
+    assert np.array_equal(steps, g["rl/alexnet3/steps"])
+    assert np.array_equal(_flat(agent["params"]), g["rl/alexnet3/params"])

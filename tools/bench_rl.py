@@ -1,10 +1,11 @@
-"""bench.py --workload rl: the PPO + adaptive-sampling tuning step (configs[1]-shaped).
+"""bench.py --workload rl: the PPO + adaptive-sampling tuning step of configs[1].
 
-Per step and rank: 5 independent ResNet-18 conv tasks, each runs one search round
+Per step and rank: AlexNet's 5 conv tasks (workloads.ALEXNET_TASKS; surrogates
+and landscapes in data/models/alexnet_task*.json), each runs one search round
 with 4096 PPO agents (K1 rollout, K2 scoring, K4 GAE, K5 PPO update) followed by
 adaptive_sample on its trajectory (K6/K7/K8/K9).  Metric: trajectory candidates
-scored + clustered per second.  (AlexNet's 5 tasks need knob cardinalities > 255,
-outside the engine's uint8 row layout; the ResNet-18 tasks have the same shape.)
+scored + clustered per second.  conv3/conv4 have tile_f cardinality 480, so
+their rows use the bit-field layout (space.row_layout).
 """
 
 from __future__ import annotations
@@ -20,7 +21,7 @@ N_TASKS, AGENTS = 5, 4096
 
 
 def task_docs():
-    return [json.loads((ROOT / "data" / "models" / f"resnet18_task{i}.json").read_text()) for i in range(N_TASKS)]
+    return [json.loads((ROOT / "data" / "models" / f"alexnet_task{i}.json").read_text()) for i in range(N_TASKS)]
 
 
 def cpu_rl_step(docs, rng_seed: int, agents: int):
@@ -54,7 +55,7 @@ def run(args, rank: int, world: int, local_rank: int, kt, torch, dist, helpers) 
         agent = kt.init_agent(space, kt.AgentHyperparams(episodes_per_round=AGENTS), seed=1000 * rank + i)
         cards = np.array(space.cardinalities)
         host_starts = [torch.from_numpy(sp.pack(np.random.default_rng(100 * rank + 10 * i + s)
-                                                .integers(0, cards, size=(AGENTS, cards.size))).view(np.int64))
+                                                .integers(0, cards, size=(AGENTS, cards.size)), cards).view(np.int64))
                        .pin_memory() for s in range(2)]
         tasks.append((space, model, agent, host_starts))
     no_visited = np.zeros(0, dtype=np.uint64)
@@ -125,7 +126,7 @@ def run(args, rank: int, world: int, local_rank: int, kt, torch, dist, helpers) 
         "metric": "candidate configs scored+clustered/sec per tuning step", "value": value, "unit": "candidates/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+fp32/tf32", "data": "synthetic",
-        "config": {"workload": f"{N_TASKS} ResNet-18 conv tasks x {AGENTS} PPO agents per step: run_search_round "
+        "config": {"workload": f"AlexNet's {N_TASKS} conv tasks x {AGENTS} PPO agents per step: run_search_round "
                                f"(rollout, scoring, GAE, 3 PPO epochs) + adaptive_sample per task",
                    "candidates_per_step": n_total / args.steps / world, "parallelism": f"tasks x{world}",
                    "l2": "flushed between steps"},
