@@ -405,14 +405,18 @@ __global__ void __launch_bounds__(kInitThreads) init_kernel(InitArgs a) {
 
 // ================================================================= Lloyd (K8)
 // One cooperative launch runs Lloyd iterations for up to 8 values of k at once
-// (speculative knee scan): every pass reads each point once and assigns it
-// under every active k.  Per point and k the kernel keeps Hamerly bounds —
-// u >= |p - c_a|, l <= min_{j != a} |p - c_j| — maintained with directed
-// rounding and widened by each centroid's drift; a point whose bounds prove
-// its assignment cannot change is skipped (no distance work).  Points that are
-// re-evaluated use fp32 distances with a proven error bound, and the
-// reference's float64 expression whenever the bound cannot separate the two
-// nearest centroids, so assignments equal numpy's argmin bit for bit.
+// (speculative knee scan): every pass visits each point once under every
+// active k.  Per point and k the kernel keeps ONE float, a Hamerly "budget":
+// when the point was last evaluated (pass s) with bounds u >= |p - c_a| and
+// l <= min_{j != a} |p - c_j|, it stores b = (l - u) + D_a(s), where D_a is a
+// per-cluster running sum (directed rounding, every block computes the same
+// table) of the amount pass t can shrink l - u: drift_a(t) + the largest drift
+// of any other centroid.  At pass t the assignment provably cannot change while
+// b - D_a(t) > margin, so a settled point costs a 1-byte assignment and a
+// 4-byte budget read — no row, no distance, no write.  Points that are
+// re-evaluated fetch their row and use fp32 distances with a proven error bound,
+// and the reference's float64 expression whenever the bound cannot separate
+// the two nearest centroids, so assignments equal numpy's argmin bit for bit.
 // Cluster sums are exact integers, updated by the deltas of points that
 // changed cluster; every block keeps an identical copy and derives the next
 // centroids itself, so an iteration needs one grid barrier.
@@ -447,9 +451,13 @@ struct LloydArgs {
     int coff[kMaxRuns];
     int K;  // total clusters
     int it0, it_end, max_iters;
-    int64_t stride;            // per-run row stride of assign/bounds (m rounded up to 16)
+    int64_t stride;            // per-run row stride of assign/budget (m rounded up to 16)
     uint8_t* assign;           // [R][stride], 255 = unassigned
-    float2* bounds;            // [R][stride] (u, l)
+    float* budget;             // [R][stride] (l - u) + D_a(s) of the last evaluation
+    float* dcum;               // [K] cumulative bound shrink D_j (carried across launches)
+    int64_t per_block;         // resident kernel: points owned by each block (multiple of 16)
+    int tile;                  // resident kernel: points per queue tile (multiple of 4)
+    int rows_resident;         // resident kernel: the block's rows live in shared memory too
     double* cent;              // [K][8] centroids of the latest pass
     const uint64_t* init_rows; // k-means++ rows (prefix shared by all runs)
     long long* S;              // [K][9] running sums
@@ -459,12 +467,12 @@ struct LloydArgs {
     int* run_state;            // [R]
     int* run_iter;             // [R]
     int* ctrl;                 // [0] next iteration
-    unsigned long long* stats; // optional [R][3]: bound-skips, tightened skips, full evaluations
+    unsigned long long* stats; // optional [R][3]: point visits, unused, evaluations
     long long* timeline;       // optional [100][4] globaltimer stamps of block 0 per pass
 };
 
 struct LloydLayout {
-    size_t S, c64, c32, delta, drift, total;
+    size_t S, c64, c32, delta, drift, dcum, total;
 };
 
 __host__ __device__ inline LloydLayout lloyd_layout(int K) {
@@ -480,15 +488,15 @@ __host__ __device__ inline LloydLayout lloyd_layout(int K) {
     o += size_t(K) * kDeltaW * 4;
     L.drift = o;
     o += size_t(K) * 4;
+    L.dcum = o;
+    o += size_t(K) * 4;
     L.total = (o + 15) & ~size_t(15);
     return L;
 }
 
 struct LloydQueueEntry {
-    uint64_t row;
     uint32_t point;
     int32_t old;
-    float u, l;
 };
 constexpr int kLloydThreads = 256;
 
@@ -512,8 +520,10 @@ __device__ __forceinline__ float dist_dn(float d2, float k1) {
     const float lo = __fsub_rd(d2, d2_bound(d2, k1));
     return lo > 0.0f ? __fsqrt_rd(lo) : 0.0f;
 }
-// u < l with a margin far above float64 rounding of the reference's distances
-__device__ __forceinline__ bool surely_less(float u, float l) { return __fadd_ru(u, 1e-6f * (u + 1.0f)) < l; }
+// Settled iff (l - u) > margin: distances are <= 255*sqrt(8) ~ 721, so float64
+// rounding of the reference's squared distances (< 1e-10) cannot reorder two
+// centroids whose true distances differ by this much.
+constexpr float kSettleMargin = 1e-3f;
 
 __device__ __forceinline__ void unpack_row(uint64_t row, float p[kMaxKnobs], const RowFmt& f) {
     if (!f.bytes) {
@@ -582,11 +592,59 @@ __device__ __forceinline__ int full_assign(const float* c32, const double* c64, 
     return bj;
 }
 
-__global__ void __launch_bounds__(256, 3) lloyd_kernel(LloydArgs a) {
+// Resident variant: block b owns points [b*P, (b+1)*P) for the whole launch and
+// keeps their assignments and budgets in shared memory, so a settled point costs
+// two shared-memory reads per pass and no global traffic at all; the points the
+// budgets cannot settle go through a block-wide queue (tiles of `tile` points,
+// so the queue never overflows) and only they fetch their rows from L2.
+constexpr int kLloydResThreads = 512;
+constexpr int kLloydQueueMax = 16384;  // block queue entries (point | run << 16 | old << 24)
+constexpr int kLloydQueueMin = 2048;
+
+// Shared-memory bytes of the resident kernel before the queue: tables, [R][P]
+// assignments, [R][P] budgets and (optionally) the block's P rows.
+__host__ __device__ inline size_t lloyd_resident_bytes(int K, int R, int64_t P, bool rows) {
+    return lloyd_layout(K).total + ((size_t(R) * P + 15) & ~size_t(15)) + size_t(R) * P * 4 + (rows ? size_t(P) * 8 : 0);
+}
+
+// Evaluate one point under run r: full assignment, new budget, deltas of a move.
+__device__ __forceinline__ int lloyd_eval(const LloydArgs& a, const float* c32, const double* c64, const float* dcum,
+                                          int* delta, int r, uint64_t row, int old, float& budget) {
+    const int co = a.coff[r];
+    float p[kMaxKnobs];
+    unpack_row(row, p, a.fmt);
+    float u, l;
+    const int j = full_assign(c32 + co * kMaxKnobs, c64 + co * kMaxKnobs, row, p, a.k[r], a.n, a.fmt, a.bk1, u, l);
+    budget = __fadd_rd(__fsub_rd(l, u), dcum[co + j]);
+    if (j != old) {
+        int* dn = delta + (co + j) * kDeltaW;
+        for (int c = 0; c < a.n; ++c) {
+            const int v = a.fmt.get(row, c);
+            atomicAdd(dn + c, v & 0xff);
+            if (v >> 8) atomicAdd(dn + 9 + c, v >> 8);
+        }
+        atomicAdd(dn + 8, 1);
+        if (old != 255) {
+            int* dold = delta + (co + old) * kDeltaW;
+            for (int c = 0; c < a.n; ++c) {
+                const int v = a.fmt.get(row, c);
+                atomicSub(dold + c, v & 0xff);
+                if (v >> 8) atomicSub(dold + 9 + c, v >> 8);
+            }
+            atomicSub(dold + 8, 1);
+        }
+    }
+    return j;
+}
+
+template <bool RESIDENT>
+__global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, RESIDENT ? 1 : 3)
+    lloyd_kernel(LloydArgs a) {
     extern __shared__ __align__(16) unsigned char s_dyn[];
     __shared__ RunShared rs;
     __shared__ uint8_t run_of[kMaxClusters];
-    __shared__ LloydQueueEntry wqueue[kLloydThreads / 32 * 128];
+    __shared__ LloydQueueEntry wqueue[RESIDENT ? 1 : kLloydThreads / 32 * 128];
+    __shared__ int s_qn[2];
     // the dynamic window is only guaranteed 8-byte aligned after static smem (tools add their
     // own static smem): align explicitly for the float4 centroid loads (16 spare bytes allocated)
     unsigned char* s_raw = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(s_dyn) + 15) & ~uintptr_t(15));
@@ -596,18 +654,42 @@ __global__ void __launch_bounds__(256, 3) lloyd_kernel(LloydArgs a) {
     float* c32 = reinterpret_cast<float*>(s_raw + L.c32);
     int* delta = reinterpret_cast<int*>(s_raw + L.delta);
     float* drift = reinterpret_cast<float*>(s_raw + L.drift);
+    float* dcum = reinterpret_cast<float*>(s_raw + L.dcum);
     cg::grid_group grid = cg::this_grid();
     const int tid = threadIdx.x;
     const int K = a.K, R = a.R, n = a.n;
     const int64_t m = a.m;
+    const int lane = tid & 31;
+
+    // resident state of this block's points
+    const int64_t P = a.per_block;
+    const int64_t b0 = RESIDENT ? int64_t(blockIdx.x) * P : 0;
+    const int np = RESIDENT ? int(b0 < m ? (m - b0 < P ? m - b0 : P) : 0) : 0;
+    uint8_t* s_asg = s_raw + L.total;                                          // [R][P]
+    float* s_bud = reinterpret_cast<float*>(s_asg + ((size_t(R) * P + 15) & ~size_t(15)));  // [R][P]
+    uint64_t* s_rows = reinterpret_cast<uint64_t*>(s_bud + size_t(R) * P);   // [P] if rows_resident
+    uint32_t* s_queue = reinterpret_cast<uint32_t*>(s_rows + (a.rows_resident ? P : 0));  // [tile * R]
 
     for (int i = tid; i < K * kSumW; i += blockDim.x) S[i] = a.S[i];
     for (int i = tid; i < K * kMaxKnobs; i += blockDim.x) c64[i] = a.cent[i];  // centroids of the previous pass
+    for (int i = tid; i < K; i += blockDim.x) dcum[i] = a.dcum[i];
     if (tid < R) rs.state[tid] = a.run_state[tid];
     if (tid < kMaxRuns * 3) rs.cnt[tid / 3][tid % 3] = 0;
+    if (tid < 2) s_qn[tid] = 0;
     for (int r = 0; r < R; ++r)
         for (int j = tid; j < a.k[r]; j += blockDim.x) run_of[a.coff[r] + j] = uint8_t(r);
-    grid.sync();  // every block has read a.cent before block 0 overwrites it
+    if (RESIDENT) {
+        for (int r = 0; r < R; ++r) {
+            for (int i = tid; i < np; i += blockDim.x) {
+                s_asg[r * P + i] = a.assign[int64_t(r) * a.stride + b0 + i];
+                s_bud[r * P + i] = a.budget[int64_t(r) * a.stride + b0 + i];
+            }
+            for (int i = np + tid; i < ((np + 3) & ~3); i += blockDim.x) s_asg[r * P + i] = 255;  // quad padding
+        }
+        if (a.rows_resident)
+            for (int i = tid; i < np; i += blockDim.x) s_rows[i] = a.pts[b0 + i];
+    }
+    grid.sync();  // every block has read a.cent / a.dcum before block 0 overwrites them
 
     int it = a.it0;
     auto stamp = [&](int phase) {
@@ -617,6 +699,7 @@ __global__ void __launch_bounds__(256, 3) lloyd_kernel(LloydArgs a) {
             a.timeline[it * 4 + phase] = t;
         }
     };
+    int tile_parity = 0;
     while (it < a.it_end) {
         stamp(0);
         // ---- this pass's centroids and each centroid's drift from the previous pass:
@@ -666,132 +749,183 @@ __global__ void __launch_bounds__(256, 3) lloyd_kernel(LloydArgs a) {
             rs.amax[tid] = am;
         }
         __syncthreads();
+        // ---- cumulative shrink of (l - u): own drift + largest drift among the other centroids
+        for (int g = tid; g < K; g += blockDim.x) {
+            const int r = run_of[g];
+            const int st = rs.state[r];
+            if (!run_active(st)) continue;
+            if (st != kActiveFromSums) {
+                dcum[g] = 0.0f;  // every point is evaluated afresh this pass
+            } else {
+                const float other = (g - a.coff[r]) == rs.amax[r] ? rs.m2[r] : rs.m1[r];
+                dcum[g] = __fadd_ru(dcum[g], __fadd_ru(drift[g], other));
+            }
+        }
+        __syncthreads();
 
         stamp(1);
-        // ---- assignment pass.  Per warp and round: each lane filters 4 consecutive
-        // points with its Hamerly bounds; the points the bounds cannot settle are
-        // queued in shared memory and then evaluated by all 32 lanes together.
-        const int64_t nq = (m + 3) >> 2;
-        const int lane = tid & 31;
-        LloydQueueEntry* queue = wqueue + (tid >> 5) * 128;
-        // warps grab 32-quad chunks from a per-pass counter: work-balanced passes
-        unsigned int* work = a.work + (it % 3);
-        while (true) {
-            unsigned int chunk = 0;
-            if (lane == 0) chunk = atomicAdd(work, 32u);
-            chunk = __shfl_sync(0xffffffffu, chunk, 0);
-            if (int64_t(chunk) >= nq) break;
-            const int64_t q = int64_t(chunk) + lane;
-            const int64_t p0 = q << 2;
-            const int cnt = q < nq ? int(m - p0 < 4 ? m - p0 : 4) : 0;
-            // the quad's rows are fetched with its state (one round trip) and ride in the queue
-            uint64_t rw[4] = {0, 0, 0, 0};
-            if (cnt == 4) {
-                const ulonglong2 v0 = __ldg(reinterpret_cast<const ulonglong2*>(a.pts + p0));
-                const ulonglong2 v1 = __ldg(reinterpret_cast<const ulonglong2*>(a.pts + p0 + 2));
-                rw[0] = v0.x, rw[1] = v0.y, rw[2] = v1.x, rw[3] = v1.y;
-            } else {
+        if constexpr (RESIDENT) {
+            // ---- assignment pass over this block's resident points, one tile at a time
+            for (int t0 = 0; t0 < np; t0 += a.tile) {
+                const int t1 = t0 + a.tile < np ? t0 + a.tile : np;
+                int* qn = s_qn + tile_parity;
+                // scan: one quad per thread and round; unsettled (point, run, old) -> block queue
+                for (int qd0 = t0 >> 2; qd0 < ((t1 + 3) >> 2); qd0 += blockDim.x) {
+                    const int qd = qd0 + tid;
+                    const bool valid = qd < ((t1 + 3) >> 2);
+                    const int p0 = qd << 2;
+                    const int cnt = valid ? (t1 - p0 < 4 ? t1 - p0 : 4) : 0;
+                    for (int r = 0; r < R; ++r) {
+                        const int st = rs.state[r];
+                        if (!run_active(st)) continue;
+                        const int co = a.coff[r];
+                        unsigned todo = 0;
+                        uint32_t as4 = 0xffffffffu;
+                        if (cnt > 0) {
+                            as4 = *reinterpret_cast<const uint32_t*>(s_asg + r * P + p0);
+                            if (st == kActiveFromSums) {
+                                const float4 b4 = *reinterpret_cast<const float4*>(s_bud + r * P + p0);
+                                const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    if (e < cnt) rw[e] = a.pts[p0 + e];
+                                for (int e = 0; e < 4; ++e) {
+                                    const int old = (as4 >> (8 * e)) & 0xff;
+                                    if (e >= cnt) continue;
+                                    if (old == 255 || !(__fsub_rd(bb[e], dcum[co + old]) > kSettleMargin))
+                                        todo |= 1u << e;
+                                }
+                            } else {
+                                todo = (1u << cnt) - 1u;
+                            }
+                        }
+                        // warp-aggregated append
+                        const int c = __popc(todo);
+                        int incl = c;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                            if (lane >= o) incl += y;
+                        }
+                        int wbase = 0;
+                        if (lane == 31 && incl) wbase = atomicAdd(qn, incl);
+                        wbase = __shfl_sync(0xffffffffu, wbase, 31);
+                        int pos = wbase + incl - c;
+                        while (todo) {
+                            const int e = __ffs(todo) - 1;
+                            todo &= todo - 1;
+                            s_queue[pos++] = uint32_t(p0 + e) | (uint32_t(r) << 16) | (((as4 >> (8 * e)) & 0xffu) << 24);
+                        }
+                    }
+                }
+                __syncthreads();
+                if (tid == 0) s_qn[tile_parity ^ 1] = 0;
+                const int nqueued = *qn;
+                if (a.stats && tid == 0)
+                    for (int r = 0; r < R; ++r)
+                        if (run_active(rs.state[r])) rs.cnt[r][0] += unsigned(t1 - t0);
+                // evaluate: rows gathered from L2 four at a time per thread
+                for (int i0 = 0; i0 < nqueued; i0 += 4 * blockDim.x) {
+                    uint32_t ent[4];
+                    uint64_t row[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int i = i0 + u * blockDim.x + tid;
+                        ent[u] = i < nqueued ? s_queue[i] : 0xffffffffu;
+                        if (ent[u] == 0xffffffffu) row[u] = 0ull;
+                        else if (a.rows_resident) row[u] = s_rows[ent[u] & 0xffffu];
+                        else row[u] = __ldg(a.pts + b0 + (ent[u] & 0xffffu));
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        if (ent[u] == 0xffffffffu) continue;
+                        const int pl = int(ent[u] & 0xffffu), r = int((ent[u] >> 16) & 0xff), old = int(ent[u] >> 24);
+                        float bud;
+                        const int j = lloyd_eval(a, c32, c64, dcum, delta, r, row[u], old, bud);
+                        s_bud[r * P + pl] = bud;
+                        if (a.stats) atomicAdd(&rs.cnt[r][2], 1u);
+                        if (j != old) {
+                            s_asg[r * P + pl] = uint8_t(j);
+                            rs.changed[r] = 1;
+                        }
+                    }
+                }
+                tile_parity ^= 1;
+                __syncthreads();
             }
-            for (int r = 0; r < R; ++r) {
-                const int st = rs.state[r];
-                if (!run_active(st)) continue;
-                const int co = a.coff[r];
-                uint8_t* as_r = a.assign + int64_t(r) * a.stride;
-                float2* bd_r = a.bounds + int64_t(r) * a.stride;
-                unsigned todo = 0;  // bit e: point e needs distance work
-                uint32_t as4 = 0xffffffffu;
-                float bu[4] = {0.f, 0.f, 0.f, 0.f}, bl[4] = {0.f, 0.f, 0.f, 0.f};
-                if (cnt > 0) {
-                    as4 = *reinterpret_cast<const uint32_t*>(as_r + p0);
-                    if (st == kActiveFromSums) {
-                        const float4 b01 = reinterpret_cast<const float4*>(bd_r)[q * 2];
-                        const float4 b23 = reinterpret_cast<const float4*>(bd_r)[q * 2 + 1];
-                        bu[0] = b01.x, bl[0] = b01.y, bu[1] = b01.z, bl[1] = b01.w;
-                        bu[2] = b23.x, bl[2] = b23.y, bu[3] = b23.z, bl[3] = b23.w;
-                        const float m1 = rs.m1[r], m2 = rs.m2[r];
-                        const int am = rs.amax[r];
+        } else {
+            // ---- assignment pass.  Per warp and round: each lane tests 4 consecutive
+            // points against their budgets; the points the budgets cannot settle are
+            // queued in shared memory and then evaluated by all 32 lanes together.
+            const int64_t nq = (m + 3) >> 2;
+            LloydQueueEntry* queue = wqueue + (tid >> 5) * 128;
+            // warps grab 32-quad chunks from a per-pass counter (claimed one chunk ahead)
+            unsigned int* work = a.work + (it % 3);
+            unsigned int next = 0, ahead = 0;
+            if (lane == 0) next = atomicAdd(work, 32u);
+            next = __shfl_sync(0xffffffffu, next, 0);
+            while (int64_t(next) < nq) {
+                const unsigned int chunk = next;
+                if (lane == 0) ahead = atomicAdd(work, 32u);
+                const int64_t q = int64_t(chunk) + lane;
+                const int64_t p0 = q << 2;
+                const int cnt = q < nq ? int(m - p0 < 4 ? m - p0 : 4) : 0;
+                for (int r = 0; r < R; ++r) {
+                    const int st = rs.state[r];
+                    if (!run_active(st)) continue;
+                    const int co = a.coff[r];
+                    uint8_t* as_r = a.assign + int64_t(r) * a.stride;
+                    float* bg_r = a.budget + int64_t(r) * a.stride;
+                    unsigned todo = 0;  // bit e: point e needs distance work
+                    uint32_t as4 = 0xffffffffu;
+                    if (cnt > 0) {
+                        as4 = *reinterpret_cast<const uint32_t*>(as_r + p0);
+                        if (st == kActiveFromSums) {
+                            const float4 b4 = reinterpret_cast<const float4*>(bg_r)[q];
+                            const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const int old = (as4 >> (8 * e)) & 0xff;
-                            if (e >= cnt) continue;
-                            if (old == 255) {
-                                todo |= 1u << e;
-                                continue;
+                            for (int e = 0; e < 4; ++e) {
+                                const int old = (as4 >> (8 * e)) & 0xff;
+                                if (e >= cnt) continue;
+                                if (old == 255 || !(__fsub_rd(bb[e], dcum[co + old]) > kSettleMargin)) todo |= 1u << e;
                             }
-                            bu[e] = __fadd_ru(bu[e], drift[co + old]);
-                            bl[e] = __fsub_rd(bl[e], old == am ? m2 : m1);
-                            if (!surely_less(bu[e], bl[e])) todo |= 1u << e;
+                        } else {
+                            todo = (1u << cnt) - 1u;
                         }
-                        // settled points keep their widened bounds (queued ones are rewritten below)
-                        reinterpret_cast<float4*>(bd_r)[q * 2] = make_float4(bu[0], bl[0], bu[1], bl[1]);
-                        reinterpret_cast<float4*>(bd_r)[q * 2 + 1] = make_float4(bu[2], bl[2], bu[3], bl[3]);
-                    } else {
-                        todo = (1u << cnt) - 1u;
                     }
-                }
-                // warp-level compaction of the unsettled points
-                int base = 0;
+                    // warp-level compaction of the unsettled points
+                    int base = 0;
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const bool mine = (todo >> e) & 1u;
-                    const unsigned bal = __ballot_sync(0xffffffffu, mine);
-                    if (mine) {
-                        LloydQueueEntry& qe = queue[base + __popc(bal & ((1u << lane) - 1u))];
-                        qe.row = rw[e];
-                        qe.point = uint32_t(p0 + e);
-                        qe.old = (as4 >> (8 * e)) & 0xff;
-                        qe.u = bu[e];
-                        qe.l = bl[e];
-                    }
-                    base += __popc(bal);
-                }
-                __syncwarp();
-                const bool bounded = st == kActiveFromSums;
-                for (int i = lane; i < base; i += 32) {
-                    const LloydQueueEntry qe = queue[i];
-                    const uint64_t row = qe.row;
-                    float p[kMaxKnobs];
-                    unpack_row(row, p, a.fmt);
-                    const int old = qe.old;
-                    float u = qe.u, l = qe.l;
-                    int j = -1;
-                    if (bounded && old != 255) {
-                        u = dist_up(f32_d2(p, c32 + (co + old) * kMaxKnobs), a.bk1);
-                        if (surely_less(u, l)) j = old;
-                    }
-                    if (a.stats) atomicAdd(&rs.cnt[r][j < 0 ? 2 : 1], 1u);
-                    if (j < 0)
-                        j = full_assign(c32 + co * kMaxKnobs, c64 + co * kMaxKnobs, row, p, a.k[r], n, a.fmt, a.bk1, u, l);
-                    bd_r[qe.point] = make_float2(u, l);
-                    if (j != old) {
-                        as_r[qe.point] = uint8_t(j);
-                        rs.changed[r] = 1;
-                        int* dn = delta + (co + j) * kDeltaW;
-                        for (int c = 0; c < n; ++c) {
-                            const int v = a.fmt.get(row, c);
-                            atomicAdd(dn + c, v & 0xff);
-                            if (v >> 8) atomicAdd(dn + 9 + c, v >> 8);
+                    for (int e = 0; e < 4; ++e) {
+                        const bool mine = (todo >> e) & 1u;
+                        const unsigned bal = __ballot_sync(0xffffffffu, mine);
+                        if (mine) {
+                            LloydQueueEntry& qe = queue[base + __popc(bal & ((1u << lane) - 1u))];
+                            qe.point = uint32_t(p0 + e);
+                            qe.old = (as4 >> (8 * e)) & 0xff;
                         }
-                        atomicAdd(dn + 8, 1);
-                        if (old != 255) {
-                            int* dold = delta + (co + old) * kDeltaW;
-                            for (int c = 0; c < n; ++c) {
-                                const int v = a.fmt.get(row, c);
-                                atomicSub(dold + c, v & 0xff);
-                                if (v >> 8) atomicSub(dold + 9 + c, v >> 8);
-                            }
-                            atomicSub(dold + 8, 1);
+                        base += __popc(bal);
+                    }
+                    __syncwarp();
+                    for (int i = lane; i < base; i += 32) {
+                        const LloydQueueEntry qe = queue[i];
+                        const uint64_t row = __ldg(a.pts + qe.point);
+                        float bud;
+                        const int j = lloyd_eval(a, c32, c64, dcum, delta, r, row, qe.old, bud);
+                        bg_r[qe.point] = bud;
+                        if (j != qe.old) {
+                            as_r[qe.point] = uint8_t(j);
+                            rs.changed[r] = 1;
                         }
                     }
+                    if (a.stats) {
+                        const unsigned valid = __reduce_add_sync(0xffffffffu, unsigned(cnt));
+                        if (lane == 0) {
+                            atomicAdd(&rs.cnt[r][0], valid);
+                            atomicAdd(&rs.cnt[r][2], unsigned(base));
+                        }
+                    }
+                    __syncwarp();
                 }
-                if (a.stats) {
-                    const unsigned valid = __reduce_add_sync(0xffffffffu, unsigned(cnt));
-                    if (lane == 0) atomicAdd(&rs.cnt[r][0], valid - unsigned(base));
-                }
-                __syncwarp();
+                next = __shfl_sync(0xffffffffu, ahead, 0);
             }
         }
         __syncthreads();
@@ -849,9 +983,17 @@ __global__ void __launch_bounds__(256, 3) lloyd_kernel(LloydArgs a) {
         ++it;
         if (rs.exit_flag || rs.n_active == 0) break;
     }
+    if (RESIDENT) {
+        for (int r = 0; r < R; ++r)
+            for (int i = tid; i < np; i += blockDim.x) {
+                a.assign[int64_t(r) * a.stride + b0 + i] = s_asg[r * P + i];
+                a.budget[int64_t(r) * a.stride + b0 + i] = s_bud[r * P + i];
+            }
+    }
     if (a.stats && tid < R * 3) atomicAdd(a.stats + tid, (unsigned long long)rs.cnt[tid / 3][tid % 3]);
     if (blockIdx.x == 0) {
         for (int i = tid; i < K * kSumW; i += blockDim.x) a.S[i] = S[i];
+        for (int i = tid; i < K; i += blockDim.x) a.dcum[i] = dcum[i];
         if (tid < R) a.run_state[tid] = rs.state[tid];
         if (tid == 0) a.ctrl[0] = it;
     }
@@ -1025,23 +1167,71 @@ struct KmeansSession {
         static const bool want_timeline = std::getenv("KT_LLOYD_TIMELINE") != nullptr;
         a.timeline = want_timeline ? static_cast<long long*>(e->scratch("km.timeline", 400 * 8)) : nullptr;
         double* d_loss = static_cast<double*>(e->scratch("km.loss", kMaxRuns * 8));
-        a.bounds = static_cast<float2*>(e->scratch("km.bounds", size_t(R) * a.stride * sizeof(float2)));
+        a.budget = static_cast<float*>(e->scratch("km.budget", size_t(R) * a.stride * sizeof(float)));
+        a.dcum = static_cast<float*>(e->scratch("km.dcum", size_t(K) * sizeof(float)));
         a.init_rows = cent_rows;
         KT_CUDA(cudaMemsetAsync(a.assign, 0xff, size_t(R) * a.stride, e->stream));
         KT_CUDA(cudaMemsetAsync(a.S, 0, size_t(K) * kSumW * 8, e->stream));
         KT_CUDA(cudaMemsetAsync(a.cent, 0, size_t(K) * kMaxKnobs * 8, e->stream));
+        KT_CUDA(cudaMemsetAsync(a.dcum, 0, size_t(K) * sizeof(float), e->stream));
         auto* h_state = static_cast<int*>(e->staging("km.state", 64));
         for (int r = 0; r < R; ++r) h_state[r] = kActiveFromRows;
         KT_CUDA(cudaMemcpyAsync(a.run_state, h_state, R * 4, cudaMemcpyHostToDevice, e->stream));
 
-        const size_t smem = lloyd_layout(K).total + 16;
-        KT_CUDA(cudaFuncSetAttribute(lloyd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        const int occ = std::max(1, occupancy_blocks((const void*)lloyd_kernel, 256, smem));
-        // Passes are latency-bound: small point sets run fastest with one block per SM
-        // (cheaper grid barrier), large ones with every resident block (measured on
-        // B200: m = 134K -> 148 blocks, m = 1M -> 444); ~900 points per block between.
-        const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(occ, ceil_div(m, int64_t(900) * e->num_sms)));
-        const int grid = int(std::max<int64_t>(1, std::min<int64_t>(per_sm * e->num_sms, ceil_div(m, 256))));
+        // Resident kernel (one block per SM keeps its points' assignments and budgets
+        // in shared memory for the whole launch) whenever they fit; else the
+        // streaming kernel (state in global memory, dynamic chunk scheduling).
+        const char* mode = std::getenv("KT_LLOYD_MODE");
+        const bool force_stream = mode && std::strcmp(mode, "stream") == 0;
+        const int64_t P = ((ceil_div(m, int64_t(e->num_sms)) + 15) & ~int64_t(15));
+        const void* kres = (const void*)lloyd_kernel<true>;
+        const void* kstr = (const void*)lloyd_kernel<false>;
+        cudaFuncAttributes fa{};
+        KT_CUDA(cudaFuncGetAttributes(&fa, kres));
+        int optin = 0;
+        KT_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
+        // smem plan: state (+ rows when they fit) + a queue of >= kLloydQueueMin entries
+        const int64_t avail = int64_t(optin) - int64_t(fa.sharedSizeBytes) - 16;
+        const char* rows_env = std::getenv("KT_LLOYD_ROWS");  // tests: "global" = rows gathered from L2
+        bool rows_res = int64_t(lloyd_resident_bytes(K, R, P, true)) + 4 * kLloydQueueMin <= avail &&
+                        !(rows_env && std::strcmp(rows_env, "global") == 0);
+        const int64_t base_bytes = int64_t(lloyd_resident_bytes(K, R, P, rows_res));
+        const int64_t qcap = std::min<int64_t>(kLloydQueueMax, (avail - base_bytes) / 4);
+        const int64_t tile = std::min<int64_t>(P, (qcap / R) & ~int64_t(3));
+        const size_t res_smem = size_t(base_bytes + tile * R * 4 + 16);
+        bool resident = !force_stream && P < 65536 && qcap >= kLloydQueueMin && tile >= 4;
+        size_t smem;
+        int grid, threads;
+        const void* kern;
+        if (resident) {
+            KT_CUDA(cudaFuncSetAttribute(kres, cudaFuncAttributeMaxDynamicSharedMemorySize, int(res_smem)));
+            resident = occupancy_blocks(kres, kLloydResThreads, res_smem) >= 1;
+        }
+        if (resident) {
+            smem = res_smem;
+            grid = e->num_sms;
+            threads = kLloydResThreads;
+            kern = kres;
+            a.per_block = P;
+            a.tile = int(tile);
+            a.rows_resident = rows_res ? 1 : 0;
+            if (const char* t = std::getenv("KT_LLOYD_TILE"))  // tests: force many tiles per block
+                a.tile = std::max(4, std::min(a.tile, std::atoi(t) & ~3));
+        } else {
+            smem = lloyd_layout(K).total + 16;
+            KT_CUDA(cudaFuncSetAttribute(kstr, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            const int occ = std::max(1, occupancy_blocks(kstr, kLloydThreads, smem));
+            // Passes are latency-bound: small point sets run fastest with one block per SM
+            // (cheaper grid barrier), large ones with every resident block (measured on
+            // B200: m = 134K -> 148 blocks, m = 1M -> 444); ~900 points per block between.
+            const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(occ, ceil_div(m, int64_t(900) * e->num_sms)));
+            grid = int(std::max<int64_t>(1, std::min<int64_t>(per_sm * e->num_sms, ceil_div(m, 256))));
+            threads = kLloydThreads;
+            kern = kstr;
+            a.per_block = 0;
+            a.tile = 0;
+            a.rows_resident = 0;
+        }
         int it = 0;
         auto* h_ctrl = static_cast<int*>(e->staging("km.ctrl", 64));
         auto* h_iter = static_cast<int*>(e->staging("km.iter", 64));
@@ -1055,7 +1245,7 @@ struct KmeansSession {
             a.it_end = history ? it + 1 : a.max_iters;
             void* params[] = {&a};
             e->pre_launch("lloyd");
-            KT_CUDA(cudaLaunchCooperativeKernel((const void*)lloyd_kernel, grid, 256, params, smem, e->stream));
+            KT_CUDA(cudaLaunchCooperativeKernel(kern, grid, threads, params, smem, e->stream));
             e->check_launch("lloyd");
             ++lloyd_launches;
             KT_CUDA(cudaMemcpyAsync(h_ctrl, a.ctrl, 4, cudaMemcpyDeviceToHost, e->stream));
@@ -1095,7 +1285,7 @@ struct KmeansSession {
             unsigned long long hs[kMaxRuns * 3];
             KT_CUDA(cudaMemcpy(hs, a.stats, R * 3 * 8, cudaMemcpyDeviceToHost));
             for (int r = 0; r < R; ++r)
-                std::fprintf(stderr, "[lloyd] k=%d passes=%d skip=%llu tightened=%llu full=%llu\n", ks[r], h_iter[r] + 1,
+                std::fprintf(stderr, "[lloyd] k=%d passes=%d visits=%llu unused=%llu evaluated=%llu\n", ks[r], h_iter[r] + 1,
                              hs[r * 3], hs[r * 3 + 1], hs[r * 3 + 2]);
         }
         if (a.timeline) {
@@ -1116,7 +1306,7 @@ struct KmeansSession {
         for (int it = 0; it < max_passes; ++it) {  // algorithmic bytes of the fused passes
             int active = 0;
             for (int r = 0; r < R; ++r) active += out[r].passes > it;
-            lloyd_bytes += m * n + 2 * m * active;
+            lloyd_bytes += m * (n + 1) * active;  // (n + 1) B per point per pass per k
         }
         last_args = a;
         return out;

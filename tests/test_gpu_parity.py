@@ -175,6 +175,50 @@ def test_adaptive_sample_uniform_s2_vs_oracle(seed):
     assert [tuple(r) for r in sp.unpack(got, 8).tolist()] == want
 
 
+@pytest.mark.parametrize("mode", ["stream", "tile64", "gather"])
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_lloyd_variants_vs_oracle(mode, seed, monkeypatch):
+    """Both Lloyd kernels (streaming, and resident with many queue tiles per block) agree with the oracle."""
+    if mode == "stream":
+        monkeypatch.setenv("KT_LLOYD_MODE", "stream")
+    elif mode == "gather":
+        monkeypatch.setenv("KT_LLOYD_ROWS", "global")
+    else:
+        monkeypatch.setenv("KT_LLOYD_TILE", "64")
+    test_kmeans_random_lattice_vs_oracle(seed)
+    test_adaptive_sample_uniform_s2_vs_oracle(seed + 1)
+
+
+LARGE = json.loads((GOLDEN / "large.json").read_text())
+
+
+@pytest.mark.parametrize("mode", ["resident", "stream", "tile64", "gather"])
+@pytest.mark.parametrize("name", sorted(LARGE))
+def test_knee_large_vs_oracle_golden(name, mode, monkeypatch):
+    """131K / 262K candidates (config C3 size): knee curve, centroids, assignment and batch bit-exact."""
+    import hashlib
+
+    if mode == "stream":
+        monkeypatch.setenv("KT_LLOYD_MODE", "stream")
+    elif mode == "tile64":
+        monkeypatch.setenv("KT_LLOYD_TILE", "64")
+    elif mode == "gather":
+        monkeypatch.setenv("KT_LLOYD_ROWS", "global")
+    g = LARGE[name]
+    space = space_of(MODELS["s2_resnet18"]["values"])
+    cards = np.array(space.cardinalities)
+    idx = np.random.default_rng(g["cand_seed"]).integers(0, cards, size=(g["n"], cards.size))
+    uniq = osamp.distinct_rows(idx)
+    assert len(uniq) == g["m"]
+    res, curve = kt.knee_scan(uniq.astype(np.float64), g["seed"])
+    assert [[k, float(x).hex()] for k, x in curve] == g["curve"]
+    assert [[float(x).hex() for x in c] for c in res.centroids] == g["centroids"]
+    asg = np.asarray(res.assignment, dtype=np.int64)
+    assert hashlib.sha256(asg.tobytes()).hexdigest() == g["assignment_sha256"]
+    got = kt.adaptive_sample_rows(dev_rows(idx), np.zeros(0, dtype=np.uint64), space, seed=g["seed"])
+    assert sp.unpack(got, 8).tolist() == g["batch"]
+
+
 def test_adaptive_sample_1m_candidates_properties():
     """North-star size: 1,048,576 uniform S2 candidates — dedup count, batch contract, knee k."""
     m = MODELS["s2_resnet18"]
