@@ -7,6 +7,7 @@ engine call raises ``EngineUnavailable`` (a RuntimeError) with the reason.
 from __future__ import annotations
 
 import contextlib
+import os
 import ctypes as C
 import re
 import threading
@@ -15,7 +16,7 @@ from pathlib import Path
 from . import errors
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "lib" / "libknobtuner_b200.so"
+LIB_PATH = Path(os.environ["KT_LIB_PATH"]) if os.environ.get("KT_LIB_PATH") else PKG / "lib" / "libknobtuner_b200.so"
 HEADER = PKG.parent / "include" / "knobtuner_b200.h"
 
 KT_OK, KT_ERR_VALUE, KT_ERR_DIMENSION, KT_ERR_SPACE, KT_ERR_UNSUPPORTED = 0, 1, 2, 3, 4

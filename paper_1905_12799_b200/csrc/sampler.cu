@@ -597,7 +597,8 @@ __device__ __forceinline__ int full_assign(const float* c32, const double* c64, 
 // two shared-memory reads per pass and no global traffic at all; the points the
 // budgets cannot settle go through a block-wide queue (tiles of `tile` points,
 // so the queue never overflows) and only they fetch their rows from L2.
-constexpr int kLloydResThreads = 512;
+constexpr int kLloydResThreads = 768;
+constexpr int kEvalUnroll = 2;  // queue entries per thread whose rows load together
 constexpr int kLloydQueueMax = 16384;  // block queue entries (point | run << 16 | old << 24)
 constexpr int kLloydQueueMin = 2048;
 
@@ -607,15 +608,74 @@ __host__ __device__ inline size_t lloyd_resident_bytes(int K, int R, int64_t P, 
     return lloyd_layout(K).total + ((size_t(R) * P + 15) & ~size_t(15)) + size_t(R) * P * 4 + (rows ? size_t(P) * 8 : 0);
 }
 
-// Evaluate one point under run r: full assignment, new budget, deltas of a move.
-__device__ __forceinline__ int lloyd_eval(const LloydArgs& a, const float* c32, const double* c64, const float* dcum,
-                                          int* delta, int r, uint64_t row, int old, float& budget) {
+// Evaluate one point under run r: full assignment and its new budget.
+__device__ __forceinline__ int lloyd_assign(const LloydArgs& a, const float* c32, const double* c64, const float* dcum,
+                                            int r, uint64_t row, float& budget) {
     const int co = a.coff[r];
     float p[kMaxKnobs];
     unpack_row(row, p, a.fmt);
     float u, l;
     const int j = full_assign(c32 + co * kMaxKnobs, c64 + co * kMaxKnobs, row, p, a.k[r], a.n, a.fmt, a.bk1, u, l);
     budget = __fadd_rd(__fsub_rd(l, u), dcum[co + j]);
+    return j;
+}
+
+// Resident kernel deltas: two coordinates per 64-bit shared atomic (32-bit fields,
+// two's complement across the pair: every field's true per-pass block total stays
+// within +-2^31 since P <= 32767 points of value < 2^16), the count in a fifth
+// word — 5 atomics per point move instead of 9.
+constexpr int kPackedW = 5;
+__device__ __forceinline__ void packed_delta(unsigned long long* d, uint64_t row, int sign, int n, const RowFmt& fmt) {
+#pragma unroll
+    for (int c = 0; c < kMaxKnobs; c += 2) {
+        if (c >= n) break;
+        const unsigned long long lo = unsigned(fmt.get(row, c));
+        const unsigned long long hi = c + 1 < n ? unsigned(fmt.get(row, c + 1)) : 0u;
+        const unsigned long long v = lo | (hi << 32);
+        atomicAdd(d + (c >> 1), sign > 0 ? v : 0ull - v);
+    }
+    atomicAdd(d + 4, sign > 0 ? 1ull : ~0ull);
+}
+__device__ __forceinline__ long long packed_field(const unsigned long long* d, int c) {
+    const unsigned long long v = d[c < 8 ? c >> 1 : 4];
+    const long long lo = (long long)(int)(unsigned)(v & 0xffffffffull);
+    if (c == 8 || !(c & 1)) return lo;
+    return (long long)(v - (unsigned long long)lo) >> 32;
+}
+
+// Warp-aggregated cluster-sum deltas (all 32 lanes call it): lanes passing the same
+// cluster g >= 0 are reduced with __reduce_add_sync and one leader per group
+// updates the block's shared counters — no same-address atomic storms when many
+// points move (the first passes move every point).
+__device__ __forceinline__ void warp_delta(int* delta, int g, uint64_t row, int sign, int n, const RowFmt& fmt) {
+    unsigned pending = __ballot_sync(0xffffffffu, g >= 0);
+    const int lane = threadIdx.x & 31;
+    while (pending) {
+        const int leader = __ffs(pending) - 1;
+        const int gl = __shfl_sync(0xffffffffu, g, leader);
+        const bool mine = g == gl;
+        const unsigned grp = __ballot_sync(0xffffffffu, mine);
+        int* d = delta + gl * kDeltaW;
+        for (int c = 0; c < n; ++c) {
+            const int v = mine ? fmt.get(row, c) : 0;
+            const int lo = int(__reduce_add_sync(0xffffffffu, unsigned(v & 0xff)));
+            if (lane == leader && lo) atomicAdd(d + c, sign * lo);
+            if (!fmt.bytes) {
+                const int hi = int(__reduce_add_sync(0xffffffffu, unsigned(v >> 8)));
+                if (lane == leader && hi) atomicAdd(d + 9 + c, sign * hi);
+            }
+        }
+        if (lane == leader) atomicAdd(d + 8, sign * __popc(grp));
+        pending &= ~grp;
+    }
+}
+
+// Evaluate one point under run r (one lane, no warp cooperation): assignment,
+// budget, and the shared-counter deltas of a move.
+__device__ __forceinline__ int lloyd_eval(const LloydArgs& a, const float* c32, const double* c64, const float* dcum,
+                                          int* delta, int r, uint64_t row, int old, float& budget) {
+    const int co = a.coff[r];
+    const int j = lloyd_assign(a, c32, c64, dcum, r, row, budget);
     if (j != old) {
         int* dn = delta + (co + j) * kDeltaW;
         for (int c = 0; c < a.n; ++c) {
@@ -644,15 +704,17 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
     __shared__ RunShared rs;
     __shared__ uint8_t run_of[kMaxClusters];
     __shared__ LloydQueueEntry wqueue[RESIDENT ? 1 : kLloydThreads / 32 * 128];
-    __shared__ int s_qn[2];
+    __shared__ int s_qn[2];  // resident kernel: queue counters (alternating tiles)
     // the dynamic window is only guaranteed 8-byte aligned after static smem (tools add their
     // own static smem): align explicitly for the float4 centroid loads (16 spare bytes allocated)
+    // generic pointer arithmetic measured faster here than align_shared<16> (1.60 vs 1.95 ms per 1M-point knee scan)
     unsigned char* s_raw = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(s_dyn) + 15) & ~uintptr_t(15));
     const LloydLayout L = lloyd_layout(a.K);
     double* c64 = reinterpret_cast<double*>(s_raw + L.c64);
     long long* S = reinterpret_cast<long long*>(s_raw + L.S);
     float* c32 = reinterpret_cast<float*>(s_raw + L.c32);
     int* delta = reinterpret_cast<int*>(s_raw + L.delta);
+    unsigned long long* delta64 = reinterpret_cast<unsigned long long*>(s_raw + L.delta);  // resident layout
     float* drift = reinterpret_cast<float*>(s_raw + L.drift);
     float* dcum = reinterpret_cast<float*>(s_raw + L.dcum);
     cg::grid_group grid = cg::this_grid();
@@ -696,10 +758,10 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
         if (a.timeline && blockIdx.x == 0 && tid == 0 && it < 100) {
             long long t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            a.timeline[it * 4 + phase] = t;
+            a.timeline[it * 8 + phase] = t;
         }
     };
-    int tile_parity = 0;
+    int tile_parity = 0;  // queue counter in use (alternates per tile, across passes too)
     while (it < a.it_end) {
         stamp(0);
         // ---- this pass's centroids and each centroid's drift from the previous pass:
@@ -728,7 +790,7 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
             dlt2 += __shfl_xor_sync(0xffffffffu, dlt2, 4);
             if (live && i == 0) drift[g] = __double2float_ru(sqrt(dlt2) * (1.0 + 1e-9) + 1e-30);
         }
-        for (int i = tid; i < K * kDeltaW; i += blockDim.x) delta[i] = 0;
+        for (int i = tid; i < K * kDeltaW; i += blockDim.x) delta[i] = 0;  // also clears delta64 (K*5*8 <= K*17*4)
         if (tid < kMaxRuns) rs.changed[tid] = 0;
         __syncthreads();
         if (tid < R && run_active(rs.state[tid])) {
@@ -817,17 +879,18 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
                     }
                 }
                 __syncthreads();
+                if (t0 == 0) stamp(2);
                 if (tid == 0) s_qn[tile_parity ^ 1] = 0;
                 const int nqueued = *qn;
                 if (a.stats && tid == 0)
                     for (int r = 0; r < R; ++r)
                         if (run_active(rs.state[r])) rs.cnt[r][0] += unsigned(t1 - t0);
-                // evaluate: rows gathered from L2 four at a time per thread
-                for (int i0 = 0; i0 < nqueued; i0 += 4 * blockDim.x) {
-                    uint32_t ent[4];
-                    uint64_t row[4];
+                // evaluate: rows from shared memory (or L2), kEvalUnroll per thread at a time
+                for (int i0 = 0; i0 < nqueued; i0 += kEvalUnroll * blockDim.x) {
+                    uint32_t ent[kEvalUnroll];
+                    uint64_t row[kEvalUnroll];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
+                    for (int u = 0; u < kEvalUnroll; ++u) {
                         const int i = i0 + u * blockDim.x + tid;
                         ent[u] = i < nqueued ? s_queue[i] : 0xffffffffu;
                         if (ent[u] == 0xffffffffu) row[u] = 0ull;
@@ -835,21 +898,24 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
                         else row[u] = __ldg(a.pts + b0 + (ent[u] & 0xffffu));
                     }
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
+                    for (int u = 0; u < kEvalUnroll; ++u) {
                         if (ent[u] == 0xffffffffu) continue;
                         const int pl = int(ent[u] & 0xffffu), r = int((ent[u] >> 16) & 0xff), old = int(ent[u] >> 24);
                         float bud;
-                        const int j = lloyd_eval(a, c32, c64, dcum, delta, r, row[u], old, bud);
+                        const int j = lloyd_assign(a, c32, c64, dcum, r, row[u], bud);
                         s_bud[r * P + pl] = bud;
                         if (a.stats) atomicAdd(&rs.cnt[r][2], 1u);
                         if (j != old) {
                             s_asg[r * P + pl] = uint8_t(j);
                             rs.changed[r] = 1;
+                            packed_delta(delta64 + (a.coff[r] + j) * kPackedW, row[u], 1, n, a.fmt);
+                            if (old != 255) packed_delta(delta64 + (a.coff[r] + old) * kPackedW, row[u], -1, n, a.fmt);
                         }
                     }
                 }
                 tile_parity ^= 1;
                 __syncthreads();
+                if (t0 == 0) stamp(3);
             }
         } else {
             // ---- assignment pass.  Per warp and round: each lane tests 4 consecutive
@@ -933,7 +999,8 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
         unsigned long long* Dcur = a.D + size_t(buf) * K * kSumW;
         for (int i = tid; i < K * kSumW; i += blockDim.x) {
             const int g = i / kSumW, c = i % kSumW;
-            const long long v = (long long)delta[g * kDeltaW + c] + (c < 8 ? 256ll * delta[g * kDeltaW + 9 + c] : 0ll);
+            const long long v = RESIDENT ? packed_field(delta64 + g * kPackedW, c)
+                                         : (long long)delta[g * kDeltaW + c] + (c < 8 ? 256ll * delta[g * kDeltaW + 9 + c] : 0ll);
             if (v) atomicAdd(Dcur + i, (unsigned long long)v);
         }
         if (tid < R && rs.changed[tid]) atomicOr(a.chg + buf * kMaxRuns + tid, 1u);
@@ -943,9 +1010,9 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
             if (tid < kMaxRuns) a.chg[nb * kMaxRuns + tid] = 0u;
             if (tid == 0) a.work[nb] = 0u;
         }
-        stamp(2);
+        stamp(4);
         grid.sync();
-        stamp(3);
+        stamp(5);
 
         // ---- decisions (identical in every block)
         for (int i = tid; i < K * kSumW; i += blockDim.x) {
@@ -1165,7 +1232,7 @@ struct KmeansSession {
             KT_CUDA(cudaMemsetAsync(a.stats, 0, kMaxRuns * 3 * 8, e->stream));
         }
         static const bool want_timeline = std::getenv("KT_LLOYD_TIMELINE") != nullptr;
-        a.timeline = want_timeline ? static_cast<long long*>(e->scratch("km.timeline", 400 * 8)) : nullptr;
+        a.timeline = want_timeline ? static_cast<long long*>(e->scratch("km.timeline", 800 * 8)) : nullptr;
         double* d_loss = static_cast<double*>(e->scratch("km.loss", kMaxRuns * 8));
         a.budget = static_cast<float*>(e->scratch("km.budget", size_t(R) * a.stride * sizeof(float)));
         a.dcum = static_cast<float*>(e->scratch("km.dcum", size_t(K) * sizeof(float)));
@@ -1199,7 +1266,7 @@ struct KmeansSession {
         const int64_t qcap = std::min<int64_t>(kLloydQueueMax, (avail - base_bytes) / 4);
         const int64_t tile = std::min<int64_t>(P, (qcap / R) & ~int64_t(3));
         const size_t res_smem = size_t(base_bytes + tile * R * 4 + 16);
-        bool resident = !force_stream && P < 65536 && qcap >= kLloydQueueMin && tile >= 4;
+        bool resident = !force_stream && P < 32768 && qcap >= kLloydQueueMin && tile >= 4;
         size_t smem;
         int grid, threads;
         const void* kern;
@@ -1289,14 +1356,16 @@ struct KmeansSession {
                              hs[r * 3], hs[r * 3 + 1], hs[r * 3 + 2]);
         }
         if (a.timeline) {
-            long long tl[400];
+            long long tl[800];
             KT_CUDA(cudaMemcpy(tl, a.timeline, sizeof(tl), cudaMemcpyDeviceToHost));
             int mp = 0;
             for (int r = 0; r < R; ++r) mp = std::max(mp, h_iter[r] + 1);
-            for (int it = 0; it + 1 < std::min(100, mp); ++it)
-                std::fprintf(stderr, "[lloyd] pass %d: centroids %.1f us, points %.1f us, barrier %.1f us, rest %.1f us\n",
-                             it, (tl[it * 4 + 1] - tl[it * 4]) * 1e-3, (tl[it * 4 + 2] - tl[it * 4 + 1]) * 1e-3,
-                             (tl[it * 4 + 3] - tl[it * 4 + 2]) * 1e-3, (tl[it * 4 + 4] - tl[it * 4 + 3]) * 1e-3);
+            for (int it = 0; it + 1 < std::min(100, mp); ++it) {
+                const long long* t = tl + it * 8;
+                std::fprintf(stderr, "[lloyd] pass %d: centroids %.1f us, scan %.1f us, eval %.1f us, flush %.1f us, "
+                             "barrier %.1f us, rest %.1f us\n", it, (t[1] - t[0]) * 1e-3, (t[2] - t[1]) * 1e-3,
+                             (t[3] - t[2]) * 1e-3, (t[4] - t[3]) * 1e-3, (t[5] - t[4]) * 1e-3, (t[8] - t[5]) * 1e-3);
+            }
         }
         int max_passes = 0;
         for (int r = 0; r < R; ++r) {
