@@ -598,12 +598,12 @@ __device__ __forceinline__ int full_assign(const float* c32, const double* c64, 
 // budgets cannot settle go through a block-wide queue (tiles of `tile` points,
 // so the queue never overflows) and only they fetch their rows from L2.
 constexpr int kLloydResThreads = 768;
-constexpr int kEvalUnroll = 2;
+constexpr int kEvalUnroll = 2;  // queue entries per thread whose rows load together
 // Resident-kernel cluster-sum deltas: 0 = packed 64-bit shared words (5 CAS atomics per
 // move), 1 = 17-wide int32 shared counters (9 native atomics), 2 = a private int32
 // copy per warp (9 native atomics, contention only within a warp).  Measured on B200
 // (1M-point knee scan, 100 passes): 1.61 / 1.79 / 1.97 ms -> mode 0.
-constexpr int kDeltaMode = 0;  // queue entries per thread whose rows load together
+constexpr int kDeltaMode = 0;
 constexpr int kLloydQueueMax = 16384;  // block queue entries (point | run << 16 | old << 24)
 constexpr int kLloydQueueMin = 2048;
 
