@@ -215,6 +215,40 @@ int kt_search_round(kt_engine* e, kt_agent* a, const kt_forest* f, const uint64_
                     double* scores_out_dev, int32_t* steps_out_dev, int64_t* n_out, kt_round_info* info,
                     double* logp_out_dev /* T or NULL */, double* values_out_dev /* T or NULL */);
 
+/* ------------------------------------------------ sharded k-means (multi-GPU)
+ * One rank's contiguous, pairwise-tree-aligned shard of the distinct points
+ * (SURVEY §8(e)); replaces the Lloyd loop of kmeans (sampler.py:91-116) for that
+ * shard.  Per pass the host calls kt_lloyd_pass (fills ext_dev, int64
+ * [K*9 + R]: per-cluster coordinate/count deltas, then per-run changed counts),
+ * all-reduces ext_dev with SUM over the ranks (NCCL), then kt_lloyd_apply (sums
+ * += deltas; converged / maxed / reseed / active per run, identical on every
+ * rank).  init_rows: host, max(ks) k-means++ rows (kt_kmeanspp_rows).         */
+typedef struct kt_lloyd kt_lloyd;
+int kt_lloyd_create(kt_engine* e, const uint64_t* shard_pts_dev, int64_t shard_m, int n_knobs, const int32_t* cards,
+                    int n_runs, const int32_t* ks, const uint64_t* init_rows, kt_lloyd** out);
+int kt_lloyd_destroy(kt_lloyd* l);
+int kt_lloyd_clusters(const kt_lloyd* l, int32_t* n_clusters);
+int kt_lloyd_pass(kt_engine* e, kt_lloyd* l, uint64_t* ext_dev);
+/* states_out[r]: 0/1/5 active, 2 converged, 3 maxed (100 passes), 4 needs reseed. */
+int kt_lloyd_apply(kt_engine* e, kt_lloyd* l, const uint64_t* ext_dev, int32_t* states_out, int32_t* passes_out);
+/* Global cluster sums (host int64 [K][9]: 8 coordinate sums, count). */
+int kt_lloyd_sums(kt_engine* e, kt_lloyd* l, int64_t* sums_out);
+/* Empty-cluster reseed (sampler.py:108-115): the shard's farthest point from its
+ * assigned centroid under the last pass, skipping `blocked` (shard-local indices);
+ * *idx_out = -1 when none is left.                                          */
+int kt_lloyd_farthest(kt_engine* e, kt_lloyd* l, int run, const int64_t* blocked, int n_blocked, double* d2_out,
+                      int64_t* idx_out);
+/* Centroids for the next pass of `run` (host double [k*n]), e.g. after a reseed. */
+int kt_lloyd_set_centroids(kt_engine* e, kt_lloyd* l, int run, const double* centroids);
+/* Centroids the last pass of `run` used (host double [k*n]). */
+int kt_lloyd_centroids(kt_engine* e, kt_lloyd* l, int run, double* centroids_out);
+int kt_lloyd_assignment(kt_engine* e, kt_lloyd* l, int run, int64_t* assignment_out /* shard_m */);
+/* numpy pairwise loss of each leaf [bounds[i], bounds[i+1]) of the shard (host double [n_leaves]). */
+int kt_lloyd_leaf_losses(kt_engine* e, kt_lloyd* l, int run, const int64_t* bounds, int n_leaves, double* out);
+/* k-means++ rows (_plus_plus_init, sampler.py:56-69) of k centroids; host uint64 [k]. */
+int kt_kmeanspp_rows(kt_engine* e, const uint64_t* points_dev, int64_t m, int n_knobs, const int32_t* cards,
+                     uint64_t seed, int k, uint64_t* rows_out);
+
 /* ------------------------------------------------------------ utilities */
 /* fp32 GEMM on the tensor cores (tcgen05 kind::tf32, 3xTF32 split, fp32 accumulate
  * in TMEM): C[m][n] = sum_k A(m,k) B(k,n), row-major device arrays;

@@ -83,6 +83,18 @@ SIGNATURES = {
     "kt_knee_scan": (C.c_int, [P, P, i64, C.c_int, pi32, u64, f64, C.c_int, pi32, pf64, pi32, pf64, pi64]),
     "kt_adaptive_sample": (C.c_int, [P, P, i64, C.c_int, pi32, pu64, i64, u64, f64, pu64, pi32,
                                      C.POINTER(SampleInfo)]),
+    "kt_lloyd_create": (C.c_int, [P, P, i64, C.c_int, pi32, C.c_int, pi32, pu64, C.POINTER(P)]),
+    "kt_lloyd_destroy": (C.c_int, [P]),
+    "kt_lloyd_clusters": (C.c_int, [P, pi32]),
+    "kt_lloyd_pass": (C.c_int, [P, P, P]),
+    "kt_lloyd_apply": (C.c_int, [P, P, P, pi32, pi32]),
+    "kt_lloyd_sums": (C.c_int, [P, P, pi64]),
+    "kt_lloyd_farthest": (C.c_int, [P, P, C.c_int, pi64, C.c_int, pf64, pi64]),
+    "kt_lloyd_set_centroids": (C.c_int, [P, P, C.c_int, pf64]),
+    "kt_lloyd_centroids": (C.c_int, [P, P, C.c_int, pf64]),
+    "kt_lloyd_assignment": (C.c_int, [P, P, C.c_int, pi64]),
+    "kt_lloyd_leaf_losses": (C.c_int, [P, P, C.c_int, pi64, C.c_int, pf64]),
+    "kt_kmeanspp_rows": (C.c_int, [P, P, i64, C.c_int, pi32, u64, C.c_int, pu64]),
     "kt_agent_create": (C.c_int, [P, C.c_int, C.c_int, C.c_int, pf64, pf64, pf64, i64, C.POINTER(P)]),
     "kt_agent_destroy": (C.c_int, [P]),
     "kt_agent_get_state": (C.c_int, [P, P, pf64, pf64, pf64, pi64]),

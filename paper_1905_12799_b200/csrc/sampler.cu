@@ -458,6 +458,8 @@ struct LloydArgs {
     int64_t per_block;         // resident kernel: points owned by each block (multiple of 16)
     int tile;                  // resident kernel: points per queue tile (multiple of 4)
     int rows_resident;         // resident kernel: the block's rows live in shared memory too
+    int external;              // 1: one pass, deltas + changed counts -> ext, no in-kernel decisions
+    unsigned long long* ext;   // external: [K][9] int64 deltas then [R] changed counts (all-reduced by the host)
     double* cent;              // [K][8] centroids of the latest pass
     const uint64_t* init_rows; // k-means++ rows (prefix shared by all runs)
     long long* S;              // [K][9] running sums
@@ -590,6 +592,17 @@ __device__ __forceinline__ int full_assign(const float* c32, const double* c64, 
     u = dist_up(best, k1);
     l = k > 1 ? dist_dn(second, k1) : INFINITY;
     return bj;
+}
+
+// Per-run decision after a pass whose summed deltas are already in S (sampler.py:99-116):
+// unchanged -> converged; last iteration -> maxed; an empty cluster -> reseed (host);
+// else active with centroids = sums / counts.  Returns the new state.
+__device__ __forceinline__ int lloyd_decide(const LloydArgs& a, const long long* S, int r, int st, bool changed, int it) {
+    if (!changed) return kConverged;
+    if (it == a.max_iters - 1) return kMaxed;
+    for (int j = 0; j < a.k[r]; ++j)
+        if (S[(a.coff[r] + j) * kSumW + 8] == 0) return kNeedsReseed;
+    return kActiveFromSums;
 }
 
 // Resident variant: block b owns points [b*P, (b+1)*P) for the whole launch and
@@ -1021,7 +1034,7 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
         }
         __syncthreads();
         const int buf = it % 3;
-        unsigned long long* Dcur = a.D + size_t(buf) * K * kSumW;
+        unsigned long long* Dcur = a.external ? a.ext : a.D + size_t(buf) * K * kSumW;
         for (int i = tid; i < K * kSumW; i += blockDim.x) {
             const int g = i / kSumW, c = i % kSumW;
             long long vw = 0;
@@ -1034,6 +1047,12 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
                               : (RESIDENT && kDeltaMode == 0) ? packed_field(delta64 + g * kPackedW, c)
                                          : (long long)delta[g * kDeltaW + c] + (c < 8 ? 256ll * delta[g * kDeltaW + 9 + c] : 0ll);
             if (v) atomicAdd(Dcur + i, (unsigned long long)v);
+        }
+        if (a.external) {  // sharded k-means: the host all-reduces ext, then kt_lloyd_apply decides
+            if (tid < R && rs.changed[tid]) atomicAdd(a.ext + size_t(K) * kSumW + tid, 1ull);
+            stamp(4);
+            ++it;
+            break;
         }
         if (tid < R && rs.changed[tid]) atomicOr(a.chg + buf * kMaxRuns + tid, 1u);
         if (blockIdx.x == 0) {
@@ -1059,21 +1078,9 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
                 int st = rs.state[r];
                 if (!run_active(st)) continue;
                 const unsigned changed = __ldcg(a.chg + buf * kMaxRuns + r);
-                if (!changed) {
-                    st = kConverged;
-                } else if (it == a.max_iters - 1) {
-                    st = kMaxed;
-                } else {
-                    bool empty = false;
-                    for (int j = 0; j < a.k[r]; ++j) empty |= S[(a.coff[r] + j) * kSumW + 8] == 0;
-                    if (empty) {
-                        st = kNeedsReseed;
-                        rs.exit_flag = 1;
-                    } else {
-                        st = kActiveFromSums;
-                        ++rs.n_active;
-                    }
-                }
+                st = lloyd_decide(a, S, r, st, changed != 0, it);
+                if (st == kNeedsReseed) rs.exit_flag = 1;
+                if (st == kActiveFromSums) ++rs.n_active;
                 if (st != kActiveFromSums && blockIdx.x == 0) a.run_iter[r] = it;
                 rs.state[r] = st;
             }
@@ -1095,6 +1102,24 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
         for (int i = tid; i < K; i += blockDim.x) a.dcum[i] = dcum[i];
         if (tid < R) a.run_state[tid] = rs.state[tid];
         if (tid == 0) a.ctrl[0] = it;
+    }
+}
+
+// Sharded k-means: S += all-reduced deltas, then every run's decision (one block).
+__global__ void lloyd_apply_kernel(LloydArgs a, const long long* __restrict__ ext, int it) {
+    __shared__ long long S[kMaxClusters * kSumW];
+    const int K = a.K;
+    for (int i = threadIdx.x; i < K * kSumW; i += blockDim.x) S[i] = a.S[i] + ext[i];
+    __syncthreads();
+    for (int i = threadIdx.x; i < K * kSumW; i += blockDim.x) a.S[i] = S[i];
+    if (threadIdx.x < a.R) {
+        const int r = threadIdx.x;
+        const int st = a.run_state[r];
+        if (run_active(st)) {
+            const int ns = lloyd_decide(a, S, r, st, ext[size_t(K) * kSumW + r] != 0, it);
+            if (ns != kActiveFromSums) a.run_iter[r] = it;
+            a.run_state[r] = ns;
+        }
     }
 }
 
@@ -1148,6 +1173,75 @@ __global__ void __launch_bounds__(256) argmax_kernel(const double* __restrict__ 
 
 
 // ============================================================ orchestration
+// Launch plan of one Lloyd launch over m points and K clusters in R runs: the resident
+// kernel whenever the state fits shared memory, else the streaming kernel.
+struct LloydPlan {
+    const void* kern;
+    int grid, threads;
+    size_t smem;
+};
+
+static LloydPlan plan_lloyd(kt_engine* e, int64_t m, int K, int R, LloydArgs& a) {
+    // Resident kernel (one block per SM keeps its points' assignments and budgets
+    // in shared memory for the whole launch) whenever they fit; else the
+    // streaming kernel (state in global memory, dynamic chunk scheduling).
+    const char* mode = std::getenv("KT_LLOYD_MODE");
+    const bool force_stream = mode && std::strcmp(mode, "stream") == 0;
+    const int64_t P = ((ceil_div(m, int64_t(e->num_sms)) + 15) & ~int64_t(15));
+    const void* kres = (const void*)lloyd_kernel<true>;
+    const void* kstr = (const void*)lloyd_kernel<false>;
+    cudaFuncAttributes fa{};
+    KT_CUDA(cudaFuncGetAttributes(&fa, kres));
+    int optin = 0;
+    KT_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
+    // smem plan: state (+ rows when they fit) + a queue of >= kLloydQueueMin entries
+    const int64_t dw_bytes = kDeltaMode == 2 ? int64_t(kLloydResThreads / 32) * K * kDeltaW * 4 : 0;
+    const int64_t avail = int64_t(optin) - int64_t(fa.sharedSizeBytes) - 16 - dw_bytes;
+    const char* rows_env = std::getenv("KT_LLOYD_ROWS");  // tests: "global" = rows gathered from L2
+    bool rows_res = int64_t(lloyd_resident_bytes(K, R, P, true)) + 4 * kLloydQueueMin <= avail &&
+                    !(rows_env && std::strcmp(rows_env, "global") == 0);
+    const int64_t base_bytes = int64_t(lloyd_resident_bytes(K, R, P, rows_res));
+    const int64_t qcap = std::min<int64_t>(kLloydQueueMax, (avail - base_bytes) / 4);
+    const int64_t tile = std::min<int64_t>(P, (qcap / R) & ~int64_t(3));
+    const size_t res_smem = size_t(base_bytes + tile * R * 4 + 16 + dw_bytes);
+    bool resident = !force_stream && P < 32768 && qcap >= kLloydQueueMin && tile >= 4;
+    LloydPlan pl;
+    size_t& smem = pl.smem;
+    int& grid = pl.grid;
+    int& threads = pl.threads;
+    const void*& kern = pl.kern;
+    if (resident) {
+        KT_CUDA(cudaFuncSetAttribute(kres, cudaFuncAttributeMaxDynamicSharedMemorySize, int(res_smem)));
+        resident = occupancy_blocks(kres, kLloydResThreads, res_smem) >= 1;
+    }
+    if (resident) {
+        smem = res_smem;
+        grid = e->num_sms;
+        threads = kLloydResThreads;
+        kern = kres;
+        a.per_block = P;
+        a.tile = int(tile);
+        a.rows_resident = rows_res ? 1 : 0;
+        if (const char* t = std::getenv("KT_LLOYD_TILE"))  // tests: force many tiles per block
+            a.tile = std::max(4, std::min(a.tile, std::atoi(t) & ~3));
+    } else {
+        smem = lloyd_layout(K).total + 16;
+        KT_CUDA(cudaFuncSetAttribute(kstr, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        const int occ = std::max(1, occupancy_blocks(kstr, kLloydThreads, smem));
+        // Passes are latency-bound: small point sets run fastest with one block per SM
+        // (cheaper grid barrier), large ones with every resident block (measured on
+        // B200: m = 134K -> 148 blocks, m = 1M -> 444); ~900 points per block between.
+        const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(occ, ceil_div(m, int64_t(900) * e->num_sms)));
+        grid = int(std::max<int64_t>(1, std::min<int64_t>(per_sm * e->num_sms, ceil_div(m, 256))));
+        threads = kLloydThreads;
+        kern = kstr;
+        a.per_block = 0;
+        a.tile = 0;
+        a.rows_resident = 0;
+    }
+    return pl;
+}
+
 struct KmeansSession {
     kt_engine* e;
     const uint64_t* pts;
@@ -1277,61 +1371,10 @@ struct KmeansSession {
         for (int r = 0; r < R; ++r) h_state[r] = kActiveFromRows;
         KT_CUDA(cudaMemcpyAsync(a.run_state, h_state, R * 4, cudaMemcpyHostToDevice, e->stream));
 
-        // Resident kernel (one block per SM keeps its points' assignments and budgets
-        // in shared memory for the whole launch) whenever they fit; else the
-        // streaming kernel (state in global memory, dynamic chunk scheduling).
-        const char* mode = std::getenv("KT_LLOYD_MODE");
-        const bool force_stream = mode && std::strcmp(mode, "stream") == 0;
-        const int64_t P = ((ceil_div(m, int64_t(e->num_sms)) + 15) & ~int64_t(15));
-        const void* kres = (const void*)lloyd_kernel<true>;
-        const void* kstr = (const void*)lloyd_kernel<false>;
-        cudaFuncAttributes fa{};
-        KT_CUDA(cudaFuncGetAttributes(&fa, kres));
-        int optin = 0;
-        KT_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
-        // smem plan: state (+ rows when they fit) + a queue of >= kLloydQueueMin entries
-        const int64_t dw_bytes = kDeltaMode == 2 ? int64_t(kLloydResThreads / 32) * K * kDeltaW * 4 : 0;
-        const int64_t avail = int64_t(optin) - int64_t(fa.sharedSizeBytes) - 16 - dw_bytes;
-        const char* rows_env = std::getenv("KT_LLOYD_ROWS");  // tests: "global" = rows gathered from L2
-        bool rows_res = int64_t(lloyd_resident_bytes(K, R, P, true)) + 4 * kLloydQueueMin <= avail &&
-                        !(rows_env && std::strcmp(rows_env, "global") == 0);
-        const int64_t base_bytes = int64_t(lloyd_resident_bytes(K, R, P, rows_res));
-        const int64_t qcap = std::min<int64_t>(kLloydQueueMax, (avail - base_bytes) / 4);
-        const int64_t tile = std::min<int64_t>(P, (qcap / R) & ~int64_t(3));
-        const size_t res_smem = size_t(base_bytes + tile * R * 4 + 16 + dw_bytes);
-        bool resident = !force_stream && P < 32768 && qcap >= kLloydQueueMin && tile >= 4;
-        size_t smem;
-        int grid, threads;
-        const void* kern;
-        if (resident) {
-            KT_CUDA(cudaFuncSetAttribute(kres, cudaFuncAttributeMaxDynamicSharedMemorySize, int(res_smem)));
-            resident = occupancy_blocks(kres, kLloydResThreads, res_smem) >= 1;
-        }
-        if (resident) {
-            smem = res_smem;
-            grid = e->num_sms;
-            threads = kLloydResThreads;
-            kern = kres;
-            a.per_block = P;
-            a.tile = int(tile);
-            a.rows_resident = rows_res ? 1 : 0;
-            if (const char* t = std::getenv("KT_LLOYD_TILE"))  // tests: force many tiles per block
-                a.tile = std::max(4, std::min(a.tile, std::atoi(t) & ~3));
-        } else {
-            smem = lloyd_layout(K).total + 16;
-            KT_CUDA(cudaFuncSetAttribute(kstr, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-            const int occ = std::max(1, occupancy_blocks(kstr, kLloydThreads, smem));
-            // Passes are latency-bound: small point sets run fastest with one block per SM
-            // (cheaper grid barrier), large ones with every resident block (measured on
-            // B200: m = 134K -> 148 blocks, m = 1M -> 444); ~900 points per block between.
-            const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(occ, ceil_div(m, int64_t(900) * e->num_sms)));
-            grid = int(std::max<int64_t>(1, std::min<int64_t>(per_sm * e->num_sms, ceil_div(m, 256))));
-            threads = kLloydThreads;
-            kern = kstr;
-            a.per_block = 0;
-            a.tile = 0;
-            a.rows_resident = 0;
-        }
+        const LloydPlan plan = plan_lloyd(e, m, K, R, a);
+        const void* kern = plan.kern;
+        const int grid = plan.grid, threads = plan.threads;
+        const size_t smem = plan.smem;
         int it = 0;
         auto* h_ctrl = static_cast<int*>(e->staging("km.ctrl", 64));
         auto* h_iter = static_cast<int*>(e->staging("km.iter", 64));
@@ -1684,6 +1727,262 @@ int kt_adaptive_sample(kt_engine* e, const uint64_t* rows_dev, int64_t count, in
         batch_out[len++] = row;
     }
     *batch_len = len;
+    KT_API_END
+}
+
+}  // extern "C"
+
+// ====================================================== sharded k-means
+// One rank's contiguous shard of the distinct points.  The host drives the passes
+// and all-reduces (sum) the int64 buffer [K][9] cluster deltas + [R] changed counts
+// between kt_lloyd_pass and kt_lloyd_apply; every rank then holds the same global
+// sums, so decisions and centroids are identical everywhere (exact integers).
+struct kt_lloyd {
+    kt_engine* e = nullptr;
+    const uint64_t* pts = nullptr;
+    int64_t m = 0;
+    int n = 0;
+    RowFmt fmt{};
+    kt::LloydArgs a{};
+    kt::LloydPlan plan{};
+    int it = 0;
+    std::vector<void*> bufs;
+    double* pd2 = nullptr;
+
+    void* alloc(size_t bytes) {
+        void* p = nullptr;
+        KT_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+        bufs.push_back(p);
+        return p;
+    }
+    ~kt_lloyd() {
+        for (void* p : bufs) cudaFree(p);
+    }
+};
+
+extern "C" {
+
+int kt_lloyd_create(kt_engine* e, const uint64_t* shard_pts_dev, int64_t shard_m, int n_knobs, const int32_t* cards,
+                    int n_runs, const int32_t* ks, const uint64_t* init_rows, kt_lloyd** out) {
+    KT_API_BEGIN
+    if (shard_m < 1) fail(KT_ERR_VALUE, "a k-means shard needs at least one point");
+    if (n_knobs < 1 || n_knobs > kMaxKnobs) fail(KT_ERR_UNSUPPORTED, "1..8 knobs supported");
+    if (n_runs < 1 || n_runs > kMaxRuns) fail(KT_ERR_VALUE, "1..8 runs per launch");
+    auto l = std::make_unique<kt_lloyd>();
+    l->e = e;
+    l->pts = shard_pts_dev;
+    l->m = shard_m;
+    l->n = n_knobs;
+    l->fmt = row_fmt(cards, n_knobs);
+    LloydArgs& a = l->a;
+    a.pts = shard_pts_dev;
+    a.m = shard_m;
+    a.n = n_knobs;
+    a.fmt = l->fmt;
+    a.bk1 = float(6.5e-5 * std::max(1.0, double(l->fmt.cmax) / 255.0));
+    a.R = n_runs;
+    int K = 0, kmax = 0;
+    for (int r = 0; r < n_runs; ++r) {
+        if (ks[r] < 1 || ks[r] > 63) fail(KT_ERR_VALUE, "1 <= k <= 63");
+        a.k[r] = ks[r];
+        a.coff[r] = K;
+        K += ks[r];
+        kmax = std::max(kmax, ks[r]);
+    }
+    if (K > kMaxClusters) fail(KT_ERR_VALUE, "too many clusters in one launch");
+    a.K = K;
+    a.max_iters = 100;
+    a.stride = (shard_m + 15) & ~int64_t(15);
+    a.assign = static_cast<uint8_t*>(l->alloc(size_t(n_runs) * a.stride));
+    a.budget = static_cast<float*>(l->alloc(size_t(n_runs) * a.stride * 4));
+    a.dcum = static_cast<float*>(l->alloc(size_t(K) * 4));
+    a.cent = static_cast<double*>(l->alloc(size_t(K) * kMaxKnobs * 8));
+    a.S = static_cast<long long*>(l->alloc(size_t(K) * kSumW * 8));
+    a.D = static_cast<unsigned long long*>(l->alloc(size_t(3) * K * kSumW * 8));
+    a.chg = static_cast<unsigned int*>(l->alloc(3 * kMaxRuns * 4));
+    a.work = static_cast<unsigned int*>(l->alloc(16));
+    a.run_state = static_cast<int*>(l->alloc(kMaxRuns * 4));
+    a.run_iter = static_cast<int*>(l->alloc(kMaxRuns * 4));
+    a.ctrl = static_cast<int*>(l->alloc(16));
+    auto* rows = static_cast<uint64_t*>(l->alloc(size_t(kmax) * 8));
+    a.init_rows = rows;
+    a.external = 1;
+    cudaStream_t st = e->stream;
+    KT_CUDA(cudaMemcpyAsync(rows, init_rows, size_t(kmax) * 8, cudaMemcpyHostToDevice, st));
+    KT_CUDA(cudaMemsetAsync(a.assign, 0xff, size_t(n_runs) * a.stride, st));
+    KT_CUDA(cudaMemsetAsync(a.S, 0, size_t(K) * kSumW * 8, st));
+    KT_CUDA(cudaMemsetAsync(a.cent, 0, size_t(K) * kMaxKnobs * 8, st));
+    KT_CUDA(cudaMemsetAsync(a.dcum, 0, size_t(K) * 4, st));
+    std::vector<int> h(kMaxRuns, kActiveFromRows), zero(kMaxRuns, 0);
+    KT_CUDA(cudaMemcpyAsync(a.run_state, h.data(), kMaxRuns * 4, cudaMemcpyHostToDevice, st));
+    KT_CUDA(cudaMemsetAsync(a.run_iter, 0, kMaxRuns * 4, st));
+    l->plan = plan_lloyd(e, shard_m, K, n_runs, a);
+    e->sync();  // host vectors above go out of scope
+    *out = l.release();
+    KT_API_END
+}
+
+int kt_lloyd_destroy(kt_lloyd* l) {
+    KT_API_BEGIN
+    delete l;
+    KT_API_END
+}
+
+int kt_lloyd_clusters(const kt_lloyd* l, int32_t* n_clusters) {
+    KT_API_BEGIN
+    *n_clusters = l->a.K;
+    KT_API_END
+}
+
+int kt_lloyd_pass(kt_engine* e, kt_lloyd* l, uint64_t* ext_dev) {
+    KT_API_BEGIN
+    LloydArgs& a = l->a;
+    KT_CUDA(cudaMemsetAsync(ext_dev, 0, (size_t(a.K) * kSumW + a.R) * 8, e->stream));
+    KT_CUDA(cudaMemsetAsync(a.work, 0, 16, e->stream));
+    a.ext = reinterpret_cast<unsigned long long*>(ext_dev);
+    a.it0 = l->it;
+    a.it_end = l->it + 1;
+    a.stats = nullptr;
+    a.timeline = nullptr;
+    void* params[] = {&a};
+    // the dynamic-smem limit is a per-function attribute: other shards / sessions may have lowered it
+    KT_CUDA(cudaFuncSetAttribute(l->plan.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(l->plan.smem)));
+    e->pre_launch("lloyd");
+    KT_CUDA(cudaLaunchCooperativeKernel(l->plan.kern, l->plan.grid, l->plan.threads, params, l->plan.smem, e->stream));
+    e->check_launch("lloyd");
+    KT_API_END
+}
+
+int kt_lloyd_apply(kt_engine* e, kt_lloyd* l, const uint64_t* ext_dev, int32_t* states_out, int32_t* passes_out) {
+    KT_API_BEGIN
+    LloydArgs& a = l->a;
+    e->pre_launch("lloyd_apply");
+    lloyd_apply_kernel<<<1, 256, 0, e->stream>>>(a, reinterpret_cast<const long long*>(ext_dev), l->it);
+    e->check_launch("lloyd_apply");
+    ++l->it;
+    auto* hs = static_cast<int*>(e->staging("lloyd.state", 2 * kMaxRuns * 4));
+    KT_CUDA(cudaMemcpyAsync(hs, a.run_state, a.R * 4, cudaMemcpyDeviceToHost, e->stream));
+    KT_CUDA(cudaMemcpyAsync(hs + kMaxRuns, a.run_iter, a.R * 4, cudaMemcpyDeviceToHost, e->stream));
+    e->sync();
+    for (int r = 0; r < a.R; ++r) {
+        states_out[r] = hs[r];
+        if (passes_out) passes_out[r] = run_active(hs[r]) ? l->it : hs[kMaxRuns + r] + 1;
+    }
+    KT_API_END
+}
+
+int kt_lloyd_sums(kt_engine* e, kt_lloyd* l, int64_t* sums_out) {
+    KT_API_BEGIN
+    KT_CUDA(cudaMemcpyAsync(sums_out, l->a.S, size_t(l->a.K) * kSumW * 8, cudaMemcpyDeviceToHost, e->stream));
+    e->sync();
+    KT_API_END
+}
+
+int kt_lloyd_farthest(kt_engine* e, kt_lloyd* l, int run, const int64_t* blocked, int n_blocked, double* d2_out,
+                      int64_t* idx_out) {
+    KT_API_BEGIN
+    LloydArgs& a = l->a;
+    if (run < 0 || run >= a.R) fail(KT_ERR_VALUE, "bad run");
+    const int64_t m = l->m;
+    if (!l->pd2) l->pd2 = static_cast<double*>(l->alloc(size_t(m) * 8));
+    const int grid = int(std::min<int64_t>(ceil_div(m, 256), int64_t(e->num_sms) * 4));
+    e->pre_launch("point_d2");
+    point_d2_kernel<<<grid, 256, 0, e->stream>>>(l->pts, m, l->n, l->fmt, a.assign + size_t(run) * a.stride,
+                                                 a.cent + size_t(a.coff[run]) * kMaxKnobs, l->pd2);
+    e->check_launch("point_d2");
+    auto* d_blocked = static_cast<int64_t*>(e->scratch("lloyd.blocked", 64 * 8));
+    if (n_blocked > 64) fail(KT_ERR_VALUE, "at most 64 blocked points");
+    if (n_blocked)
+        KT_CUDA(cudaMemcpyAsync(d_blocked, blocked, size_t(n_blocked) * 8, cudaMemcpyHostToDevice, e->stream));
+    auto* pv = static_cast<double*>(e->scratch("lloyd.part_v", size_t(grid) * 8));
+    auto* pi = static_cast<int64_t*>(e->scratch("lloyd.part_i", size_t(grid) * 8));
+    e->pre_launch("argmax");
+    argmax_kernel<<<grid, 256, 0, e->stream>>>(l->pd2, m, d_blocked, n_blocked, pv, pi);
+    e->check_launch("argmax");
+    std::vector<double> hv(grid);
+    std::vector<int64_t> hi(grid);
+    KT_CUDA(cudaMemcpyAsync(hv.data(), pv, size_t(grid) * 8, cudaMemcpyDeviceToHost, e->stream));
+    KT_CUDA(cudaMemcpyAsync(hi.data(), pi, size_t(grid) * 8, cudaMemcpyDeviceToHost, e->stream));
+    e->sync();
+    double bv = -1.0;
+    int64_t bi = -1;
+    for (int b = 0; b < grid; ++b)
+        if (hi[b] >= 0 && (bi < 0 || hv[b] > bv || (hv[b] == bv && hi[b] < bi))) {
+            bv = hv[b];
+            bi = hi[b];
+        }
+    *d2_out = bv;
+    *idx_out = bi;
+    KT_API_END
+}
+
+int kt_lloyd_set_centroids(kt_engine* e, kt_lloyd* l, int run, const double* centroids) {
+    KT_API_BEGIN
+    LloydArgs& a = l->a;
+    if (run < 0 || run >= a.R) fail(KT_ERR_VALUE, "bad run");
+    const int k = a.k[run];
+    std::vector<double> c(size_t(k) * kMaxKnobs, 0.0);
+    for (int j = 0; j < k; ++j)
+        for (int i = 0; i < l->n; ++i) c[size_t(j) * kMaxKnobs + i] = centroids[size_t(j) * l->n + i];
+    const int given = kActiveGiven;
+    KT_CUDA(cudaMemcpyAsync(a.cent + size_t(a.coff[run]) * kMaxKnobs, c.data(), c.size() * 8, cudaMemcpyHostToDevice,
+                            e->stream));
+    KT_CUDA(cudaMemcpyAsync(a.run_state + run, &given, 4, cudaMemcpyHostToDevice, e->stream));
+    e->sync();
+    KT_API_END
+}
+
+int kt_lloyd_centroids(kt_engine* e, kt_lloyd* l, int run, double* centroids_out) {
+    KT_API_BEGIN
+    LloydArgs& a = l->a;
+    if (run < 0 || run >= a.R) fail(KT_ERR_VALUE, "bad run");
+    const int k = a.k[run];
+    std::vector<double> c(size_t(k) * kMaxKnobs);
+    KT_CUDA(cudaMemcpyAsync(c.data(), a.cent + size_t(a.coff[run]) * kMaxKnobs, c.size() * 8, cudaMemcpyDeviceToHost,
+                            e->stream));
+    e->sync();
+    for (int j = 0; j < k; ++j)
+        for (int i = 0; i < l->n; ++i) centroids_out[size_t(j) * l->n + i] = c[size_t(j) * kMaxKnobs + i];
+    KT_API_END
+}
+
+int kt_lloyd_assignment(kt_engine* e, kt_lloyd* l, int run, int64_t* assignment_out) {
+    KT_API_BEGIN
+    LloydArgs& a = l->a;
+    if (run < 0 || run >= a.R) fail(KT_ERR_VALUE, "bad run");
+    std::vector<uint8_t> h(size_t(l->m));
+    KT_CUDA(cudaMemcpyAsync(h.data(), a.assign + size_t(run) * a.stride, size_t(l->m), cudaMemcpyDeviceToHost,
+                            e->stream));
+    e->sync();
+    for (int64_t p = 0; p < l->m; ++p) assignment_out[p] = h[size_t(p)];
+    KT_API_END
+}
+
+int kt_lloyd_leaf_losses(kt_engine* e, kt_lloyd* l, int run, const int64_t* bounds, int n_leaves, double* out) {
+    KT_API_BEGIN
+    LloydArgs& a = l->a;
+    if (run < 0 || run >= a.R) fail(KT_ERR_VALUE, "bad run");
+    auto* d = static_cast<double*>(e->scratch("lloyd.leaf", size_t(std::max(n_leaves, 1)) * 8));
+    for (int i = 0; i < n_leaves; ++i) {
+        const int64_t lo = bounds[i], hi = bounds[i + 1];
+        if (lo < 0 || hi > l->m || hi <= lo) fail(KT_ERR_VALUE, "bad leaf bounds");
+        pairwise_loss(e, l->pts + lo, hi - lo, l->n, l->fmt, a.assign + size_t(run) * a.stride + lo,
+                      a.cent + size_t(a.coff[run]) * kMaxKnobs, d + i);
+    }
+    KT_CUDA(cudaMemcpyAsync(out, d, size_t(n_leaves) * 8, cudaMemcpyDeviceToHost, e->stream));
+    e->sync();
+    KT_API_END
+}
+
+int kt_kmeanspp_rows(kt_engine* e, const uint64_t* points_dev, int64_t m, int n_knobs, const int32_t* cards,
+                     uint64_t seed, int k, uint64_t* rows_out) {
+    KT_API_BEGIN
+    if (k < 1 || k > 63) fail(KT_ERR_VALUE, "1 <= k <= 63");
+    if (m < 1) fail(KT_ERR_VALUE, "k-means++ needs at least one point");
+    KmeansSession ses(e, points_dev, m, n_knobs, row_fmt(cards, n_knobs), seed);
+    ses.ensure_init(k);
+    KT_CUDA(cudaMemcpyAsync(rows_out, ses.cent_rows, size_t(k) * 8, cudaMemcpyDeviceToHost, e->stream));
+    e->sync();
     KT_API_END
 }
 
