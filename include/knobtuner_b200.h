@@ -249,6 +249,27 @@ int kt_lloyd_leaf_losses(kt_engine* e, kt_lloyd* l, int run, const int64_t* boun
 int kt_kmeanspp_rows(kt_engine* e, const uint64_t* points_dev, int64_t m, int n_knobs, const int32_t* cards,
                      uint64_t seed, int k, uint64_t* rows_out);
 
+/* Sharded search round: this rank's episodes are the global
+ * episodes [episode_offset, episode_offset + E) — their uniforms come from
+ * SeedSequence(seed, spawn_key=(round_index, episode_offset + e)) — and the
+ * reward / advantage statistics, the PPO batch size, the per-epoch gradients
+ * (float64, PARAM_KEYS order) and the loss report are summed over the ranks
+ * through all_reduce_sum_f64: an in-place SUM of `count` device doubles,
+ * ordered on the engine stream (NCCL under torch.distributed in the Python
+ * layer), returning 0 on success.  Every rank then applies the same Adam step.
+ * Replaces run_search_round (agent.py:267-366) for one shard of the agents.  */
+typedef int (*kt_all_reduce_f64_fn)(void* user, double* dev_buf, int64_t count);
+typedef struct kt_collective {
+    kt_all_reduce_f64_fn all_reduce_sum_f64;
+    void* user;
+    int64_t episode_offset;
+} kt_collective;
+int kt_search_round_ex(kt_engine* e, kt_agent* a, const kt_forest* f, const uint64_t* starts_dev, int32_t E,
+                       const int32_t* cards, int n_knobs, const uint32_t* seed_words, int n_seed_words,
+                       int64_t round_index, const kt_ppo_hyper* hyper, uint64_t* rows_out_dev,
+                       double* scores_out_dev, int32_t* steps_out_dev, int64_t* n_out, kt_round_info* info,
+                       double* logp_out_dev, double* values_out_dev, const kt_collective* coll /* NULL: 1 rank */);
+
 /* ------------------------------------------------------------ utilities */
 /* fp32 GEMM on the tensor cores (tcgen05 kind::tf32, 3xTF32 split, fp32 accumulate
  * in TMEM): C[m][n] = sum_k A(m,k) B(k,n), row-major device arrays;

@@ -57,6 +57,29 @@ class PPOHyper(C.Structure):
 
 
 # name -> (restype, argtypes); every entry must exist in the header and the .so
+ALL_REDUCE_F64 = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64)
+
+
+class Collective(C.Structure):
+    """kt_collective: in-place SUM of device doubles over the ranks + this shard's episode offset."""
+
+    _fields_ = [("all_reduce_sum_f64", ALL_REDUCE_F64), ("user", C.c_void_p), ("episode_offset", C.c_int64)]
+
+
+class _DeviceArray:
+    """Zero-copy view of raw device memory for torch.as_tensor (__cuda_array_interface__ v2)."""
+
+    def __init__(self, ptr: int, count: int, typestr: str = "<f8"):
+        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 2}
+
+
+def device_tensor(ptr: int, count: int, device: int, typestr: str = "<f8"):
+    import torch
+
+    return torch.as_tensor(_DeviceArray(ptr, count, typestr), device=f"cuda:{device}")
+
+
 SIGNATURES = {
     "kt_last_error": (C.c_char_p, []),
     "kt_version": (C.c_char_p, []),
@@ -100,6 +123,8 @@ SIGNATURES = {
     "kt_agent_get_state": (C.c_int, [P, P, pf64, pf64, pf64, pi64]),
     "kt_search_round": (C.c_int, [P, P, P, P, i32, pi32, C.c_int, pu32, C.c_int, i64, C.POINTER(PPOHyper), P, P, P,
                                   pi64, C.POINTER(RoundInfo), P, P]),
+    "kt_search_round_ex": (C.c_int, [P, P, P, P, i32, pi32, C.c_int, pu32, C.c_int, i64, C.POINTER(PPOHyper), P, P, P,
+                                  pi64, C.POINTER(RoundInfo), P, P, C.POINTER(Collective)]),
     "kt_gemm_f32": (C.c_int, [P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P, C.c_int, P, C.c_int, P, C.c_int]),
     "kt_sa_chains": (C.c_int, [P, P, P, i32, i32, i32, pi32, C.c_int, pu32, C.c_int, C.c_int, f64, f64, P, P, P,
                                pi64]),

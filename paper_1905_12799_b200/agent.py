@@ -206,11 +206,16 @@ PPOHyper = _lib.PPOHyper
 
 
 def run_search_rows(agent, model, space, start_rows, engine=None, info: RoundInfo | None = None,
-                    rollout_out: dict | None = None):
+                    rollout_out: dict | None = None, all_reduce=None, episode_offset: int = 0):
     """Array path: CUDA int64 start rows -> (rows, scores, step indices) CUDA tensors; mutates ``agent``.
 
     ``rollout_out`` (optional dict) receives the rollout's per-step log-probs and
     values (Rollout.log_probs / values, agent.py:351-363) as CUDA float64 tensors.
+
+    Sharded rounds (shard.run_search_rows_sharded): ``start_rows`` are the global
+    episodes [episode_offset, episode_offset + E) and ``all_reduce(t)`` sums a CUDA
+    float64 tensor in place over the ranks (reward / advantage statistics, batch
+    size, per-epoch gradients, loss report).
     """
     import torch
 
@@ -238,11 +243,26 @@ def run_search_rows(agent, model, space, start_rows, engine=None, info: RoundInf
         if rollout_out is not None:
             lp = torch.empty(E * S, dtype=torch.float64, device=start_rows.device)
             vals = torch.empty(E * S, dtype=torch.float64, device=start_rows.device)
-        _lib.call("kt_search_round", engine.handle, dev_agent.handle, f.handle, _lib.ptr(start_rows), E,
+        coll = None
+        if all_reduce is not None:
+            errors_seen = []
+
+            def _cb(user, ptr, count):
+                try:
+                    all_reduce(_lib.device_tensor(ptr, count, engine.device))
+                    return 0
+                except Exception as ex:  # surfaced as an engine error
+                    errors_seen.append(ex)
+                    return 1
+
+            cb = _lib.ALL_REDUCE_F64(_cb)
+            coll = _lib.Collective(cb, None, int(episode_offset))
+        _lib.call("kt_search_round_ex", engine.handle, dev_agent.handle, f.handle, _lib.ptr(start_rows), E,
                   _lib.as_ptr(cards, _lib.C.c_int32), int(cards.size), _lib.as_ptr(words, _lib.C.c_uint32),
                   int(words.size), int(agent.rounds_completed), _lib.C.byref(hp), _lib.ptr(rows), _lib.ptr(scores),
                   _lib.ptr(steps), _lib.C.byref(total), _lib.C.byref(info),
-                  _lib.ptr(lp) if lp is not None else None, _lib.ptr(vals) if vals is not None else None)
+                  _lib.ptr(lp) if lp is not None else None, _lib.ptr(vals) if vals is not None else None,
+                  _lib.C.byref(coll) if coll is not None else None)
         if rollout_out is not None:
             rollout_out["log_probs"] = lp[: info.steps]
             rollout_out["values"] = vals[: info.steps]

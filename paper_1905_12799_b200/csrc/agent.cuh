@@ -67,6 +67,7 @@ struct RolloutArgs {
     uint32_t round_words[2];
     int n_round_words;
     const uint64_t* starts;
+    int64_t ep_offset;   // global index of episode 0 (sharded rounds: RNG spawn key = (round, ep_offset + e))
     // outputs (slots)
     uint64_t* visited;   // [E][S+1]
     uint64_t* states;    // [E][S]  config row before the move

@@ -158,10 +158,11 @@ __global__ void gather_rewards_kernel(const double* scores, const int32_t* lengt
     for (int s = threadIdx.x; s < len; s += blockDim.x) rewards[step_off[ep] + s] = scores[visit_off[ep] + 1 + s];
 }
 
-__global__ void normalize_kernel(double* x, int64_t count, const double* sum, const double* sumsq, double floor_std,
-                                 int center_only_returns, double* returns, const double* values) {
-    const double mean = __ddiv_rn(*sum, double(count));
-    const double sd = __dsqrt_rn(__ddiv_rn(*sumsq, double(count)));
+// count: local rows; n_stat: rows of the whole round (all shards) the statistics are over
+__global__ void normalize_kernel(double* x, int64_t count, int64_t n_stat, const double* sum, const double* sumsq,
+                                 double floor_std, int center_only_returns, double* returns, const double* values) {
+    const double mean = __ddiv_rn(*sum, double(n_stat));
+    const double sd = __dsqrt_rn(__ddiv_rn(*sumsq, double(n_stat)));
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x) {
         const double v = x[i];
         if (sd < floor_std) {
@@ -196,7 +197,7 @@ __global__ void gae_kernel(const double* rewards, const double* values, const in
 // ============================================================ PPO row-wise part
 // Inputs per row: logits+value z[row][3n+1], actions, old logp, advantages, returns.
 // Outputs: dz[row][3n+1] (d total / d logits, d values) and per-row loss terms.
-__global__ void ppo_rows_kernel(const float* z, int ldz, int n, int64_t T, const uint16_t* actions,
+__global__ void ppo_rows_kernel(const float* z, int ldz, int n, int64_t T, int64_t T_batch, const uint16_t* actions,
                                 const double* old_logp, const double* adv, const double* ret, double clip,
                                 double value_coef, double entropy_coef, float* dz, double* terms /* [T][3] */) {
     for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < T; r += int64_t(gridDim.x) * blockDim.x) {
@@ -224,7 +225,7 @@ __global__ void ppo_rows_kernel(const float* z, int ldz, int n, int64_t T, const
         const double objective = fmin(raw, cl);
         const double v = zr[3 * n];
         const double err = v - ret[r];
-        const double invB = 1.0 / double(T);
+        const double invB = 1.0 / double(T_batch);  // mean over the whole round's rows (all shards)
         const double coeff = raw <= cl ? A * ratio * invB : 0.0;
         float* d = dz + size_t(r) * ldz;
         for (int k = 0; k < n; ++k) {
@@ -447,6 +448,16 @@ int kt_search_round(kt_engine* e, kt_agent* ag, const kt_forest* f, const uint64
                     int64_t round_index, const kt_ppo_hyper* hp, uint64_t* rows_out_dev, double* scores_out_dev,
                     int32_t* steps_out_dev, int64_t* n_out, kt_round_info* info, double* logp_out_dev,
                     double* values_out_dev) {
+    return kt_search_round_ex(e, ag, f, starts_dev, E, cards, n_knobs, seed_words, n_seed_words, round_index, hp,
+                              rows_out_dev, scores_out_dev, steps_out_dev, n_out, info, logp_out_dev, values_out_dev,
+                              nullptr);
+}
+
+int kt_search_round_ex(kt_engine* e, kt_agent* ag, const kt_forest* f, const uint64_t* starts_dev, int32_t E,
+                       const int32_t* cards, int n_knobs, const uint32_t* seed_words, int n_seed_words,
+                       int64_t round_index, const kt_ppo_hyper* hp, uint64_t* rows_out_dev, double* scores_out_dev,
+                       int32_t* steps_out_dev, int64_t* n_out, kt_round_info* info, double* logp_out_dev,
+                       double* values_out_dev, const kt_collective* coll) {
     KT_API_BEGIN
     using namespace kt;
     if (E < 1) fail(KT_ERR_VALUE, "run_search_round needs at least one start configuration");
@@ -471,6 +482,13 @@ int kt_search_round(kt_engine* e, kt_agent* ag, const kt_forest* f, const uint64
     ra.n_seed_words = n_seed_words;
     ra.n_round_words = u64_words(uint64_t(round_index), ra.round_words);
     ra.starts = starts_dev;
+    ra.ep_offset = coll ? coll->episode_offset : 0;
+    // in-place SUM over the ranks of a sharded round (agents split by episode), ordered on e->stream
+    auto all_reduce = [&](double* buf, int64_t count) {
+        if (!coll) return;
+        const int rc = coll->all_reduce_sum_f64(coll->user, buf, count);
+        if (rc != 0) fail(KT_ERR_INTERNAL, "collective all-reduce failed");
+    };
     const size_t slots = size_t(E) * S;
     ra.visited = static_cast<uint64_t*>(e->scratch("rl.visited", size_t(E) * (S + 1) * 8));
     ra.states = static_cast<uint64_t*>(e->scratch("rl.states", slots * 8));
@@ -496,6 +514,17 @@ int kt_search_round(kt_engine* e, kt_agent* ag, const kt_forest* f, const uint64
     KT_CUDA(cudaMemcpyAsync(&totals[1], off_v + E, 8, cudaMemcpyDeviceToHost, e->stream));
     e->sync();
     const int64_t T = totals[0], N = totals[1];
+    int64_t T_all = T;  // rows of the whole round (all shards): the PPO batch and statistics size
+    if (coll) {
+        auto* tb = static_cast<double*>(e->scratch("rl.tglobal", 8));
+        const double tv = double(T);
+        KT_CUDA(cudaMemcpyAsync(tb, &tv, 8, cudaMemcpyHostToDevice, e->stream));
+        all_reduce(tb, 1);
+        double th = 0.0;
+        KT_CUDA(cudaMemcpyAsync(&th, tb, 8, cudaMemcpyDeviceToHost, e->stream));
+        e->sync();
+        T_all = int64_t(th);
+    }
     auto* st_c = static_cast<uint64_t*>(e->scratch("rl.st_c", size_t(T) * 8));
     auto* ac_c = static_cast<uint16_t*>(e->scratch("rl.ac_c", size_t(T) * 2));
     auto* lp_c = static_cast<double*>(e->scratch("rl.lp_c", size_t(T) * 8));
@@ -518,12 +547,14 @@ int kt_search_round(kt_engine* e, kt_agent* ag, const kt_forest* f, const uint64
     auto* sc = static_cast<double*>(e->scratch("rl.scalars", 16 * 8));  // sum, mean, sumsq per statistic
     const int nb = int(std::min<int64_t>(2048, ceil_div(T, 256)));
     pairwise_sum(e, rew, T, nullptr, sc + 0);
+    all_reduce(sc + 0, 1);
     e->pre_launch("mean");
-    mean_kernel<<<1, 1, 0, e->stream>>>(sc + 0, T, sc + 1);
+    mean_kernel<<<1, 1, 0, e->stream>>>(sc + 0, T_all, sc + 1);
     e->check_launch("mean");
     pairwise_sum(e, rew, T, sc + 1, sc + 2);
+    all_reduce(sc + 2, 1);
     e->pre_launch("normalize");
-    normalize_kernel<<<nb, 256, 0, e->stream>>>(rew, T, sc + 0, sc + 2, 1e-8, 0, nullptr, nullptr);
+    normalize_kernel<<<nb, 256, 0, e->stream>>>(rew, T, T_all, sc + 0, sc + 2, 1e-8, 0, nullptr, nullptr);
     e->check_launch("normalize");
 
     // ---- K4 GAE + advantage normalisation (agent.py:229-242)
@@ -534,12 +565,14 @@ int kt_search_round(kt_engine* e, kt_agent* ag, const kt_forest* f, const uint64
                                                               hp->gae_parameter, adv);
     e->check_launch("gae");
     pairwise_sum(e, adv, T, nullptr, sc + 4);
+    all_reduce(sc + 4, 1);
     e->pre_launch("mean");
-    mean_kernel<<<1, 1, 0, e->stream>>>(sc + 4, T, sc + 5);
+    mean_kernel<<<1, 1, 0, e->stream>>>(sc + 4, T_all, sc + 5);
     e->check_launch("mean");
     pairwise_sum(e, adv, T, sc + 5, sc + 6);
+    all_reduce(sc + 6, 1);
     e->pre_launch("normalize");
-    normalize_kernel<<<nb, 256, 0, e->stream>>>(adv, T, sc + 4, sc + 6, 1e-8, 0, ret, v_c);
+    normalize_kernel<<<nb, 256, 0, e->stream>>>(adv, T, T_all, sc + 4, sc + 6, 1e-8, 0, ret, v_c);
     e->check_launch("normalize");
 
     // ---- K5 PPO epochs (nets.py:94-200)
@@ -573,7 +606,7 @@ int kt_search_round(kt_engine* e, kt_agent* ag, const kt_forest* f, const uint64
         tc_gemm(e, false, true, int(T), g2, h, H1, h, w.w2, h, H2, g2, kEpiBiasTanh, w.b2, nullptr, 0, 1);
         tc_gemm(e, false, true, int(T), n3, g2, H2, g2, w.w3, g2, Z, n3, kEpiBias, w.b3, nullptr, 0, 1);
         e->pre_launch("ppo_rows");
-        ppo_rows_kernel<<<nb, 256, 0, e->stream>>>(Z, n3, n, T, ac_c, lp_c, adv, ret, hp->clip, hp->value_coef,
+        ppo_rows_kernel<<<nb, 256, 0, e->stream>>>(Z, n3, n, T, T_all, ac_c, lp_c, adv, ret, hp->clip, hp->value_coef,
                                                     hp->entropy_coef, dZ, terms);
         e->check_launch("ppo_rows");
         wgrad(e, n3, g2, T, dZ, n3, H2, g2, gw3);
@@ -587,6 +620,7 @@ int kt_search_round(kt_engine* e, kt_agent* ag, const kt_forest* f, const uint64
         e->pre_launch("gather_grads");
         gather_grads_kernel<<<32, 256, 0, e->stream>>>(n, ag->h, ag->g, gw1, gb1, gw2, gb2, gw3, gb3, gflat);
         e->check_launch("gather_grads");
+        all_reduce(gflat, ag->P);  // PPO gradient all-reduce: every rank applies the same Adam step
         ag->t += 1;
         const double bias1 = 1.0 - std::pow(0.9, double(ag->t));
         const double bias2 = 1.0 - std::pow(0.999, double(ag->t));
@@ -597,8 +631,9 @@ int kt_search_round(kt_engine* e, kt_agent* ag, const kt_forest* f, const uint64
         if (ep == hp->epochs - 1) {
             auto* tsum = static_cast<double*>(e->scratch("ppo.tsum", 3 * 8));
             colsum(e, terms, T, 3, 3, tsum);
+            all_reduce(tsum, 3);
             e->pre_launch("loss_report");
-            loss_report_kernel<<<1, 1, 0, e->stream>>>(tsum, T, hp->value_coef, hp->entropy_coef, report);
+            loss_report_kernel<<<1, 1, 0, e->stream>>>(tsum, T_all, hp->value_coef, hp->entropy_coef, report);
             e->check_launch("loss_report");
         }
     }

@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(kRolloutThreads, 1) rollout_kernel(RolloutArgs
         uint32_t spawn[4];
         int ns = 0;
         for (int i = 0; i < a.n_round_words; ++i) spawn[ns++] = a.round_words[i];
-        ns += u64_words(uint64_t(e), spawn + ns);
+        ns += u64_words(uint64_t(e + a.ep_offset), spawn + ns);
         rng = pcg64_from_seed_sequence(a.seed_words, a.n_seed_words, spawn, ns);
         a.visited[int64_t(e) * (a.S + 1)] = row;
     }

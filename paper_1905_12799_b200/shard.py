@@ -449,3 +449,21 @@ def assemble_batch(centroids: np.ndarray, mode, visited_rows: np.ndarray, cards)
         taken.add(row)
         out.append(row)
     return np.array(out, dtype=np.uint64)
+
+
+# ------------------------------------------------------------------ sharded search round (GPU)
+def run_search_rows_sharded(agent, model, space, start_rows_local, episode_offset: int, group=None, engine=None,
+                            info=None):
+    """run_search_round (agent.py:267-366) with the round's episodes sharded over ``group``.
+
+    This rank runs episodes [episode_offset, episode_offset + len(start_rows_local)) —
+    rollouts and scoring need no communication — and the PPO update all-reduces the
+    reward / advantage statistics and the float64 gradients of every epoch (19,289
+    values for 8 knobs), so every rank applies the same Adam step and the agent
+    replicas stay identical.  Returns this shard's (rows, scores, steps).
+    """
+    from .agent import run_search_rows
+
+    comm = Comm(group)
+    return run_search_rows(agent, model, space, start_rows_local, engine=engine, info=info,
+                           all_reduce=comm.all_reduce_sum, episode_offset=episode_offset)

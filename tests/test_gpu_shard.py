@@ -210,3 +210,89 @@ def test_adaptive_sample_sharded_world1_nccl():
         assert [tuple(r) for r in sp.unpack(got, 8).tolist()] == want
     finally:
         dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------ sharded PPO search round
+@pytest.mark.parametrize("world", [2, 3])
+def test_gpu_sharded_search_round_vs_oracle(world):
+    """Episodes split over `world` shards (one engine + thread each): the concatenated
+    trajectory equals the oracle's bit for bit, the agent replicas stay identical, and the
+    update is within the TF32 tier of the unsharded float64 reference."""
+    from test_gpu_rl import LR, MODELS as RL_MODELS, assert_update_close, oracle_from, space_of as rl_space
+
+    from oracle import agent as oagent
+    from paper_1905_12799_b200.agent import PARAM_KEYS, _flat
+
+    mm = RL_MODELS["table1"]
+    space = rl_space(mm["values"])
+    model = kt.CostModel.from_dict(mm["model"])
+    hyper = kt.AgentHyperparams(episodes_per_round=1536)
+    E = 1536
+    replicas = [kt.init_agent(space, hyper, seed=21) for _ in range(world)]
+    ref = oracle_from(replicas[0])
+    before = _flat(replicas[0].params)
+    starts = np.random.default_rng(4).integers(0, np.array(space.cardinalities), size=(E, 8))
+    o_idx, o_sc, o_st = oagent.search_round(ref, mm["model"], mm["values"], starts, hyper.to_dict())
+    engines = [kt.engine(0)] + [_lib.Engine(0) for _ in range(world - 1)]
+    comm = ThreadComm(world)
+
+    def job(rank, view):
+        lo, hi = shard.shard_range(E, rank, world)
+        rows = torch.from_numpy(kt.pack(starts[lo:hi]).view(np.int64)).cuda()
+        r, s, st = kt.run_search_rows(replicas[rank], model, space, rows, engine=engines[rank],
+                                      all_reduce=view.all_reduce_sum, episode_offset=lo)
+        torch.cuda.synchronize()
+        return r.cpu().numpy(), s.cpu().numpy(), st.cpu().numpy()
+
+    outs = [None] * world
+    errs = []
+
+    def body(r):
+        try:
+            outs[r] = job(r, comm.view(r))
+        except Exception as ex:  # pragma: no cover
+            errs.append(ex)
+            comm.bar.abort()
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errs:
+        raise errs[0]
+    rows = np.concatenate([o[0] for o in outs])
+    assert np.array_equal(kt.unpack(rows.view(np.uint64), 8), o_idx)
+    assert np.array_equal(np.concatenate([o[1] for o in outs]), o_sc)
+    assert np.array_equal(np.concatenate([o[2] for o in outs]), o_st)
+    p0 = _flat(replicas[0].params)
+    for a in replicas[1:]:
+        assert np.array_equal(_flat(a.params), p0)  # every rank applied the same Adam step
+        assert a.adam.t == replicas[0].adam.t
+    want = np.concatenate([ref["params"][k].ravel() for k in PARAM_KEYS])
+    assert_update_close(before, p0, want, replicas[0].params, 8)
+    assert LR > 0
+
+
+def test_sharded_search_round_world1_nccl_equals_unsharded():
+    import torch.distributed as dist
+
+    mm = MODELS["table1"]
+    space = space_of(mm["values"])
+    model = kt.CostModel.from_dict(mm["model"])
+    hyper = kt.AgentHyperparams(episodes_per_round=512)
+    a1, a2 = kt.init_agent(space, hyper, seed=3), kt.init_agent(space, hyper, seed=3)
+    starts = np.random.default_rng(9).integers(0, np.array(space.cardinalities), size=(512, 8))
+    rows = torch.from_numpy(kt.pack(starts).view(np.int64)).cuda()
+    r1, s1, t1 = kt.run_search_rows(a1, model, space, rows)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(_free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+    try:
+        r2, s2, t2 = shard.run_search_rows_sharded(a2, model, space, rows, episode_offset=0)
+    finally:
+        dist.destroy_process_group()
+    assert torch.equal(r1, r2) and torch.equal(s1, s2) and torch.equal(t1, t2)
+    from paper_1905_12799_b200.agent import _flat
+
+    assert np.array_equal(_flat(a1.params), _flat(a2.params))
