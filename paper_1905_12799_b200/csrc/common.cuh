@@ -179,6 +179,7 @@ struct kt_engine {
 
 namespace kt {
 // Launch helpers shared across translation units.
+void allow_dynamic_smem(const void* kernel);
 int occupancy_blocks(const void* kernel, int threads, size_t smem);
 // out[i] = sum(in[0..i)), out[n] = total; n <= 16M (single-block scan).
 void exclusive_scan(kt_engine* e, const int64_t* in, int64_t* out, int n);

@@ -7,6 +7,10 @@
 #include "common.cuh"
 #include "rng.cuh"
 
+#include <mutex>
+#include <set>
+#include <utility>
+
 namespace kt {
 
 static thread_local std::string g_last_error;
@@ -14,6 +18,24 @@ static thread_local std::string g_last_error;
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 
 [[noreturn]] void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+
+// Raise a kernel's dynamic shared-memory limit to the device's opt-in maximum, once
+// per (device, kernel).  Setting the limit per launch to that launch's size races
+// when several host threads (several engines) launch the same kernel.
+void allow_dynamic_smem(const void* kernel) {
+    static std::mutex mu;
+    static std::set<std::pair<int, const void*>> done;
+    int dev = 0;
+    KT_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count({dev, kernel})) return;
+    int optin = 0;
+    KT_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    cudaFuncAttributes fa{};
+    KT_CUDA(cudaFuncGetAttributes(&fa, kernel));
+    KT_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - int(fa.sharedSizeBytes)));
+    done.insert({dev, kernel});
+}
 
 int occupancy_blocks(const void* kernel, int threads, size_t smem) {
     int blocks = 0;

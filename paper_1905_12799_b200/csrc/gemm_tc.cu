@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(kTcThreads, 3) tc_gemm_kernel(TcGemmArgs g) {
 template <bool TA, bool TB>
 static void launch_tc(kt_engine* e, const TcGemmArgs& a, dim3 grid, size_t smem) {
     auto kern = tc_gemm_kernel<TA, TB>;
-    KT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    allow_dynamic_smem((const void*)kern);
     // per-role names so kernel_stats separates the PPO GEMM shapes
     const char* name = TA ? "tc_gemm_wgrad" : (a.epi == 2 ? "tc_gemm_dgrad" : "tc_gemm_fwd");
     e->pre_launch(name);

@@ -224,7 +224,7 @@ namespace kt {
 
 void launch_rollout(kt_engine* e, const RolloutArgs& a) {
     const size_t smem = sizeof(RolloutSmem) + 128;
-    KT_CUDA(cudaFuncSetAttribute(rollout_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    allow_dynamic_smem((const void*)rollout_kernel);
     const int grid = int(ceil_div(a.E, kAgentsPerCta));
     e->pre_launch("policy_rollout");
     rollout_kernel<<<grid, kRolloutThreads, smem, e->stream>>>(a);

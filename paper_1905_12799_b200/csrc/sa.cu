@@ -134,7 +134,7 @@ static void launch_chains(kt_engine* e, const kt_forest* f, const SAArgs& a) {
     const size_t smem = size_t(f->n_trees) * f->words_per_tree * 8;
     if (smem > 200 * 1024) fail(KT_ERR_UNSUPPORTED, "forest too large for the in-kernel SA walk");
     auto kern = sa_chain_kernel<D>;
-    KT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    allow_dynamic_smem((const void*)kern);
     e->pre_launch("sa_chains");
     kern<<<int(ceil_div(a.chains, 128)), 128, smem, e->stream>>>(a);
     e->check_launch("sa_chains");

@@ -236,7 +236,7 @@ void mode_vote(kt_engine* e, const uint64_t* rows, int64_t count, int n, const R
     if (smem > 200 * 1024) fail(KT_ERR_UNSUPPORTED, "mode vote supports at most 51200 knob settings in all");
     auto* hist = static_cast<unsigned int*>(e->scratch("mode.hist", smem));
     KT_CUDA(cudaMemsetAsync(hist, 0, smem, e->stream));
-    KT_CUDA(cudaFuncSetAttribute(mode_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    allow_dynamic_smem((const void*)mode_hist_kernel);
     int grid = int(std::min<int64_t>(ceil_div(count, 256), int64_t(e->num_sms) * 4));
     e->pre_launch("mode_hist");
     mode_hist_kernel<<<grid, 256, smem, e->stream>>>(rows, count, a, hist);
@@ -1211,7 +1211,7 @@ static LloydPlan plan_lloyd(kt_engine* e, int64_t m, int K, int R, LloydArgs& a)
     int& threads = pl.threads;
     const void*& kern = pl.kern;
     if (resident) {
-        KT_CUDA(cudaFuncSetAttribute(kres, cudaFuncAttributeMaxDynamicSharedMemorySize, int(res_smem)));
+        allow_dynamic_smem((const void*)kres);
         resident = occupancy_blocks(kres, kLloydResThreads, res_smem) >= 1;
     }
     if (resident) {
@@ -1226,7 +1226,7 @@ static LloydPlan plan_lloyd(kt_engine* e, int64_t m, int K, int R, LloydArgs& a)
             a.tile = std::max(4, std::min(a.tile, std::atoi(t) & ~3));
     } else {
         smem = lloyd_layout(K).total + 16;
-        KT_CUDA(cudaFuncSetAttribute(kstr, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        allow_dynamic_smem((const void*)kstr);
         const int occ = std::max(1, occupancy_blocks(kstr, kLloydThreads, smem));
         // Passes are latency-bound: small point sets run fastest with one block per SM
         // (cheaper grid barrier), large ones with every resident block (measured on
@@ -1846,7 +1846,7 @@ int kt_lloyd_pass(kt_engine* e, kt_lloyd* l, uint64_t* ext_dev) {
     a.timeline = nullptr;
     void* params[] = {&a};
     // the dynamic-smem limit is a per-function attribute: other shards / sessions may have lowered it
-    KT_CUDA(cudaFuncSetAttribute(l->plan.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(l->plan.smem)));
+    allow_dynamic_smem((const void*)l->plan.kern);
     e->pre_launch("lloyd");
     KT_CUDA(cudaLaunchCooperativeKernel(l->plan.kern, l->plan.grid, l->plan.threads, params, l->plan.smem, e->stream));
     e->check_launch("lloyd");

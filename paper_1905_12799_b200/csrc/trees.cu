@@ -152,7 +152,7 @@ static void launch_score_t(kt_engine* e, const kt_forest* f, const uint64_t* row
     per_chunk = std::min(per_chunk, f->n_trees);
     const size_t smem = size_t(per_chunk) * bytes_per_tree;
     auto kern = score_trees_kernel<D, WIDE>;
-    KT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    allow_dynamic_smem((const void*)kern);
     int occ = occupancy_blocks((const void*)kern, threads, smem);
     int64_t want = ceil_div(count, threads * 2);
     int grid = int(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(e->num_sms) * std::max(occ, 1))));
