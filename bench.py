@@ -279,7 +279,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     dom_name, (dom_count, dom_ms) = dom
     if dom_name == "lloyd":
         alg_bytes = sum(i.lloyd_bytes for i in kinfo)
-        note = "per Lloyd pass: m*8 B point rows + 2*m B assignment (read+write) per active k"
+        note = ("SURVEY §8(d) K8: (n + 1) B per distinct point per Lloyd pass per active k (8 B row + 1 B assignment); "
+                "the resident kernel keeps state in shared memory, so DRAM traffic is far below this")
     elif dom_name == "score_trees":
         alg_bytes = K * N * 16
         note = "8 B row read + 8 B float64 score written per candidate"
