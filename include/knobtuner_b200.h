@@ -270,6 +270,18 @@ int kt_search_round_ex(kt_engine* e, kt_agent* a, const kt_forest* f, const uint
                        double* scores_out_dev, int32_t* steps_out_dev, int64_t* n_out, kt_round_info* info,
                        double* logp_out_dev, double* values_out_dev, const kt_collective* coll /* NULL: 1 rank */);
 
+/* ------------------------------------------------ surrogate refit
+ * Gradient-boosted regression trees, exact greedy squared error (fit,
+ * cost_model.py:367-398; _grow :328-364; _best_split :292-325), host code in
+ * numpy's operation order: byte-identical models.  features: host double
+ * [m][n] row-major; outputs: every tree's nodes in preorder (feature -1 =
+ * leaf), concatenated; tree_offsets_out[r] = first node of tree r (rounds + 1
+ * entries); node_capacity >= rounds * (2^(depth+1) - 1).  No device work.   */
+int kt_fit_trees(const double* features, const double* targets, int64_t m, int n, int rounds, int depth,
+                 double learning_rate, int32_t* feature_out, double* threshold_out, int32_t* left_out,
+                 int32_t* right_out, double* value_out, int64_t node_capacity, int32_t* tree_offsets_out,
+                 double* base_out);
+
 /* ------------------------------------------------------------ utilities */
 /* fp32 GEMM on the tensor cores (tcgen05 kind::tf32, 3xTF32 split, fp32 accumulate
  * in TMEM): C[m][n] = sum_k A(m,k) B(k,n), row-major device arrays;

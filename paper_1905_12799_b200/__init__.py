@@ -15,7 +15,7 @@ its unchanged driver and CLI run on the B200.
 from . import errors
 from ._lib import EngineUnavailable, engine
 from .agent import Agent, AgentHyperparams, init_agent, run_search_round, run_search_rows
-from .cost_model import CostModel, Tree, device_forest, predict, predict_rows
+from .cost_model import BoostParams, CostModel, Tree, device_forest, fit, predict, predict_rows
 from .landscape import SyntheticBackend, SyntheticLandscape, batch_runtimes, best_runtime, runtimes_rows, synthetic_runtime, true_fitness
 from .sa import SAParams, run_sa_round, run_sa_rows
 from .sampler import (
@@ -37,8 +37,8 @@ __version__ = "0.1.0"
 __all__ = [
     "Agent", "AgentHyperparams", "init_agent", "run_search_round", "run_search_rows",
     "ClusteringResult", "Configuration", "CostModel", "DesignSpace", "EngineUnavailable", "KNEE_CONSTANT", "KnobDef",
-    "SAParams", "SyntheticBackend", "SyntheticLandscape", "Trajectory", "Tree", "VisitedSet", "adaptive_sample",
-    "adaptive_sample_rows", "batch_runtimes", "best_runtime", "device_forest", "engine", "errors", "grid", "install",
+    "BoostParams", "SAParams", "SyntheticBackend", "SyntheticLandscape", "Trajectory", "Tree", "VisitedSet", "adaptive_sample",
+    "adaptive_sample_rows", "batch_runtimes", "best_runtime", "device_forest", "engine", "errors", "fit", "grid", "install",
     "kmeans", "knee_scan", "mode_config", "pack", "predict", "predict_rows", "round_to_config", "run_sa_round",
     "run_sa_rows", "runtimes_rows", "space_from_dict", "synthetic_runtime", "true_fitness", "unpack",
 ]
@@ -59,6 +59,7 @@ def install() -> dict:
     errors.adopt(mods["errors"])
     patches = [
         (mods["driver"], "predict", predict), (mods["driver"], "run_sa_round", run_sa_round),
+        (mods["driver"], "fit", fit),
         (mods["driver"], "adaptive_sample", adaptive_sample), (mods["driver"], "run_search_round", run_search_round),
         (mods["agent"], "predict", predict),
         (mods["sa"], "predict", predict), (kt, "predict", predict), (kt, "run_sa_round", run_sa_round),

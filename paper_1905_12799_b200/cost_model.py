@@ -197,3 +197,57 @@ def predict(model, space, configs) -> np.ndarray:
         raise ValueError("featurize requires non-negative knob values")
     rows = torch.from_numpy(sp.pack(idx, sp.cardinalities(space)).view(np.int64)).to(f"cuda:{engine.device}")
     return predict_rows(model, space, rows, engine=engine).cpu().numpy()
+
+
+# ------------------------------------------------------------------ fit
+@dataclass(frozen=True)
+class BoostParams:
+    """cost_model.py:24-35."""
+
+    rounds: int = 50
+    depth: int = 4
+    learning_rate: float = 0.3
+
+    def validate(self) -> None:
+        if self.rounds < 1:
+            raise ValueError(f"rounds must be >= 1, got {self.rounds}")
+        if self.depth < 1:
+            raise ValueError(f"depth must be >= 1, got {self.depth}")
+        if not 0.0 < self.learning_rate <= 1.0:
+            raise ValueError(f"learning_rate must be in (0, 1], got {self.learning_rate}")
+
+
+def fit(training, params=BoostParams(), seed: int = 0) -> CostModel:
+    """Gradient boosting under squared error (fit, cost_model.py:367-398) — native exact-greedy
+    restatement (csrc/fit.cu) in numpy's operation order: the model is byte-identical to the
+    reference's (its JSON compares equal).  ``training`` is the reference's TrainingSet (or any
+    object with ``features`` (m, n) and ``targets`` (m,)); ``seed`` is unused, as in the reference.
+    """
+    params.validate()
+    X = np.ascontiguousarray(np.asarray(training.features, dtype=np.float64))
+    y = np.ascontiguousarray(np.asarray(training.targets, dtype=np.float64))
+    if y.size == 0:
+        raise ValueError("training set is empty")
+    if X.ndim != 2 or y.ndim != 1 or X.shape[0] != y.shape[0]:
+        raise errors.DimensionMismatchError(f"features {X.shape} and targets {y.shape} do not align")
+    m, n = X.shape
+    per_tree = (1 << (int(params.depth) + 1)) - 1
+    cap = int(params.rounds) * per_tree
+    feat = np.zeros(cap, dtype=np.int32)
+    thr = np.zeros(cap, dtype=np.float64)
+    left = np.zeros(cap, dtype=np.int32)
+    right = np.zeros(cap, dtype=np.int32)
+    val = np.zeros(cap, dtype=np.float64)
+    offs = np.zeros(int(params.rounds) + 1, dtype=np.int32)
+    base = _lib.C.c_double(0.0)
+    C = _lib.C
+    _lib.call("kt_fit_trees", _lib.as_ptr(X, C.c_double), _lib.as_ptr(y, C.c_double), m, n, int(params.rounds),
+              int(params.depth), float(params.learning_rate), _lib.as_ptr(feat, C.c_int32),
+              _lib.as_ptr(thr, C.c_double), _lib.as_ptr(left, C.c_int32), _lib.as_ptr(right, C.c_int32),
+              _lib.as_ptr(val, C.c_double), cap, _lib.as_ptr(offs, C.c_int32), C.byref(base))
+    trees = []
+    for r in range(int(params.rounds)):
+        a, b = int(offs[r]), int(offs[r + 1])
+        trees.append(Tree(feature=feat[a:b].copy(), threshold=thr[a:b].copy(), child_left=left[a:b].copy(),
+                          child_right=right[a:b].copy(), value=val[a:b].copy()))
+    return CostModel(trees=tuple(trees), base_score=float(base.value), feature_count=n)
