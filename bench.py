@@ -126,6 +126,74 @@ def cpu_baseline(doc, cards, n_sample: int, reps: int = 1) -> dict:
                       f"predict_features + adaptive_sample, single-threaded), {reps} step(s), {dt:.2f} s/step"}
 
 
+# ------------------------------------------------- wall time to 95% best (metric 2)
+W95_STRATEGY, W95_BUDGET, W95_SEED = "sa+as", 1000, 0
+
+
+def w95_fixture():
+    return json.loads((ROOT / "data" / "landscapes" / "bench_grid4d.json").read_text())
+
+
+def f_star(land_doc, values) -> float:
+    """1 / enumerated optimum runtime (the 10^4-config fixture space is brute-forced on the host)."""
+    from oracle.landscape import synthetic_runtimes  # bench reference arm / baseline leg only
+
+    grid = np.indices(tuple(len(v) for v in values)).reshape(len(values), -1).T
+    return 1.0 / float(np.min(synthetic_runtimes(land_doc, grid)))
+
+
+def w95_summary(per: list, impl: str, cores: int) -> dict:
+    reached = [r["seconds_to_95"] for r in per if r["seconds_to_95"] is not None]
+    return {"metric": "wall time to 95% best", "unit": "s", "higher_is_better": False,
+            "value": float(np.mean(reached)) if reached else None, "reached": f"{len(reached)}/{len(per)}",
+            "strategy": W95_STRATEGY, "budget": W95_BUDGET, "seed": W95_SEED,
+            "workload": "reference fixture space bench_grid4d (10^4 configs) x its 5 synthetic landscapes; f* = "
+                        "enumerated optimum; value = mean over landscapes of seconds from tune start until best-so-far "
+                        "fitness >= 0.95 f* (the tune stops there)", "impl": impl, "cores": cores, "per_landscape": per}
+
+
+def w95_ours(engine) -> dict:
+    import paper_1905_12799_b200 as kt
+    from paper_1905_12799_b200 import tune
+    from paper_1905_12799_b200.landscape import landscape_from_dict
+
+    fx = w95_fixture()
+    space = kt.space_from_dict(fx["space"])
+    tune.tune_rows(space, landscape_from_dict(fx["landscapes"][0], space), W95_STRATEGY, 100, 1, engine=engine)  # warm
+    per = []
+    for i, doc in enumerate(fx["landscapes"]):
+        land = landscape_from_dict(doc, space)
+        fs = 1.0 / kt.best_runtime(land)[0]
+        run = tune.tune_rows(space, land, W95_STRATEGY, W95_BUDGET, W95_SEED, engine=engine, stop_fitness=0.95 * fs)
+        per.append({"landscape": i, "seconds_to_95": run.wall_to_fraction(fs, 0.95), "tune_seconds": run.seconds,
+                    "rounds": run.rounds, "best_over_fstar": run.best_fitness / fs,
+                    "measurements_to_95": next((m for _, m, b in run.trace if b >= 0.95 * fs), None)})
+    return w95_summary(per, "ours (B200)", 1)
+
+
+def _w95_ref_job(i):
+    from oracle import tune as otune
+
+    fx = w95_fixture()
+    values = [k["values"] for k in fx["space"]["knobs"]]
+    doc = fx["landscapes"][i]
+    fs = f_star(doc, values)
+    configs, rts, trace, rounds = otune.tune(values, doc, W95_STRATEGY, W95_BUDGET, W95_SEED, stop_fitness=0.95 * fs)
+    t95 = next((t for t, _, b in trace if b >= 0.95 * fs), None)
+    return {"landscape": i, "seconds_to_95": t95, "tune_seconds": trace[-1][0], "rounds": rounds,
+            "best_over_fstar": max(1.0 / r for r in rts) / fs,
+            "measurements_to_95": next((m for _, m, b in trace if b >= 0.95 * fs), None)}
+
+
+def w95_reference() -> dict:
+    import multiprocessing as mp
+
+    n = len(w95_fixture()["landscapes"])
+    with mp.get_context("fork").Pool(n) as pool:
+        per = pool.map(_w95_ref_job, range(n))
+    return w95_summary(per, "reference algorithm (oracle numpy port), one host process per landscape", n)
+
+
 def _ref_job(job):
     n, cand_seed, seed = job
     doc = load_model()
@@ -164,6 +232,8 @@ def run_reference(args, rank: int, world: int) -> None:
                                    f"(predict_features + adaptive_sample), {procs} processes x {args.steps} steps"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if not args.no_wall95:
+        line["wall_to_95"] = w95_reference()
     print(json.dumps(line), flush=True)
 
 
@@ -310,6 +380,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         "clocks": clk.summary(),
         "cpu_baseline": base,
     }
+    if not args.no_wall95:
+        line["wall_to_95"] = w95_ours(eng)
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
@@ -351,6 +423,7 @@ def main() -> None:
     ap.add_argument("--ref-sample", type=int, default=16384)
     ap.add_argument("--ref-procs", type=int, default=0, help="host processes for --impl reference (0: all cores)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-wall95", action="store_true", help="skip the wall-time-to-95%%-best tune runs")
     ap.add_argument("--workload", choices=("s2", "rl"), default="s2",
                     help="s2: the headline scored+clustered step; rl: 5 tasks x 4096 PPO agents per step")
     args = ap.parse_args()

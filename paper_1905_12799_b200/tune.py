@@ -114,13 +114,14 @@ class TuneRun:
 def tune_rows(space, landscape, strategy: str, budget: int, seed: int = 0,
               agent_params: AgentHyperparams | None = None, sa_params: SAParams | None = None,
               boost_params: BoostParams = BoostParams(), clock=time.perf_counter, engine=None,
-              runtimes=None) -> TuneRun:
+              runtimes=None, stop_fitness: float | None = None) -> TuneRun:
     """One tuning task to budget exhaustion (driver.py:161-243) on the B200.
 
     ``runtimes(batch) -> runtimes`` overrides the K3 landscape measurement (the reference's
     ``replay:LOG`` backend, backends.py:300-345, is the analogous hook): tests replay the
     reference's own measured runtimes, because CUDA's exp differs from glibc's by <= 1 ulp
     and a tune loop amplifies any last-bit difference into a different trajectory.
+    ``stop_fitness``: stop once best-so-far fitness reaches it (wall-time-to-95% harness).
     """
     import torch
 
@@ -160,7 +161,7 @@ def tune_rows(space, landscape, strategy: str, budget: int, seed: int = 0,
     if bootstrap:
         measure(bootstrap)
         rounds = 1
-    while len(run.configs) < budget:
+    while len(run.configs) < budget and not (stop_fitness is not None and best >= stop_fitness):
         round_index = rounds
         remaining = budget - len(run.configs)
         traj = None
