@@ -459,6 +459,7 @@ struct LloydArgs {
     int tile;                  // resident kernel: points per queue tile (multiple of 4)
     int rows_resident;         // resident kernel: the block's rows live in shared memory too
     int external;              // 1: one pass, deltas + changed counts -> ext, no in-kernel decisions
+    unsigned int* barrier;     // grid-barrier counter, zeroed before every launch
     unsigned long long* ext;   // external: [K][9] int64 deltas then [R] changed counts (all-reduced by the host)
     double* cent;              // [K][8] centroids of the latest pass
     const uint64_t* init_rows; // k-means++ rows (prefix shared by all runs)
@@ -592,6 +593,24 @@ __device__ __forceinline__ int full_assign(const float* c32, const double* c64, 
     u = dist_up(best, k1);
     l = k > 1 ? dist_dn(second, k1) : INFINITY;
     return bj;
+}
+
+// Grid barrier for the Lloyd launches: one release-add per block on a monotonic
+// counter (zeroed by the host before the launch) and an acquire spin by thread 0;
+// bar.sync on both sides makes it cumulative for the whole block.  Cheaper than
+// cooperative_groups' grid.sync (no separate fences, no generation flip).
+constexpr bool kCustomGridBarrier = true;
+__device__ __forceinline__ void lloyd_grid_barrier(unsigned int* ctr, unsigned int target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned int old, cur;
+        (void)old;
+        asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
+        do {
+            asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(ctr) : "memory");
+        } while (cur < target);
+    }
+    __syncthreads();
 }
 
 // Per-run decision after a pass whose summed deltas are already in S (sampler.py:99-116):
@@ -780,7 +799,12 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
         if (a.rows_resident)
             for (int i = tid; i < np; i += blockDim.x) s_rows[i] = a.pts[b0 + i];
     }
-    grid.sync();  // every block has read a.cent / a.dcum before block 0 overwrites them
+    unsigned int n_bar = 0;  // grid barriers passed (custom barrier target = n_bar * gridDim.x)
+    auto grid_barrier = [&]() {
+        if (kCustomGridBarrier) lloyd_grid_barrier(a.barrier, ++n_bar * gridDim.x);
+        else grid.sync();
+    };
+    grid_barrier();  // every block has read a.cent / a.dcum before block 0 overwrites them
 
     int it = a.it0;
     auto stamp = [&](int phase) {
@@ -1062,7 +1086,7 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
             if (tid == 0) a.work[nb] = 0u;
         }
         stamp(4);
-        grid.sync();
+        grid_barrier();
         stamp(5);
 
         // ---- decisions (identical in every block)
@@ -1351,6 +1375,7 @@ struct KmeansSession {
         a.run_state = static_cast<int*>(e->scratch("km.state", kMaxRuns * 4));
         a.run_iter = static_cast<int*>(e->scratch("km.iter", kMaxRuns * 4));
         a.ctrl = static_cast<int*>(e->scratch("km.ctrl", 16));
+        a.barrier = static_cast<unsigned int*>(e->scratch("km.barrier", 16));
         static const bool want_stats = std::getenv("KT_LLOYD_STATS") != nullptr;
         a.stats = nullptr;
         if (want_stats) {
@@ -1384,6 +1409,7 @@ struct KmeansSession {
             KT_CUDA(cudaMemsetAsync(a.D, 0, size_t(3) * K * kSumW * 8, e->stream));
             KT_CUDA(cudaMemsetAsync(a.chg, 0, 3 * kMaxRuns * 4, e->stream));
             KT_CUDA(cudaMemsetAsync(a.work, 0, 16, e->stream));
+            KT_CUDA(cudaMemsetAsync(a.barrier, 0, 16, e->stream));
             a.it0 = it;
             a.it_end = history ? it + 1 : a.max_iters;
             void* params[] = {&a};
@@ -1804,6 +1830,7 @@ int kt_lloyd_create(kt_engine* e, const uint64_t* shard_pts_dev, int64_t shard_m
     a.run_state = static_cast<int*>(l->alloc(kMaxRuns * 4));
     a.run_iter = static_cast<int*>(l->alloc(kMaxRuns * 4));
     a.ctrl = static_cast<int*>(l->alloc(16));
+    a.barrier = static_cast<unsigned int*>(l->alloc(16));
     auto* rows = static_cast<uint64_t*>(l->alloc(size_t(kmax) * 8));
     a.init_rows = rows;
     a.external = 1;
@@ -1839,6 +1866,7 @@ int kt_lloyd_pass(kt_engine* e, kt_lloyd* l, uint64_t* ext_dev) {
     LloydArgs& a = l->a;
     KT_CUDA(cudaMemsetAsync(ext_dev, 0, (size_t(a.K) * kSumW + a.R) * 8, e->stream));
     KT_CUDA(cudaMemsetAsync(a.work, 0, 16, e->stream));
+    KT_CUDA(cudaMemsetAsync(a.barrier, 0, 16, e->stream));
     a.ext = reinterpret_cast<unsigned long long*>(ext_dev);
     a.it0 = l->it;
     a.it_end = l->it + 1;
