@@ -475,7 +475,7 @@ struct LloydArgs {
 };
 
 struct LloydLayout {
-    size_t S, c64, c32, delta, drift, dcum, total;
+    size_t S, c64, c32, delta, drift, dcum, cnext, total;
 };
 
 __host__ __device__ inline LloydLayout lloyd_layout(int K) {
@@ -493,6 +493,9 @@ __host__ __device__ inline LloydLayout lloyd_layout(int K) {
     o += size_t(K) * 4;
     L.dcum = o;
     o += size_t(K) * 4;
+    o = (o + 7) & ~size_t(7);
+    L.cnext = o;  // next pass's centroids, computed right after the grid barrier
+    o += size_t(K) * kMaxKnobs * 8;
     L.total = (o + 15) & ~size_t(15);
     return L;
 }
@@ -510,6 +513,8 @@ struct RunShared {
     float m1[kMaxRuns], m2[kMaxRuns];  // largest / second largest drift
     int amax[kMaxRuns];
     int exit_flag, n_active;
+    unsigned int chg_g[kMaxRuns];  // changed flags of the whole grid (after the barrier)
+    int empty[kMaxRuns];           // a cluster of the run ended the pass empty
 };
 
 // Conservative |fp32 - exact| bound for sum_i (p_i - c_i)^2 with p_i, |c_i| <= 255
@@ -763,6 +768,7 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
     unsigned long long* delta64 = reinterpret_cast<unsigned long long*>(s_raw + L.delta);  // resident layout
     float* drift = reinterpret_cast<float*>(s_raw + L.drift);
     float* dcum = reinterpret_cast<float*>(s_raw + L.dcum);
+    double* cnext = reinterpret_cast<double*>(s_raw + L.cnext);
     cg::grid_group grid = cg::this_grid();
     const int tid = threadIdx.x;
     const int K = a.K, R = a.R, n = a.n;
@@ -784,6 +790,7 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
     for (int i = tid; i < K * kMaxKnobs; i += blockDim.x) c64[i] = a.cent[i];  // centroids of the previous pass
     for (int i = tid; i < K; i += blockDim.x) dcum[i] = a.dcum[i];
     if (tid < R) rs.state[tid] = a.run_state[tid];
+    if (tid < kMaxRuns) rs.empty[tid] = 0;
     if (tid < kMaxRuns * 3) rs.cnt[tid / 3][tid % 3] = 0;
     if (tid < 2) s_qn[tid] = 0;
     for (int r = 0; r < R; ++r)
@@ -815,8 +822,11 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
         }
     };
     int tile_parity = 0;  // queue counter in use (alternates per tile, across passes too)
+    bool entry = true;
     while (it < a.it_end) {
         stamp(0);
+        if (entry) {  // launch entry; later passes get their centroids from the fused update below
+        entry = false;
         // ---- this pass's centroids and each centroid's drift from the previous pass:
         // one thread per (cluster, coordinate); 8 consecutive lanes reduce a drift
         for (int x0 = 0; x0 < K * kMaxKnobs; x0 += blockDim.x) {
@@ -879,6 +889,7 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
             }
         }
         __syncthreads();
+        }
 
         stamp(1);
         if constexpr (RESIDENT) {
@@ -1089,24 +1100,99 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
         grid_barrier();
         stamp(5);
 
-        // ---- decisions (identical in every block)
-        for (int i = tid; i < K * kSumW; i += blockDim.x) {
-            const long long v = (long long)__ldcg(Dcur + i);
-            if (v) S[i] += v;
-        }
-        __syncthreads();
+        // ---- fused update (identical in every block): sums += grid deltas, the next pass's
+        // centroids and drifts (one thread per (cluster, coordinate)), then one warp per run
+        // decides (sampler.py:99-116), reduces its drifts and advances its shrink table.
         if (tid == 0) {
             rs.exit_flag = 0;
             rs.n_active = 0;
-            for (int r = 0; r < R; ++r) {
+        }
+        if (tid < R) rs.chg_g[tid] = __ldcg(a.chg + buf * kMaxRuns + tid);
+        for (int x0 = 0; x0 < K * kMaxKnobs; x0 += blockDim.x) {
+            const int x = x0 + tid;
+            const int g = x >> 3, i = x & 7;
+            const int r = x < K * kMaxKnobs ? run_of[g] : 0;
+            const bool live = x < K * kMaxKnobs && run_active(rs.state[r]);
+            double dlt2 = 0.0;
+            if (live) {
+                const long long cnt = S[g * kSumW + 8] + (long long)__ldcg(Dcur + g * kSumW + 8);
+                double c = 0.0;
+                if (i < n) {
+                    const long long sv = S[g * kSumW + i] + (long long)__ldcg(Dcur + g * kSumW + i);
+                    S[g * kSumW + i] = sv;
+                    if (cnt > 0) c = __ddiv_rn(double(sv), double(cnt));
+                }
+                cnext[g * kMaxKnobs + i] = c;
+                const double dlt = c - c64[g * kMaxKnobs + i];
+                dlt2 = dlt * dlt;
+                if (i == 7) {  // the count after all lanes read it
+                    if (cnt == 0) rs.empty[r] = 1;
+                }
+            }
+            dlt2 += __shfl_xor_sync(0xffffffffu, dlt2, 1);
+            dlt2 += __shfl_xor_sync(0xffffffffu, dlt2, 2);
+            dlt2 += __shfl_xor_sync(0xffffffffu, dlt2, 4);
+            if (live && i == 0) drift[g] = __double2float_ru(sqrt(dlt2) * (1.0 + 1e-9) + 1e-30);
+        }
+        for (int i = tid; i < K * kDeltaW; i += blockDim.x) delta[i] = 0;  // also clears delta64
+        if (RESIDENT && kDeltaMode == 2)
+            for (int i = tid; i < nwarps_blk * K * kDeltaW; i += blockDim.x) delta_w[i] = 0;
+        __syncthreads();
+        for (int g = tid; g < K; g += blockDim.x)  // count sums, after every lane above has read them
+            if (run_active(rs.state[run_of[g]])) S[g * kSumW + 8] += (long long)__ldcg(Dcur + g * kSumW + 8);
+        {
+            const int w = tid >> 5;
+            if (w < R) {
+                const int r = w;
                 int st = rs.state[r];
-                if (!run_active(st)) continue;
-                const unsigned changed = __ldcg(a.chg + buf * kMaxRuns + r);
-                st = lloyd_decide(a, S, r, st, changed != 0, it);
-                if (st == kNeedsReseed) rs.exit_flag = 1;
-                if (st == kActiveFromSums) ++rs.n_active;
-                if (st != kActiveFromSums && blockIdx.x == 0) a.run_iter[r] = it;
-                rs.state[r] = st;
+                if (run_active(st)) {
+                    if (!rs.chg_g[r]) st = kConverged;
+                    else if (it == a.max_iters - 1) st = kMaxed;
+                    else if (rs.empty[r]) st = kNeedsReseed;
+                    else st = kActiveFromSums;
+                    if (lane == 0) {
+                        if (st != kActiveFromSums && blockIdx.x == 0) a.run_iter[r] = it;
+                        if (st == kNeedsReseed) rs.exit_flag = 1;
+                        if (st == kActiveFromSums) atomicAdd(&rs.n_active, 1);
+                    }
+                    if (st == kActiveFromSums && it + 1 < a.it_end) {
+                        // m1 = largest drift, amax = its first index, m2 = largest of the others
+                        // (at the launch's last pass the next launch's entry phase does this)
+                        const int k = a.k[r], co = a.coff[r];
+                        const float d0 = lane < k ? drift[co + lane] : 0.0f;
+                        const float d1 = lane + 32 < k ? drift[co + lane + 32] : 0.0f;
+                        const unsigned b0 = __float_as_uint(d0), b1 = __float_as_uint(d1);
+                        const unsigned mx = __reduce_max_sync(0xffffffffu, b0 > b1 ? b0 : b1);
+                        const unsigned h0 = __ballot_sync(0xffffffffu, lane < k && b0 == mx);
+                        const unsigned h1 = __ballot_sync(0xffffffffu, lane + 32 < k && b1 == mx);
+                        const int am = h0 ? __ffs(h0) - 1 : 32 + __ffs(h1) - 1;
+                        const unsigned o0 = (lane < k && lane != am) ? b0 : 0u;
+                        const unsigned o1 = (lane + 32 < k && lane + 32 != am) ? b1 : 0u;
+                        const float m1 = __uint_as_float(mx);
+                        const float m2 = __uint_as_float(__reduce_max_sync(0xffffffffu, o0 > o1 ? o0 : o1));
+                        if (lane < k)
+                            dcum[co + lane] = __fadd_ru(dcum[co + lane], __fadd_ru(d0, lane == am ? m2 : m1));
+                        if (lane + 32 < k)
+                            dcum[co + lane + 32] = __fadd_ru(dcum[co + lane + 32], __fadd_ru(d1, lane + 32 == am ? m2 : m1));
+                    }
+                    if (lane == 0) {
+                        rs.state[r] = st;
+                        rs.empty[r] = 0;
+                        rs.changed[r] = 0;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        // commit the next pass's centroids of the runs that go on (converged / maxed runs keep
+        // the centroids of their last pass: the reference's result; reseeds are set by the host)
+        for (int x = tid; x < K * kMaxKnobs && it + 1 < a.it_end; x += blockDim.x) {
+            const int g = x >> 3;
+            if (rs.state[run_of[g]] == kActiveFromSums) {
+                const double c = cnext[x];
+                c64[x] = c;
+                c32[x] = float(c);
+                if (blockIdx.x == 0) a.cent[x] = c;
             }
         }
         __syncthreads();
