@@ -636,6 +636,7 @@ __device__ __forceinline__ int lloyd_decide(const LloydArgs& a, const long long*
 // so the queue never overflows) and only they fetch their rows from L2.
 constexpr int kLloydResThreads = 768;
 constexpr int kEvalUnroll = 2;  // queue entries per thread whose rows load together
+constexpr int kScanQuads = 4;   // quads per thread per scan round
 // Resident-kernel cluster-sum deltas: 0 = packed 64-bit shared words (5 CAS atomics per
 // move), 1 = 17-wide int32 shared counters (9 native atomics), 2 = a private int32
 // copy per warp (9 native atomics, contention only within a warp).  Measured on B200
@@ -897,32 +898,37 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
             for (int t0 = 0; t0 < np; t0 += a.tile) {
                 const int t1 = t0 + a.tile < np ? t0 + a.tile : np;
                 int* qn = s_qn + tile_parity;
-                // scan: one quad per thread and round; unsettled (point, run, old) -> block queue
-                for (int qd0 = t0 >> 2; qd0 < ((t1 + 3) >> 2); qd0 += blockDim.x) {
-                    const int qd = qd0 + tid;
-                    const bool valid = qd < ((t1 + 3) >> 2);
-                    const int p0 = qd << 2;
-                    const int cnt = valid ? (t1 - p0 < 4 ? t1 - p0 : 4) : 0;
+                // scan: kScanQuads quads per thread and round (independent loads, one warp
+                // scan + one queue atomic per warp and round); unsettled (point, run, old) -> queue
+                const int tq1 = (t1 + 3) >> 2;
+                for (int qd0 = t0 >> 2; qd0 < tq1; qd0 += kScanQuads * blockDim.x) {
                     for (int r = 0; r < R; ++r) {
                         const int st = rs.state[r];
                         if (!run_active(st)) continue;
                         const int co = a.coff[r];
-                        unsigned todo = 0;
-                        uint32_t as4 = 0xffffffffu;
-                        if (cnt > 0) {
-                            as4 = *reinterpret_cast<const uint32_t*>(s_asg + r * P + p0);
-                            if (st == kActiveFromSums) {
-                                const float4 b4 = *reinterpret_cast<const float4*>(s_bud + r * P + p0);
-                                const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
+                        unsigned todo = 0;  // bit 4q + e: point e of quad q
+                        uint32_t as4[kScanQuads];
 #pragma unroll
-                                for (int e = 0; e < 4; ++e) {
-                                    const int old = (as4 >> (8 * e)) & 0xff;
-                                    if (e >= cnt) continue;
-                                    if (old == 255 || !(__fsub_rd(bb[e], dcum[co + old]) > kSettleMargin))
-                                        todo |= 1u << e;
+                        for (int q = 0; q < kScanQuads; ++q) {
+                            const int qd = qd0 + q * blockDim.x + tid;
+                            const int p0 = qd << 2;
+                            const int cnt = qd < tq1 ? (t1 - p0 < 4 ? t1 - p0 : 4) : 0;
+                            as4[q] = 0xffffffffu;
+                            if (cnt > 0) {
+                                as4[q] = *reinterpret_cast<const uint32_t*>(s_asg + r * P + p0);
+                                if (st == kActiveFromSums) {
+                                    const float4 b4 = *reinterpret_cast<const float4*>(s_bud + r * P + p0);
+                                    const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+                                    for (int e = 0; e < 4; ++e) {
+                                        const int old = (as4[q] >> (8 * e)) & 0xff;
+                                        if (e >= cnt) continue;
+                                        if (old == 255 || !(__fsub_rd(bb[e], dcum[co + old]) > kSettleMargin))
+                                            todo |= 1u << (4 * q + e);
+                                    }
+                                } else {
+                                    todo |= ((1u << cnt) - 1u) << (4 * q);
                                 }
-                            } else {
-                                todo = (1u << cnt) - 1u;
                             }
                         }
                         // warp-aggregated append
@@ -938,9 +944,14 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
                         wbase = __shfl_sync(0xffffffffu, wbase, 31);
                         int pos = wbase + incl - c;
                         while (todo) {
-                            const int e = __ffs(todo) - 1;
+                            const int bit = __ffs(todo) - 1;
                             todo &= todo - 1;
-                            s_queue[pos++] = uint32_t(p0 + e) | (uint32_t(r) << 16) | (((as4 >> (8 * e)) & 0xffu) << 24);
+                            const int q = bit >> 2, e = bit & 3;
+                            const int p0 = (qd0 + q * int(blockDim.x) + tid) << 2;
+                            uint32_t aq = as4[0];  // select without dynamic register indexing
+#pragma unroll
+                            for (int qq = 1; qq < kScanQuads; ++qq) aq = q == qq ? as4[qq] : aq;
+                            s_queue[pos++] = uint32_t(p0 + e) | (uint32_t(r) << 16) | (((aq >> (8 * e)) & 0xffu) << 24);
                         }
                     }
                 }
