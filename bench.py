@@ -373,6 +373,11 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         alg_bytes = None
         note = "no byte model"
     achieved = (alg_bytes / dom_count) / (dom_ms / dom_count / 1e3) / 1e9 if alg_bytes else None
+    # DRAM traffic per launch of the same kernel from the committed ncu --set full capture
+    tr_doc = ROOT / "profiles" / "r1" / "traffic.json"
+    traffic = None
+    if tr_doc.exists():
+        traffic = json.loads(tr_doc.read_text())["kernels"].get(dom_name, {}).get("dram_bytes_per_launch")
     kernel_table = {k: {"launches": c, "ms_total": round(ms, 4), "ms_per_step": round(ms / K, 4)}
                     for k, (c, ms) in sorted(stats.items(), key=lambda kv: -kv[1][1])}
     base = cpu_baseline(doc, cards, args.cpu_sample) if not args.no_cpu_baseline else None
@@ -390,7 +395,9 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": N * 8, "d2h_bytes_per_step": d2h // K},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                     "frac": (achieved / pk["hbm_gbs"]) if achieved else None, "traffic": None,
+                     "frac": (achieved / pk["hbm_gbs"]) if achieved else None, "traffic": traffic,
+                     "traffic_source": "profiles/r1/traffic.json (ncu --set full, bytes per launch)",
+                     "alg_bytes_per_launch": (alg_bytes / dom_count) if alg_bytes else None,
                      "peak_source": pk["source"], "bytes_model": note,
                      "kernel_share_of_step": dom_ms / sum(ms for _, ms in stats.values())},
         "kernels": kernel_table,
