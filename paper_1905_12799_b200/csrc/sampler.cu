@@ -275,6 +275,7 @@ struct InitArgs {
     int* d2[2];
     long long* sums[2];
     int nchunks;
+    unsigned int* barrier;  // grid-barrier counter, zeroed before the launch
 };
 
 // Block-wide exclusive scan of one int64 per thread; returns the block total.
@@ -306,19 +307,55 @@ __device__ __forceinline__ long long block_exclusive_scan(long long v, long long
     return total;
 }
 
+// Block-wide inclusive scan of one int64 per thread with one barrier: warp scans, warp
+// totals through shared memory, every warp adds the totals of the warps before it.
+// Returns the thread's exclusive prefix; *total receives the block total.
+__device__ __forceinline__ long long block_excl_scan1(long long v, long long* s_warp, long long* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    long long incl = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const long long t = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += t;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    long long before = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < kInitThreads / 32; ++w) {
+        const long long x = s_warp[w];
+        before += w < warp ? x : 0;
+        tot += x;
+    }
+    *total = tot;
+    return before + incl - v;
+}
+
+__device__ __forceinline__ void init_grid_barrier(unsigned int* ctr, unsigned int target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned int cur;
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+        do {
+            asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(ctr) : "memory");
+        } while (cur < target);
+    }
+    __syncthreads();
+}
+
 __global__ void __launch_bounds__(kInitThreads) init_kernel(InitArgs a) {
-    cg::grid_group grid = cg::this_grid();
-    __shared__ long long s_warp[33];
-    __shared__ long long s_T, s_before;
+    __shared__ long long s_warp[2][kInitThreads / 32];  // double-buffered: no barrier between scans
+    __shared__ long long s_before;
     __shared__ int s_chunk;
     __shared__ unsigned long long s_found;
-    __shared__ uint64_t s_c;
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31;
     constexpr int per = kInitChunk / kInitThreads;  // 16
+    unsigned int n_bar = 0;
     for (int j = a.j0; j < a.j1; ++j) {
         // ---- centroid j (every block computes the same choice)
+        uint64_t c;
         if (j == 0) {
-            if (tid == 0) s_c = a.pts[a.first_idx];
+            c = a.pts[a.first_idx];
         } else {
             const long long* cs = a.sums[(j - 1) & 1];
             const int* w = a.d2[(j - 1) & 1];
@@ -327,15 +364,10 @@ __global__ void __launch_bounds__(kInitThreads) init_kernel(InitArgs a) {
             const int lo = min(a.nchunks, tid * cper), hi = min(a.nchunks, lo + cper);
             long long mine = 0;
             for (int i = lo; i < hi; ++i) mine += __ldcg(cs + i);
-            long long excl;
-            const long long total = block_exclusive_scan(mine, excl, s_warp);
-            if (tid == 0) {
-                s_T = (long long)floor(__dmul_rn(a.uniforms[j - 1], double(total)));
-                s_chunk = -1;
-                s_found = ~0ull;
-            }
-            __syncthreads();
-            const long long T = s_T;
+            if (tid == 0) s_found = ~0ull;
+            long long total;
+            const long long excl = block_excl_scan1(mine, s_warp[0], &total);
+            const long long T = (long long)floor(__dmul_rn(a.uniforms[j - 1], double(total)));
             long long run = excl;
             for (int i = lo; i < hi; ++i) {
                 const long long next = run + __ldcg(cs + i);
@@ -345,46 +377,49 @@ __global__ void __launch_bounds__(kInitThreads) init_kernel(InitArgs a) {
                 }
                 run = next;
             }
+            if (tid == 0 && T >= total) s_chunk = -1;
             __syncthreads();
             const int ch = s_chunk;
             if (ch >= 0) {
                 const int64_t p0 = int64_t(ch) * kInitChunk + tid * per;
-                long long v[per];
+                int v[per];
                 long long tsum = 0;
+                if (p0 + per <= a.m && (reinterpret_cast<uintptr_t>(w + p0) & 15) == 0) {
+                    const int4* w4 = reinterpret_cast<const int4*>(w + p0);
 #pragma unroll
-                for (int q = 0; q < per; ++q) {
-                    v[q] = (p0 + q < a.m) ? __ldcg(w + p0 + q) : 0;
-                    tsum += v[q];
+                    for (int q = 0; q < per / 4; ++q) {
+                        const int4 x = __ldcg(w4 + q);
+                        v[4 * q] = x.x, v[4 * q + 1] = x.y, v[4 * q + 2] = x.z, v[4 * q + 3] = x.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < per; ++q) v[q] = (p0 + q < a.m) ? __ldcg(w + p0 + q) : 0;
                 }
-                long long ex;
-                block_exclusive_scan(tsum, ex, s_warp);
-                long long acc = s_before + ex;
+#pragma unroll
+                for (int q = 0; q < per; ++q) tsum += v[q];
+                long long tot2;
+                long long acc = s_before + block_excl_scan1(tsum, s_warp[1], &tot2);
+                int first = -1;  // first point of the slice whose inclusive prefix passes T
 #pragma unroll
                 for (int q = 0; q < per; ++q) {
                     acc += v[q];
-                    if (acc > T && p0 + q < a.m) {
-                        atomicMin(&s_found, (unsigned long long)(p0 + q));
-                        break;
-                    }
+                    if (first < 0 && acc > T && p0 + q < a.m) first = q;
                 }
+                if (first >= 0) atomicMin(&s_found, (unsigned long long)(p0 + first));
             }
             __syncthreads();
-            if (tid == 0) {
-                int64_t idx = s_found == ~0ull ? a.m - 1 : int64_t(s_found);
-                if (idx > a.m - 1) idx = a.m - 1;
-                s_c = a.pts[idx];
-            }
+            int64_t idx = s_found == ~0ull ? a.m - 1 : int64_t(s_found);
+            if (idx > a.m - 1) idx = a.m - 1;
+            c = a.pts[idx];  // same address in every thread: one broadcast load
         }
-        __syncthreads();
-        const uint64_t c = s_c;
         if (blockIdx.x == 0 && tid == 0) a.cent_rows[j] = c;
-        // ---- weights for the next centroid
+        // ---- weights for the next centroid: d2 = min(d2, |p - c|^2), per-chunk sums
         const int* wold = a.d2[(j - 1) & 1];
         int* wnew = a.d2[j & 1];
         long long* snew = a.sums[j & 1];
         for (int ch = blockIdx.x; ch < a.nchunks; ch += gridDim.x) {
             const int64_t base = int64_t(ch) * kInitChunk;
-            long long s = 0;
+            long long sum = 0;
 #pragma unroll 4
             for (int q = 0; q < per; ++q) {
                 const int64_t p = base + q * kInitThreads + tid;
@@ -392,14 +427,21 @@ __global__ void __launch_bounds__(kInitThreads) init_kernel(InitArgs a) {
                     int v = int(int_sq_dist(a.pts[p], c, a.n, a.fmt));  // < 2^31 (host check)
                     if (j > 0) v = min(v, __ldcg(wold + p));
                     wnew[p] = v;
-                    s += v;
+                    sum += v;
                 }
             }
-            long long ex;
-            const long long tot = block_exclusive_scan(s, ex, s_warp);
-            if (tid == 0) snew[ch] = tot;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+            __syncthreads();  // s_warp[0] reuse (previous chunk / selection scan)
+            if (lane == 0) s_warp[0][tid >> 5] = sum;
+            __syncthreads();
+            if (tid == 0) {
+                long long t = 0;
+                for (int w = 0; w < kInitThreads / 32; ++w) t += s_warp[0][w];
+                snew[ch] = t;
+            }
         }
-        grid.sync();
+        init_grid_barrier(a.barrier, ++n_bar * gridDim.x);
     }
 }
 
@@ -1399,7 +1441,7 @@ struct KmeansSession {
         uniforms.resize(64);
         for (auto& u : uniforms) u = g.random();
         cent_rows = static_cast<uint64_t*>(e->scratch("km.cent_rows", 64 * 8));
-        d2 = static_cast<int*>(e->scratch("km.d2", size_t(m) * 8));  // two buffers
+        d2 = static_cast<int*>(e->scratch("km.d2", size_t((m + 3) & ~int64_t(3)) * 8));  // two 16 B-aligned buffers
         nchunks = int(ceil_div(m, kInitChunk));
         chunk_sums = static_cast<long long*>(e->scratch("km.chunk_sums", size_t(nchunks) * 16));
         d_uniforms = static_cast<double*>(e->scratch("km.uniforms", 64 * 8));
@@ -1422,10 +1464,12 @@ struct KmeansSession {
         ia.uniforms = d_uniforms;
         ia.cent_rows = cent_rows;
         ia.d2[0] = d2;
-        ia.d2[1] = d2 + m;
+        ia.d2[1] = d2 + ((m + 3) & ~int64_t(3));
         ia.sums[0] = chunk_sums;
         ia.sums[1] = chunk_sums + nchunks;
         ia.nchunks = nchunks;
+        ia.barrier = static_cast<unsigned int*>(e->scratch("km.init_barrier", 16));
+        KT_CUDA(cudaMemsetAsync(ia.barrier, 0, 16, e->stream));
         const int occ = std::max(1, occupancy_blocks((const void*)init_kernel, kInitThreads, 0));
         const int grid = int(std::max<int64_t>(1, std::min<int64_t>(int64_t(occ) * e->num_sms, nchunks)));
         void* params[] = {&ia};
