@@ -278,35 +278,6 @@ struct InitArgs {
     unsigned int* barrier;  // grid-barrier counter, zeroed before the launch
 };
 
-// Block-wide exclusive scan of one int64 per thread; returns the block total.
-__device__ __forceinline__ long long block_exclusive_scan(long long v, long long& excl, long long* s_warp) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    long long incl = v;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const long long t = __shfl_up_sync(0xffffffffu, incl, off);
-        if (lane >= off) incl += t;
-    }
-    if (lane == 31) s_warp[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-        long long w = lane < kInitThreads / 32 ? s_warp[lane] : 0;
-        long long wi = w;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const long long t = __shfl_up_sync(0xffffffffu, wi, off);
-            if (lane >= off) wi += t;
-        }
-        if (lane < kInitThreads / 32) s_warp[lane] = wi - w;
-        if (lane == kInitThreads / 32 - 1) s_warp[32] = wi;
-    }
-    __syncthreads();
-    excl = s_warp[warp] + incl - v;
-    const long long total = s_warp[32];
-    __syncthreads();
-    return total;
-}
-
 // Block-wide inclusive scan of one int64 per thread with one barrier: warp scans, warp
 // totals through shared memory, every warp adds the totals of the warps before it.
 // Returns the thread's exclusive prefix; *total receives the block total.
