@@ -1517,6 +1517,7 @@ struct KmeansSession {
         auto* h_iter = static_cast<int*>(e->staging("km.iter", 64));
         auto* h_S = static_cast<long long*>(e->staging("km.S", size_t(kMaxClusters) * kSumW * 8));
         auto* h_loss = static_cast<double*>(e->staging("km.loss", 64 * 8));
+        h_cent = static_cast<double*>(e->staging("km.cent", size_t(kMaxClusters) * kMaxKnobs * 8));
         while (true) {
             KT_CUDA(cudaMemsetAsync(a.D, 0, size_t(3) * K * kSumW * 8, e->stream));
             KT_CUDA(cudaMemsetAsync(a.chg, 0, 3 * kMaxRuns * 4, e->stream));
@@ -1534,6 +1535,15 @@ struct KmeansSession {
             if (history) {
                 pairwise_loss(e, pts, m, n, fmt, a.assign, a.cent, d_loss);
                 KT_CUDA(cudaMemcpyAsync(h_loss, d_loss, 8, cudaMemcpyDeviceToHost, e->stream));
+            } else {
+                // speculatively finish (no reseed is the common case): losses, pass counts and
+                // centroids come back with the launch state in one synchronisation
+                for (int r = 0; r < R; ++r)
+                    pairwise_loss(e, pts, m, n, fmt, a.assign + size_t(r) * a.stride,
+                                  a.cent + size_t(a.coff[r]) * kMaxKnobs, d_loss + r);
+                KT_CUDA(cudaMemcpyAsync(h_loss, d_loss, R * 8, cudaMemcpyDeviceToHost, e->stream));
+                KT_CUDA(cudaMemcpyAsync(h_iter, a.run_iter, R * 4, cudaMemcpyDeviceToHost, e->stream));
+                KT_CUDA(cudaMemcpyAsync(h_cent, a.cent, size_t(K) * kMaxKnobs * 8, cudaMemcpyDeviceToHost, e->stream));
             }
             e->sync();
             it = h_ctrl[0];
@@ -1556,12 +1566,15 @@ struct KmeansSession {
             if (!active) break;
         }
         std::vector<RunResult> out(R);
-        for (int r = 0; r < R; ++r)
-            pairwise_loss(e, pts, m, n, fmt, a.assign + size_t(r) * a.stride, a.cent + size_t(a.coff[r]) * kMaxKnobs,
-                          d_loss + r);
-        KT_CUDA(cudaMemcpyAsync(h_loss, d_loss, R * 8, cudaMemcpyDeviceToHost, e->stream));
-        KT_CUDA(cudaMemcpyAsync(h_iter, a.run_iter, R * 4, cudaMemcpyDeviceToHost, e->stream));
-        e->sync();
+        if (history) {
+            for (int r = 0; r < R; ++r)
+                pairwise_loss(e, pts, m, n, fmt, a.assign + size_t(r) * a.stride,
+                              a.cent + size_t(a.coff[r]) * kMaxKnobs, d_loss + r);
+            KT_CUDA(cudaMemcpyAsync(h_loss, d_loss, R * 8, cudaMemcpyDeviceToHost, e->stream));
+            KT_CUDA(cudaMemcpyAsync(h_iter, a.run_iter, R * 4, cudaMemcpyDeviceToHost, e->stream));
+            KT_CUDA(cudaMemcpyAsync(h_cent, a.cent, size_t(K) * kMaxKnobs * 8, cudaMemcpyDeviceToHost, e->stream));
+            e->sync();
+        }
         if (a.stats) {
             unsigned long long hs[kMaxRuns * 3];
             KT_CUDA(cudaMemcpy(hs, a.stats, R * 3 * 8, cudaMemcpyDeviceToHost));
@@ -1654,6 +1667,7 @@ struct KmeansSession {
     }
 
     LloydArgs last_args{};
+    double* h_cent = nullptr;  // host copy of the last run's centroids [K][8] (pinned staging)
     int64_t lloyd_bytes = 0;
     int lloyd_launches = 0;
 };
@@ -1710,10 +1724,7 @@ static KneeResult knee_scan(kt_engine* e, const uint64_t* pts, int64_t m, int n,
         if (done) {
             res.chosen_k = ks[pick];
             const LloydArgs& a = ses.last_args;
-            std::vector<double> c(size_t(ks[pick]) * kMaxKnobs);
-            KT_CUDA(cudaMemcpyAsync(c.data(), a.cent + size_t(a.coff[pick]) * kMaxKnobs, c.size() * 8,
-                                    cudaMemcpyDeviceToHost, e->stream));
-            e->sync();
+            const double* c = ses.h_cent + size_t(a.coff[pick]) * kMaxKnobs;  // copied with the losses
             res.centroids.resize(size_t(ks[pick]) * n);
             for (int j = 0; j < ks[pick]; ++j)
                 for (int i = 0; i < n; ++i) res.centroids[size_t(j) * n + i] = c[size_t(j) * kMaxKnobs + i];
