@@ -18,11 +18,11 @@ for w in $WHAT; do
       timeout 900 python bench.py --impl reference > "$OUT/bench_ref.json" 2> "$OUT/bench_ref.err"; echo "ref rc=$?"; cut -c1-300 "$OUT/bench_ref.json";;
     launches)
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$OUT/launches.csv" \
-        python bench.py --steps 2 --warmup 1 --no-cpu-baseline > "$OUT/launches_bench.log" 2>&1; echo "launches rc=$?";;
+        python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-wall95 > "$OUT/launches_bench.log" 2>&1; echo "launches rc=$?";;
     full)
       for k in lloyd score_trees dedup_insert init_kernel; do
         timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 -o "$OUT/prof_$k" \
-          python bench.py --steps 1 --warmup 1 --no-cpu-baseline > "$OUT/prof_$k.log" 2>&1; echo "full $k rc=$?"
+          python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-wall95 > "$OUT/prof_$k.log" 2>&1; echo "full $k rc=$?"
       done;;
     rl)
       timeout 900 python bench.py --workload rl > "$OUT/bench_rl.json" 2> "$OUT/bench_rl.err"; echo "bench rl rc=$?"; cut -c1-400 "$OUT/bench_rl.json";;
