@@ -57,6 +57,7 @@ struct Grower {
     int max_depth;
     double shrink;
     std::vector<double> resid;
+    double* pred = nullptr;  // running prediction, canonical row order
     // output (one tree)
     std::vector<int32_t> feature, left, right;
     std::vector<double> threshold, value;
@@ -74,9 +75,22 @@ struct Grower {
 
     double x(int64_t row, int j) const { return X[size_t(row) * n + j]; }
 
-    // _best_split (cost_model.py:292-325); returns false when no feature has a boundary
-    bool best_split(const std::vector<std::vector<int64_t>>& orders, int& bf, double& bt) {
-        const int64_t mm = int64_t(orders[0].size());
+    // Row-id storage without per-node allocation: the rows and the n per-feature orders of
+    // every node at depth d live in the node's segment [off, off + cnt) of level d's arrays
+    // (children partition their parent's segment: left part first, stable).
+    std::vector<std::vector<int64_t>> lvl_rows;   // [depth + 1][m]
+    std::vector<std::vector<int64_t>> lvl_ord;    // [depth + 1][n * m]
+
+    void setup_levels(const std::vector<std::vector<int64_t>>& root_orders) {
+        lvl_rows.assign(size_t(max_depth) + 1, std::vector<int64_t>(size_t(m)));
+        lvl_ord.assign(size_t(max_depth) + 1, std::vector<int64_t>(size_t(n) * size_t(m)));
+        for (int64_t i = 0; i < m; ++i) lvl_rows[0][i] = i;
+        for (int f = 0; f < n; ++f) std::copy(root_orders[f].begin(), root_orders[f].end(), lvl_ord[0].begin() + size_t(f) * m);
+        in_left.assign(size_t(m), 0);
+    }
+
+    // _best_split (cost_model.py:292-325) over feature orders ord[f * m + off .. + cnt)
+    bool best_split(const int64_t* ord, int64_t off, int64_t mm, int& bf, double& bt) {
         bool have = false;
         double best_gain = 0.0;
         xs.resize(mm);
@@ -84,21 +98,21 @@ struct Grower {
         csum.resize(mm);
         csq.resize(mm);
         for (int j = 0; j < n; ++j) {
-            const auto& ord = orders[j];
-            for (int64_t k = 0; k < mm; ++k) {
-                xs[k] = x(ord[k], j);
-                rs[k] = resid[ord[k]];
-            }
-            bool any = false;
-            for (int64_t k = 0; k + 1 < mm && !any; ++k) any = xs[k] != xs[k + 1];
-            if (!any) continue;
+            const int64_t* o = ord + size_t(j) * m + off;
+            // one pass: gather, sequential cumsums (np.cumsum order), boundary detection
             double c = 0.0, q = 0.0;
+            bool any = false;
             for (int64_t k = 0; k < mm; ++k) {
-                c = k ? c + rs[k] : rs[k];
-                q = k ? q + rs[k] * rs[k] : rs[k] * rs[k];
+                const int64_t row = o[k];
+                const double xv = x(row, j), rv = resid[row];
+                xs[k] = xv;
+                any |= k > 0 && xv != xs[k - 1];
+                c = k ? c + rv : rv;
+                q = k ? q + rv * rv : rv * rv;
                 csum[k] = c;
                 csq[k] = q;
             }
+            if (!any) continue;
             const double total = csum[mm - 1], total_sq = csq[mm - 1];
             const double parent_sse = total_sq - total * total / double(mm);
             double g_best = 0.0;
@@ -131,10 +145,10 @@ struct Grower {
         return have;
     }
 
-    // _grow (cost_model.py:328-364)
-    int grow(const std::vector<int64_t>& rows, const std::vector<std::vector<int64_t>>& orders, int depth) {
+    // _grow (cost_model.py:328-364) for the node owning segment [off, off + cnt) of level `depth`
+    int grow(int64_t off, int64_t cnt, int depth) {
         const int node = add();
-        const int64_t cnt = int64_t(rows.size());
+        const int64_t* rows = lvl_rows[depth].data() + off;
         buf.resize(cnt);
         for (int64_t i = 0; i < cnt; ++i) buf[i] = resid[rows[i]];
         const double mean = pw_sum(buf.data(), cnt) / double(cnt);
@@ -145,32 +159,43 @@ struct Grower {
         const double sse = pw_sum(buf.data(), cnt);
         int j = -1;
         double t = 0.0;
-        const bool split = depth < max_depth && sse > 0.0 && best_split(orders, j, t);
+        const bool split = depth < max_depth && sse > 0.0 && best_split(lvl_ord[depth].data(), off, cnt, j, t);
         if (!split) {
-            value[node] = shrink * mean;
+            const double v = shrink * mean;
+            value[node] = v;
+            // pred += tree.predict(X): the rows this leaf owns are exactly the training rows
+            // Tree.predict routes here (same x[f] <= t rule), so no tree walk is needed
+            for (int64_t i = 0; i < cnt; ++i) pred[rows[i]] += v;
             return node;
         }
-        std::vector<int64_t> lrows, rrows;
-        in_left.assign(size_t(m), 0);
-        for (int64_t r : rows) {
-            if (x(r, j) <= t) {
-                lrows.push_back(r);
-                in_left[r] = 1;
-            } else {
-                rrows.push_back(r);
-            }
+        // stable partition of the rows and of every feature order into level depth + 1
+        int64_t* nrows = lvl_rows[depth + 1].data() + off;
+        int64_t nl = 0;
+        for (int64_t i = 0; i < cnt; ++i) {
+            const int64_t r = rows[i];
+            const bool lft = x(r, j) <= t;
+            in_left[r] = lft;
+            nl += lft;
         }
-        std::vector<std::vector<int64_t>> lo(n), ro(n);
-        for (int f = 0; f < n; ++f) {
-            lo[f].reserve(lrows.size());
-            ro[f].reserve(rrows.size());
-            for (int64_t r : orders[f]) (in_left[r] ? lo[f] : ro[f]).push_back(r);
+        int64_t li = 0, ri = nl;
+        for (int64_t i = 0; i < cnt; ++i) {
+            const int64_t r = rows[i];
+            nrows[in_left[r] ? li++ : ri++] = r;
+        }
+        for (int f = 0; f < n && depth + 1 < max_depth; ++f) {  // children at max depth are leaves: no orders
+            const int64_t* o = lvl_ord[depth].data() + size_t(f) * m + off;
+            int64_t* no = lvl_ord[depth + 1].data() + size_t(f) * m + off;
+            int64_t a2 = 0, b2 = nl;
+            for (int64_t i = 0; i < cnt; ++i) {
+                const int64_t r = o[i];
+                no[in_left[r] ? a2++ : b2++] = r;
+            }
         }
         feature[node] = j;
         threshold[node] = t;
-        const int l = grow(lrows, lo, depth + 1);
+        const int l = grow(off, nl, depth + 1);
         left[node] = l;
-        const int rr = grow(rrows, ro, depth + 1);
+        const int rr = grow(off + nl, cnt - nl, depth + 1);
         right[node] = rr;
         return node;
     }
@@ -221,11 +246,13 @@ extern "C" int kt_fit_trees(const double* features, const double* targets, int64
     g.max_depth = depth;
     g.shrink = learning_rate;
     g.resid.resize(size_t(m));
+    g.setup_levels(root);
+    g.pred = pred.data();
     int64_t used = 0;
     for (int r = 0; r < rounds; ++r) {
         for (int64_t i = 0; i < m; ++i) g.resid[i] = y[i] - pred[i];
         g.feature.clear(), g.left.clear(), g.right.clear(), g.threshold.clear(), g.value.clear();
-        g.grow(all_rows, root, 0);
+        g.grow(0, m, 0);
         const int64_t nodes = int64_t(g.feature.size());
         if (used + nodes > node_capacity) fail(KT_ERR_VALUE, "node capacity exceeded");
         tree_offsets_out[r] = int32_t(used);
@@ -236,14 +263,7 @@ extern "C" int kt_fit_trees(const double* features, const double* targets, int64
             right_out[used + k] = g.right[k];
             value_out[used + k] = g.value[k];
         }
-        used += nodes;
-        // pred += tree.predict(X)
-        for (int64_t i = 0; i < m; ++i) {
-            int node = 0;
-            while (g.feature[node] >= 0)
-                node = X[size_t(i) * n + g.feature[node]] <= g.threshold[node] ? g.left[node] : g.right[node];
-            pred[i] += g.value[node];
-        }
+        used += nodes;  // pred was updated at the leaves during growth
     }
     tree_offsets_out[rounds] = int32_t(used);
     *base_out = base;
