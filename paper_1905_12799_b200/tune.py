@@ -141,14 +141,29 @@ def tune_rows(space, landscape, strategy: str, budget: int, seed: int = 0,
     run = TuneRun()
     t0 = clock()
     best = 0.0
+    # measurement records kept as growing arrays: packed rows (the visited set the sampler
+    # takes), feature rows (the refit's training matrix) and fitness — no per-round rebuild
+    cap = max(budget, 1)
+    m_rows = np.zeros(cap, dtype=np.uint64)
+    m_feat = np.zeros((cap, n), dtype=np.float64)
+    m_fit = np.zeros(cap, dtype=np.float64)
+    m_cnt = 0
+    knob_ix = np.arange(n)
 
     def measure(batch: list[tuple]) -> None:
-        nonlocal best
+        nonlocal best, m_cnt
+        idx = np.asarray(batch, dtype=np.int64)
+        packed = sp.pack(idx, cards)
         if runtimes is not None:
             rt = np.asarray(runtimes(batch), dtype=np.float64)
         else:
-            rows = torch.from_numpy(sp.pack(np.asarray(batch, dtype=np.int64), cards).view(np.int64)).to(dev)
+            rows = torch.from_numpy(packed.view(np.int64)).to(dev)
             rt = runtimes_rows(landscape, rows, engine=eng).cpu().numpy()
+        k = len(batch)
+        m_rows[m_cnt:m_cnt + k] = packed
+        m_feat[m_cnt:m_cnt + k] = table[knob_ix, idx]
+        m_fit[m_cnt:m_cnt + k] = 1.0 / rt
+        m_cnt += k
         run.configs.extend(batch)
         run.runtimes.extend(rt.tolist())
         visited.update(batch)
@@ -166,9 +181,8 @@ def tune_rows(space, landscape, strategy: str, budget: int, seed: int = 0,
         remaining = budget - len(run.configs)
         traj = None
         if strategy in ("rl", "rl+as", "sa", "sa+as"):
-            idx = np.asarray(run.configs, dtype=np.int64)
-            fitness = 1.0 / np.asarray(run.runtimes, dtype=np.float64)
-            model = fit(_TS(table[np.arange(n), idx], fitness), boost_params)  # _fit_model, driver.py:142-148
+            fitness = m_fit[:m_cnt]
+            model = fit(_TS(m_feat[:m_cnt], fitness), boost_params)  # _fit_model, driver.py:142-148
             if strategy.startswith("rl"):
                 order = np.argsort(-fitness, kind="stable")  # _restart_configs, driver.py:118-139
                 starts = [run.configs[int(i)] for i in order[: agent_params.episodes_per_round]]
@@ -181,8 +195,7 @@ def tune_rows(space, landscape, strategy: str, budget: int, seed: int = 0,
                 srows = torch.from_numpy(sp.pack(np.asarray(starts), cards).view(np.int64)).to(dev)
                 traj = run_sa_rows(sa_params, model, space, srows, round_seed(seed, round_index), engine=eng)
         if strategy.endswith("+as"):
-            vis = sp.pack(np.asarray(sorted(visited), dtype=np.int64), cards) if visited else np.zeros(0, np.uint64)
-            brows = adaptive_sample_rows(traj[0], vis, space, round_seed(seed, round_index), engine=eng)
+            brows = adaptive_sample_rows(traj[0], m_rows[:m_cnt], space, round_seed(seed, round_index), engine=eng)
             batch = [tuple(r) for r in sp.unpack(brows, n, cards).tolist()]
         elif traj is not None:
             batch = top_unvisited(traj[0].cpu().numpy().view(np.uint64), traj[1].cpu().numpy(), visited,
