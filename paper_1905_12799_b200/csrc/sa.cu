@@ -115,6 +115,74 @@ __global__ void __launch_bounds__(128) sa_chain_kernel(SAArgs a) {
     a.counts[c] = kept;
 }
 
+// Warp-per-chain variant for few chains (a tuning round runs 64): the 32 lanes walk
+// the trees of a proposal in parallel (lane l takes trees l, l + 32, ...), then every
+// lane accumulates the leaf values in tree order from shuffles — the same sequential
+// float64 sum as score_row, so the chain is bit-identical.  Every lane runs the chain's
+// PCG64 stream redundantly (identical draws, no broadcast); lane 0 writes the slots.
+template <int D>
+__global__ void __launch_bounds__(128) sa_chain_warp_kernel(SAArgs a) {
+    extern __shared__ uint64_t s_forest[];
+    const int total = a.n_trees * a.words_per_tree;
+    for (int i = threadIdx.x; i < total; i += blockDim.x) s_forest[i] = a.forest[i];
+    __syncthreads();
+    const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (c >= a.chains) return;  // whole warps
+    const uint32_t spawn = uint32_t(c);
+    Pcg64 g = pcg64_from_seed_sequence(a.seed_words, a.n_seed_words, &spawn, 1);
+    uint64_t row = a.starts[c];
+    double score = a.start_scores[c];
+    double temp = *a.temperature;
+    const int64_t slot0 = int64_t(c) * (a.steps + 1);
+    if (lane == 0) {
+        a.slot_rows[slot0] = row;
+        a.slot_scores[slot0] = score;
+        a.slot_steps[slot0] = 0;
+    }
+    const bool wide = !a.fmt.bytes;
+    int64_t kept = 1;
+    for (int s = 1; s <= a.steps; ++s) {
+        const int knob = int(g.bounded32(uint32_t(a.n - 1)));
+        const int sign = int(g.bounded32(1u)) * 2 - 1;
+        int v = a.fmt.get(row, knob) + sign;
+        v = v < 0 ? 0 : (v > a.cards[knob] - 1 ? a.cards[knob] - 1 : v);
+        const uint64_t prop = a.fmt.set(row, knob, v);
+        double leaf[2] = {0.0, 0.0};
+        const uint32_t lo = uint32_t(prop), hi = uint32_t(prop >> 32);
+        WideRow x{};
+        if (wide) x = widen_row(prop, a.fmt);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int t = lane + 32 * q;
+            if (t < a.n_trees) {
+                const uint64_t* tr = s_forest + t * a.words_per_tree;
+                leaf[q] = wide ? walk_tree_wide<D>(tr, x) : walk_tree<D>(tr, lo, hi);
+            }
+        }
+        double acc = 0.0;
+        for (int t = 0; t < a.n_trees; ++t) {
+            const double lv = t < 32 ? __shfl_sync(0xffffffffu, leaf[0], t) : __shfl_sync(0xffffffffu, leaf[1], t - 32);
+            acc = t ? __dadd_rn(acc, lv) : lv;
+        }
+        const double ps = __dadd_rn(a.base, acc);
+        const double delta = __dsub_rn(ps, score);
+        bool accept = delta >= 0.0;
+        if (!accept) accept = g.random() < exp(__ddiv_rn(delta, temp));
+        if (accept) {
+            row = prop;
+            score = ps;
+            if (lane == 0) {
+                a.slot_rows[slot0 + kept] = row;
+                a.slot_scores[slot0 + kept] = score;
+                a.slot_steps[slot0 + kept] = s;
+            }
+            ++kept;
+        }
+        temp = __dmul_rn(temp, a.cooling);
+    }
+    if (lane == 0) a.counts[c] = kept;
+}
+
 __global__ void sa_compact_kernel(const uint64_t* slot_rows, const double* slot_scores, const int32_t* slot_steps,
                                   const int64_t* counts, const int64_t* offsets, int chains, int steps,
                                   uint64_t* rows_out, double* scores_out, int32_t* steps_out) {
@@ -129,10 +197,20 @@ __global__ void sa_compact_kernel(const uint64_t* slot_rows, const double* slot_
     }
 }
 
+constexpr int kSaWarpChains = 8192;  // up to this many chains the warp-per-chain kernel is used
+
 template <int D>
 static void launch_chains(kt_engine* e, const kt_forest* f, const SAArgs& a) {
     const size_t smem = size_t(f->n_trees) * f->words_per_tree * 8;
     if (smem > 200 * 1024) fail(KT_ERR_UNSUPPORTED, "forest too large for the in-kernel SA walk");
+    if (a.n_trees <= 64 && a.chains <= kSaWarpChains) {  // few chains: a warp per chain
+        auto kern = sa_chain_warp_kernel<D>;
+        allow_dynamic_smem((const void*)kern);
+        e->pre_launch("sa_chains");
+        kern<<<int(ceil_div(int64_t(a.chains) * 32, 128)), 128, smem, e->stream>>>(a);
+        e->check_launch("sa_chains");
+        return;
+    }
     auto kern = sa_chain_kernel<D>;
     allow_dynamic_smem((const void*)kern);
     e->pre_launch("sa_chains");
