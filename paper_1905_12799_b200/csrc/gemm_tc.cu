@@ -53,32 +53,51 @@ struct Frag {
 template <bool MN_MAJOR, int ROWS_MAX>
 __device__ __forceinline__ void load_tile(Frag<ROWS_MAX>& fr, const float* __restrict__ G, int ld, int rows, int r0,
                                           int rlimit, int k0, int klimit, bool vec_ok) {
+    if constexpr (MN_MAJOR) {
+        // MN-major G[k * ld + r]: a thread owns a 4-row x 4-k block — four 16-byte loads along r
+        // (coalesced across lanes), transposed to K-major in store_tile
+        static_assert(Frag<ROWS_MAX>::kPer == 4, "one 4x4 block per thread");
+        const int b = threadIdx.x, rgn = rows >> 2;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) fr.v[kk] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (b < rows) {
+            const int rb = b % rgn, kb = b / rgn;
+            const int gr = r0 + 4 * rb;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                const int gk = k0 + 4 * kb + kk;
+                if (gk >= klimit) continue;
+                const float* src = G + size_t(gk) * ld + gr;
+                if (vec_ok && gr + 3 < rlimit) {
+                    fr.v[kk] = __ldg(reinterpret_cast<const float4*>(src));
+                } else {
+                    float v[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        if (gr + e < rlimit) v[e] = __ldg(src + e);
+                    fr.v[kk] = make_float4(v[0], v[1], v[2], v[3]);
+                }
+            }
+        }
+        return;
+    }
 #pragma unroll
     for (int i = 0; i < Frag<ROWS_MAX>::kPer; ++i) {
         const int f = threadIdx.x + i * kTcThreads;
         float v[4] = {0.f, 0.f, 0.f, 0.f};
         if (f < rows * (kTcBK / 4)) {
-            if (!MN_MAJOR) {  // K-major: G[(r0 + r) * ld + k0 + k]
-                const int r = f / (kTcBK / 4), kq = f % (kTcBK / 4);
-                const int gr = r0 + r, gk = k0 + 4 * kq;
-                if (gr < rlimit) {
-                    const float* src = G + size_t(gr) * ld + gk;
-                    if (vec_ok && gk + 3 < klimit) {
-                        const float4 q = __ldg(reinterpret_cast<const float4*>(src));
-                        v[0] = q.x, v[1] = q.y, v[2] = q.z, v[3] = q.w;
-                    } else {
-#pragma unroll
-                        for (int e = 0; e < 4; ++e)
-                            if (gk + e < klimit) v[e] = __ldg(src + e);
-                    }
-                }
-            } else {  // MN-major: G[(k0 + k) * ld + r0 + r], lanes walk r (coalesced)
-                const int r = f % rows, kq = f / rows;
-                const int gr = r0 + r, gk = k0 + 4 * kq;
-                if (gr < rlimit) {
+            // K-major: G[(r0 + r) * ld + k0 + k]
+            const int r = f / (kTcBK / 4), kq = f % (kTcBK / 4);
+            const int gr = r0 + r, gk = k0 + 4 * kq;
+            if (gr < rlimit) {
+                const float* src = G + size_t(gr) * ld + gk;
+                if (vec_ok && gk + 3 < klimit) {
+                    const float4 q = __ldg(reinterpret_cast<const float4*>(src));
+                    v[0] = q.x, v[1] = q.y, v[2] = q.z, v[3] = q.w;
+                } else {
 #pragma unroll
                     for (int e = 0; e < 4; ++e)
-                        if (gk + e < klimit) v[e] = __ldg(G + size_t(gk + e) * ld + gr);
+                        if (gk + e < klimit) v[e] = __ldg(src + e);
                 }
             }
         }
@@ -88,12 +107,33 @@ __device__ __forceinline__ void load_tile(Frag<ROWS_MAX>& fr, const float* __res
 
 template <bool MN_MAJOR, int ROWS_MAX>
 __device__ __forceinline__ void store_tile(const Frag<ROWS_MAX>& fr, float* hi, float* lo, int rows) {
+    if constexpr (MN_MAJOR) {
+        const int b = threadIdx.x, rgn = rows >> 2;
+        if (b >= rows) return;
+        const int rb = b % rgn, kb = b / rgn;
+        const float* f0 = reinterpret_cast<const float*>(&fr.v[0]);
+        const float* f1 = reinterpret_cast<const float*>(&fr.v[1]);
+        const float* f2 = reinterpret_cast<const float*>(&fr.v[2]);
+        const float* f3 = reinterpret_cast<const float*>(&fr.v[3]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {  // row 4rb + j: its four k values of k-quad kb
+            const int r = 4 * rb + j;
+            const int off = kb * rows * 4 + (r >> 3) * 32 + (r & 7) * 4;
+            float4 h, l;
+            umma::split_tf32(f0[j], h.x, l.x);
+            umma::split_tf32(f1[j], h.y, l.y);
+            umma::split_tf32(f2[j], h.z, l.z);
+            umma::split_tf32(f3[j], h.w, l.w);
+            *reinterpret_cast<float4*>(hi + off) = h;
+            *reinterpret_cast<float4*>(lo + off) = l;
+        }
+        return;
+    }
 #pragma unroll
     for (int i = 0; i < Frag<ROWS_MAX>::kPer; ++i) {
         const int f = threadIdx.x + i * kTcThreads;
         if (f >= rows * (kTcBK / 4)) break;
-        const int r = MN_MAJOR ? f % rows : f / (kTcBK / 4);
-        const int kq = MN_MAJOR ? f / rows : f % (kTcBK / 4);
+        const int r = f / (kTcBK / 4), kq = f % (kTcBK / 4);
         const int off = kq * rows * 4 + (r >> 3) * 32 + (r & 7) * 4;
         float4 h, l;
         umma::split_tf32(fr.v[i].x, h.x, l.x);

@@ -121,6 +121,25 @@ def run(args, rank: int, world: int, local_rank: int, kt, torch, dist, helpers) 
         base = {"value": nc / dt, "unit": "candidates/s", "cores": 1, "kind": "port",
                 "sample": f"{N_TASKS} tasks x 256 agents (oracle numpy port of run_search_round + adaptive_sample), "
                           f"{dt:.1f} s"}
+    # PPO GEMM roofline (tensor): algorithmic fp32 FLOPs of the 3 epochs' forward, data-gradient and
+    # weight-gradient GEMMs (n = knobs, h = 128 shared, 2g = 128 heads, 3n + 1 outputs) over the
+    # tc_gemm kernels' time; they run as 3xTF32 (three tf32 MMAs per fp32 product)
+    gemm_ms = sum(ms for k, (c, ms) in stats.items() if k.startswith("tc_gemm"))
+    flops = 0.0
+    for d, inf in zip(docs, infos):
+        n = len(d["values"])
+        macs = (n * 128 + 128 * 128 + 128 * (3 * n + 1)) + ((3 * n + 1) * 128 + 128 * 128) + \
+               ((3 * n + 1) * 128 + 128 * 128 + 128 * n)
+        flops += 3 * 2.0 * macs * (inf["entries"] - AGENTS)  # 3 epochs, T = entries - agents rows
+    pk = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else None
+    tf32_peak = (float(pk["bf16_tflops"]) / 2.0) if pk else 1100.0
+    gemm_tflops = flops / (gemm_ms / 1e3) / 1e12 if gemm_ms else None
+    gemm_roof = {"bound": "tensor", "kernel": "tc_gemm (fwd + dgrad + wgrad, 3xTF32)", "achieved": gemm_tflops,
+                 "peak": tf32_peak, "unit": "TFLOP/s", "frac": gemm_tflops / tf32_peak if gemm_tflops else None,
+                 "tensor_work_frac": 3 * gemm_tflops / tf32_peak if gemm_tflops else None, "traffic": None,
+                 "peak_source": "MEASURED_PEAKS bf16 / 2 (dense tf32)" if pk else "fallback 1.1 PF tf32",
+                 "flops_model": "2 * 60.8K MACs per trajectory row per epoch (8 knobs), 3 epochs, fp32-equivalent",
+                 "gemm_ms_per_step": gemm_ms, "kernel_share_of_step": gemm_ms / sum(ms for _, ms in stats.values())}
     dom = max(stats.items(), key=lambda kv: kv[1][1])
     return {
         "metric": "candidate configs scored+clustered/sec per tuning step", "value": value, "unit": "candidates/s",
@@ -135,7 +154,7 @@ def run(args, rank: int, world: int, local_rank: int, kt, torch, dist, helpers) 
         "gpu_launches": int(launches),
         "sample_info": infos,
         "kernels": {k: {"launches": c, "ms": round(ms, 3)} for k, (c, ms) in sorted(stats.items(), key=lambda kv: -kv[1][1])},
-        "roofline": {"bound": "tensor" if dom[0].startswith("tc_gemm") else "hbm", "kernel": dom[0], "achieved": None,
-                     "peak": None, "unit": None, "frac": None, "traffic": None},
+        "roofline": gemm_roof,
+        "dominant_single_kernel": dom[0],
         "clocks": clk.summary(), "cpu_baseline": base,
     }
