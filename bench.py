@@ -436,6 +436,31 @@ def run_rl(args, rank: int, world: int, local_rank: int) -> None:
         dist.destroy_process_group()
 
 
+def run_c4(args, rank: int, world: int, local_rank: int) -> None:
+    import torch
+
+    import paper_1905_12799_b200 as kt
+    from tools import bench_c4
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+
+    line = bench_c4.run(args, rank, world, local_rank, kt, torch, dist, {"barrier": barrier, "clock": ClockSampler})
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -448,8 +473,9 @@ def main() -> None:
     ap.add_argument("--ref-procs", type=int, default=0, help="host processes for --impl reference (0: all cores)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-wall95", action="store_true", help="skip the wall-time-to-95%%-best tune runs")
-    ap.add_argument("--workload", choices=("s2", "rl"), default="s2",
-                    help="s2: the headline scored+clustered step; rl: 5 tasks x 4096 PPO agents per step")
+    ap.add_argument("--workload", choices=("s2", "rl", "c4"), default="s2",
+                    help="s2: the headline scored+clustered step; rl: 5 tasks x 4096 PPO agents per step; "
+                         "c4: ResNet-18's 12 tasks x 1M candidates placed over the ranks (configs[3])")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -458,6 +484,8 @@ def main() -> None:
         run_reference(args, rank, world)
     elif args.workload == "rl":
         run_rl(args, rank, world, local_rank)
+    elif args.workload == "c4":
+        run_c4(args, rank, world, local_rank)
     else:
         run_ours(args, rank, world, local_rank)
 
