@@ -282,6 +282,18 @@ int kt_fit_trees(const double* features, const double* targets, int64_t m, int n
                  int32_t* right_out, double* value_out, int64_t node_capacity, int32_t* tree_offsets_out,
                  double* base_out);
 
+/* ------------------------------------------------ trajectory analysis
+ * per_step_best (report.py:53-69): best_out[s] = max score of the entries landing at step s
+ * (-inf if none), s < cap; *horizon_out = max step index.  pca_project (report.py:227-253):
+ * exact int64 moments sums_out[n] = sum x_i, gram_out[n*n] = sum x_i x_j, then projections
+ * xs/ys (device doubles) = (x - mean) . v1 / v2.                                         */
+int kt_step_best(kt_engine* e, const double* scores_dev, const int32_t* steps_dev, int64_t count, int cap,
+                 double* best_out, int32_t* horizon_out);
+int kt_pca_moments(kt_engine* e, const uint64_t* rows_dev, int64_t count, int n_knobs, const int32_t* cards,
+                   int64_t* sums_out, int64_t* gram_out);
+int kt_pca_project(kt_engine* e, const uint64_t* rows_dev, int64_t count, int n_knobs, const int32_t* cards,
+                   const double* mean, const double* v1, const double* v2, double* xs_dev, double* ys_dev);
+
 /* ------------------------------------------------------------ utilities */
 /* fp32 GEMM on the tensor cores (tcgen05 kind::tf32, 3xTF32 split, fp32 accumulate
  * in TMEM): C[m][n] = sum_k A(m,k) B(k,n), row-major device arrays;
