@@ -12,7 +12,7 @@ or a CUDA device every engine call raises ``EngineUnavailable``.
 its unchanged driver and CLI run on the B200.
 """
 
-from . import errors
+from . import errors, report
 from ._lib import EngineUnavailable, engine
 from .agent import Agent, AgentHyperparams, init_agent, run_search_round, run_search_rows
 from .cost_model import BoostParams, CostModel, Tree, device_forest, fit, predict, predict_rows
@@ -55,11 +55,14 @@ def install() -> dict:
 
     kt = importlib.import_module("knobtuner")
     mods = {name: importlib.import_module(f"knobtuner.{name}") for name in
-            ("driver", "agent", "sa", "sampler", "cost_model", "backends", "errors")}
+            ("driver", "agent", "sa", "sampler", "cost_model", "backends", "errors", "report")}
     errors.adopt(mods["errors"])
     patches = [
         (mods["driver"], "predict", predict), (mods["driver"], "run_sa_round", run_sa_round),
         (mods["driver"], "fit", fit),
+        (mods["report"], "per_step_best", report.per_step_best),
+        (mods["report"], "convergence_steps_for_round", report.convergence_steps_for_round),
+        (mods["report"], "pca_project", report.pca_project),
         (mods["driver"], "adaptive_sample", adaptive_sample), (mods["driver"], "run_search_round", run_search_round),
         (mods["agent"], "predict", predict),
         (mods["sa"], "predict", predict), (kt, "predict", predict), (kt, "run_sa_round", run_sa_round),

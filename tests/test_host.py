@@ -1,6 +1,7 @@
 """CPU-side checks of the engine boundary: the C ABI library, host RNG, packing, scope rules."""
 
 import re
+import sys
 from pathlib import Path
 
 import numpy as np
@@ -174,3 +175,31 @@ def test_gpu_box_imports_never_need_the_reference():
         for line in f.read_text().splitlines():
             if re.match(r"^(from|import)\s+knobtuner", line):
                 raise AssertionError(f"{f.name}: module-level import of the reference: {line!r}")
+
+
+def test_install_rebinds_the_reference_driver_names():
+    """install() (driver.py:12-23 names, agent/sa predict, report analysis, errors) — needs the
+    reference source tree, so it runs in the build container only."""
+    src = Path("/root/reference/pkg/src")
+    if not src.exists():
+        pytest.skip("reference not present (GPU box)")
+    sys.path.insert(0, str(src))
+    try:
+        import knobtuner
+        import knobtuner.driver as drv
+        import knobtuner.report as rep
+
+        saved = kt.install()
+        try:
+            assert drv.run_search_round is kt.run_search_round and drv.run_sa_round is kt.run_sa_round
+            assert drv.adaptive_sample is kt.adaptive_sample and drv.predict is kt.predict and drv.fit is kt.fit
+            assert rep.pca_project is kt.report.pca_project and rep.per_step_best is kt.report.per_step_best
+            assert knobtuner.adaptive_sample is kt.adaptive_sample
+        finally:
+            import importlib
+
+            for (mod, name), fn in saved.items():
+                setattr(importlib.import_module(mod), name, fn)
+        assert drv.run_search_round is not kt.run_search_round
+    finally:
+        sys.path.remove(str(src))
