@@ -665,13 +665,13 @@ __host__ __device__ inline size_t lloyd_resident_bytes(int K, int R, int64_t P, 
 }
 
 // Evaluate one point under run r: full assignment and its new budget.
-__device__ __forceinline__ int lloyd_assign(const LloydArgs& a, const float* c32, const double* c64, const float* dcum,
-                                            int r, uint64_t row, float& budget) {
+__device__ __forceinline__ int lloyd_assign(const LloydArgs& a, const RowFmt& fmt, const float* c32, const double* c64,
+                                            const float* dcum, int r, uint64_t row, float& budget) {
     const int co = a.coff[r];
     float p[kMaxKnobs];
-    unpack_row(row, p, a.fmt);
+    unpack_row(row, p, fmt);
     float u, l;
-    const int j = full_assign(c32 + co * kMaxKnobs, c64 + co * kMaxKnobs, row, p, a.k[r], a.n, a.fmt, a.bk1, u, l);
+    const int j = full_assign(c32 + co * kMaxKnobs, c64 + co * kMaxKnobs, row, p, a.k[r], a.n, fmt, a.bk1, u, l);
     budget = __fadd_rd(__fsub_rd(l, u), dcum[co + j]);
     return j;
 }
@@ -737,14 +737,14 @@ __device__ __forceinline__ void warp_delta(int* delta, int g, uint64_t row, int 
 
 // Evaluate one point under run r (one lane, no warp cooperation): assignment,
 // budget, and the shared-counter deltas of a move.
-__device__ __forceinline__ int lloyd_eval(const LloydArgs& a, const float* c32, const double* c64, const float* dcum,
-                                          int* delta, int r, uint64_t row, int old, float& budget) {
+__device__ __forceinline__ int lloyd_eval(const LloydArgs& a, const RowFmt& fmt, const float* c32, const double* c64,
+                                          const float* dcum, int* delta, int r, uint64_t row, int old, float& budget) {
     const int co = a.coff[r];
-    const int j = lloyd_assign(a, c32, c64, dcum, r, row, budget);
+    const int j = lloyd_assign(a, fmt, c32, c64, dcum, r, row, budget);
     if (j != old) {
         int* dn = delta + (co + j) * kDeltaW;
         for (int c = 0; c < a.n; ++c) {
-            const int v = a.fmt.get(row, c);
+            const int v = fmt.get(row, c);
             atomicAdd(dn + c, v & 0xff);
             if (v >> 8) atomicAdd(dn + 9 + c, v >> 8);
         }
@@ -752,7 +752,7 @@ __device__ __forceinline__ int lloyd_eval(const LloydArgs& a, const float* c32, 
         if (old != 255) {
             int* dold = delta + (co + old) * kDeltaW;
             for (int c = 0; c < a.n; ++c) {
-                const int v = a.fmt.get(row, c);
+                const int v = fmt.get(row, c);
                 atomicSub(dold + c, v & 0xff);
                 if (v >> 8) atomicSub(dold + 9 + c, v >> 8);
             }
@@ -762,7 +762,9 @@ __device__ __forceinline__ int lloyd_eval(const LloydArgs& a, const float* c32, 
     return j;
 }
 
-template <bool RESIDENT>
+// BYTES: the byte-per-knob row layout as a compile-time RowFmt (constant shifts, no
+// generic-width code in the loop bodies); the bit-field layout reads a.fmt.
+template <bool RESIDENT, bool BYTES>
 __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, RESIDENT ? 1 : 3)
     lloyd_kernel(LloydArgs a) {
     extern __shared__ __align__(16) unsigned char s_dyn[];
@@ -788,6 +790,18 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
     const int K = a.K, R = a.R, n = a.n;
     const int64_t m = a.m;
     const int lane = tid & 31;
+    RowFmt fmt;
+    if constexpr (BYTES) {
+#pragma unroll
+        for (int i = 0; i < kMaxKnobs; ++i) {
+            fmt.shift[i] = uint8_t(8 * i);
+            fmt.width[i] = 8;
+        }
+        fmt.cmax = 255;
+        fmt.bytes = 1;
+    } else {
+        fmt = a.fmt;
+    }
 
     // resident state of this block's points
     const int64_t P = a.per_block;
@@ -992,7 +1006,7 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
                         if (ent[u] == 0xffffffffu) continue;
                         const int pl = int(ent[u] & 0xffffu), r = int((ent[u] >> 16) & 0xff), old = int(ent[u] >> 24);
                         float bud;
-                        const int j = lloyd_assign(a, c32, c64, dcum, r, row[u], bud);
+                        const int j = lloyd_assign(a, fmt, c32, c64, dcum, r, row[u], bud);
                         s_bud[r * P + pl] = bud;
                         if (a.stats) atomicAdd(&rs.cnt[r][2], 1u);
                         if (j != old) {
@@ -1000,12 +1014,12 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
                             rs.changed[r] = 1;
                             const int gn = a.coff[r] + j, go = a.coff[r] + old;
                             if (kDeltaMode == 0) {
-                                packed_delta(delta64 + gn * kPackedW, row[u], 1, n, a.fmt);
-                                if (old != 255) packed_delta(delta64 + go * kPackedW, row[u], -1, n, a.fmt);
+                                packed_delta(delta64 + gn * kPackedW, row[u], 1, n, fmt);
+                                if (old != 255) packed_delta(delta64 + go * kPackedW, row[u], -1, n, fmt);
                             } else {
                                 int* dw = kDeltaMode == 2 ? delta_w + (tid >> 5) * K * kDeltaW : delta;
-                                lane_delta(dw + gn * kDeltaW, row[u], 1, n, a.fmt);
-                                if (old != 255) lane_delta(dw + go * kDeltaW, row[u], -1, n, a.fmt);
+                                lane_delta(dw + gn * kDeltaW, row[u], 1, n, fmt);
+                                if (old != 255) lane_delta(dw + go * kDeltaW, row[u], -1, n, fmt);
                             }
                         }
                     }
@@ -1072,7 +1086,7 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
                         const LloydQueueEntry qe = queue[i];
                         const uint64_t row = __ldg(a.pts + qe.point);
                         float bud;
-                        const int j = lloyd_eval(a, c32, c64, dcum, delta, r, row, qe.old, bud);
+                        const int j = lloyd_eval(a, fmt, c32, c64, dcum, delta, r, row, qe.old, bud);
                         bg_r[qe.point] = bud;
                         if (j != qe.old) {
                             as_r[qe.point] = uint8_t(j);
@@ -1322,8 +1336,9 @@ static LloydPlan plan_lloyd(kt_engine* e, int64_t m, int K, int R, LloydArgs& a)
     const char* mode = std::getenv("KT_LLOYD_MODE");
     const bool force_stream = mode && std::strcmp(mode, "stream") == 0;
     const int64_t P = ((ceil_div(m, int64_t(e->num_sms)) + 15) & ~int64_t(15));
-    const void* kres = (const void*)lloyd_kernel<true>;
-    const void* kstr = (const void*)lloyd_kernel<false>;
+    const bool bytes = a.fmt.bytes != 0;
+    const void* kres = bytes ? (const void*)lloyd_kernel<true, true> : (const void*)lloyd_kernel<true, false>;
+    const void* kstr = bytes ? (const void*)lloyd_kernel<false, true> : (const void*)lloyd_kernel<false, false>;
     cudaFuncAttributes fa{};
     KT_CUDA(cudaFuncGetAttributes(&fa, kres));
     int optin = 0;
