@@ -545,6 +545,10 @@ __device__ __forceinline__ float dist_dn(float d2, float k1) {
 // rounding of the reference's squared distances (< 1e-10) cannot reorder two
 // centroids whose true distances differ by this much.
 constexpr float kSettleMargin = 1e-3f;
+#ifndef KT_ASSIGN_UNROLL
+#define KT_ASSIGN_UNROLL 4
+#endif
+constexpr int kAssignUnroll = KT_ASSIGN_UNROLL;  // centroid loop of the f32 assignment (4: 1.30 ms, 2: 1.33, 1: 1.35)
 
 __device__ __forceinline__ void unpack_row(uint64_t row, float p[kMaxKnobs], const RowFmt& f) {
     if (!f.bytes) {
@@ -583,6 +587,7 @@ __device__ __forceinline__ int full_assign(const float* c32, const double* c64, 
                                            int k, int n, const RowFmt& fmt, float k1, float& u, float& l) {
     float best = INFINITY, second = INFINITY;
     int bj = 0;
+#pragma unroll (kAssignUnroll)
     for (int j = 0; j < k; ++j) {
         const float d = f32_d2(p, c32 + j * kMaxKnobs);
         if (d < best) {
@@ -595,7 +600,9 @@ __device__ __forceinline__ int full_assign(const float* c32, const double* c64, 
     }
     if (k > 1 && !(second - best > d2_bound(best, k1) + d2_bound(second, k1))) {
         // ambiguous: the reference's own float64 expression decides (ties -> lowest j)
+        // (rare: rolled loops keep the resident kernel's loop body small)
         double bd = INFINITY;
+#pragma unroll 1
         for (int j = 0; j < k; ++j) {
             const double d = np_sq_dist(row, c64 + j * kMaxKnobs, n, fmt);
             if (d < bd) {
@@ -603,10 +610,13 @@ __device__ __forceinline__ int full_assign(const float* c32, const double* c64, 
                 bj = j;
             }
         }
-        best = f32_d2(p, c32 + bj * kMaxKnobs);
         second = INFINITY;
-        for (int j = 0; j < k; ++j)
-            if (j != bj) second = fminf(second, f32_d2(p, c32 + j * kMaxKnobs));
+#pragma unroll 1
+        for (int j = 0; j < k; ++j) {
+            const float d = f32_d2(p, c32 + j * kMaxKnobs);
+            if (j == bj) best = d;
+            else second = fminf(second, d);
+        }
     }
     u = dist_up(best, k1);
     l = k > 1 ? dist_dn(second, k1) : INFINITY;
@@ -764,6 +774,14 @@ __device__ __forceinline__ int lloyd_eval(const LloydArgs& a, const RowFmt& fmt,
 
 // BYTES: the byte-per-knob row layout as a compile-time RowFmt (constant shifts, no
 // generic-width code in the loop bodies); the bit-field layout reads a.fmt.
+// Probe builds (-DKT_LLOYD_PROBES=1) compile in the per-run visit counters and the
+// per-pass timeline that KT_LLOYD_STATS / KT_LLOYD_TIMELINE read; the default build
+// leaves them out of the kernel (a smaller loop body measured faster).
+#ifndef KT_LLOYD_PROBES
+#define KT_LLOYD_PROBES 0
+#endif
+constexpr bool kLloydProbes = KT_LLOYD_PROBES != 0;
+
 template <bool RESIDENT, bool BYTES>
 __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, RESIDENT ? 1 : 3)
     lloyd_kernel(LloydArgs a) {
@@ -843,7 +861,7 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
 
     int it = a.it0;
     auto stamp = [&](int phase) {
-        if (a.timeline && blockIdx.x == 0 && tid == 0 && it < 100) {
+        if (kLloydProbes && a.timeline && blockIdx.x == 0 && tid == 0 && it < 100) {
             long long t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
             a.timeline[it * 8 + phase] = t;
@@ -986,7 +1004,7 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
                 if (t0 == 0) stamp(2);
                 if (tid == 0) s_qn[tile_parity ^ 1] = 0;
                 const int nqueued = *qn;
-                if (a.stats && tid == 0)
+                if (kLloydProbes && a.stats && tid == 0)
                     for (int r = 0; r < R; ++r)
                         if (run_active(rs.state[r])) rs.cnt[r][0] += unsigned(t1 - t0);
                 // evaluate: rows from shared memory (or L2), kEvalUnroll per thread at a time
@@ -1008,7 +1026,7 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
                         float bud;
                         const int j = lloyd_assign(a, fmt, c32, c64, dcum, r, row[u], bud);
                         s_bud[r * P + pl] = bud;
-                        if (a.stats) atomicAdd(&rs.cnt[r][2], 1u);
+                        if (kLloydProbes && a.stats) atomicAdd(&rs.cnt[r][2], 1u);
                         if (j != old) {
                             s_asg[r * P + pl] = uint8_t(j);
                             rs.changed[r] = 1;
@@ -1093,7 +1111,7 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
                             rs.changed[r] = 1;
                         }
                     }
-                    if (a.stats) {
+                    if (kLloydProbes && a.stats) {
                         const unsigned valid = __reduce_add_sync(0xffffffffu, unsigned(cnt));
                         if (lane == 0) {
                             atomicAdd(&rs.cnt[r][0], valid);
@@ -1244,7 +1262,7 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
                 a.budget[int64_t(r) * a.stride + b0 + i] = s_bud[r * P + i];
             }
     }
-    if (a.stats && tid < R * 3) atomicAdd(a.stats + tid, (unsigned long long)rs.cnt[tid / 3][tid % 3]);
+    if (kLloydProbes && a.stats && tid < R * 3) atomicAdd(a.stats + tid, (unsigned long long)rs.cnt[tid / 3][tid % 3]);
     if (blockIdx.x == 0) {
         for (int i = tid; i < K * kSumW; i += blockDim.x) a.S[i] = S[i];
         for (int i = tid; i < K; i += blockDim.x) a.dcum[i] = dcum[i];
@@ -1503,13 +1521,13 @@ struct KmeansSession {
         a.run_iter = static_cast<int*>(e->scratch("km.iter", kMaxRuns * 4));
         a.ctrl = static_cast<int*>(e->scratch("km.ctrl", 16));
         a.barrier = static_cast<unsigned int*>(e->scratch("km.barrier", 16));
-        static const bool want_stats = std::getenv("KT_LLOYD_STATS") != nullptr;
+        static const bool want_stats = kLloydProbes && std::getenv("KT_LLOYD_STATS") != nullptr;
         a.stats = nullptr;
         if (want_stats) {
             a.stats = static_cast<unsigned long long*>(e->scratch("km.stats", kMaxRuns * 3 * 8));
             KT_CUDA(cudaMemsetAsync(a.stats, 0, kMaxRuns * 3 * 8, e->stream));
         }
-        static const bool want_timeline = std::getenv("KT_LLOYD_TIMELINE") != nullptr;
+        static const bool want_timeline = kLloydProbes && std::getenv("KT_LLOYD_TIMELINE") != nullptr;
         a.timeline = want_timeline ? static_cast<long long*>(e->scratch("km.timeline", 800 * 8)) : nullptr;
         double* d_loss = static_cast<double*>(e->scratch("km.loss", kMaxRuns * 8));
         a.budget = static_cast<float*>(e->scratch("km.budget", size_t(R) * a.stride * sizeof(float)));
