@@ -1170,8 +1170,10 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
             const int r = x < K * kMaxKnobs ? run_of[g] : 0;
             const bool live = x < K * kMaxKnobs && run_active(rs.state[r]);
             double dlt2 = 0.0;
+            long long cnt_new = 0;
             if (live) {
                 const long long cnt = S[g * kSumW + 8] + (long long)__ldcg(Dcur + g * kSumW + 8);
+                cnt_new = cnt;
                 double c = 0.0;
                 if (i < n) {
                     const long long sv = S[g * kSumW + i] + (long long)__ldcg(Dcur + g * kSumW + i);
@@ -1181,10 +1183,10 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
                 cnext[g * kMaxKnobs + i] = c;
                 const double dlt = c - c64[g * kMaxKnobs + i];
                 dlt2 = dlt * dlt;
-                if (i == 7) {  // the count after all lanes read it
-                    if (cnt == 0) rs.empty[r] = 1;
-                }
+                if (i == 7 && cnt == 0) rs.empty[r] = 1;
             }
+            __syncwarp();  // every lane of the cluster has read the old count
+            if (live && i == 7) S[g * kSumW + 8] = cnt_new;
             dlt2 += __shfl_xor_sync(0xffffffffu, dlt2, 1);
             dlt2 += __shfl_xor_sync(0xffffffffu, dlt2, 2);
             dlt2 += __shfl_xor_sync(0xffffffffu, dlt2, 4);
@@ -1194,8 +1196,6 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
         if (RESIDENT && kDeltaMode == 2)
             for (int i = tid; i < nwarps_blk * K * kDeltaW; i += blockDim.x) delta_w[i] = 0;
         __syncthreads();
-        for (int g = tid; g < K; g += blockDim.x)  // count sums, after every lane above has read them
-            if (run_active(rs.state[run_of[g]])) S[g * kSumW + 8] += (long long)__ldcg(Dcur + g * kSumW + 8);
         {
             const int w = tid >> 5;
             if (w < R) {
