@@ -79,29 +79,29 @@ __device__ __forceinline__ void load_tile(Frag<ROWS_MAX>& fr, const float* __res
                 }
             }
         }
-        return;
-    }
+    } else {
 #pragma unroll
-    for (int i = 0; i < Frag<ROWS_MAX>::kPer; ++i) {
-        const int f = threadIdx.x + i * kTcThreads;
-        float v[4] = {0.f, 0.f, 0.f, 0.f};
-        if (f < rows * (kTcBK / 4)) {
-            // K-major: G[(r0 + r) * ld + k0 + k]
-            const int r = f / (kTcBK / 4), kq = f % (kTcBK / 4);
-            const int gr = r0 + r, gk = k0 + 4 * kq;
-            if (gr < rlimit) {
-                const float* src = G + size_t(gr) * ld + gk;
-                if (vec_ok && gk + 3 < klimit) {
-                    const float4 q = __ldg(reinterpret_cast<const float4*>(src));
-                    v[0] = q.x, v[1] = q.y, v[2] = q.z, v[3] = q.w;
-                } else {
+        for (int i = 0; i < Frag<ROWS_MAX>::kPer; ++i) {
+            const int f = threadIdx.x + i * kTcThreads;
+            float v[4] = {0.f, 0.f, 0.f, 0.f};
+            if (f < rows * (kTcBK / 4)) {
+                // K-major: G[(r0 + r) * ld + k0 + k]
+                const int r = f / (kTcBK / 4), kq = f % (kTcBK / 4);
+                const int gr = r0 + r, gk = k0 + 4 * kq;
+                if (gr < rlimit) {
+                    const float* src = G + size_t(gr) * ld + gk;
+                    if (vec_ok && gk + 3 < klimit) {
+                        const float4 q = __ldg(reinterpret_cast<const float4*>(src));
+                        v[0] = q.x, v[1] = q.y, v[2] = q.z, v[3] = q.w;
+                    } else {
 #pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        if (gk + e < klimit) v[e] = __ldg(src + e);
+                        for (int e = 0; e < 4; ++e)
+                            if (gk + e < klimit) v[e] = __ldg(src + e);
+                    }
                 }
             }
+            fr.v[i] = make_float4(v[0], v[1], v[2], v[3]);
         }
-        fr.v[i] = make_float4(v[0], v[1], v[2], v[3]);
     }
 }
 
@@ -127,21 +127,21 @@ __device__ __forceinline__ void store_tile(const Frag<ROWS_MAX>& fr, float* hi, 
             *reinterpret_cast<float4*>(hi + off) = h;
             *reinterpret_cast<float4*>(lo + off) = l;
         }
-        return;
-    }
+    } else {
 #pragma unroll
-    for (int i = 0; i < Frag<ROWS_MAX>::kPer; ++i) {
-        const int f = threadIdx.x + i * kTcThreads;
-        if (f >= rows * (kTcBK / 4)) break;
-        const int r = f / (kTcBK / 4), kq = f % (kTcBK / 4);
-        const int off = kq * rows * 4 + (r >> 3) * 32 + (r & 7) * 4;
-        float4 h, l;
-        umma::split_tf32(fr.v[i].x, h.x, l.x);
-        umma::split_tf32(fr.v[i].y, h.y, l.y);
-        umma::split_tf32(fr.v[i].z, h.z, l.z);
-        umma::split_tf32(fr.v[i].w, h.w, l.w);
-        *reinterpret_cast<float4*>(hi + off) = h;
-        *reinterpret_cast<float4*>(lo + off) = l;
+        for (int i = 0; i < Frag<ROWS_MAX>::kPer; ++i) {
+            const int f = threadIdx.x + i * kTcThreads;
+            if (f >= rows * (kTcBK / 4)) break;
+            const int r = f / (kTcBK / 4), kq = f % (kTcBK / 4);
+            const int off = kq * rows * 4 + (r >> 3) * 32 + (r & 7) * 4;
+            float4 h, l;
+            umma::split_tf32(fr.v[i].x, h.x, l.x);
+            umma::split_tf32(fr.v[i].y, h.y, l.y);
+            umma::split_tf32(fr.v[i].z, h.z, l.z);
+            umma::split_tf32(fr.v[i].w, h.w, l.w);
+            *reinterpret_cast<float4*>(hi + off) = h;
+            *reinterpret_cast<float4*>(lo + off) = l;
+        }
     }
 }
 

@@ -631,9 +631,8 @@ constexpr bool kCustomGridBarrier = true;
 __device__ __forceinline__ void lloyd_grid_barrier(unsigned int* ctr, unsigned int target) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        unsigned int old, cur;
-        (void)old;
-        asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
+        unsigned int cur;
+        asm volatile("atom.add.release.gpu.u32 _, [%0], 1;" ::"l"(ctr) : "memory");  // (red.release: same speed)
         do {
             asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(ctr) : "memory");
         } while (cur < target);
