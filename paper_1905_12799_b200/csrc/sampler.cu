@@ -276,11 +276,15 @@ struct InitArgs {
     long long* sums[2];
     int nchunks;
     unsigned int* barrier;  // grid-barrier counter, zeroed before the launch
+    int64_t per_block;      // resident kernel: points per block (P); sums are per sub-chunk
+    int nsub;               // resident kernel: sub-chunks per block
+    int sub;                // resident kernel: points per sub-chunk (multiple of 32, <= kInitFinPer * threads)
 };
 
 // Block-wide inclusive scan of one int64 per thread with one barrier: warp scans, warp
 // totals through shared memory, every warp adds the totals of the warps before it.
 // Returns the thread's exclusive prefix; *total receives the block total.
+template <int NT = kInitThreads>
 __device__ __forceinline__ long long block_excl_scan1(long long v, long long* s_warp, long long* total) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     long long incl = v;
@@ -293,7 +297,7 @@ __device__ __forceinline__ long long block_excl_scan1(long long v, long long* s_
     __syncthreads();
     long long before = 0, tot = 0;
 #pragma unroll
-    for (int w = 0; w < kInitThreads / 32; ++w) {
+    for (int w = 0; w < NT / 32; ++w) {
         const long long x = s_warp[w];
         before += w < warp ? x : 0;
         tot += x;
@@ -411,6 +415,141 @@ __global__ void __launch_bounds__(kInitThreads) init_kernel(InitArgs a) {
                 for (int w = 0; w < kInitThreads / 32; ++w) t += s_warp[0][w];
                 snew[ch] = t;
             }
+        }
+        init_grid_barrier(a.barrier, ++n_bar * gridDim.x);
+    }
+}
+
+// Resident k-means++ (one block per SM): block b keeps its P points' rows and weights in
+// shared memory for the whole launch, so a centroid's weight update reads no global
+// memory; the weights are also written to global memory for the selection, which
+// every block makes identically from per-sub-chunk sums (a.sub points each): a
+// block scan over the sums finds the sub-chunk holding u * total, a second scan over
+// its weights the point.  Same exact-integer arithmetic as init_kernel.
+constexpr int kInitResThreads = 512;
+constexpr int kInitSelPer = 8;   // sub-chunk sums per thread in the selection scan (independent loads)
+constexpr int kInitFinPer = 4;   // weights per thread in the sub-chunk scan
+constexpr int kInitMaxSub = 128; // sub-chunks per block
+
+// Squared distance of two byte-layout rows: per-byte |a - b| (vabsdiffu4), then the
+// byte dot products (dp4a) — exact, < 8 * 255^2.
+__device__ __forceinline__ int byte_sq_dist(uint64_t a, uint64_t b) {
+    const unsigned lo = __vabsdiffu4(unsigned(a), unsigned(b));
+    const unsigned hi = __vabsdiffu4(unsigned(a >> 32), unsigned(b >> 32));
+    return __dp4a(lo, lo, __dp4a(hi, hi, 0u));
+}
+
+template <bool BYTES>
+__global__ void __launch_bounds__(kInitResThreads, 1) init_res_kernel(InitArgs a) {
+    extern __shared__ __align__(16) unsigned char s_dyn[];
+    __shared__ long long s_warp[2][kInitResThreads / 32];
+    __shared__ long long s_sub[kInitMaxSub];
+    __shared__ long long s_before;
+    __shared__ int s_chunk;
+    __shared__ unsigned long long s_found;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int64_t P = a.per_block, b0 = int64_t(blockIdx.x) * P;
+    const int np = int(b0 < a.m ? (a.m - b0 < P ? a.m - b0 : P) : 0);
+    uint64_t* s_rows = reinterpret_cast<uint64_t*>(s_dyn);
+    int* s_d2 = reinterpret_cast<int*>(s_rows + P);
+    const int* w_in = a.d2[(a.j0 - 1) & 1];
+    for (int i = tid; i < np; i += kInitResThreads) {
+        s_rows[i] = a.pts[b0 + i];
+        if (a.j0 > 0) s_d2[i] = __ldcg(w_in + b0 + i);
+    }
+    for (int i = tid; i < a.nsub; i += kInitResThreads) s_sub[i] = 0;
+    const int L = int(gridDim.x) * a.nsub;  // sub-chunks in point order: (block, sub)
+    unsigned int n_bar = 0;
+    __syncthreads();
+    for (int j = a.j0; j < a.j1; ++j) {
+        uint64_t c;
+        if (j == 0) {
+            c = a.pts[a.first_idx];
+        } else {
+            const long long* cs = a.sums[(j - 1) & 1];
+            const int* w = a.d2[(j - 1) & 1];
+            const int cper = (L + kInitResThreads - 1) / kInitResThreads;  // <= kInitSelPer (host)
+            const int lo = min(L, tid * cper), hi = min(L, lo + cper);
+            long long vals[kInitSelPer];
+            long long mine = 0;
+#pragma unroll
+            for (int q = 0; q < kInitSelPer; ++q) {
+                vals[q] = lo + q < hi ? __ldcg(cs + lo + q) : 0;
+                mine += vals[q];
+            }
+            if (tid == 0) s_found = ~0ull;
+            long long total;
+            const long long excl = block_excl_scan1<kInitResThreads>(mine, s_warp[0], &total);
+            const long long T = (long long)floor(__dmul_rn(a.uniforms[j - 1], double(total)));
+            long long run = excl;
+#pragma unroll
+            for (int q = 0; q < kInitSelPer; ++q) {
+                const long long next = run + vals[q];
+                if (lo + q < hi && run <= T && next > T) {
+                    s_chunk = lo + q;
+                    s_before = run;
+                }
+                run = next;
+            }
+            if (tid == 0 && T >= total) s_chunk = -1;
+            __syncthreads();
+            const int ch = s_chunk;
+            if (ch >= 0) {
+                const int blk = ch / a.nsub, sb = ch % a.nsub;
+                const int64_t pb = int64_t(blk) * P + int64_t(sb) * a.sub;  // first point of the sub-chunk
+                const int64_t nb = blk * P + P < a.m ? blk * P + P : a.m;       // end of the block's points
+                const int64_t len = pb < nb ? (nb - pb < a.sub ? nb - pb : a.sub) : 0;
+                const int o0 = tid * kInitFinPer;
+                int v[kInitFinPer];
+                long long tsum = 0;
+#pragma unroll
+                for (int q = 0; q < kInitFinPer; ++q) {
+                    v[q] = o0 + q < len ? __ldcg(w + pb + o0 + q) : 0;
+                    tsum += v[q];
+                }
+                long long tot2;
+                long long acc = s_before + block_excl_scan1<kInitResThreads>(tsum, s_warp[1], &tot2);
+                int first = -1;
+#pragma unroll
+                for (int q = 0; q < kInitFinPer; ++q) {
+                    acc += v[q];
+                    if (first < 0 && acc > T && o0 + q < len) first = q;
+                }
+                if (first >= 0) atomicMin(&s_found, (unsigned long long)(pb + o0 + first));
+            }
+            __syncthreads();
+            int64_t idx = s_found == ~0ull ? a.m - 1 : int64_t(s_found);
+            if (idx > a.m - 1) idx = a.m - 1;
+            c = a.pts[idx];
+        }
+        if (blockIdx.x == 0 && tid == 0) a.cent_rows[j] = c;
+        // ---- weights for the next centroid, from shared memory
+        int* wg = a.d2[j & 1];
+        for (int i0 = 0; i0 < np; i0 += kInitResThreads) {  // warp-uniform trip count
+            const int i = i0 + tid;
+            int v = 0;
+            if (i < np) {
+                v = BYTES ? byte_sq_dist(s_rows[i], c) : int(int_sq_dist(s_rows[i], c, a.n, a.fmt));
+                if (j > 0) v = min(v, s_d2[i]);
+                s_d2[i] = v;
+                wg[b0 + i] = v;
+            }
+            long long sum64;
+            if (BYTES) {  // 32 weights < 2^19 each: one 32-bit warp reduction
+                sum64 = (long long)__reduce_add_sync(0xffffffffu, unsigned(v));
+            } else {  // int64: 32 weights < 2^31 each
+                sum64 = v;
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) sum64 += __shfl_xor_sync(0xffffffffu, sum64, off);
+            }
+            if (lane == 0 && i < np)  // a warp's 32 points lie in one sub-chunk
+                atomicAdd(reinterpret_cast<unsigned long long*>(s_sub + i / a.sub), (unsigned long long)sum64);
+        }
+        __syncthreads();
+        long long* snew = a.sums[j & 1];
+        for (int i = tid; i < a.nsub; i += kInitResThreads) {
+            snew[int64_t(blockIdx.x) * a.nsub + i] = s_sub[i];
+            s_sub[i] = 0;
         }
         init_grid_barrier(a.barrier, ++n_bar * gridDim.x);
     }
@@ -1424,6 +1563,14 @@ struct KmeansSession {
     long long* chunk_sums = nullptr;
     double* d_uniforms = nullptr;
     int nchunks = 0;
+    // resident init (init_res_kernel) when a block's rows + weights fit in shared memory
+    bool init_res = false;
+    int64_t init_P = 0;
+    int init_nsub = 0;
+    int init_sub = 0;
+    size_t init_smem = 0;
+    const void* init_kern = nullptr;
+    long long* sub_sums = nullptr;
 
     KmeansSession(kt_engine* e_, const uint64_t* p, int64_t m_, int n_, const RowFmt& f, uint64_t s)
         : e(e_), pts(p), m(m_), n(n_), fmt(f), seed(s) {
@@ -1448,6 +1595,33 @@ struct KmeansSession {
         nchunks = int(ceil_div(m, kInitChunk));
         chunk_sums = static_cast<long long*>(e->scratch("km.chunk_sums", size_t(nchunks) * 16));
         d_uniforms = static_cast<double*>(e->scratch("km.uniforms", 64 * 8));
+        {
+            const char* mode = std::getenv("KT_INIT_MODE");  // tests: "chunked" = init_kernel
+            // sub-chunks: at most kInitSelPer sums per thread in the selection scan, at most
+            // kInitFinPer weights per thread in the sub-chunk scan, warp-aligned
+            init_P = (ceil_div(m, int64_t(e->num_sms)) + 31) & ~int64_t(31);
+            const int64_t max_sub_blocks = int64_t(kInitSelPer) * kInitResThreads / e->num_sms;
+            init_sub = int((ceil_div(init_P, std::max<int64_t>(1, std::min<int64_t>(max_sub_blocks, kInitMaxSub))) + 31) &
+                           ~int64_t(31));
+            init_nsub = int(ceil_div(init_P, int64_t(init_sub)));
+            init_smem = size_t(init_P) * 12;
+            int optin = 0;
+            KT_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
+            cudaFuncAttributes fa{};
+            init_kern = f.bytes ? (const void*)init_res_kernel<true> : (const void*)init_res_kernel<false>;
+            KT_CUDA(cudaFuncGetAttributes(&fa, init_kern));
+            init_res = !(mode && std::strcmp(mode, "chunked") == 0) && init_nsub <= kInitMaxSub &&
+                       int64_t(init_nsub) * e->num_sms <= int64_t(kInitSelPer) * kInitResThreads &&
+                       init_sub <= kInitFinPer * kInitResThreads &&
+                       init_smem + fa.sharedSizeBytes <= size_t(optin);
+            if (init_res) {
+                allow_dynamic_smem(init_kern);
+                init_res = occupancy_blocks(init_kern, kInitResThreads, init_smem) >= 1;
+            }
+            if (init_res)
+                sub_sums = static_cast<long long*>(
+                    e->scratch("km.init_sub", size_t(e->num_sms) * size_t(init_nsub) * 16));
+        }
         auto* h = static_cast<double*>(e->staging("km.uniforms", 64 * 8));
         std::copy(uniforms.begin(), uniforms.end(), h);
         KT_CUDA(cudaMemcpyAsync(d_uniforms, h, 64 * 8, cudaMemcpyHostToDevice, e->stream));
@@ -1473,6 +1647,20 @@ struct KmeansSession {
         ia.nchunks = nchunks;
         ia.barrier = static_cast<unsigned int*>(e->scratch("km.init_barrier", 16));
         KT_CUDA(cudaMemsetAsync(ia.barrier, 0, 16, e->stream));
+        if (init_res) {
+            ia.per_block = init_P;
+            ia.nsub = init_nsub;
+            ia.sub = init_sub;
+            ia.sums[0] = sub_sums;
+            ia.sums[1] = sub_sums + size_t(e->num_sms) * init_nsub;
+            void* params[] = {&ia};
+            e->pre_launch("kmeanspp_init");
+            KT_CUDA(cudaLaunchCooperativeKernel(init_kern, e->num_sms, kInitResThreads, params,
+                                                init_smem, e->stream));
+            e->check_launch("kmeanspp_init");
+            chosen = k;
+            return;
+        }
         const int occ = std::max(1, occupancy_blocks((const void*)init_kernel, kInitThreads, 0));
         const int grid = int(std::max<int64_t>(1, std::min<int64_t>(int64_t(occ) * e->num_sms, nchunks)));
         void* params[] = {&ia};

@@ -175,11 +175,14 @@ def test_adaptive_sample_uniform_s2_vs_oracle(seed):
     assert [tuple(r) for r in sp.unpack(got, 8).tolist()] == want
 
 
-@pytest.mark.parametrize("mode", ["stream", "tile64", "gather"])
+@pytest.mark.parametrize("mode", ["stream", "tile64", "gather", "init_chunked"])
 @pytest.mark.parametrize("seed", [0, 1, 2])
 def test_lloyd_variants_vs_oracle(mode, seed, monkeypatch):
-    """Both Lloyd kernels (streaming, and resident with many queue tiles per block) agree with the oracle."""
-    if mode == "stream":
+    """Both Lloyd kernels (streaming, and resident with many queue tiles per block) and both k-means++
+    kernels (resident, chunked) agree with the oracle."""
+    if mode == "init_chunked":
+        monkeypatch.setenv("KT_INIT_MODE", "chunked")
+    elif mode == "stream":
         monkeypatch.setenv("KT_LLOYD_MODE", "stream")
     elif mode == "gather":
         monkeypatch.setenv("KT_LLOYD_ROWS", "global")
@@ -192,13 +195,15 @@ def test_lloyd_variants_vs_oracle(mode, seed, monkeypatch):
 LARGE = json.loads((GOLDEN / "large.json").read_text())
 
 
-@pytest.mark.parametrize("mode", ["resident", "stream", "tile64", "gather"])
+@pytest.mark.parametrize("mode", ["resident", "stream", "tile64", "gather", "init_chunked"])
 @pytest.mark.parametrize("name", sorted(LARGE))
 def test_knee_large_vs_oracle_golden(name, mode, monkeypatch):
     """131K / 262K candidates (config C3 size): knee curve, centroids, assignment and batch bit-exact."""
     import hashlib
 
-    if mode == "stream":
+    if mode == "init_chunked":
+        monkeypatch.setenv("KT_INIT_MODE", "chunked")
+    elif mode == "stream":
         monkeypatch.setenv("KT_LLOYD_MODE", "stream")
     elif mode == "tile64":
         monkeypatch.setenv("KT_LLOYD_TILE", "64")
