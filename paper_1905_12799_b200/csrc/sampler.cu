@@ -318,6 +318,15 @@ __device__ __forceinline__ void init_grid_barrier(unsigned int* ctr, unsigned in
     __syncthreads();
 }
 
+// Squared distance of two byte-layout rows: per-byte |a - b| (vabsdiffu4), then the
+// byte dot products (dp4a) — exact, < 8 * 255^2.
+__device__ __forceinline__ int byte_sq_dist(uint64_t a, uint64_t b) {
+    const unsigned lo = __vabsdiffu4(unsigned(a), unsigned(b));
+    const unsigned hi = __vabsdiffu4(unsigned(a >> 32), unsigned(b >> 32));
+    return __dp4a(lo, lo, __dp4a(hi, hi, 0u));
+}
+
+template <bool BYTES>
 __global__ void __launch_bounds__(kInitThreads) init_kernel(InitArgs a) {
     __shared__ long long s_warp[2][kInitThreads / 32];  // double-buffered: no barrier between scans
     __shared__ long long s_before;
@@ -399,7 +408,7 @@ __global__ void __launch_bounds__(kInitThreads) init_kernel(InitArgs a) {
             for (int q = 0; q < per; ++q) {
                 const int64_t p = base + q * kInitThreads + tid;
                 if (p < a.m) {
-                    int v = int(int_sq_dist(a.pts[p], c, a.n, a.fmt));  // < 2^31 (host check)
+                    int v = BYTES ? byte_sq_dist(a.pts[p], c) : int(int_sq_dist(a.pts[p], c, a.n, a.fmt));  // < 2^31
                     if (j > 0) v = min(v, __ldcg(wold + p));
                     wnew[p] = v;
                     sum += v;
@@ -430,14 +439,6 @@ constexpr int kInitResThreads = 512;
 constexpr int kInitSelPer = 8;   // sub-chunk sums per thread in the selection scan (independent loads)
 constexpr int kInitFinPer = 4;   // weights per thread in the sub-chunk scan
 constexpr int kInitMaxSub = 128; // sub-chunks per block
-
-// Squared distance of two byte-layout rows: per-byte |a - b| (vabsdiffu4), then the
-// byte dot products (dp4a) — exact, < 8 * 255^2.
-__device__ __forceinline__ int byte_sq_dist(uint64_t a, uint64_t b) {
-    const unsigned lo = __vabsdiffu4(unsigned(a), unsigned(b));
-    const unsigned hi = __vabsdiffu4(unsigned(a >> 32), unsigned(b >> 32));
-    return __dp4a(lo, lo, __dp4a(hi, hi, 0u));
-}
 
 template <bool BYTES>
 __global__ void __launch_bounds__(kInitResThreads, 1) init_res_kernel(InitArgs a) {
@@ -1661,11 +1662,12 @@ struct KmeansSession {
             chosen = k;
             return;
         }
-        const int occ = std::max(1, occupancy_blocks((const void*)init_kernel, kInitThreads, 0));
+        const void* kchunk = fmt.bytes ? (const void*)init_kernel<true> : (const void*)init_kernel<false>;
+        const int occ = std::max(1, occupancy_blocks(kchunk, kInitThreads, 0));
         const int grid = int(std::max<int64_t>(1, std::min<int64_t>(int64_t(occ) * e->num_sms, nchunks)));
         void* params[] = {&ia};
         e->pre_launch("kmeanspp_init");
-        KT_CUDA(cudaLaunchCooperativeKernel((const void*)init_kernel, grid, kInitThreads, params, 0, e->stream));
+        KT_CUDA(cudaLaunchCooperativeKernel(kchunk, grid, kInitThreads, params, 0, e->stream));
         e->check_launch("kmeanspp_init");
         chosen = k;
     }
