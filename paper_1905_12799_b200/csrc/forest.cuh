@@ -27,15 +27,15 @@ __device__ __forceinline__ double walk_tree(const uint64_t* __restrict__ t, uint
     int base = 0;    // offset of the current super-node level
 #pragma unroll
     for (int d = 0; d < D; d += 2) {
-        uint64_t w = t[base + pos];
-        uint32_t e = uint32_t(w) & 0xffffu;
-        uint32_t b = __byte_perm(lo, hi, e & 7u) & 0xffu;
-        int go = b >= (e >> 8);
+        // entry = knob << 12 | cut: PRMT reads only the selector's low 16 bits and puts
+        // byte[knob] in the top byte (junk below), so byte >= cut <=> result >= cut << 24
+        const uint64_t w = t[base + pos];
+        const uint32_t wlo = uint32_t(w), whi = uint32_t(w >> 32);
+        const int go = __byte_perm(lo, hi, wlo) >= (wlo << 24);
         pos = 2 * pos + go;
         if (d + 1 < D) {
-            uint32_t e1 = uint32_t(w >> (16 * (1 + go))) & 0xffffu;
-            uint32_t b1 = __byte_perm(lo, hi, e1 & 7u) & 0xffu;
-            pos = 2 * pos + int(b1 >= (e1 >> 8));
+            const uint32_t e1 = go ? whi : (wlo >> 16);
+            pos = 2 * pos + int(__byte_perm(lo, hi, e1) >= (e1 << 24));
         }
         base += 1 << d;
     }

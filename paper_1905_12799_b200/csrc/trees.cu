@@ -12,7 +12,8 @@
 //     non-decreasing in the index, "x[f] <= threshold" <=> "idx[f] < t", so the
 //     device never touches floating-point features (exactly the reference's
 //     routing, cost_model.py:197-198);
-//   * node entries are 16 bit (feature | cut << 8); a node and its two children
+//   * node entries are 16 bit (feature << 12 | cut: one PRMT with the entry as its
+//     selector puts the knob's byte on top, one compare against cut << 24); a node and its two children
 //     are packed into one 64-bit "super node", so one shared-memory load
 //     resolves two levels (3 LDS per depth-4 tree instead of 5).
 //
@@ -63,7 +64,7 @@ struct Packer {
         const double* row = table + size_t(f) * max_card;
         int cut = 0;
         while (cut < card && row[cut] <= thr[node]) ++cut;  // table is non-decreasing
-        return uint16_t(wide ? (f | (cut << 3)) : (f | (cut << 8)));
+        return uint16_t(wide ? (f | (cut << 3)) : ((f << 12) | cut));
     }
     void fill(int node, int h, int depth) {
         if (depth == D) {
@@ -71,7 +72,7 @@ struct Packer {
             return;
         }
         if (feat[node] < 0) {
-            heap[h] = uint16_t(wide ? (8191 << 3) : (255 << 8));  // idx < cut always: left
+            heap[h] = uint16_t(wide ? (8191 << 3) : 255);  // idx < cut always: left
             fill(node, 2 * h + 1, depth + 1);
             fill(node, 2 * h + 2, depth + 1);
         } else {
