@@ -169,10 +169,47 @@ __global__ void __launch_bounds__(1024) combine_kernel(double* vals, int L, cons
     if (threadIdx.x == 0) *out = vals[root];
 }
 
+// Same combine with the node values and the tree in shared memory (one block): a level
+// costs a block barrier instead of a global-memory round trip (14 levels at 1M points).
+__global__ void __launch_bounds__(1024) combine_smem_kernel(const double* __restrict__ vals, int L, int I,
+                                                            const int32_t* __restrict__ left,
+                                                            const int32_t* __restrict__ right,
+                                                            const int32_t* __restrict__ level_start, int n_levels,
+                                                            int root, double* out) {
+    extern __shared__ double sv[];  // [L + I] values, then [I] left, [I] right, [n_levels + 1] level starts
+    int32_t* sl = reinterpret_cast<int32_t*>(sv + L + I);
+    int32_t* sr = sl + I;
+    int32_t* slv = sr + I;
+    for (int i = threadIdx.x; i < L; i += blockDim.x) sv[i] = vals[i];
+    for (int i = threadIdx.x; i < I; i += blockDim.x) {
+        sl[i] = left[i];
+        sr[i] = right[i];
+    }
+    for (int i = threadIdx.x; i <= n_levels; i += blockDim.x) slv[i] = level_start[i];
+    __syncthreads();
+    for (int lv = 0; lv < n_levels; ++lv) {
+        const int a = slv[lv], b = slv[lv + 1];
+        for (int i = a + threadIdx.x; i < b; i += blockDim.x) sv[L + i] = __dadd_rn(sv[sl[i]], sv[sr[i]]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = sv[root];
+}
+
 static void combine(kt_engine* e, const PairwiseTree& t, double* vals, double* out_dev) {
     const int L = int(t.leaf_start.size());
+    const int I = int(t.node_left.size());
+    const size_t smem = size_t(L + I) * 8 + size_t(I) * 8 + size_t(t.n_levels + 1) * 4;
+    static int optin = -1;  // per process; every device in the pool is a B200
+    if (optin < 0) KT_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
     e->pre_launch("pairwise_combine");
-    combine_kernel<<<1, 1024, 0, e->stream>>>(vals, L, t.d_left, t.d_right, t.d_level, t.n_levels, t.root, out_dev);
+    if (smem <= size_t(optin)) {
+        allow_dynamic_smem((const void*)combine_smem_kernel);
+        combine_smem_kernel<<<1, 1024, smem, e->stream>>>(vals, L, I, t.d_left, t.d_right, t.d_level, t.n_levels,
+                                                         t.root, out_dev);
+    } else {
+        combine_kernel<<<1, 1024, 0, e->stream>>>(vals, L, t.d_left, t.d_right, t.d_level, t.n_levels, t.root,
+                                                  out_dev);
+    }
     e->check_launch("pairwise_combine");
 }
 
