@@ -796,7 +796,7 @@ __device__ __forceinline__ int lloyd_decide(const LloydArgs& a, const long long*
 // two shared-memory reads per pass and no global traffic at all; the points the
 // budgets cannot settle go through a block-wide queue (tiles of `tile` points,
 // so the queue never overflows) and only they fetch their rows from L2.
-constexpr int kLloydResThreads = 768;
+constexpr int kLloydResThreads = 640;  // 20 warps (A/B at 1M points: 640 1.285 ms, 768 1.295, 896 1.287; 512 and 1024 slower)
 constexpr int kEvalUnroll = 1;  // queue entries per thread per iteration (1 measured best: smaller code, 1.45 -> 1.41 ms)
 constexpr int kScanQuads = 4;   // quads per thread per scan round
 // Resident-kernel cluster-sum deltas: 0 = packed 64-bit shared words (5 CAS atomics per
