@@ -128,17 +128,26 @@ __device__ __forceinline__ void warp_leaf(int l, const int64_t* leaf_start, cons
     }
 }
 
+// Run r = blockIdx.y: assignments assign + r * astride, centroids cent + coff[r] * 8, leaf
+// values vals + r * vstride.
+struct RunOffsets {
+    int coff[kMaxLossRuns];
+};
 __global__ void __launch_bounds__(kLeafWarps * 32) loss_leaf_kernel(const uint64_t* __restrict__ pts,
-                                                                    const uint8_t* __restrict__ assign,
-                                                                    const double* __restrict__ cent, int n,
-                                                                    const RowFmt fmt, const int64_t* leaf_start, const int32_t* leaf_len,
-                                                                    int L, double* vals) {
+                                                                    const uint8_t* __restrict__ assign, int64_t astride,
+                                                                    const double* __restrict__ cent, RunOffsets ro,
+                                                                    int n, const RowFmt fmt, const int64_t* leaf_start,
+                                                                    const int32_t* leaf_len, int L, double* vals,
+                                                                    int64_t vstride) {
     __shared__ double s_buf[kLeafWarps][128];
     const int w = threadIdx.x >> 5;
     const int l = blockIdx.x * kLeafWarps + w;
     if (l >= L) return;
-    warp_leaf(l, leaf_start, leaf_len, vals, s_buf[w],
-              [&](int64_t p) { return np_sq_dist(pts[p], cent + int(assign[p]) * kMaxKnobs, n, fmt); });
+    const int r = blockIdx.y;
+    const uint8_t* as = assign + r * astride;
+    const double* cr = cent + size_t(ro.coff[r]) * kMaxKnobs;
+    warp_leaf(l, leaf_start, leaf_len, vals + r * vstride, s_buf[w],
+              [&](int64_t p) { return np_sq_dist(pts[p], cr + int(as[p]) * kMaxKnobs, n, fmt); });
 }
 
 __global__ void __launch_bounds__(kLeafWarps * 32) array_leaf_kernel(const double* __restrict__ x,
@@ -160,7 +169,9 @@ __global__ void __launch_bounds__(kLeafWarps * 32) array_leaf_kernel(const doubl
 
 __global__ void __launch_bounds__(1024) combine_kernel(double* vals, int L, const int32_t* left, const int32_t* right,
                                                        const int32_t* level_start, int n_levels, int root,
-                                                       double* out) {
+                                                       double* out, int64_t vstride) {
+    vals += blockIdx.x * vstride;  // one block per independent sum
+    out += blockIdx.x;
     for (int lv = 0; lv < n_levels; ++lv) {
         const int a = level_start[lv], b = level_start[lv + 1];
         for (int i = a + threadIdx.x; i < b; i += blockDim.x) vals[L + i] = __dadd_rn(vals[left[i]], vals[right[i]]);
@@ -175,8 +186,10 @@ __global__ void __launch_bounds__(1024) combine_smem_kernel(const double* __rest
                                                             const int32_t* __restrict__ left,
                                                             const int32_t* __restrict__ right,
                                                             const int32_t* __restrict__ level_start, int n_levels,
-                                                            int root, double* out) {
+                                                            int root, double* out, int64_t vstride) {
     extern __shared__ double sv[];  // [L + I] values, then [I] left, [I] right, [n_levels + 1] level starts
+    vals += blockIdx.x * vstride;  // one block per independent sum
+    out += blockIdx.x;
     int32_t* sl = reinterpret_cast<int32_t*>(sv + L + I);
     int32_t* sr = sl + I;
     int32_t* slv = sr + I;
@@ -195,7 +208,8 @@ __global__ void __launch_bounds__(1024) combine_smem_kernel(const double* __rest
     if (threadIdx.x == 0) *out = sv[root];
 }
 
-static void combine(kt_engine* e, const PairwiseTree& t, double* vals, double* out_dev) {
+static void combine(kt_engine* e, const PairwiseTree& t, double* vals, double* out_dev, int nsums = 1,
+                    int64_t vstride = 0) {
     const int L = int(t.leaf_start.size());
     const int I = int(t.node_left.size());
     const size_t smem = size_t(L + I) * 8 + size_t(I) * 8 + size_t(t.n_levels + 1) * 4;
@@ -204,26 +218,35 @@ static void combine(kt_engine* e, const PairwiseTree& t, double* vals, double* o
     e->pre_launch("pairwise_combine");
     if (smem <= size_t(optin)) {
         allow_dynamic_smem((const void*)combine_smem_kernel);
-        combine_smem_kernel<<<1, 1024, smem, e->stream>>>(vals, L, I, t.d_left, t.d_right, t.d_level, t.n_levels,
-                                                         t.root, out_dev);
+        combine_smem_kernel<<<nsums, 1024, smem, e->stream>>>(vals, L, I, t.d_left, t.d_right, t.d_level,
+                                                             t.n_levels, t.root, out_dev, vstride);
     } else {
-        combine_kernel<<<1, 1024, 0, e->stream>>>(vals, L, t.d_left, t.d_right, t.d_level, t.n_levels, t.root,
-                                                  out_dev);
+        combine_kernel<<<nsums, 1024, 0, e->stream>>>(vals, L, t.d_left, t.d_right, t.d_level, t.n_levels, t.root,
+                                                      out_dev, vstride);
     }
     e->check_launch("pairwise_combine");
 }
 
 void pairwise_loss(kt_engine* e, const uint64_t* pts, int64_t m, int n, const RowFmt& fmt, const uint8_t* assign,
                    const double* cent, double* out_dev) {
+    const int zero = 0;
+    pairwise_loss_runs(e, pts, m, n, fmt, assign, 0, cent, &zero, 1, out_dev);
+}
+
+void pairwise_loss_runs(kt_engine* e, const uint64_t* pts, int64_t m, int n, const RowFmt& fmt, const uint8_t* assign,
+                        int64_t astride, const double* cent, const int* coff, int R, double* out_dev) {
+    if (R < 1 || R > kMaxLossRuns) fail(KT_ERR_VALUE, "pairwise_loss_runs: 1..8 runs");
     const PairwiseTree& t = pairwise_tree(e->device, m);
     const int L = int(t.leaf_start.size());
-    auto* vals = static_cast<double*>(e->scratch("loss.vals", size_t(L + t.node_left.size()) * 8));
+    const int64_t vstride = int64_t(L) + int64_t(t.node_left.size());
+    auto* vals = static_cast<double*>(e->scratch("loss.vals", size_t(vstride) * R * 8));
+    RunOffsets ro{};
+    for (int r = 0; r < R; ++r) ro.coff[r] = coff[r];
     e->pre_launch("loss_leaf");
-    loss_leaf_kernel<<<int(ceil_div(L, kLeafWarps)), kLeafWarps * 32, 0, e->stream>>>(pts, assign, cent, n, fmt,
-                                                                                    t.d_leaf_start, t.d_leaf_len, L,
-                                                                                    vals);
+    loss_leaf_kernel<<<dim3(unsigned(ceil_div(L, kLeafWarps)), unsigned(R)), kLeafWarps * 32, 0, e->stream>>>(
+        pts, assign, astride, cent, ro, n, fmt, t.d_leaf_start, t.d_leaf_len, L, vals, vstride);
     e->check_launch("loss_leaf");
-    combine(e, t, vals, out_dev);
+    combine(e, t, vals, out_dev, R, vstride);
 }
 
 void pairwise_sum(kt_engine* e, const double* x, int64_t m, const double* center, double* out_dev) {

@@ -45,6 +45,12 @@ void pairwise_loss(kt_engine* e, const uint64_t* pts, int64_t m, int n, const Ro
                    const double* cent,
                    double* out_dev);
 
+// The losses of R <= kMaxLossRuns runs over the same points in two launches: run r's
+// assignment is assign + r * astride, its centroids cent + coff[r] * kMaxKnobs.
+constexpr int kMaxLossRuns = 8;
+void pairwise_loss_runs(kt_engine* e, const uint64_t* pts, int64_t m, int n, const RowFmt& fmt, const uint8_t* assign,
+                        int64_t astride, const double* cent, const int* coff, int R, double* out_dev);
+
 // numpy sum of x[0..m) (center == nullptr) or of (x - *center)^2 (center: device scalar).
 void pairwise_sum(kt_engine* e, const double* x, int64_t m, const double* center, double* out_dev);
 

@@ -1760,9 +1760,7 @@ struct KmeansSession {
             } else {
                 // speculatively finish (no reseed is the common case): losses, pass counts and
                 // centroids come back with the launch state in one synchronisation
-                for (int r = 0; r < R; ++r)
-                    pairwise_loss(e, pts, m, n, fmt, a.assign + size_t(r) * a.stride,
-                                  a.cent + size_t(a.coff[r]) * kMaxKnobs, d_loss + r);
+                pairwise_loss_runs(e, pts, m, n, fmt, a.assign, a.stride, a.cent, a.coff, R, d_loss);
                 KT_CUDA(cudaMemcpyAsync(h_loss, d_loss, R * 8, cudaMemcpyDeviceToHost, e->stream));
                 KT_CUDA(cudaMemcpyAsync(h_iter, a.run_iter, R * 4, cudaMemcpyDeviceToHost, e->stream));
                 KT_CUDA(cudaMemcpyAsync(h_cent, a.cent, size_t(K) * kMaxKnobs * 8, cudaMemcpyDeviceToHost, e->stream));
@@ -1789,9 +1787,7 @@ struct KmeansSession {
         }
         std::vector<RunResult> out(R);
         if (history) {
-            for (int r = 0; r < R; ++r)
-                pairwise_loss(e, pts, m, n, fmt, a.assign + size_t(r) * a.stride,
-                              a.cent + size_t(a.coff[r]) * kMaxKnobs, d_loss + r);
+            pairwise_loss_runs(e, pts, m, n, fmt, a.assign, a.stride, a.cent, a.coff, R, d_loss);
             KT_CUDA(cudaMemcpyAsync(h_loss, d_loss, R * 8, cudaMemcpyDeviceToHost, e->stream));
             KT_CUDA(cudaMemcpyAsync(h_iter, a.run_iter, R * 4, cudaMemcpyDeviceToHost, e->stream));
             KT_CUDA(cudaMemcpyAsync(h_cent, a.cent, size_t(K) * kMaxKnobs * 8, cudaMemcpyDeviceToHost, e->stream));
