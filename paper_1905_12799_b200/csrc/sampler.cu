@@ -41,7 +41,7 @@ namespace kt {
 constexpr int kDedupRowsPerBlock = 1024;  // 256 threads x 4
 
 __global__ void dedup_insert_kernel(const uint64_t* __restrict__ rows, int64_t count, uint64_t* keys,
-                                    uint32_t* first, uint64_t mask) {
+                                    uint32_t* first, uint64_t mask, uint32_t* __restrict__ slot) {
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x) {
         const uint64_t key = rows[i];
         uint64_t h = mix64(key) & mask;
@@ -53,6 +53,7 @@ __global__ void dedup_insert_kernel(const uint64_t* __restrict__ rows, int64_t c
             }
             if (cur == key) {
                 atomicMin(&first[h], uint32_t(i));
+                slot[i] = uint32_t(h);  // the flag pass reads first[slot[i]] without probing again
                 break;
             }
             h = (h + 1) & mask;
@@ -60,17 +61,10 @@ __global__ void dedup_insert_kernel(const uint64_t* __restrict__ rows, int64_t c
     }
 }
 
-__device__ __forceinline__ uint32_t dedup_lookup_first(const uint64_t* keys, const uint32_t* first, uint64_t mask,
-                                                       uint64_t key) {
-    uint64_t h = mix64(key) & mask;
-    while (__ldcg(keys + h) != key) h = (h + 1) & mask;
-    return __ldcg(first + h);
-}
-
 // One block = 1024 rows: ballot bitmask of first occurrences + block count.
-__global__ void __launch_bounds__(256) dedup_flag_kernel(const uint64_t* __restrict__ rows, int64_t count,
-                                                         const uint64_t* keys, const uint32_t* first, uint64_t mask,
-                                                         uint32_t* bits, int64_t* block_counts) {
+__global__ void __launch_bounds__(256) dedup_flag_kernel(const uint32_t* __restrict__ slot, int64_t count,
+                                                         const uint32_t* first, uint32_t* bits,
+                                                         int64_t* block_counts) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t base = int64_t(blockIdx.x) * kDedupRowsPerBlock;
     int local = 0;
@@ -79,7 +73,7 @@ __global__ void __launch_bounds__(256) dedup_flag_kernel(const uint64_t* __restr
         const int64_t w0 = base + j * 256 + warp * 32;
         const int64_t i = w0 + lane;
         bool is_first = false;
-        if (i < count) is_first = dedup_lookup_first(keys, first, mask, rows[i]) == uint32_t(i);
+        if (i < count) is_first = __ldcg(first + slot[i]) == uint32_t(i);
         uint32_t b = __ballot_sync(0xffffffffu, is_first);
         if (lane == 0 && w0 < count) bits[w0 >> 5] = b;
         local += __popc(b);
@@ -174,10 +168,11 @@ int64_t dedup(kt_engine* e, const uint64_t* rows, int64_t count, uint64_t* out) 
     auto* offsets = static_cast<int64_t*>(e->scratch("dedup.offsets", size_t(nb + 1) * 8));
     int grid = int(std::min<int64_t>(ceil_div(count, 256), int64_t(e->num_sms) * 8));
     e->pre_launch("dedup_insert");
-    dedup_insert_kernel<<<grid, 256, 0, e->stream>>>(rows, count, keys, first, cap - 1);
+    auto* slot = static_cast<uint32_t*>(e->scratch("dedup.slot", size_t(count) * 4));
+    dedup_insert_kernel<<<grid, 256, 0, e->stream>>>(rows, count, keys, first, cap - 1, slot);
     e->check_launch("dedup_insert");
     e->pre_launch("dedup_flag");
-    dedup_flag_kernel<<<nb, 256, 0, e->stream>>>(rows, count, keys, first, cap - 1, bits, counts);
+    dedup_flag_kernel<<<nb, 256, 0, e->stream>>>(slot, count, first, bits, counts);
     e->check_launch("dedup_flag");
     exclusive_scan(e, counts, offsets, nb);
     e->pre_launch("dedup_scatter");
