@@ -538,14 +538,20 @@ __global__ void __launch_bounds__(kInitResThreads, 1) init_res_kernel(InitArgs a
 #pragma unroll
                 for (int off = 16; off > 0; off >>= 1) sum64 += __shfl_xor_sync(0xffffffffu, sum64, off);
             }
-            if (lane == 0 && i < np)  // a warp's 32 points lie in one sub-chunk
-                atomicAdd(reinterpret_cast<unsigned long long*>(s_sub + i / a.sub), (unsigned long long)sum64);
+            if (lane == 0 && i < np) {  // a warp's 32 points lie in one sub-chunk
+                if (BYTES)  // sub-chunk sums < 2048 * 2^19 < 2^32: native 32-bit shared atomics
+                    atomicAdd(reinterpret_cast<unsigned int*>(s_sub) + i / a.sub, unsigned(sum64));
+                else  // (64-bit shared atomicAdd is a CAS loop)
+                    atomicAdd(reinterpret_cast<unsigned long long*>(s_sub + i / a.sub), (unsigned long long)sum64);
+            }
         }
         __syncthreads();
         long long* snew = a.sums[j & 1];
         for (int i = tid; i < a.nsub; i += kInitResThreads) {
-            snew[int64_t(blockIdx.x) * a.nsub + i] = s_sub[i];
-            s_sub[i] = 0;
+            snew[int64_t(blockIdx.x) * a.nsub + i] =
+                BYTES ? (long long)reinterpret_cast<const unsigned int*>(s_sub)[i] : s_sub[i];
+            if (BYTES) reinterpret_cast<unsigned int*>(s_sub)[i] = 0;  // each thread clears what it read
+            else s_sub[i] = 0;
         }
         init_grid_barrier(a.barrier, ++n_bar * gridDim.x);
     }
