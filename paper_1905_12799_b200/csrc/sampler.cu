@@ -613,7 +613,7 @@ struct LloydArgs {
     int tile;                  // resident kernel: points per queue tile (multiple of 4)
     int rows_resident;         // resident kernel: the block's rows live in shared memory too
     int external;              // 1: one pass, deltas + changed counts -> ext, no in-kernel decisions
-    int pack3;                 // resident kernel, byte rows, P <= kPack3MaxP: 3-word cluster deltas
+    int pack3;                 // resident kernel, P * largest knob index < 2^21: 3-word cluster deltas
     unsigned int* barrier;     // grid-barrier counter, zeroed before every launch
     unsigned long long* ext;   // external: [K][9] int64 deltas then [R] changed counts (all-reduced by the host)
     double* cent;              // [K][8] centroids of the latest pass
@@ -843,11 +843,10 @@ __device__ __forceinline__ void packed_delta(unsigned long long* d, uint64_t row
     }
     atomicAdd(d + 4, sign > 0 ? 1ull : ~0ull);
 }
-// Byte rows, P <= kPack3MaxP: three 21-bit unsigned fields per 64-bit word, points joining a
-// cluster added to its words 0-2 and points leaving it to words 3-5 (each field's per-pass
-// block total <= P * 255 < 2^21, no carries between fields): 3 atomics per side instead of 5.
+// P * (largest knob index) < 2^21: three 21-bit unsigned fields per 64-bit word, points
+// joining a cluster added to its words 0-2 and points leaving it to words 3-5 (each field's
+// per-pass block total < 2^21, no carries between fields): 3 atomics per side instead of 5.
 constexpr int kPack3W = 6;
-constexpr int kPack3MaxP = 8224;  // 8224 * 255 < 2^21
 __device__ __forceinline__ void pack3_delta(unsigned long long* d, uint64_t row, int sign) {
     const unsigned long long m = 0xffull;
     const unsigned long long v0 = (row & m) | (((row >> 8) & m) << 21) | (((row >> 16) & m) << 42);
@@ -857,6 +856,18 @@ __device__ __forceinline__ void pack3_delta(unsigned long long* d, uint64_t row,
     atomicAdd(w, v0);
     atomicAdd(w + 1, v1);
     atomicAdd(w + 2, v2);
+}
+__device__ __forceinline__ void pack3_delta_fmt(unsigned long long* d, uint64_t row, int sign, int n,
+                                                const RowFmt& fmt) {
+    unsigned long long v[3] = {0ull, 0ull, 0ull};
+#pragma unroll
+    for (int c = 0; c < kMaxKnobs; ++c)
+        if (c < n) v[c / 3] |= (unsigned long long)fmt.get(row, c) << (21 * (c % 3));
+    v[2] |= 1ull << 42;
+    unsigned long long* w = d + (sign > 0 ? 0 : 3);
+    atomicAdd(w, v[0]);
+    atomicAdd(w + 1, v[1]);
+    atomicAdd(w + 2, v[2]);
 }
 __device__ __forceinline__ long long pack3_field(const unsigned long long* d, int c) {
     const int q = c / 3, sh = 21 * (c % 3);
@@ -1197,6 +1208,9 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
                                 if (BYTES && a.pack3) {
                                     pack3_delta(delta64 + gn * kPack3W, row[u], 1);
                                     if (old != 255) pack3_delta(delta64 + go * kPack3W, row[u], -1);
+                                } else if (!BYTES && a.pack3) {
+                                    pack3_delta_fmt(delta64 + gn * kPack3W, row[u], 1, n, fmt);
+                                    if (old != 255) pack3_delta_fmt(delta64 + go * kPack3W, row[u], -1, n, fmt);
                                 } else {
                                     packed_delta(delta64 + gn * kPackedW, row[u], 1, n, fmt);
                                     if (old != 255) packed_delta(delta64 + go * kPackedW, row[u], -1, n, fmt);
@@ -1303,7 +1317,7 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
                 }
             const long long v = (RESIDENT && kDeltaMode == 2) ? vw
                               : (RESIDENT && kDeltaMode == 0)
-                                  ? ((BYTES && a.pack3) ? pack3_field(delta64 + g * kPack3W, c) : packed_field(delta64 + g * kPackedW, c))
+                                  ? (a.pack3 ? pack3_field(delta64 + g * kPack3W, c) : packed_field(delta64 + g * kPackedW, c))
                                          : (long long)delta[g * kDeltaW + c] + (c < 8 ? 256ll * delta[g * kDeltaW + 9 + c] : 0ll);
             if (v) atomicAdd(Dcur + i, (unsigned long long)v);
         }
@@ -1557,7 +1571,9 @@ static LloydPlan plan_lloyd(kt_engine* e, int64_t m, int K, int R, LloydArgs& a)
         a.per_block = P;
         a.tile = int(tile);
         a.rows_resident = rows_res ? 1 : 0;
-        a.pack3 = (bytes && P <= kPack3MaxP && !std::getenv("KT_LLOYD_PACK5")) ? 1 : 0;
+        // byte rows: the byte kernel packs all 8 bytes (unused knobs are 0), field bound 255
+        const int64_t field_max = bytes ? 255 : std::max<int64_t>(1, a.fmt.cmax);
+        a.pack3 = (P * field_max < (int64_t(1) << 21) && !std::getenv("KT_LLOYD_PACK5")) ? 1 : 0;
         if (const char* t = std::getenv("KT_LLOYD_TILE"))  // tests: force many tiles per block
             a.tile = std::max(4, std::min(a.tile, std::atoi(t) & ~3));
     } else {
