@@ -33,7 +33,11 @@ METRIC = "candidate configs scored+clustered/sec per tuning step"
 UNIT = "candidates/s"
 WORKLOAD = ("resnet18.c2_3x3_64x64_56 space (S2: 84x80x80x7x2x2x3x2 = 90,316,800 configs); per step {n} "
             "uniform candidates -> K2 boosted-tree scores (50 trees, depth 4) + K6 dedup + K7/K8 knee k-means "
-            "(k=8..knee, seeded) + K9 mode + batch (predict + adaptive_sample)")
+            "(k=8..knee, seeded) + K9 mode vote + batch (predict + adaptive_sample); visited set per step = two of "
+            "the step's own rounded centroids (measured in an earlier round) + 62 earlier measurements, so batch "
+            "assembly takes the reference's mode branch (sampler.py:203-209) every step")
+GOLDEN = ROOT / "tests" / "golden" / "bench_golden.json"
+TRAFFIC_ROUND = "r1"  # profiles/<round>/traffic.json: ncu --set full DRAM bytes per launch
 
 
 def load_model():
@@ -106,24 +110,54 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------- CPU side
-def cpu_step(doc, idx: np.ndarray, seed: int):
+def bench_visited_rows(batch_rows: np.ndarray, cand_rows: np.ndarray) -> np.ndarray:
+    """The step's visited set (packed rows): the first two configurations of the step's own batch
+    without a visited set (rounded centroids 0 and 1, as if measured in an earlier round) and the
+    first 62 candidates, first occurrence kept — tests/golden/make_bench_golden.py:bench_visited."""
+    out, seen = [], set()
+    for r in list(np.asarray(batch_rows, dtype=np.uint64)[:2]) + list(np.asarray(cand_rows).view(np.uint64)[:62]):
+        if int(r) not in seen:
+            seen.add(int(r))
+            out.append(int(r))
+    return np.array(out, dtype=np.uint64)
+
+
+def cpu_step(doc, idx: np.ndarray, seed: int, visited_rows: bool = True):
     from oracle import sampler as osamp
     from oracle import trees as otrees
 
+    cards = [len(v) for v in doc["values"]]
     scores = otrees.predict_features(doc["model"], otrees.featurize_rows(doc["values"], idx))
-    batch = osamp.adaptive_sample(idx, set(), [len(v) for v in doc["values"]], seed)
+    batch, info = osamp.adaptive_sample(idx, set(), cards, seed, return_info=True)
+    if visited_rows and "result" in info:  # same visited construction as the GPU arm: mode branch
+        visited = {tuple(b) for b in batch[:2]} | {tuple(r) for r in idx[:62].tolist()}
+        batch, _ = osamp.assemble_batch(info["result"]["centroids"], idx, visited, cards)
     return scores, batch
 
 
-def cpu_baseline(doc, cards, n_sample: int, reps: int = 1) -> dict:
+def cpu_baseline(doc, cards, n_sample: int, reps: int = 1, full: int = 0) -> dict:
     idx = candidates(n_sample, 12345, cards)
     t0 = time.perf_counter()
     for r in range(reps):
         cpu_step(doc, idx, 7 + r)
     dt = (time.perf_counter() - t0) / reps
-    return {"value": n_sample / dt, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"{n_sample} uniform S2 candidates per step (oracle/ numpy restatement of "
-                      f"predict_features + adaptive_sample, single-threaded), {reps} step(s), {dt:.2f} s/step"}
+    out = {"value": n_sample / dt, "unit": UNIT, "cores": 1, "kind": "port",
+           "sample": f"{n_sample} uniform S2 candidates per step (oracle/ numpy restatement of "
+                     f"predict_features + adaptive_sample, single-threaded), {reps} step(s), {dt:.2f} s/step"}
+    if full:
+        out["full_size"] = cpu_full_size(doc, cards, full)
+    return out
+
+
+def cpu_full_size(doc, cards, n: int) -> dict:
+    """One step of the headline workload at its full size through the port on one core (~2 min)."""
+    idx = candidates(n, 0, cards)
+    t0 = time.perf_counter()
+    cpu_step(doc, idx, 1000)
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": UNIT, "cores": 1, "kind": "port", "candidates": n, "seconds": dt,
+            "sample": f"one full headline step: {n} uniform S2 candidates (rank 0's first set, seed 1000), "
+                      f"oracle numpy port, single-threaded"}
 
 
 # ------------------------------------------------- wall time to 95% best (metric 2)
@@ -226,12 +260,18 @@ def run_reference(args, rank: int, world: int) -> None:
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD.format(n=n), "candidates_per_step": n,
-                   "parallelism": f"{procs} host processes, one independent task each"},
+                   "parallelism": f"{procs} host processes, one independent task each",
+                   "same_config": False,
+                   "sample_vs_headline": f"bounded sample: {n} of the headline's {args.candidates} candidates per step "
+                                         f"(the port's per-candidate rate falls as the size grows, so this favours "
+                                         f"the CPU); cpu_baseline.full_size is one step at the headline size"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port",
                          "sample": f"{n} uniform S2 candidates per step per process, oracle numpy port "
                                    f"(predict_features + adaptive_sample), {procs} processes x {args.steps} steps"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if not args.no_cpu_full:  # one full-size step (the GPU arm's per-step workload) on one core
+        line["cpu_baseline"]["full_size"] = cpu_full_size(doc, cards, args.candidates)
     if not args.no_wall95:
         line["wall_to_95"] = w95_reference()
     print(json.dumps(line), flush=True)
@@ -270,17 +310,34 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     scores_buf = torch.empty(N, dtype=torch.float64, device=dev)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
 
-    def step(rows_dev, seed, info=None):
-        kt.predict_rows(model, space, rows_dev, out=scores_buf, engine=eng)
-        return kt.adaptive_sample_rows(rows_dev, no_visited, space, seed, engine=eng, info=info)
+    def step(rows_dev, seed, visited=no_visited, info=None, out=scores_buf):
+        kt.predict_rows(model, space, rows_dev, out=out, engine=eng)
+        return kt.adaptive_sample_rows(rows_dev, visited, space, seed, engine=eng, info=info)
 
-    def barrier():
-        torch.cuda.synchronize()
-        if dist is not None:
-            dist.barrier()
-
+    # untimed: each step's visited set, built from the same step computed without one ("an earlier
+    # round measured two of these centroids"), so every timed step runs the mode vote (K9)
+    seeds = {}
+    for base in (1000, 2000):
+        for s in range(args.steps):
+            nv = step(dev_sets[s % n_sets], base + s)
+            seeds[base + s] = bench_visited_rows(nv, host_sets[s % n_sets].numpy())
     for w in range(args.warmup):
-        step(dev_sets[w % n_sets], 50 + w)
+        step(dev_sets[w % n_sets], 1000 + w, seeds[1000 + w % args.steps])
+
+    # parity self-check (untimed) on rank 0's first set against the oracle golden of this exact step
+    parity = None
+    if rank == 0 and N == 1 << 20 and GOLDEN.exists():
+        g = json.loads(GOLDEN.read_text())["s2"]
+        pinfo = kt._lib.SampleInfo()
+        b0 = sp.unpack(step(dev_sets[0], g["seed"], info=pinfo), 8).tolist()
+        curve = [[pinfo.scanned_k[i], float(pinfo.scanned_loss[i]).hex()] for i in range(pinfo.n_scanned)]
+        vis = sp.pack(np.array(g["visited"], dtype=np.int64))
+        vinfo = kt._lib.SampleInfo()
+        b1 = sp.unpack(step(dev_sets[0], g["seed"], vis, info=vinfo), 8).tolist()
+        checks = {"distinct": pinfo.n_distinct == g["m"], "curve": curve == g["curve"], "batch": b0 == g["batch"],
+                  "batch_with_visited": b1 == g["batch_visited"], "mode_vote_ran": bool(vinfo.used_mode)}
+        parity = {"ok": all(checks.values()), **checks,
+                  "golden": "tests/golden/bench_golden.json[s2] (oracle, candidate seed 0, adaptive_sample seed 1000)"}
     barrier()
 
     # ---- timed region 1: device-resident inputs (value)
@@ -294,7 +351,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
             with eng.scope():
                 ev[s][0].record(eng.stream)
             info = kt._lib.SampleInfo()
-            step(dev_sets[s % n_sets], 1000 + s, info)
+            step(dev_sets[s % n_sets], 1000 + s, seeds[1000 + s], info)
             with eng.scope():
                 ev[s][1].record(eng.stream)
             infos.append(info)
@@ -305,11 +362,15 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
 
     # ---- timed region 2: end to end through the public API with host buffers.  One continuous
     # region over K steps: every step's candidate rows come from pinned host memory (a fresh H2D
-    # copy, never reused on the device) and its batch goes back to the host; the copy of step s+1
-    # runs on a copy stream while step s computes (double-buffered device rows).
+    # copy, never reused on the device), its float64 scores (predict's return value, 8 B per
+    # candidate) and its batch go back to the host; the copy of step s+1 runs on a copy stream
+    # while step s computes (double-buffered device rows and scores).
     copy_stream = torch.cuda.Stream(device=dev)
     bufs = [torch.empty(N, dtype=torch.int64, device=dev) for _ in range(2)]
+    sbufs = [torch.empty(N, dtype=torch.float64, device=dev) for _ in range(2)]
+    host_scores = [torch.empty(N, dtype=torch.float64).pin_memory() for _ in range(2)]
     ready = [torch.cuda.Event() for _ in range(2)]
+    scored = [torch.cuda.Event() for _ in range(2)]
     e2e_start, e2e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
     def upload(s):
@@ -327,9 +388,16 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         if s + 1 < args.steps:
             upload(s + 1)  # step s-1 has returned (host-synchronous), so its buffer is free
         eng.stream.wait_event(ready[s % 2])
-        batch = step(bufs[s % 2], 2000 + s)
-        d2h += batch.nbytes
+        kt.predict_rows(model, space, bufs[s % 2], out=sbufs[s % 2], engine=eng)
+        with eng.scope():
+            scored[s % 2].record(eng.stream)
+        with torch.cuda.stream(copy_stream):  # scores D2H overlaps the clustering of the same step
+            copy_stream.wait_event(scored[s % 2])
+            host_scores[s % 2].copy_(sbufs[s % 2], non_blocking=True)
+        batch = kt.adaptive_sample_rows(bufs[s % 2], seeds[2000 + s], space, 2000 + s, engine=eng)
+        d2h += batch.nbytes + N * 8
     with eng.scope():
+        eng.stream.wait_stream(copy_stream)
         e2e_end.record(eng.stream)
     barrier()
     t_e2e = e2e_start.elapsed_time(e2e_end) / 1e3
@@ -341,7 +409,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     for s in range(args.steps):
         flush.fill_(float(s))
         info = kt._lib.SampleInfo()
-        step(dev_sets[s % n_sets], 1000 + s, info)
+        step(dev_sets[s % n_sets], 1000 + s, seeds[1000 + s], info)
         kinfo.append(info)
     stats = eng.kernel_stats(reset=True)
     eng.set_timing(False)
@@ -374,13 +442,15 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         note = "no byte model"
     achieved = (alg_bytes / dom_count) / (dom_ms / dom_count / 1e3) / 1e9 if alg_bytes else None
     # DRAM traffic per launch of the same kernel from the committed ncu --set full capture
-    tr_doc = ROOT / "profiles" / "r1" / "traffic.json"
+    tr_doc = ROOT / "profiles" / TRAFFIC_ROUND / "traffic.json"
     traffic = None
     if tr_doc.exists():
         traffic = json.loads(tr_doc.read_text())["kernels"].get(dom_name, {}).get("dram_bytes_per_launch")
     kernel_table = {k: {"launches": c, "ms_total": round(ms, 4), "ms_per_step": round(ms / K, 4)}
                     for k, (c, ms) in sorted(stats.items(), key=lambda kv: -kv[1][1])}
-    base = cpu_baseline(doc, cards, args.cpu_sample) if not args.no_cpu_baseline else None
+    base = None
+    if not args.no_cpu_baseline:
+        base = cpu_baseline(doc, cards, args.cpu_sample, full=0 if args.no_cpu_full else N)
     chosen = sorted({i.chosen_k for i in infos})
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
@@ -391,18 +461,20 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                                 "region, every step's rows a fresh H2D copy from pinned host memory (overlapped with "
                                 "the previous step on a copy stream)",
                    "distinct_per_step": int(np.mean([i.n_distinct for i in infos])), "knee_k": chosen,
+                   "mode_vote_steps": int(sum(i.used_mode for i in infos)),
                    "lloyd_passes_per_step": float(np.mean([i.lloyd_passes for i in infos]))},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": N * 8, "d2h_bytes_per_step": d2h // K},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": (achieved / pk["hbm_gbs"]) if achieved else None, "traffic": traffic,
-                     "traffic_source": "profiles/r1/traffic.json (ncu --set full, bytes per launch)",
+                     "traffic_source": f"profiles/{TRAFFIC_ROUND}/traffic.json (ncu --set full, bytes per launch)",
                      "alg_bytes_per_launch": (alg_bytes / dom_count) if alg_bytes else None,
                      "peak_source": pk["source"], "bytes_model": note,
                      "kernel_share_of_step": dom_ms / sum(ms for _, ms in stats.values())},
         "kernels": kernel_table,
         "clocks": clk.summary(),
         "cpu_baseline": base,
+        "parity": parity,
     }
     if not args.no_wall95:
         line["wall_to_95"] = w95_ours(eng)
@@ -472,6 +544,7 @@ def main() -> None:
     ap.add_argument("--ref-sample", type=int, default=16384)
     ap.add_argument("--ref-procs", type=int, default=0, help="host processes for --impl reference (0: all cores)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cpu-full", action="store_true", help="skip the one full-size (1M) CPU step (~2 min)")
     ap.add_argument("--no-wall95", action="store_true", help="skip the wall-time-to-95%%-best tune runs")
     ap.add_argument("--workload", choices=("s2", "rl", "c4"), default="s2",
                     help="s2: the headline scored+clustered step; rl: 5 tasks x 4096 PPO agents per step; "

@@ -103,8 +103,8 @@ int kt_score_trees(kt_engine* e, const kt_forest* f, const uint64_t* rows_dev,
 
 /* ------------------------------------------------ landscape scoring (K3) */
 /* Replaces synthetic_runtime/_hash_unit (backends.py:157-174) and
- * SyntheticBackend.batch_runtimes (backends.py:272-273).  seed_text is
- * str(landscape.seed) (the blake2b payload prefix).                        */
+ * SyntheticBackend.batch_runtimes (backends.py:272-273), bit-exact (glibc's exp restated
+ * on the device).  seed_text is str(landscape.seed) (the blake2b payload prefix).                        */
 typedef struct kt_landscape kt_landscape;
 
 int kt_landscape_create(kt_engine* e, int n_knobs, const int32_t* cards, int n_centers, const int32_t* centers,
@@ -113,6 +113,11 @@ int kt_landscape_create(kt_engine* e, int n_knobs, const int32_t* cards, int n_c
 int kt_landscape_destroy(kt_landscape* l);
 int kt_score_landscape(kt_engine* e, const kt_landscape* l, const uint64_t* rows_dev,
                        int64_t count, double* runtime_dev);
+/* Brute-force optimum over the whole lattice (cli.py:77-90 _enumerated_oracle, without the
+ * enumerate_space cap of space.py:20): *best_runtime = the minimum runtime, *best_rank = its
+ * lexicographic rank in enumerate_space order (last knob fastest), the first one on ties. */
+int kt_landscape_best(kt_engine* e, const kt_landscape* l, const int32_t* cards,
+                      double* best_runtime, int64_t* best_rank);
 
 /* ---------------------------------------------------- adaptive sampling */
 /* First-occurrence dedup (sampler.py:187-192): distinct_dev receives the

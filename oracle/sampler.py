@@ -147,10 +147,18 @@ def adaptive_sample(idx: np.ndarray, visited: set, cards, seed: int,
         return (batch, info) if return_info else batch
     result, curve = knee_scan(uniq.astype(np.float64), seed, knee_constant)
     info.update(curve=curve, result=result)
+    batch, info["mode"] = assemble_batch(result["centroids"], idx, visited, cards)
+    return (batch, info) if return_info else batch
+
+
+def assemble_batch(centroids, idx: np.ndarray, visited: set, cards):
+    """Batch assembly of sampler.py:200-215: round each centroid; a visited one is replaced by the
+    trajectory's mode (computed once, lazily); visited modes and repeats are dropped.
+    Returns (batch, mode or None when the mode vote never ran)."""
     batch: list[tuple[int, ...]] = []
     taken: set = set()
     mode = None
-    for centroid in result["centroids"]:
+    for centroid in centroids:
         cand = round_centroid(centroid, cards)
         if cand in visited:
             if mode is None:
@@ -162,4 +170,4 @@ def adaptive_sample(idx: np.ndarray, visited: set, cards, seed: int,
             continue
         taken.add(cand)
         batch.append(cand)
-    return (batch, info) if return_info else batch
+    return batch, mode

@@ -6,8 +6,15 @@
 //   runtime = max(runtime, 0.01 * base)
 // |x - c_j|^2 is an integer (lattice points), so it is exact in any order; the
 // remaining float64 ops follow the reference's evaluation order with explicit
-// _rn intrinsics.  exp() is CUDA's (<= 1 ulp from glibc's), hence the
-// north-star tolerance for runtimes rather than bit equality.
+// _rn intrinsics, and exp() is a bit-exact restatement of glibc's (the
+// reference's math.exp; glibc_exp.cuh), so runtimes equal the reference's bit
+// for bit.
+//
+// kt_landscape_best: the brute-force optimum of cli.py:77-90 (_enumerated_oracle)
+// without the 10^6 enumeration cap (space.py:20): lexicographic ranks (last knob
+// fastest, enumerate_space's order) are decoded into rows on the fly, scored, and
+// reduced to (min runtime, lowest rank) — the first minimum, like the reference's
+// strict `<` scan.
 //
 // blake2b (RFC 7693), unkeyed, 8-byte digest, one 128-byte block: the payload
 // "seed:" + decimal indices joined by ',' is at most 21 + 1 + 8 * 4 bytes.
@@ -16,6 +23,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "glibc_exp.cuh"
 
 constexpr int kMaxCenters = 16;
 
@@ -92,43 +100,98 @@ __device__ __forceinline__ void put_byte(uint64_t m[16], int pos, unsigned v) {
     m[pos >> 3] |= uint64_t(v & 0xffu) << (8 * (pos & 7));
 }
 
+// runtime of one configuration row (backends.py:164-174); `tab` = the exp table in shared memory
+__device__ __forceinline__ double landscape_runtime(const LandscapeArgs& a, uint64_t row, const uint64_t* tab) {
+    double depth_term = 0.0;
+    for (int j = 0; j < a.n_centers; ++j) {
+        int64_t d2 = 0;  // exact: numpy's ((x - c) ** 2).sum() of integer-valued float64
+        for (int q = 0; q < a.n; ++q) {
+            const int64_t d = a.fmt.get(row, q) - a.centers[j][q];
+            d2 += d * d;
+        }
+        const double e = glibc_exp(__ddiv_rn(-double(d2), a.r2[j]), tab);
+        depth_term = __dadd_rn(depth_term, __dmul_rn(a.depths[j], e));
+    }
+    double rt = __dmul_rn(a.base, __dsub_rn(1.0, depth_term));
+    if (a.noise > 0.0) {
+        uint64_t m[16];
+#pragma unroll
+        for (int w = 0; w < 16; ++w) m[w] = 0;
+        int pos = 0;
+        for (; pos < a.prefix_len; ++pos) put_byte(m, pos, a.prefix[pos]);
+        for (int q = 0; q < a.n; ++q) {
+            if (q) put_byte(m, pos++, ',');
+            const int v = a.fmt.get(row, q);  // str(v): up to 5 digits
+            if (v >= 10000) put_byte(m, pos++, '0' + v / 10000);
+            if (v >= 1000) put_byte(m, pos++, '0' + (v / 1000) % 10);
+            if (v >= 100) put_byte(m, pos++, '0' + (v / 100) % 10);
+            if (v >= 10) put_byte(m, pos++, '0' + (v / 10) % 10);
+            put_byte(m, pos++, '0' + v % 10);
+        }
+        const uint64_t h = blake2b64_one_block(m, uint64_t(pos));
+        const uint64_t word = __byte_perm(uint32_t(h >> 32), 0, 0x0123) | (uint64_t(__byte_perm(uint32_t(h), 0, 0x0123)) << 32);
+        const double unit = __dsub_rn(2.0 * (__ull2double_rn(word) * 5.421010862427522e-20), 1.0);  // 2^-64
+        rt = __dmul_rn(rt, __dadd_rn(1.0, __dmul_rn(a.noise, unit)));
+    }
+    const double floor_rt = __dmul_rn(0.01, a.base);
+    return floor_rt > rt ? floor_rt : rt;
+}
+
+__device__ __forceinline__ void load_exp_table(uint64_t* tab) {
+    for (int i = threadIdx.x; i < 2 * kExpN; i += blockDim.x) tab[i] = kExpTableConst[i];
+    __syncthreads();
+}
+
 __global__ void __launch_bounds__(256) landscape_kernel(const LandscapeArgs a, const uint64_t* __restrict__ rows,
                                                         int64_t count, double* __restrict__ out) {
-    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x) {
-        const uint64_t row = rows[i];
-        double depth_term = 0.0;
-        for (int j = 0; j < a.n_centers; ++j) {
-            int64_t d2 = 0;  // exact: numpy's int64 ((x - c) ** 2).sum()
-            for (int q = 0; q < a.n; ++q) {
-                const int64_t d = a.fmt.get(row, q) - a.centers[j][q];
-                d2 += d * d;
-            }
-            const double e = exp(__ddiv_rn(-double(d2), a.r2[j]));
-            depth_term = __dadd_rn(depth_term, __dmul_rn(a.depths[j], e));
-        }
-        double rt = __dmul_rn(a.base, __dsub_rn(1.0, depth_term));
-        if (a.noise > 0.0) {
-            uint64_t m[16];
+    __shared__ uint64_t tab[2 * kExpN];
+    load_exp_table(tab);
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x)
+        out[i] = landscape_runtime(a, rows[i], tab);
+}
+
+struct EnumArgs {
+    int64_t stride[kMaxKnobs];  // lexicographic rank strides, last knob fastest
+    int32_t card[kMaxKnobs];
+};
+
+// (runtime, rank) order: smaller runtime first, then the lower rank (the first minimum)
+__device__ __forceinline__ bool better(double v, int64_t r, double bv, int64_t br) {
+    return v < bv || (v == bv && r < br);
+}
+
+constexpr int kBestThreads = 256;
+
+// Grid-stride over ranks [lo, hi); each block writes its best (runtime, rank) pair.
+__global__ void __launch_bounds__(kBestThreads) landscape_best_kernel(const LandscapeArgs a, const EnumArgs en,
+                                                                     int64_t lo, int64_t hi, double* __restrict__ bv_out,
+                                                                     int64_t* __restrict__ br_out) {
+    __shared__ uint64_t tab[2 * kExpN];
+    __shared__ double s_v[kBestThreads / 32];
+    __shared__ int64_t s_r[kBestThreads / 32];
+    load_exp_table(tab);
+    double bv = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+    int64_t br = INT64_MAX;
+    for (int64_t r = lo + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < hi; r += int64_t(gridDim.x) * blockDim.x) {
+        uint64_t row = 0;
+        for (int q = 0; q < a.n; ++q) row = a.fmt.set(row, q, int((r / en.stride[q]) % en.card[q]));
+        const double v = landscape_runtime(a, row, tab);
+        if (better(v, r, bv, br)) { bv = v; br = r; }
+    }
 #pragma unroll
-            for (int w = 0; w < 16; ++w) m[w] = 0;
-            int pos = 0;
-            for (; pos < a.prefix_len; ++pos) put_byte(m, pos, a.prefix[pos]);
-            for (int q = 0; q < a.n; ++q) {
-                if (q) put_byte(m, pos++, ',');
-                const int v = a.fmt.get(row, q);  // str(v): up to 5 digits
-                if (v >= 10000) put_byte(m, pos++, '0' + v / 10000);
-                if (v >= 1000) put_byte(m, pos++, '0' + (v / 1000) % 10);
-                if (v >= 100) put_byte(m, pos++, '0' + (v / 100) % 10);
-                if (v >= 10) put_byte(m, pos++, '0' + (v / 10) % 10);
-                put_byte(m, pos++, '0' + v % 10);
-            }
-            const uint64_t h = blake2b64_one_block(m, uint64_t(pos));
-            const uint64_t word = __byte_perm(uint32_t(h >> 32), 0, 0x0123) | (uint64_t(__byte_perm(uint32_t(h), 0, 0x0123)) << 32);
-            const double unit = __dsub_rn(2.0 * (__ull2double_rn(word) * 5.421010862427522e-20), 1.0);  // 2^-64
-            rt = __dmul_rn(rt, __dadd_rn(1.0, __dmul_rn(a.noise, unit)));
-        }
-        const double floor_rt = __dmul_rn(0.01, a.base);
-        out[i] = floor_rt > rt ? floor_rt : rt;
+    for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int64_t orr = __shfl_xor_sync(0xffffffffu, br, o);
+        if (better(ov, orr, bv, br)) { bv = ov; br = orr; }
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) { s_v[w] = bv; s_r[w] = br; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < kBestThreads / 32; ++i)
+            if (better(s_v[i], s_r[i], bv, br)) { bv = s_v[i]; br = s_r[i]; }
+        bv_out[blockIdx.x] = bv;
+        br_out[blockIdx.x] = br;
     }
 }
 
@@ -172,11 +235,10 @@ int kt_landscape_destroy(kt_landscape* l) {
     return KT_OK;
 }
 
-int kt_score_landscape(kt_engine* e, const kt_landscape* l, const uint64_t* rows_dev, int64_t count,
-                       double* runtime_dev) {
-    KT_API_BEGIN
-    using namespace kt;
-    if (count <= 0) return KT_OK;
+}  // extern "C"
+
+namespace kt {
+static LandscapeArgs landscape_args(const kt_landscape* l) {
     LandscapeArgs a{};
     a.n = l->n;
     a.fmt = l->fmt;
@@ -190,10 +252,63 @@ int kt_score_landscape(kt_engine* e, const kt_landscape* l, const uint64_t* rows
         a.depths[j] = l->depths[j];
         a.r2[j] = l->radii[j] * l->radii[j];
     }
+    return a;
+}
+}  // namespace kt
+
+extern "C" {
+
+int kt_score_landscape(kt_engine* e, const kt_landscape* l, const uint64_t* rows_dev, int64_t count,
+                       double* runtime_dev) {
+    KT_API_BEGIN
+    using namespace kt;
+    if (count <= 0) return KT_OK;
+    const LandscapeArgs a = landscape_args(l);
     const int grid = int(std::min<int64_t>(ceil_div(count, 256), int64_t(e->num_sms) * 8));
     e->pre_launch("score_landscape");
     landscape_kernel<<<grid, 256, 0, e->stream>>>(a, rows_dev, count, runtime_dev);
     e->check_launch("score_landscape");
+    KT_API_END
+}
+
+int kt_landscape_best(kt_engine* e, const kt_landscape* l, const int32_t* cards, double* best_runtime,
+                      int64_t* best_rank) {
+    KT_API_BEGIN
+    using namespace kt;
+    const LandscapeArgs a = landscape_args(l);
+    EnumArgs en{};
+    int64_t total = 1;
+    for (int q = a.n - 1; q >= 0; --q) {
+        if (cards[q] < 1) fail(KT_ERR_VALUE, "cardinalities must be positive");
+        en.stride[q] = total;
+        en.card[q] = cards[q];
+        if (total > INT64_MAX / cards[q]) fail(KT_ERR_UNSUPPORTED, "space too large to enumerate");
+        total *= cards[q];
+    }
+    const int grid = e->num_sms * 8;
+    auto* bv = static_cast<double*>(e->scratch("landscape.best", size_t(grid) * 16));
+    auto* br = reinterpret_cast<int64_t*>(bv + grid);
+    std::vector<double> hv(grid);
+    std::vector<int64_t> hr(grid);
+    double best_v = INFINITY;
+    int64_t best_r = -1;
+    constexpr int64_t kChunk = int64_t(1) << 30;  // bounded launches (watchdog-free, host can interleave)
+    for (int64_t lo = 0; lo < total; lo += kChunk) {
+        const int64_t hi = std::min(total, lo + kChunk);
+        e->pre_launch("landscape_best");
+        landscape_best_kernel<<<grid, kBestThreads, 0, e->stream>>>(a, en, lo, hi, bv, br);
+        e->check_launch("landscape_best");
+        KT_CUDA(cudaMemcpyAsync(hv.data(), bv, size_t(grid) * 8, cudaMemcpyDeviceToHost, e->stream));
+        KT_CUDA(cudaMemcpyAsync(hr.data(), br, size_t(grid) * 8, cudaMemcpyDeviceToHost, e->stream));
+        e->sync();
+        for (int b = 0; b < grid; ++b)
+            if (hr[b] >= 0 && hr[b] != INT64_MAX && (hv[b] < best_v || (hv[b] == best_v && hr[b] < best_r))) {
+                best_v = hv[b];
+                best_r = hr[b];
+            }
+    }
+    *best_runtime = best_v;
+    *best_rank = best_r;
     KT_API_END
 }
 

@@ -144,36 +144,25 @@ class SyntheticBackend:
         return batch_runtimes(self.landscape, list(configs))
 
 
-def best_runtime(landscape, chunk: int = 1 << 24):
-    """Brute-force optimum over the whole lattice (cli.py:77-90 without the 10^6 cap).
+def best_runtime(landscape):
+    """Brute-force optimum over the whole lattice (cli.py:77-90 ``_enumerated_oracle``, without the
+    10^6 cap of ``enumerate_space``, space.py:20), fused on the device: ranks decoded into rows in the
+    space's own row layout, scored, reduced to the first minimum (``kt_landscape_best``).
 
-    Returns (min runtime, argmin row as an index tuple); lexicographic order
-    breaks ties like ``enumerate_space`` + ``min``.
+    Returns (min runtime, argmin as an index tuple); the first minimum in ``enumerate_space`` order
+    (last knob fastest) wins ties, like the reference's strict ``<`` scan.
     """
-    import torch
-
     engine = _lib.engine()
-    cards = np.asarray(landscape.space.cardinalities, dtype=np.int64)
-    total = int(np.prod(cards))
-    # strides for lexicographic rank: last knob fastest
-    strides = np.ones(cards.size, dtype=np.int64)
-    for i in range(cards.size - 2, -1, -1):
-        strides[i] = strides[i + 1] * cards[i + 1]
-    best_v, best_rank = np.inf, -1
-    dev = f"cuda:{engine.device}"
+    d = device_landscape(landscape, engine)
+    cards = sp.check_engine_space(landscape.space)
+    best = _lib.C.c_double(0.0)
+    rank = _lib.C.c_int64(-1)
     with engine.scope():
-        c_t = torch.as_tensor(cards, device=dev)
-        s_t = torch.as_tensor(strides, device=dev)
-        shift = torch.arange(cards.size, device=dev, dtype=torch.int64) * 8
-        for lo in range(0, total, chunk):
-            hi = min(total, lo + chunk)
-            rank = torch.arange(lo, hi, device=dev, dtype=torch.int64)
-            idx = (rank[:, None] // s_t[None, :]) % c_t[None, :]
-            rows = (idx << shift[None, :]).sum(dim=1)
-            rt = runtimes_rows(landscape, rows, engine=engine)
-            v, j = torch.min(rt, dim=0)
-            v = float(v)
-            if v < best_v:
-                best_v, best_rank = v, lo + int(j)
-    idx = tuple(int((best_rank // strides[i]) % cards[i]) for i in range(cards.size))
-    return best_v, idx
+        _lib.call("kt_landscape_best", engine.handle, d.handle, _lib.as_ptr(cards, _lib.C.c_int32),
+                  _lib.C.byref(best), _lib.C.byref(rank))
+    r = int(rank.value)
+    idx = []
+    for c in reversed(cards.tolist()):
+        idx.append(r % c)
+        r //= c
+    return float(best.value), tuple(reversed(idx))

@@ -42,7 +42,11 @@ def steps_to_convergence(scores, window: int = CONVERGENCE_WINDOW) -> int:
 
 
 def per_step_best(trajectory) -> list[float]:
+    """report.py:53-69 for our array-backed Trajectory and for the reference's own (which carries
+    ``step_indices`` as a tuple and ``scores()`` / ``entries``; install() rebinds this name)."""
     steps = getattr(trajectory, "_steps", None)
+    if steps is None:
+        steps = getattr(trajectory, "step_indices", None)
     if steps is None:
         raise ValueError("trajectory does not carry step indices")
     import torch
@@ -54,7 +58,9 @@ def per_step_best(trajectory) -> list[float]:
         st = st.to(dev).to(torch.int32)
         sc = trajectory.scores_device() if hasattr(trajectory, "scores_device") else None
         if sc is None:
-            sc = torch.as_tensor(np.asarray(trajectory.scores(), dtype=np.float64))
+            host = (trajectory.scores() if hasattr(trajectory, "scores")
+                    else [s for _, s in trajectory.entries])
+            sc = torch.as_tensor(np.asarray(host, dtype=np.float64))
         sc = sc.to(dev).to(torch.float64)
     cap = int(st.max().item()) + 1
     best = np.zeros(cap, dtype=np.float64)

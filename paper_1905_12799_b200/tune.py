@@ -15,15 +15,16 @@ the landscape, ``landscape.best_runtime``).
 
 from __future__ import annotations
 
+import math
 import time
 from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import _lib
+from . import _lib, errors
 from . import space as sp
 from .agent import AgentHyperparams, init_agent, run_search_rows
-from .cost_model import BoostParams, CostModel, feature_table, fit
+from .cost_model import BoostParams, CostModel, feature_table, fit, predict_rows
 from .landscape import runtimes_rows
 from .sa import SAParams, run_sa_rows
 from .sampler import adaptive_sample_rows
@@ -101,7 +102,8 @@ class TuneRun:
 
     @property
     def best_fitness(self) -> float:
-        return max(1.0 / r for r in self.runtimes)
+        ok = [1.0 / r for r in self.runtimes if math.isfinite(r) and r > 0]
+        return max(ok) if ok else 0.0
 
     def wall_to_fraction(self, f_star: float, frac: float = 0.95):
         """Seconds until best-so-far fitness >= frac * f_star (None if never reached)."""
@@ -119,9 +121,11 @@ def tune_rows(space, landscape, strategy: str, budget: int, seed: int = 0,
 
     ``runtimes(batch) -> runtimes`` overrides the K3 landscape measurement (the reference's
     ``replay:LOG`` backend, backends.py:300-345, is the analogous hook): tests replay the
-    reference's own measured runtimes, because CUDA's exp differs from glibc's by <= 1 ulp
-    and a tune loop amplifies any last-bit difference into a different trajectory.
+    reference's own measured runtimes, and inject failures (inf / non-positive runtimes).
     ``stop_fitness``: stop once best-so-far fitness reaches it (wall-time-to-95% harness).
+    Failed measurements (non-finite or non-positive runtime) follow MeasurementRecord
+    (backends.py:54-71): runtime inf, fitness 0, left out of the refit (``_fit_model``,
+    driver.py:142-148) and ranked by the surrogate in the RL restart (driver.py:118-139).
     """
     import torch
 
@@ -147,6 +151,7 @@ def tune_rows(space, landscape, strategy: str, budget: int, seed: int = 0,
     m_rows = np.zeros(cap, dtype=np.uint64)
     m_feat = np.zeros((cap, n), dtype=np.float64)
     m_fit = np.zeros(cap, dtype=np.float64)
+    m_ok = np.zeros(cap, dtype=bool)
     m_cnt = 0
     knob_ix = np.arange(n)
 
@@ -160,14 +165,18 @@ def tune_rows(space, landscape, strategy: str, budget: int, seed: int = 0,
             rows = torch.from_numpy(packed.view(np.int64)).to(dev)
             rt = runtimes_rows(landscape, rows, engine=eng).cpu().numpy()
         k = len(batch)
+        ok = np.isfinite(rt) & (rt > 0)  # make_record, backends.py:61-67
+        rt = np.where(ok, rt, np.inf)
         m_rows[m_cnt:m_cnt + k] = packed
         m_feat[m_cnt:m_cnt + k] = table[knob_ix, idx]
-        m_fit[m_cnt:m_cnt + k] = 1.0 / rt
+        m_fit[m_cnt:m_cnt + k] = np.where(ok, 1.0 / np.where(ok, rt, 1.0), 0.0)
+        m_ok[m_cnt:m_cnt + k] = ok
         m_cnt += k
         run.configs.extend(batch)
         run.runtimes.extend(rt.tolist())
         visited.update(batch)
-        best = max(best, float(np.max(1.0 / rt)))
+        if ok.any():
+            best = max(best, float(np.max(m_fit[m_cnt - k:m_cnt])))
         run.trace.append((clock() - t0, len(run.configs), best))
 
     agent = init_agent(space, agent_params, seed) if strategy in ("rl", "rl+as") else None
@@ -181,10 +190,17 @@ def tune_rows(space, landscape, strategy: str, budget: int, seed: int = 0,
         remaining = budget - len(run.configs)
         traj = None
         if strategy in ("rl", "rl+as", "sa", "sa+as"):
-            fitness = m_fit[:m_cnt]
-            model = fit(_TS(m_feat[:m_cnt], fitness), boost_params)  # _fit_model, driver.py:142-148
+            ok = m_ok[:m_cnt]
+            if ok.any():  # _fit_model, driver.py:142-148: successful records only
+                model = fit(_TS(m_feat[:m_cnt][ok], m_fit[:m_cnt][ok]), boost_params)
+            else:
+                model = CostModel.sentinel(n)
             if strategy.startswith("rl"):
-                order = np.argsort(-fitness, kind="stable")  # _restart_configs, driver.py:118-139
+                fitness = m_fit[:m_cnt].copy()  # _restart_configs, driver.py:118-139
+                if not ok.all():  # failed records are ranked by the surrogate
+                    frows = torch.from_numpy(m_rows[:m_cnt][~ok].view(np.int64)).to(dev)
+                    fitness[~ok] = predict_rows(model, space, frows, engine=eng).cpu().numpy()
+                order = np.argsort(-fitness, kind="stable")
                 starts = [run.configs[int(i)] for i in order[: agent_params.episodes_per_round]]
                 while len(starts) < agent_params.episodes_per_round:
                     starts.append(random_config(cards, rng))
@@ -210,6 +226,9 @@ def tune_rows(space, landscape, strategy: str, budget: int, seed: int = 0,
         rounds += 1
     run.rounds = rounds
     run.seconds = clock() - t0
+    if m_cnt and not m_ok[:m_cnt].any():  # driver.py:229-233
+        raise errors.NoValidResultError(
+            f"no successful measurement in {m_cnt} attempts; cannot report a best configuration")
     return run
 
 

@@ -88,7 +88,40 @@ def test_landscape_vs_reference(name):
     g = npz("landscape")
     got = kt.runtimes_rows(land, dev_rows(g[f"{name}/idx"])).cpu().numpy()
     want = g[f"{name}/runtime"]
-    np.testing.assert_allclose(got, want, rtol=1e-12, atol=0)
+    assert np.array_equal(got, want)  # bit-exact: glibc's exp restated on the device
+
+
+BEST = json.loads((GOLDEN / "best.json").read_text())
+
+
+@pytest.mark.parametrize("case", BEST, ids=lambda c: c["name"])
+def test_landscape_best_vs_reference_enumeration(case):
+    """kt_landscape_best == the reference's _enumerated_oracle (cli.py:77-90) on byte and bit-field
+    row layouts; sampled runtimes bit-exact (tests/golden/make_best.py)."""
+    space = kt.space_from_dict(case["space"])
+    land = kt.landscape.landscape_from_dict(case["landscape"], space)
+    best, arg = kt.best_runtime(land)
+    assert float(best).hex() == case["best_runtime"]
+    assert list(arg) == case["best_indices"]
+    idx = np.array(case["sample_idx"])
+    rows = torch.from_numpy(sp.pack(idx, np.array(space.cardinalities)).view(np.int64)).cuda()
+    got = kt.runtimes_rows(land, rows).cpu().numpy()
+    assert [float(x).hex() for x in got] == case["sample_runtime"]
+
+
+def test_landscape_runtimes_random_vs_oracle():
+    """200K random S2 configurations against the oracle (math.exp): bit-exact."""
+    m = MODELS["s2_resnet18"]
+    space = space_of(m["values"])
+    land = kt.SyntheticLandscape(seed=77, space=space, centers=((10, 5, 70, 3, 1, 0, 2, 1), (80, 40, 2, 6, 0, 1, 0, 0)),
+                                 depths=(0.6, 0.3), radii=(9.5, 31.25), noise_rel=0.02)
+    rng = np.random.default_rng(12)
+    idx = rng.integers(0, np.array(space.cardinalities), size=(200_000, 8))
+    got = kt.runtimes_rows(land, dev_rows(idx)).cpu().numpy()
+    doc = {"seed": 77, "centers": [list(c) for c in land.centers], "depths": list(land.depths),
+           "radii": list(land.radii), "base_runtime": 1.0, "noise_rel": 0.02}
+    want = oland.synthetic_runtimes(doc, idx)
+    assert np.array_equal(got, want)
 
 
 def test_landscape_hash_noise_bit_pattern():
@@ -175,7 +208,7 @@ def test_adaptive_sample_uniform_s2_vs_oracle(seed):
     assert [tuple(r) for r in sp.unpack(got, 8).tolist()] == want
 
 
-@pytest.mark.parametrize("mode", ["stream", "tile64", "gather", "init_chunked"])
+@pytest.mark.parametrize("mode", ["stream", "tile64", "gather", "init_chunked", "pack5"])
 @pytest.mark.parametrize("seed", [0, 1, 2])
 def test_lloyd_variants_vs_oracle(mode, seed, monkeypatch):
     """Both Lloyd kernels (streaming, and resident with many queue tiles per block) and both k-means++
@@ -186,6 +219,8 @@ def test_lloyd_variants_vs_oracle(mode, seed, monkeypatch):
         monkeypatch.setenv("KT_LLOYD_MODE", "stream")
     elif mode == "gather":
         monkeypatch.setenv("KT_LLOYD_ROWS", "global")
+    elif mode == "pack5":
+        monkeypatch.setenv("KT_LLOYD_PACK5", "1")
     else:
         monkeypatch.setenv("KT_LLOYD_TILE", "64")
     test_kmeans_random_lattice_vs_oracle(seed)
@@ -195,20 +230,19 @@ def test_lloyd_variants_vs_oracle(mode, seed, monkeypatch):
 LARGE = json.loads((GOLDEN / "large.json").read_text())
 
 
-@pytest.mark.parametrize("mode", ["resident", "stream", "tile64", "gather", "init_chunked"])
+LLOYD_MODES = {"resident": {}, "stream": {"KT_LLOYD_MODE": "stream"}, "tile64": {"KT_LLOYD_TILE": "64"},
+               "gather": {"KT_LLOYD_ROWS": "global"}, "init_chunked": {"KT_INIT_MODE": "chunked"},
+               "pack5": {"KT_LLOYD_PACK5": "1"}}
+
+
+@pytest.mark.parametrize("mode", sorted(LLOYD_MODES))
 @pytest.mark.parametrize("name", sorted(LARGE))
 def test_knee_large_vs_oracle_golden(name, mode, monkeypatch):
     """131K / 262K candidates (config C3 size): knee curve, centroids, assignment and batch bit-exact."""
     import hashlib
 
-    if mode == "init_chunked":
-        monkeypatch.setenv("KT_INIT_MODE", "chunked")
-    elif mode == "stream":
-        monkeypatch.setenv("KT_LLOYD_MODE", "stream")
-    elif mode == "tile64":
-        monkeypatch.setenv("KT_LLOYD_TILE", "64")
-    elif mode == "gather":
-        monkeypatch.setenv("KT_LLOYD_ROWS", "global")
+    for k, v in LLOYD_MODES[mode].items():
+        monkeypatch.setenv(k, v)
     g = LARGE[name]
     space = space_of(MODELS["s2_resnet18"]["values"])
     cards = np.array(space.cardinalities)
@@ -285,3 +319,48 @@ def test_sa_errors():
         kt.run_sa_round(kt.SAParams(), model, space, [], 0)
     with pytest.raises(ValueError, match="chains"):
         kt.SAParams(chains=0)
+
+
+BENCH_G = json.loads((GOLDEN / "bench_golden.json").read_text())
+
+
+def _bench_case(name, mode, monkeypatch):
+    import hashlib
+
+    for k, v in LLOYD_MODES[mode].items():
+        monkeypatch.setenv(k, v)
+    g = BENCH_G[name]
+    space = space_of(MODELS["s2_resnet18"]["values"])
+    cards = np.array(space.cardinalities)
+    idx = np.random.default_rng(g["cand_seed"]).integers(0, cards, size=(g["n"], cards.size))
+    rows = dev_rows(idx)
+    info = kt._lib.SampleInfo()
+    got = kt.adaptive_sample_rows(rows, np.zeros(0, dtype=np.uint64), space, seed=g["seed"], info=info)
+    assert info.n_distinct == g["m"]
+    assert [[info.scanned_k[i], float(info.scanned_loss[i]).hex()] for i in range(info.n_scanned)] == g["curve"]
+    assert sp.unpack(got, 8).tolist() == g["batch"]
+    vinfo = kt._lib.SampleInfo()
+    got_v = kt.adaptive_sample_rows(rows, sp.pack(np.array(g["visited"])), space, seed=g["seed"], info=vinfo)
+    assert sp.unpack(got_v, 8).tolist() == g["batch_visited"]
+    assert bool(vinfo.used_mode) == (g["mode"] is not None)
+    uniq = osamp.distinct_rows(idx)
+    res, curve = kt.knee_scan(uniq.astype(np.float64), g["seed"])
+    assert [[k, float(x).hex()] for k, x in curve] == g["curve"]
+    assert [[float(x).hex() for x in c] for c in res.centroids] == g["centroids"]
+    asg = np.asarray(res.assignment, dtype=np.int64)
+    assert hashlib.sha256(asg.tobytes()).hexdigest() == g["assignment_sha256"]
+
+
+@pytest.mark.parametrize("mode", ["resident", "tile64", "pack5"])
+def test_bench_headline_config_bit_exact(mode, monkeypatch):
+    """bench.py's exact headline step (1,048,576 uniform S2 candidates, candidate seed 0, seed 1000):
+    distinct count, knee curve, centroids, assignment, batch with and without the bench's visited set
+    (mode vote) bit-exact vs the oracle (tests/golden/make_bench_golden.py)."""
+    _bench_case("s2", mode, monkeypatch)
+
+
+def test_c5_4m_candidates_streaming_bit_exact(monkeypatch):
+    """configs[4]'s large end: 4,194,304 candidates (~4M distinct points, streaming Lloyd kernel)."""
+    if "c5" not in BENCH_G:
+        pytest.skip("c5 golden not generated (tests/golden/make_bench_golden.py c5)")
+    _bench_case("c5", "resident", monkeypatch)

@@ -51,3 +51,33 @@ def test_report_errors():
                        n_knobs=2)
     with pytest.raises(ValueError, match="step indices"):
         report.per_step_best(tr)
+
+
+def test_per_step_best_accepts_reference_trajectory():
+    """install() rebinds knobtuner.report.per_step_best: the reference's own Trajectory (a frozen
+    dataclass with ``entries`` and a ``step_indices`` tuple, agent.py:100-127) must work too."""
+    from dataclasses import dataclass
+
+    @dataclass(frozen=True)
+    class RefConfiguration:
+        indices: tuple
+
+    @dataclass(frozen=True)
+    class RefTrajectory:
+        entries: tuple
+        step_indices: tuple | None = None
+
+        def configs(self):
+            return [c for c, _ in self.entries]
+
+        def scores(self):
+            return np.array([s for _, s in self.entries], dtype=np.float64)
+
+    case = GOLD[0]
+    idx, scores, steps = case_inputs(case["seed"], case["N"], case["S"], case["n"], case["card"])
+    tr = RefTrajectory(tuple((RefConfiguration(tuple(r)), float(s)) for r, s in zip(idx.tolist(), scores.tolist())),
+                       tuple(int(s) for s in steps.tolist()))
+    assert [float(x).hex() for x in report.per_step_best(tr)] == case["per_step_best"]
+    assert report.convergence_steps_for_round(tr) == case["convergence"]
+    with pytest.raises(ValueError, match="step indices"):
+        report.per_step_best(RefTrajectory(tr.entries, None))

@@ -3,8 +3,8 @@
 sa+as / sa / random, replaying the reference's measured runtimes (its ``replay:`` backend idea):
 every measured configuration equals the reference's tune log — the loop, its RNG streams, the
 refit, the SA chains and the adaptive sampler agree bit for bit.  With the on-device K3
-landscape the runtimes agree to <= 1 ulp (CUDA vs glibc exp) and the runs agree until the
-first such difference feeds a refit.  rl+as: the bootstrap and the first search round's batch are exact; later
+landscape (glibc's exp restated bit-exactly) the whole run, runtimes included, equals the
+reference's log too.  rl+as: the bootstrap and the first search round's batch are exact; later
 rounds follow the PPO update, which the north star holds to the TF32 tier, so only the
 budget accounting is checked there.
 """
@@ -29,7 +29,27 @@ G = json.loads((GOLDEN / "tune.json").read_text())
 SPACE = kt.space_from_dict(G["space"])
 
 
-@pytest.mark.parametrize("case", G["cases"], ids=lambda c: f"{c['strategy']}_b{c['budget']}_s{c['seed']}")
+CLEAN = [c for c in G["cases"] if "fail_mod" not in c]
+FAILING = [c for c in G["cases"] if "fail_mod" in c]
+
+
+@pytest.mark.parametrize("case", FAILING, ids=lambda c: f"{c['strategy']}_fail{c['fail_mod']}_{c['fail_value']}")
+def test_tune_with_failed_measurements_matches_reference(case):
+    """Failed measurements (inf / non-positive runtimes) follow MeasurementRecord: excluded from the
+    refit, fitness 0, runtime inf — the run equals the reference driver's log (make_tune.py)."""
+    land = landscape_from_dict(case["landscape"], SPACE)
+    want = [tuple(x) for x in case["indices"]]
+    table = dict(zip(want, case["runtimes"]))
+    mod, bad = case["fail_mod"], float(case["fail_value"])
+    run = tune.tune_rows(SPACE, land, case["strategy"], case["budget"], case["seed"],
+                         runtimes=lambda batch: [bad if sum(t) % mod == 0 else table[t] for t in batch])
+    assert run.configs == want
+    assert run.rounds == case["rounds"]
+    assert [r == float("inf") for r in run.runtimes] == case["failed"]
+    assert any(case["failed"])
+
+
+@pytest.mark.parametrize("case", CLEAN, ids=lambda c: f"{c['strategy']}_b{c['budget']}_s{c['seed']}")
 def test_tune_matches_reference_driver(case):
     land = landscape_from_dict(case["landscape"], SPACE)
     want = [tuple(x) for x in case["indices"]]
@@ -43,15 +63,14 @@ def test_tune_matches_reference_driver(case):
         return
     assert run.configs == want
     assert run.rounds == case["rounds"]
-    # the on-device landscape: same measurements until the first last-bit runtime difference
+    # the on-device landscape: bit-exact runtimes, so the unreplayed run is the reference's log
     dev = tune.tune_rows(SPACE, land, case["strategy"], case["budget"], case["seed"])
-    got = np.array(dev.runtimes[:64])
-    assert dev.configs[:64] == want[:64]
-    assert np.max(np.abs(got - np.array(case["runtimes"][:64])) / got) <= 1e-12
+    assert dev.configs == want
+    assert [float(x).hex() for x in dev.runtimes] == [float(x).hex() for x in case["runtimes"]]
 
 
 def test_wall_to_95_trace():
-    case = G["cases"][0]
+    case = CLEAN[0]
     land = landscape_from_dict(case["landscape"], SPACE)
     best_rt, _ = kt.best_runtime(land)
     f_star = 1.0 / best_rt

@@ -203,3 +203,38 @@ def test_install_rebinds_the_reference_driver_names():
         assert drv.run_search_round is not kt.run_search_round
     finally:
         sys.path.remove(str(src))
+
+
+def test_glibc_exp_replica_matches_libm(tmp_path):
+    """csrc/glibc_exp.cuh (the landscape kernel's exp) is bit-identical to the C library's exp, which
+    is what the reference's math.exp calls (backends.py:168): random arguments over the whole range
+    the basins produce, the out-of-range helper's band, tiny |x|, and arguments next to every
+    rounding boundary of the table index."""
+    import math
+    import shutil
+    import subprocess
+
+    gxx = shutil.which("g++")
+    if gxx is None:
+        pytest.skip("g++ not available")
+    exe = tmp_path / "exp_check"
+    subprocess.run([gxx, "-O2", "-std=c++17", "-ffp-contract=off", "-I", str(ROOT / "paper_1905_12799_b200" / "csrc"),
+                    str(ROOT / "tests" / "exp_check.cpp"), "-o", str(exe)], check=True)
+    rng = np.random.default_rng(7)
+    inv = float.fromhex("0x1.71547652b82fep0") * 128
+    k = np.arange(-96000, 96000, 7, dtype=np.float64)
+    edges = (k + 0.5) / inv
+    near = (edges[:, None].view(np.int64) + np.arange(-3, 4)[None, :]).reshape(-1).view(np.float64)
+    d2 = rng.integers(0, 8 * 255 * 255, size=200_000).astype(np.float64)
+    r = rng.uniform(0.5, 80.0, size=d2.size)
+    x = np.concatenate([
+        rng.uniform(-760.0, 0.0, 400_000), rng.uniform(-1500.0, 1500.0, 100_000), rng.uniform(-1e-15, 1e-15, 10_000),
+        -d2 / (r * r), near, np.array([0.0, -0.0, -745.2, -708.4, -512.0, 512.0, 709.7, -np.inf, np.inf]),
+    ])
+    src, dst = tmp_path / "x.bin", tmp_path / "y.bin"
+    x.tofile(src)
+    subprocess.run([str(exe), str(src), str(dst)], check=True)
+    got = np.fromfile(dst, dtype=np.float64)
+    want = np.array([math.exp(v) if v < 709.78 else math.inf for v in x.tolist()])
+    bad = np.flatnonzero(got.view(np.int64) != want.view(np.int64))
+    assert bad.size == 0, [(x[i].hex(), got[i].hex(), want[i].hex()) for i in bad[:5]]

@@ -25,7 +25,7 @@ def test_oracle_fit_matches_reference(case):
     assert json.dumps(model, sort_keys=True) == case["model"]
 
 
-@pytest.mark.parametrize("case", [c for c in TUNE["cases"] if c["strategy"] != "rl+as"],
+@pytest.mark.parametrize("case", [c for c in TUNE["cases"] if c["strategy"] != "rl+as" and "fail_mod" not in c],
                          ids=lambda c: c["strategy"])
 def test_oracle_tune_matches_reference_driver(case):
     values = [k["values"] for k in TUNE["space"]["knobs"]]

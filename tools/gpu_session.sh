@@ -25,6 +25,11 @@ for w in $WHAT; do
         timeout 900 ncu --set full --clock-control none --import-source on -k regex:$re -s 2 -c 1 -o "$OUT/prof_$k" \
           python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-wall95 > "$OUT/prof_$k.log" 2>&1; echo "full $k rc=$?"
       done;;
+    timeline)
+      KT_LIB_PATH=build/ab/probes.so KT_LLOYD_TIMELINE=1 timeout 300 python tools/lloyd_probe.py > "$OUT/timeline.txt" 2>&1; echo "timeline rc=$?"
+      python tools/timeline_sum.py "$OUT/timeline.txt" | head -4;;
+    ppoerr)
+      timeout 600 python tools/ppo_error.py > "$OUT/ppo_error.log" 2>&1; echo "ppoerr rc=$?"; tail -2 "$OUT/ppo_error.log";;
     rl)
       timeout 900 python bench.py --workload rl > "$OUT/bench_rl.json" 2> "$OUT/bench_rl.err"; echo "bench rl rc=$?"; cut -c1-400 "$OUT/bench_rl.json";;
     fullrl)
