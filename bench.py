@@ -314,15 +314,20 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         kt.predict_rows(model, space, rows_dev, out=out, engine=eng)
         return kt.adaptive_sample_rows(rows_dev, visited, space, seed, engine=eng, info=info)
 
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+
     # untimed: each step's visited set, built from the same step computed without one ("an earlier
     # round measured two of these centroids"), so every timed step runs the mode vote (K9)
-    seeds = {}
+    visited_for = {}
     for base in (1000, 2000):
         for s in range(args.steps):
             nv = step(dev_sets[s % n_sets], base + s)
-            seeds[base + s] = bench_visited_rows(nv, host_sets[s % n_sets].numpy())
+            visited_for[base + s] = bench_visited_rows(nv, host_sets[s % n_sets].numpy())
     for w in range(args.warmup):
-        step(dev_sets[w % n_sets], 1000 + w, seeds[1000 + w % args.steps])
+        step(dev_sets[w % n_sets], 1000 + w, visited_for[1000 + w % args.steps])
 
     # parity self-check (untimed) on rank 0's first set against the oracle golden of this exact step
     parity = None
@@ -351,7 +356,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
             with eng.scope():
                 ev[s][0].record(eng.stream)
             info = kt._lib.SampleInfo()
-            step(dev_sets[s % n_sets], 1000 + s, seeds[1000 + s], info)
+            step(dev_sets[s % n_sets], 1000 + s, visited_for[1000 + s], info)
             with eng.scope():
                 ev[s][1].record(eng.stream)
             infos.append(info)
@@ -394,7 +399,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         with torch.cuda.stream(copy_stream):  # scores D2H overlaps the clustering of the same step
             copy_stream.wait_event(scored[s % 2])
             host_scores[s % 2].copy_(sbufs[s % 2], non_blocking=True)
-        batch = kt.adaptive_sample_rows(bufs[s % 2], seeds[2000 + s], space, 2000 + s, engine=eng)
+        batch = kt.adaptive_sample_rows(bufs[s % 2], visited_for[2000 + s], space, 2000 + s, engine=eng)
         d2h += batch.nbytes + N * 8
     with eng.scope():
         eng.stream.wait_stream(copy_stream)
@@ -409,7 +414,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     for s in range(args.steps):
         flush.fill_(float(s))
         info = kt._lib.SampleInfo()
-        step(dev_sets[s % n_sets], 1000 + s, seeds[1000 + s], info)
+        step(dev_sets[s % n_sets], 1000 + s, visited_for[1000 + s], info)
         kinfo.append(info)
     stats = eng.kernel_stats(reset=True)
     eng.set_timing(False)
@@ -495,11 +500,6 @@ def run_rl(args, rank: int, world: int, local_rank: int) -> None:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
-
-    def barrier():
-        torch.cuda.synchronize()
-        if dist is not None:
-            dist.barrier()
 
     line = bench_rl.run(args, rank, world, local_rank, kt, torch, dist, {"barrier": barrier, "clock": ClockSampler})
     if line is not None:

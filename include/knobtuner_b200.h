@@ -163,6 +163,12 @@ typedef struct kt_sample_info {
  * round centroids -> visited/mode replacement -> dedup of the batch.
  * visited_rows: host array of measured configurations (VisitedSet).
  * batch_out: host, capacity 63 rows.                                        */
+/* _top_unvisited (driver.py:101-115), the non-adaptive arms' batch: the first occurrence of every
+ * trajectory row not in visited[0, n_visited) (host array, any order), stable-sorted by descending
+ * score; the first `cap` (<= 64) rows -> batch_out (host), their count -> *batch_len.              */
+int kt_top_unvisited(kt_engine* e, const uint64_t* rows_dev, const double* scores_dev, int64_t count,
+                     const uint64_t* visited, int64_t n_visited, int cap, uint64_t* batch_out, int32_t* batch_len);
+
 int kt_adaptive_sample(kt_engine* e, const uint64_t* rows_dev, int64_t count,
                        int n_knobs, const int32_t* cards,
                        const uint64_t* visited_rows, int64_t n_visited,

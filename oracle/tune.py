@@ -181,3 +181,19 @@ def tune(knob_values, landscape: dict, strategy: str, budget: int, seed: int = 0
         measure(batch[:left])
         rounds += 1
     return configs, runtimes, trace, rounds
+
+
+def top_unvisited(idx, scores, visited: set, cap: int = 64) -> list:
+    """driver.py:101-115 (_top_unvisited): first occurrence of every unvisited configuration, stable
+    sort by -score, first ``cap``."""
+    configs, sc, seen = [], [], set()
+    for t, s in zip(map(tuple, np.asarray(idx, dtype=np.int64).tolist()), np.asarray(scores).tolist()):
+        if t in seen or t in visited:
+            continue
+        seen.add(t)
+        configs.append(t)
+        sc.append(s)
+    if not configs:
+        return []
+    order = np.argsort(-np.asarray(sc, dtype=np.float64), kind="stable")
+    return [configs[int(i)] for i in order[:cap]]

@@ -12,7 +12,7 @@ or a CUDA device every engine call raises ``EngineUnavailable``.
 its unchanged driver and CLI run on the B200.
 """
 
-from . import errors, report
+from . import errors, report, tune
 from ._lib import EngineUnavailable, engine
 from .agent import Agent, AgentHyperparams, init_agent, run_search_round, run_search_rows
 from .cost_model import BoostParams, CostModel, Tree, device_forest, fit, predict, predict_rows
@@ -59,7 +59,7 @@ def install() -> dict:
     errors.adopt(mods["errors"])
     patches = [
         (mods["driver"], "predict", predict), (mods["driver"], "run_sa_round", run_sa_round),
-        (mods["driver"], "fit", fit),
+        (mods["driver"], "fit", fit), (mods["driver"], "_top_unvisited", tune.top_unvisited),
         (mods["report"], "per_step_best", report.per_step_best),
         (mods["report"], "convergence_steps_for_round", report.convergence_steps_for_round),
         (mods["report"], "pca_project", report.pca_project),

@@ -101,6 +101,7 @@ SIGNATURES = {
     "kt_landscape_destroy": (C.c_int, [P]),
     "kt_score_landscape": (C.c_int, [P, P, P, i64, P]),
     "kt_landscape_best": (C.c_int, [P, P, pi32, pf64, pi64]),
+    "kt_top_unvisited": (C.c_int, [P, P, P, i64, pu64, i64, C.c_int, pu64, pi32]),
     "kt_dedup": (C.c_int, [P, P, i64, P, pi64]),
     "kt_mode_vote": (C.c_int, [P, P, i64, C.c_int, pi32, pi32]),
     "kt_kmeans": (C.c_int, [P, P, i64, C.c_int, pi32, C.c_int, u64, pf64, pi64, pf64, pf64, pi32]),

@@ -183,4 +183,7 @@ void allow_dynamic_smem(const void* kernel);
 int occupancy_blocks(const void* kernel, int threads, size_t smem);
 // out[i] = sum(in[0..i)), out[n] = total; n <= 16M (single-block scan).
 void exclusive_scan(kt_engine* e, const int64_t* in, int64_t* out, int n);
+// K6's first-occurrence hash table over rows[0, count): *first = per-slot lowest row index,
+// *slot = each row's slot, so row i is a first occurrence iff first[slot[i]] == i (engine scratch).
+void dedup_table(kt_engine* e, const uint64_t* rows, int64_t count, const uint32_t** first, const uint32_t** slot);
 }  // namespace kt

@@ -154,23 +154,31 @@ static uint64_t table_capacity(int64_t count) {
     return cap;
 }
 
-int64_t dedup(kt_engine* e, const uint64_t* rows, int64_t count, uint64_t* out) {
-    if (count <= 0) return 0;
+void dedup_table(kt_engine* e, const uint64_t* rows, int64_t count, const uint32_t** first_out,
+                 const uint32_t** slot_out) {
     if (count >= (int64_t(1) << 31)) fail(KT_ERR_UNSUPPORTED, "dedup supports < 2^31 rows per call");
     const uint64_t cap = table_capacity(count);
     auto* keys = static_cast<uint64_t*>(e->scratch("dedup.keys", cap * 8));
     auto* first = static_cast<uint32_t*>(e->scratch("dedup.first", cap * 4));
     KT_CUDA(cudaMemsetAsync(keys, 0xff, cap * 8, e->stream));
     KT_CUDA(cudaMemsetAsync(first, 0xff, cap * 4, e->stream));
-    const int nb = int(ceil_div(count, kDedupRowsPerBlock));
-    auto* bits = static_cast<uint32_t*>(e->scratch("dedup.bits", size_t(ceil_div(count, 32)) * 4 + 128));
-    auto* counts = static_cast<int64_t*>(e->scratch("dedup.counts", size_t(nb) * 8));
-    auto* offsets = static_cast<int64_t*>(e->scratch("dedup.offsets", size_t(nb + 1) * 8));
     int grid = int(std::min<int64_t>(ceil_div(count, 256), int64_t(e->num_sms) * 8));
     e->pre_launch("dedup_insert");
     auto* slot = static_cast<uint32_t*>(e->scratch("dedup.slot", size_t(count) * 4));
     dedup_insert_kernel<<<grid, 256, 0, e->stream>>>(rows, count, keys, first, cap - 1, slot);
     e->check_launch("dedup_insert");
+    *first_out = first;
+    *slot_out = slot;
+}
+
+int64_t dedup(kt_engine* e, const uint64_t* rows, int64_t count, uint64_t* out) {
+    if (count <= 0) return 0;
+    const uint32_t *first, *slot;
+    dedup_table(e, rows, count, &first, &slot);
+    const int nb = int(ceil_div(count, kDedupRowsPerBlock));
+    auto* bits = static_cast<uint32_t*>(e->scratch("dedup.bits", size_t(ceil_div(count, 32)) * 4 + 128));
+    auto* counts = static_cast<int64_t*>(e->scratch("dedup.counts", size_t(nb) * 8));
+    auto* offsets = static_cast<int64_t*>(e->scratch("dedup.offsets", size_t(nb + 1) * 8));
     e->pre_launch("dedup_flag");
     dedup_flag_kernel<<<nb, 256, 0, e->stream>>>(slot, count, first, bits, counts);
     e->check_launch("dedup_flag");

@@ -70,21 +70,55 @@ def random_unvisited(cards, visited: set, count: int, rng) -> list[tuple]:
     return batch
 
 
-def top_unvisited(rows: np.ndarray, scores: np.ndarray, visited: set, cap: int, n: int, cards) -> list[tuple]:
-    """driver.py:101-115 on device results copied to the host (first-occurrence distinct,
-    unvisited, stable sort by -score)."""
-    idx = sp.unpack(rows, n, cards)
-    configs, sc, seen = [], [], set()
-    for t, s in zip(map(tuple, idx.tolist()), scores.tolist()):
-        if t in seen or t in visited:
-            continue
-        seen.add(t)
-        configs.append(t)
-        sc.append(s)
-    if not configs:
-        return []
-    order = np.argsort(-np.asarray(sc), kind="stable")
-    return [configs[int(i)] for i in order[:cap]]
+def top_unvisited_rows(rows, scores, visited_rows: np.ndarray, cap: int = GREEDY_BATCH, engine=None) -> np.ndarray:
+    """driver.py:101-115 on the device (``kt_top_unvisited``): the first occurrence of every
+    trajectory row not in ``visited_rows``, stable-sorted by descending score, first ``cap``.
+    ``rows`` / ``scores``: CUDA int64 / float64 tensors; returns packed rows (numpy uint64)."""
+    eng = engine or _lib.engine()
+    vis = np.ascontiguousarray(visited_rows, dtype=np.uint64)
+    out = np.zeros(max(cap, 1), dtype=np.uint64)
+    n_out = _lib.C.c_int32(0)
+    with eng.scope():
+        _lib.call("kt_top_unvisited", eng.handle, _lib.ptr(rows), _lib.ptr(scores), int(rows.numel()),
+                  _lib.as_ptr(vis, _lib.C.c_uint64), int(vis.size), int(cap), _lib.as_ptr(out, _lib.C.c_uint64),
+                  _lib.C.byref(n_out))
+    return out[: n_out.value].copy()
+
+
+def top_unvisited(trajectory, visited, cap: int = GREEDY_BATCH) -> list:
+    """Drop-in for the reference driver's ``_top_unvisited(trajectory, visited, cap)`` (driver.py:101-115):
+    best ``cap`` distinct unvisited trajectory configurations by surrogate score, on the device."""
+    import torch
+
+    from .sampler import visited_rows
+    from .trajectory import Trajectory, config_class_of, trajectory_rows
+
+    eng = _lib.engine()
+    space_cards = getattr(trajectory, "cards", None)
+    if isinstance(trajectory, Trajectory):
+        n = trajectory.n_knobs
+        rows = trajectory.rows_device(eng.device)
+        sc = trajectory.scores_device()
+        sc = sc if isinstance(sc, torch.Tensor) else torch.as_tensor(np.asarray(sc, dtype=np.float64))
+        cards = space_cards
+    else:
+        configs = trajectory.configs()
+        idx = np.array([c.indices for c in configs], dtype=np.int64)
+        n = idx.shape[1]
+        vis_idx = [t for t in getattr(visited, "_seen", ())]
+        ext = np.vstack([idx] + ([np.array(vis_idx, dtype=np.int64)] if vis_idx else []))
+        cards = ext.max(axis=0) + 1  # a row layout that holds every index seen here
+        rows = torch.from_numpy(sp.pack(idx, cards).view(np.int64))
+        sc = torch.as_tensor(np.asarray(trajectory.scores() if hasattr(trajectory, "scores") else
+                                        [s for _, s in trajectory.entries], dtype=np.float64))
+    dev = f"cuda:{eng.device}"
+    with eng.scope():
+        rows = rows.to(dev)
+        sc = sc.to(dev).to(torch.float64)
+    vis = visited_rows(visited, cards) if len(visited) else np.zeros(0, dtype=np.uint64)
+    out = top_unvisited_rows(rows, sc, vis, cap, engine=eng)
+    cls = config_class_of(trajectory)
+    return [cls(tuple(int(v) for v in r)) for r in sp.unpack(out, n, cards).tolist()]
 
 
 class _TS:
@@ -213,9 +247,9 @@ def tune_rows(space, landscape, strategy: str, budget: int, seed: int = 0,
         if strategy.endswith("+as"):
             brows = adaptive_sample_rows(traj[0], m_rows[:m_cnt], space, round_seed(seed, round_index), engine=eng)
             batch = [tuple(r) for r in sp.unpack(brows, n, cards).tolist()]
-        elif traj is not None:
-            batch = top_unvisited(traj[0].cpu().numpy().view(np.uint64), traj[1].cpu().numpy(), visited,
-                                  GREEDY_BATCH, n, cards)
+        elif traj is not None:  # _top_unvisited, driver.py:101-115, on the device
+            brows = top_unvisited_rows(traj[0], traj[1], m_rows[:m_cnt], GREEDY_BATCH, engine=eng)
+            batch = [tuple(r) for r in sp.unpack(brows, n, cards).tolist()]
         else:
             batch = []
         if not batch:

@@ -81,3 +81,57 @@ def test_wall_to_95_trace():
     assert bests == sorted(bests)
     if t95 is not None:
         assert 0.0 < t95 <= run.seconds
+
+
+TOPK = json.loads((GOLDEN / "topk.json").read_text())
+
+
+def _topk_inputs(case):
+    import sys
+
+    sys.path.insert(0, str(GOLDEN))
+    from make_topk import case_inputs
+
+    return case_inputs(*case)
+
+
+@pytest.mark.parametrize("g", TOPK, ids=lambda g: g["case"][0])
+def test_top_unvisited_vs_reference(g):
+    """kt_top_unvisited == the reference's _top_unvisited (driver.py:101-115) on its own goldens:
+    duplicates, score ties, signed zeros, visited overlap, short and empty batches."""
+    from paper_1905_12799_b200 import space as sp
+
+    idx, scores, vis = _topk_inputs(g["case"])
+    cards = np.array(g["case"][2])
+    tr = kt.Trajectory(torch.from_numpy(sp.pack(idx, cards).view(np.int64)).cuda(), torch.from_numpy(scores).cuda(),
+                       n_knobs=cards.size, cards=cards)
+    visited = kt.VisitedSet([kt.Configuration(tuple(r)) for r in vis.tolist()])
+    got = tune.top_unvisited(tr, visited, 64)
+    assert [list(c.indices) for c in got] == g["batch"]
+
+    class RefShaped:  # the reference's Trajectory: entries of (Configuration, score)
+        def __init__(self, entries):
+            self.entries = entries
+
+        def configs(self):
+            return [c for c, _ in self.entries]
+
+    ref_tr = RefShaped(tuple((kt.Configuration(tuple(r)), float(s)) for r, s in zip(idx.tolist(), scores.tolist())))
+    assert [list(c.indices) for c in tune.top_unvisited(ref_tr, visited, 64)] == g["batch"]
+
+
+@pytest.mark.parametrize("n", [1, 511, 1 << 20])
+def test_top_unvisited_large_vs_oracle(n):
+    from oracle import tune as otune
+    from paper_1905_12799_b200 import space as sp
+
+    rng = np.random.default_rng(n)
+    cards = np.array([84, 80, 80, 7, 2, 2, 3, 2])
+    idx = rng.integers(0, cards, size=(n, 8))
+    idx[n // 2:] = idx[: n - n // 2]  # every second half row repeats the first half
+    scores = np.round(rng.standard_normal(n), 2)  # ties
+    vis = idx[rng.integers(0, n, size=min(n, 300))]
+    visited = {tuple(r) for r in vis.tolist()}
+    got = tune.top_unvisited_rows(torch.from_numpy(sp.pack(idx).view(np.int64)).cuda(),
+                                  torch.from_numpy(scores).cuda(), sp.pack(np.array(sorted(visited))), 64)
+    assert [tuple(r) for r in sp.unpack(got, 8).tolist()] == otune.top_unvisited(idx, scores, visited, 64)

@@ -36,3 +36,16 @@ def test_oracle_tune_matches_reference_driver(case):
     assert rounds == case["rounds"]
     assert [t[1] for t in trace][-1] == case["budget"]
     assert np.all(np.diff([t[2] for t in trace]) >= 0)
+
+
+TOPK = json.loads((GOLDEN / "topk.json").read_text())
+
+
+@pytest.mark.parametrize("g", TOPK, ids=lambda g: g["case"][0])
+def test_oracle_top_unvisited_matches_reference(g):
+    sys.path.insert(0, str(GOLDEN))
+    from make_topk import case_inputs
+
+    idx, scores, vis = case_inputs(*g["case"])
+    got = otune.top_unvisited(idx, scores, {tuple(r) for r in vis.tolist()}, 64)
+    assert [list(t) for t in got] == g["batch"]
