@@ -14,12 +14,6 @@ from pathlib import Path
 
 import numpy as np
 
-sys.path.insert(0, "/root/reference/pkg/src")
-from knobtuner import driver  # noqa: E402
-from knobtuner.agent import Trajectory  # noqa: E402
-from knobtuner.sampler import VisitedSet  # noqa: E402
-from knobtuner.space import Configuration  # noqa: E402
-
 HERE = Path(__file__).resolve().parent
 CASES = [  # (name, entries, cards, score levels (0 = continuous), visited count, seed)
     ("tiny_all_distinct", 40, [5, 5, 5], 0, 3, 1), ("ties", 2000, [6, 6, 6, 6], 7, 40, 2),
@@ -45,6 +39,12 @@ def case_inputs(name, n, cards, levels, nvis, seed):
 
 
 def main() -> None:
+    sys.path.insert(0, "/root/reference/pkg/src")  # the reference is imported here only (tests import case_inputs)
+    from knobtuner import driver
+    from knobtuner.agent import Trajectory
+    from knobtuner.sampler import VisitedSet
+    from knobtuner.space import Configuration
+
     out = []
     for case in CASES:
         name = case[0]
