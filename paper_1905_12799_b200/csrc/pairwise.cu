@@ -1,6 +1,7 @@
 // pairwise.cu — see pairwise.cuh.
 #include <algorithm>
 #include <map>
+#include <mutex>
 #include <string>
 
 #include "pairwise.cuh"
@@ -77,16 +78,20 @@ std::shared_ptr<PairwiseTree> make_tree(int64_t m) {
     return t;
 }
 
+// Shared by every engine of the process (shard threads run concurrently): the cache is
+// locked, and callers hold a reference so an eviction never frees a tree in use.
+static std::mutex g_trees_mu;
 static std::map<std::pair<int, int64_t>, std::shared_ptr<PairwiseTree>> g_trees;
 
-const PairwiseTree& pairwise_tree(int device, int64_t m) {
+std::shared_ptr<const PairwiseTree> pairwise_tree(int device, int64_t m) {
     auto key = std::make_pair(device, m);
+    std::lock_guard<std::mutex> lock(g_trees_mu);
     auto it = g_trees.find(key);
-    if (it != g_trees.end()) return *it->second;
+    if (it != g_trees.end()) return it->second;
     if (g_trees.size() > 64) g_trees.clear();
     auto t = make_tree(m);
     g_trees[key] = t;
-    return *t;
+    return t;
 }
 
 // ---------------------------------------------------------------- kernels
@@ -236,7 +241,8 @@ void pairwise_loss(kt_engine* e, const uint64_t* pts, int64_t m, int n, const Ro
 void pairwise_loss_runs(kt_engine* e, const uint64_t* pts, int64_t m, int n, const RowFmt& fmt, const uint8_t* assign,
                         int64_t astride, const double* cent, const int* coff, int R, double* out_dev) {
     if (R < 1 || R > kMaxLossRuns) fail(KT_ERR_VALUE, "pairwise_loss_runs: 1..8 runs");
-    const PairwiseTree& t = pairwise_tree(e->device, m);
+    const auto tree = pairwise_tree(e->device, m);
+    const PairwiseTree& t = *tree;
     const int L = int(t.leaf_start.size());
     const int64_t vstride = int64_t(L) + int64_t(t.node_left.size());
     auto* vals = static_cast<double*>(e->scratch("loss.vals", size_t(vstride) * R * 8));
@@ -250,7 +256,8 @@ void pairwise_loss_runs(kt_engine* e, const uint64_t* pts, int64_t m, int n, con
 }
 
 void pairwise_sum(kt_engine* e, const double* x, int64_t m, const double* center, double* out_dev) {
-    const PairwiseTree& t = pairwise_tree(e->device, m);
+    const auto tree = pairwise_tree(e->device, m);
+    const PairwiseTree& t = *tree;
     const int L = int(t.leaf_start.size());
     auto* vals = static_cast<double*>(e->scratch("psum.vals", size_t(L + t.node_left.size()) * 8));
     e->pre_launch("psum_leaf");

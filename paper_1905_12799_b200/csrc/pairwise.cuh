@@ -38,7 +38,7 @@ struct PairwiseTree {
     }
 };
 
-const PairwiseTree& pairwise_tree(int device, int64_t m);
+std::shared_ptr<const PairwiseTree> pairwise_tree(int device, int64_t m);
 
 // k-means loss: sum over points of the float64 squared distance to the assigned centroid.
 void pairwise_loss(kt_engine* e, const uint64_t* pts, int64_t m, int n, const RowFmt& fmt, const uint8_t* assign,

@@ -589,6 +589,14 @@ constexpr int kSumW = 9;           // 8 coordinate sums + count
 // coordinates, count, then high bytes (nonzero only in wide row layouts), so
 // every counter grows by at most 255 per point in any layout.
 constexpr int kDeltaW = 17;
+// Grid exchange slot spacing (uint64 units).  Packed (1) measured faster than one slot per
+// 128-byte line (16: 1.21 -> 1.23 ms per 1M-point knee scan): the per-pass reads of all
+// K x 9 sums are latency-, not L2-slice-bound.
+#ifndef KT_DSTRIDE
+#define KT_DSTRIDE 1
+#endif
+constexpr int kDStride = KT_DSTRIDE;          // uint64 per exchange slot
+constexpr int kChgStride = 2 * KT_DSTRIDE;    // uint32 per changed flag
 enum RunState : int {
     kActiveFromSums = 0,  // centroids = sums / counts of the previous pass (bounds valid)
     kActiveGiven = 1,     // centroids given in LloydArgs::cent (after a reseed)
@@ -627,8 +635,8 @@ struct LloydArgs {
     double* cent;              // [K][8] centroids of the latest pass
     const uint64_t* init_rows; // k-means++ rows (prefix shared by all runs)
     long long* S;              // [K][9] running sums
-    unsigned long long* D;     // [3][K][9] per-pass deltas
-    unsigned int* chg;         // [3][kMaxRuns]
+    unsigned long long* D;     // [3][K][9] per-pass deltas, kDStride apart
+    unsigned int* chg;         // [3][kMaxRuns], kChgStride apart
     unsigned int* work;        // [3] per-pass chunk counters
     int* run_state;            // [R]
     int* run_iter;             // [R]
@@ -638,7 +646,7 @@ struct LloydArgs {
 };
 
 struct LloydLayout {
-    size_t S, c64, c32, delta, drift, dcum, cnext, total;
+    size_t S, c64, c32, c2, delta, drift, dcum, cnext, total;
 };
 
 __host__ __device__ inline LloydLayout lloyd_layout(int K) {
@@ -648,6 +656,8 @@ __host__ __device__ inline LloydLayout lloyd_layout(int K) {
     o += size_t(K) * kMaxKnobs * 8;
     L.c32 = o;
     o += size_t(K) * kMaxKnobs * 4;
+    L.c2 = o;  // centroid pairs of each run, knob-interleaved (f32x2 distances); odd k padded with NaN
+    o += size_t(K + kMaxRuns) * kMaxKnobs * 4;
     L.S = o;
     o += size_t(K) * kSumW * 8;
     L.delta = o;
@@ -675,20 +685,41 @@ struct RunShared {
     int changed[kMaxRuns];
     float m1[kMaxRuns], m2[kMaxRuns];  // largest / second largest drift
     int amax[kMaxRuns];
-    int exit_flag, n_active;
+    int exit_flag[2], n_active[2];  // by pass parity: reset two passes before they are read again
     unsigned int chg_g[kMaxRuns];  // changed flags of the whole grid (after the barrier)
     int empty[kMaxRuns];           // a cluster of the run ended the pass empty
+    float dmax[kMaxRuns];          // largest shrink D_j of the run's clusters (scan prefilter)
 };
 
 // Conservative |fp32 - exact| bound for sum_i (p_i - c_i)^2 with p_i, |c_i| <= 255
 // (derivation in DESIGN.md §K8).
 // k1 = 6.5e-5 for coordinates <= 255 and grows linearly with the largest coordinate.
+// Square roots of the bounds use the MUFU approximation widened by kSqrtSlack (relative):
+// sqrt.approx.f32's relative error is below 2^-22 on normal inputs (measured exhaustively
+// over [2^-30, 2^30] by tools/sqrt_approx_check.cu: 1.7e-7), so the widened values stay
+// on the safe side of the directed-rounding ones they replace (__fsqrt_ru / __fsqrt_rd
+// are multi-instruction sequences; this is one MUFU + one FMUL).
+#ifndef KT_FAST_SQRT
+#define KT_FAST_SQRT 1
+#endif
+constexpr float kSqrtSlack = 1.0f / (1 << 20);
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float r;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
 __device__ __forceinline__ float d2_bound(float d, float k1) {
+    if (KT_FAST_SQRT) return (k1 * (1.0f + 4.0f * kSqrtSlack)) * sqrt_approx(8.0f * d + 8.0f) + 5.5e-7f * d + 1e-6f;
     return k1 * sqrtf(8.0f * d + 8.0f) + 5.5e-7f * d + 1e-6f;
 }
-__device__ __forceinline__ float dist_up(float d2, float k1) { return __fsqrt_ru(__fadd_ru(d2, d2_bound(d2, k1))); }
+__device__ __forceinline__ float dist_up(float d2, float k1) {
+    const float x = __fadd_ru(d2, d2_bound(d2, k1));
+    if (KT_FAST_SQRT) return __fmul_ru(sqrt_approx(x), 1.0f + kSqrtSlack);
+    return __fsqrt_ru(x);
+}
 __device__ __forceinline__ float dist_dn(float d2, float k1) {
     const float lo = __fsub_rd(d2, d2_bound(d2, k1));
+    if (KT_FAST_SQRT) return lo > 1e-30f ? __fmul_rd(sqrt_approx(lo), 1.0f - kSqrtSlack) : 0.0f;
     return lo > 0.0f ? __fsqrt_rd(lo) : 0.0f;
 }
 // Settled iff (l - u) > margin: distances are <= 255*sqrt(8) ~ 721, so float64
@@ -732,20 +763,61 @@ __device__ __forceinline__ float f32_d2(const float p[kMaxKnobs], const float* c
     return d;
 }
 
+// Upper bound of sqrt(d2) in float (centroid drift): d2 rounded up to float, the MUFU
+// square root widened by kSqrtSlack (one MUFU instead of a float64 square root).
+__device__ __forceinline__ float drift_up(double d2) {
+    const float x = __double2float_ru(d2 * (1.0 + 1e-12));
+    return x > 1e-30f ? __fmul_ru(sqrt_approx(x), 1.0f + kSqrtSlack) : 1e-15f;
+}
+
+// Centroid pairs: run r's clusters (2q, 2q+1) share 16 floats {c_2q[i], c_2q+1[i]} for
+// i = 0..7 at c2 + (pair offset of r + q) * 16, so one packed f32x2 subtract and one
+// f32x2 FMA per knob advance two distances (Blackwell FADD2 / FFMA2): per lane the
+// same rn operations in the same order as f32_d2, so the distances are bit-identical.
+__device__ __forceinline__ int pair_base(const int* k, int r) {
+    int o = 0;
+    for (int q = 0; q < r; ++q) o += (k[q] + 1) >> 1;
+    return o;
+}
+__device__ __forceinline__ unsigned long long f2_pack(float x) {
+    unsigned long long v;
+    asm("mov.b64 %0, {%1,%1};" : "=l"(v) : "f"(x));
+    return v;
+}
+__device__ __forceinline__ void f32x2_d2(const float p[kMaxKnobs], const float* c, float& d0, float& d1) {
+    const ulonglong2* c4 = reinterpret_cast<const ulonglong2*>(c);
+    unsigned long long d = 0ull, t;
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+        const ulonglong2 cc = c4[h];
+        asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(f2_pack(p[2 * h])), "l"(cc.x));
+        asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(d) : "l"(t));
+        asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(f2_pack(p[2 * h + 1])), "l"(cc.y));
+        asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(d) : "l"(t));
+    }
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(d0), "=f"(d1) : "l"(d));
+}
+
 // Full assignment of one point under one k; returns the cluster and fresh bounds.
-__device__ __forceinline__ int full_assign(const float* c32, const double* c64, uint64_t row, const float p[kMaxKnobs],
+__device__ __forceinline__ int full_assign(const float* c32, const float* c2, const double* c64, uint64_t row,
+                                           const float p[kMaxKnobs],
                                            int k, int n, const RowFmt& fmt, float k1, float& u, float& l) {
     float best = INFINITY, second = INFINITY;
     int bj = 0;
 #pragma unroll (kAssignUnroll)
-    for (int j = 0; j < k; ++j) {
-        const float d = f32_d2(p, c32 + j * kMaxKnobs);
-        if (d < best) {
-            second = best;
-            best = d;
-            bj = j;
-        } else if (d < second) {
-            second = d;
+    for (int j = 0; j < k; j += 2) {
+        float dd[2];
+        f32x2_d2(p, c2 + j * kMaxKnobs, dd[0], dd[1]);  // odd k: the pad lane is NaN, never below
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const float d = dd[h];
+            if (d < best) {
+                second = best;
+                best = d;
+                bj = j + h;
+            } else if (d < second) {
+                second = d;
+            }
         }
     }
     if (k > 1 && !(second - best > d2_bound(best, k1) + d2_bound(second, k1))) {
@@ -783,9 +855,11 @@ __device__ __forceinline__ void lloyd_grid_barrier(unsigned int* ctr, unsigned i
     if (threadIdx.x == 0) {
         unsigned int cur;
         asm volatile("atom.add.release.gpu.u32 _, [%0], 1;" ::"l"(ctr) : "memory");  // (red.release: same speed)
+        // spin relaxed (an acquire load invalidates L1 on every poll), then acquire once
         do {
-            asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(ctr) : "memory");
+            asm volatile("ld.relaxed.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(ctr) : "memory");
         } while (cur < target);
+        asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(ctr) : "memory");
     }
     __syncthreads();
 }
@@ -824,13 +898,15 @@ __host__ __device__ inline size_t lloyd_resident_bytes(int K, int R, int64_t P, 
 }
 
 // Evaluate one point under run r: full assignment and its new budget.
-__device__ __forceinline__ int lloyd_assign(const LloydArgs& a, const RowFmt& fmt, const float* c32, const double* c64,
-                                            const float* dcum, int r, uint64_t row, float& budget) {
+__device__ __forceinline__ int lloyd_assign(const LloydArgs& a, const RowFmt& fmt, const float* c32, const float* c2,
+                                            const int* pcoff, const double* c64, const float* dcum, int r, uint64_t row,
+                                            float& budget) {
     const int co = a.coff[r];
     float p[kMaxKnobs];
     unpack_row(row, p, fmt);
     float u, l;
-    const int j = full_assign(c32 + co * kMaxKnobs, c64 + co * kMaxKnobs, row, p, a.k[r], a.n, fmt, a.bk1, u, l);
+    const int j = full_assign(c32 + co * kMaxKnobs, c2 + pcoff[r] * 2 * kMaxKnobs, c64 + co * kMaxKnobs, row, p, a.k[r],
+                              a.n, fmt, a.bk1, u, l);
     budget = __fadd_rd(__fsub_rd(l, u), dcum[co + j]);
     return j;
 }
@@ -928,10 +1004,11 @@ __device__ __forceinline__ void warp_delta(int* delta, int g, uint64_t row, int 
 
 // Evaluate one point under run r (one lane, no warp cooperation): assignment,
 // budget, and the shared-counter deltas of a move.
-__device__ __forceinline__ int lloyd_eval(const LloydArgs& a, const RowFmt& fmt, const float* c32, const double* c64,
-                                          const float* dcum, int* delta, int r, uint64_t row, int old, float& budget) {
+__device__ __forceinline__ int lloyd_eval(const LloydArgs& a, const RowFmt& fmt, const float* c32, const float* c2,
+                                          const int* pcoff, const double* c64, const float* dcum, int* delta, int r,
+                                          uint64_t row, int old, float& budget) {
     const int co = a.coff[r];
-    const int j = lloyd_assign(a, fmt, c32, c64, dcum, r, row, budget);
+    const int j = lloyd_assign(a, fmt, c32, c2, pcoff, c64, dcum, r, row, budget);
     if (j != old) {
         int* dn = delta + (co + j) * kDeltaW;
         for (int c = 0; c < a.n; ++c) {
@@ -979,6 +1056,9 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
     double* c64 = reinterpret_cast<double*>(s_raw + L.c64);
     long long* S = reinterpret_cast<long long*>(s_raw + L.S);
     float* c32 = reinterpret_cast<float*>(s_raw + L.c32);
+    float* c2 = reinterpret_cast<float*>(s_raw + L.c2);
+    __shared__ int s_pcoff[kMaxRuns];
+    __shared__ uint8_t s_pslot[kMaxClusters];  // in-run index j of cluster g (its pair slot: pcoff[r] * 2 + j)
     int* delta = reinterpret_cast<int*>(s_raw + L.delta);
     unsigned long long* delta64 = reinterpret_cast<unsigned long long*>(s_raw + L.delta);  // resident layout
     float* drift = reinterpret_cast<float*>(s_raw + L.drift);
@@ -1021,7 +1101,12 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
     if (tid < kMaxRuns * 3) rs.cnt[tid / 3][tid % 3] = 0;
     if (tid < 2) s_qn[tid] = 0;
     for (int r = 0; r < R; ++r)
-        for (int j = tid; j < a.k[r]; j += blockDim.x) run_of[a.coff[r] + j] = uint8_t(r);
+        for (int j = tid; j < a.k[r]; j += blockDim.x) {
+            run_of[a.coff[r] + j] = uint8_t(r);
+            s_pslot[a.coff[r] + j] = uint8_t(j);
+        }
+    if (tid < R) s_pcoff[tid] = pair_base(a.k, tid);
+    for (int i = tid; i < (K + kMaxRuns) * kMaxKnobs; i += blockDim.x) c2[i] = __int_as_float(0x7fc00000);  // NaN pads
     if (RESIDENT) {
         for (int r = 0; r < R; ++r) {
             for (int i = tid; i < np; i += blockDim.x) {
@@ -1033,6 +1118,10 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
         if (a.rows_resident)
             for (int i = tid; i < np; i += blockDim.x) s_rows[i] = a.pts[b0 + i];
     }
+    auto c2_slot = [&](int g, int i) {
+        const int j = s_pslot[g];
+        return (s_pcoff[run_of[g]] * 2 + (j & ~1)) * kMaxKnobs + 2 * i + (j & 1);
+    };
     unsigned int n_bar = 0;  // grid barriers passed (custom barrier target = n_bar * gridDim.x)
     auto grid_barrier = [&]() {
         if (kCustomGridBarrier) lloyd_grid_barrier(a.barrier, ++n_bar * gridDim.x);
@@ -1052,6 +1141,11 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
     bool entry = true;
     while (it < a.it_end) {
         stamp(0);
+        if (tid == 0) {  // written by this pass's update, read after its final barrier
+            rs.exit_flag[it & 1] = 0;
+            rs.n_active[it & 1] = 0;
+        }
+        if (tid < kMaxRuns) rs.empty[tid] = 0;  // likewise (ordered by the tile / grid barriers)
         if (entry) {  // launch entry; later passes get their centroids from the fused update below
         entry = false;
         // ---- this pass's centroids and each centroid's drift from the previous pass:
@@ -1073,12 +1167,13 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
                 dlt2 = dlt * dlt;
                 c64[g * kMaxKnobs + i] = c;
                 c32[g * kMaxKnobs + i] = float(c);
+                c2[c2_slot(g, i)] = float(c);
                 if (blockIdx.x == 0) a.cent[g * kMaxKnobs + i] = c;
             }
             dlt2 += __shfl_xor_sync(0xffffffffu, dlt2, 1);
             dlt2 += __shfl_xor_sync(0xffffffffu, dlt2, 2);
             dlt2 += __shfl_xor_sync(0xffffffffu, dlt2, 4);
-            if (live && i == 0) drift[g] = __double2float_ru(sqrt(dlt2) * (1.0 + 1e-9) + 1e-30);
+            if (live && i == 0) drift[g] = drift_up(dlt2);
         }
         for (int i = tid; i < K * kDeltaW; i += blockDim.x) delta[i] = 0;  // also clears delta64 (K*5*8 <= K*17*4)
         if (RESIDENT && kDeltaMode == 2)
@@ -1098,22 +1193,16 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
                     m2 = d;
                 }
             }
-            rs.m1[tid] = m1;
-            rs.m2[tid] = m2;
-            rs.amax[tid] = am;
-        }
-        __syncthreads();
-        // ---- cumulative shrink of (l - u): own drift + largest drift among the other centroids
-        for (int g = tid; g < K; g += blockDim.x) {
-            const int r = run_of[g];
-            const int st = rs.state[r];
-            if (!run_active(st)) continue;
-            if (st != kActiveFromSums) {
-                dcum[g] = 0.0f;  // every point is evaluated afresh this pass
-            } else {
-                const float other = (g - a.coff[r]) == rs.amax[r] ? rs.m2[r] : rs.m1[r];
-                dcum[g] = __fadd_ru(dcum[g], __fadd_ru(drift[g], other));
+            // ---- cumulative shrink of (l - u): own drift + largest drift among the other centroids
+            const int st = rs.state[tid];
+            float dm = 0.0f;
+            for (int j = 0; j < a.k[tid]; ++j) {
+                const int g = a.coff[tid] + j;
+                if (st != kActiveFromSums) dcum[g] = 0.0f;  // every point is evaluated afresh this pass
+                else dcum[g] = __fadd_ru(dcum[g], __fadd_ru(drift[g], j == am ? m2 : m1));
+                dm = fmaxf(dm, dcum[g]);
             }
+            rs.dmax[tid] = dm;
         }
         __syncthreads();
         }
@@ -1205,7 +1294,7 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
                         if (ent[u] == 0xffffffffu) continue;
                         const int pl = int(ent[u] & 0xffffu), r = int((ent[u] >> 16) & 0xff), old = int(ent[u] >> 24);
                         float bud;
-                        const int j = lloyd_assign(a, fmt, c32, c64, dcum, r, row[u], bud);
+                        const int j = lloyd_assign(a, fmt, c32, c2, s_pcoff, c64, dcum, r, row[u], bud);
                         s_bud[r * P + pl] = bud;
                         if (kLloydProbes && a.stats) atomicAdd(&rs.cnt[r][2], 1u);
                         if (j != old) {
@@ -1293,7 +1382,7 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
                         const LloydQueueEntry qe = queue[i];
                         const uint64_t row = __ldg(a.pts + qe.point);
                         float bud;
-                        const int j = lloyd_eval(a, fmt, c32, c64, dcum, delta, r, row, qe.old, bud);
+                        const int j = lloyd_eval(a, fmt, c32, c2, s_pcoff, c64, dcum, delta, r, row, qe.old, bud);
                         bg_r[qe.point] = bud;
                         if (j != qe.old) {
                             as_r[qe.point] = uint8_t(j);
@@ -1312,9 +1401,10 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
                 next = __shfl_sync(0xffffffffu, ahead, 0);
             }
         }
-        __syncthreads();
+        if (!RESIDENT) __syncthreads();  // the resident tile loop ends with one
         const int buf = it % 3;
-        unsigned long long* Dcur = a.external ? a.ext : a.D + size_t(buf) * K * kSumW;
+        unsigned long long* Dcur = a.external ? a.ext : a.D + size_t(buf) * K * kSumW * kDStride;
+        const int ds = a.external ? 1 : kDStride;
         for (int i = tid; i < K * kSumW; i += blockDim.x) {
             const int g = i / kSumW, c = i % kSumW;
             long long vw = 0;
@@ -1327,7 +1417,7 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
                               : (RESIDENT && kDeltaMode == 0)
                                   ? (a.pack3 ? pack3_field(delta64 + g * kPack3W, c) : packed_field(delta64 + g * kPackedW, c))
                                          : (long long)delta[g * kDeltaW + c] + (c < 8 ? 256ll * delta[g * kDeltaW + 9 + c] : 0ll);
-            if (v) atomicAdd(Dcur + i, (unsigned long long)v);
+            if (v) atomicAdd(Dcur + size_t(i) * ds, (unsigned long long)v);
         }
         if (a.external) {  // sharded k-means: the host all-reduces ext, then kt_lloyd_apply decides
             if (tid < R && rs.changed[tid]) atomicAdd(a.ext + size_t(K) * kSumW + tid, 1ull);
@@ -1335,11 +1425,11 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
             ++it;
             break;
         }
-        if (tid < R && rs.changed[tid]) atomicOr(a.chg + buf * kMaxRuns + tid, 1u);
+        if (tid < R && rs.changed[tid]) atomicOr(a.chg + (buf * kMaxRuns + tid) * kChgStride, 1u);
         if (blockIdx.x == 0) {
             const int nb = (it + 1) % 3;
-            for (int i = tid; i < K * kSumW; i += blockDim.x) a.D[size_t(nb) * K * kSumW + i] = 0ull;
-            if (tid < kMaxRuns) a.chg[nb * kMaxRuns + tid] = 0u;
+            for (int i = tid; i < K * kSumW; i += blockDim.x) a.D[(size_t(nb) * K * kSumW + i) * kDStride] = 0ull;
+            if (tid < kMaxRuns) a.chg[(nb * kMaxRuns + tid) * kChgStride] = 0u;
             if (tid == 0) a.work[nb] = 0u;
         }
         stamp(4);
@@ -1348,12 +1438,9 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
 
         // ---- fused update (identical in every block): sums += grid deltas, the next pass's
         // centroids and drifts (one thread per (cluster, coordinate)), then one warp per run
-        // decides (sampler.py:99-116), reduces its drifts and advances its shrink table.
-        if (tid == 0) {
-            rs.exit_flag = 0;
-            rs.n_active = 0;
-        }
-        if (tid < R) rs.chg_g[tid] = __ldcg(a.chg + buf * kMaxRuns + tid);
+        // decides (sampler.py:99-116), reduces its drifts, advances its shrink table, and
+        // every thread commits the centroids of the runs that go on.
+        if (tid < R) rs.chg_g[tid] = __ldcg(a.chg + (buf * kMaxRuns + tid) * kChgStride);
         for (int x0 = 0; x0 < K * kMaxKnobs; x0 += blockDim.x) {
             const int x = x0 + tid;
             const int g = x >> 3, i = x & 7;
@@ -1362,11 +1449,11 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
             double dlt2 = 0.0;
             long long cnt_new = 0;
             if (live) {
-                const long long cnt = S[g * kSumW + 8] + (long long)__ldcg(Dcur + g * kSumW + 8);
+                const long long cnt = S[g * kSumW + 8] + (long long)__ldcg(Dcur + size_t(g * kSumW + 8) * ds);
                 cnt_new = cnt;
                 double c = 0.0;
                 if (i < n) {
-                    const long long sv = S[g * kSumW + i] + (long long)__ldcg(Dcur + g * kSumW + i);
+                    const long long sv = S[g * kSumW + i] + (long long)__ldcg(Dcur + size_t(g * kSumW + i) * ds);
                     S[g * kSumW + i] = sv;
                     if (cnt > 0) c = __ddiv_rn(double(sv), double(cnt));
                 }
@@ -1380,12 +1467,14 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
             dlt2 += __shfl_xor_sync(0xffffffffu, dlt2, 1);
             dlt2 += __shfl_xor_sync(0xffffffffu, dlt2, 2);
             dlt2 += __shfl_xor_sync(0xffffffffu, dlt2, 4);
-            if (live && i == 0) drift[g] = __double2float_ru(sqrt(dlt2) * (1.0 + 1e-9) + 1e-30);
+            if (live && i == 0) drift[g] = drift_up(dlt2);
         }
         for (int i = tid; i < K * kDeltaW; i += blockDim.x) delta[i] = 0;  // also clears delta64
         if (RESIDENT && kDeltaMode == 2)
             for (int i = tid; i < nwarps_blk * K * kDeltaW; i += blockDim.x) delta_w[i] = 0;
+        stamp(6);
         __syncthreads();
+        stamp(7);
         {
             const int w = tid >> 5;
             if (w < R) {
@@ -1398,8 +1487,8 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
                     else st = kActiveFromSums;
                     if (lane == 0) {
                         if (st != kActiveFromSums && blockIdx.x == 0) a.run_iter[r] = it;
-                        if (st == kNeedsReseed) rs.exit_flag = 1;
-                        if (st == kActiveFromSums) atomicAdd(&rs.n_active, 1);
+                        if (st == kNeedsReseed) rs.exit_flag[it & 1] = 1;
+                        if (st == kActiveFromSums) atomicAdd(&rs.n_active[it & 1], 1);
                     }
                     if (st == kActiveFromSums && it + 1 < a.it_end) {
                         // m1 = largest drift, amax = its first index, m2 = largest of the others
@@ -1423,27 +1512,29 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
                     }
                     if (lane == 0) {
                         rs.state[r] = st;
-                        rs.empty[r] = 0;
                         rs.changed[r] = 0;
                     }
                 }
             }
         }
-        __syncthreads();
-        // commit the next pass's centroids of the runs that go on (converged / maxed runs keep
-        // the centroids of their last pass: the reference's result; reseeds are set by the host)
+        // same phase: commit the next pass's centroids of the runs that go on (converged /
+        // maxed runs keep the centroids of their last pass: the reference's result; reseeds
+        // are set by the host).  "Goes on" is decided from inputs this phase does not write
+        // (a run that was inactive never sets its changed flag), so no barrier in between.
         for (int x = tid; x < K * kMaxKnobs && it + 1 < a.it_end; x += blockDim.x) {
-            const int g = x >> 3;
-            if (rs.state[run_of[g]] == kActiveFromSums) {
+            const int g = x >> 3, r = run_of[g];
+            if (rs.chg_g[r] && it != a.max_iters - 1 && !rs.empty[r]) {
                 const double c = cnext[x];
                 c64[x] = c;
                 c32[x] = float(c);
+                c2[c2_slot(g, x & 7)] = float(c);
                 if (blockIdx.x == 0) a.cent[x] = c;
             }
         }
         __syncthreads();
+        const bool stop = rs.exit_flag[it & 1] || rs.n_active[it & 1] == 0;
         ++it;
-        if (rs.exit_flag || rs.n_active == 0) break;
+        if (stop) break;
     }
     if (RESIDENT) {
         for (int r = 0; r < R; ++r)
@@ -1758,8 +1849,8 @@ struct KmeansSession {
         a.assign = static_cast<uint8_t*>(e->scratch("km.assign", size_t(R) * a.stride));
         a.cent = static_cast<double*>(e->scratch("km.cent", size_t(K) * kMaxKnobs * 8));
         a.S = static_cast<long long*>(e->scratch("km.S", size_t(K) * kSumW * 8));
-        a.D = static_cast<unsigned long long*>(e->scratch("km.D", size_t(3) * K * kSumW * 8));
-        a.chg = static_cast<unsigned int*>(e->scratch("km.chg", 3 * kMaxRuns * 4));
+        a.D = static_cast<unsigned long long*>(e->scratch("km.D", size_t(3) * K * kSumW * kDStride * 8));
+        a.chg = static_cast<unsigned int*>(e->scratch("km.chg", 3 * kMaxRuns * kChgStride * 4));
         a.work = static_cast<unsigned int*>(e->scratch("km.work", 16));
         a.run_state = static_cast<int*>(e->scratch("km.state", kMaxRuns * 4));
         a.run_iter = static_cast<int*>(e->scratch("km.iter", kMaxRuns * 4));
@@ -1796,8 +1887,8 @@ struct KmeansSession {
         auto* h_loss = static_cast<double*>(e->staging("km.loss", 64 * 8));
         h_cent = static_cast<double*>(e->staging("km.cent", size_t(kMaxClusters) * kMaxKnobs * 8));
         while (true) {
-            KT_CUDA(cudaMemsetAsync(a.D, 0, size_t(3) * K * kSumW * 8, e->stream));
-            KT_CUDA(cudaMemsetAsync(a.chg, 0, 3 * kMaxRuns * 4, e->stream));
+            KT_CUDA(cudaMemsetAsync(a.D, 0, size_t(3) * K * kSumW * kDStride * 8, e->stream));
+            KT_CUDA(cudaMemsetAsync(a.chg, 0, 3 * kMaxRuns * kChgStride * 4, e->stream));
             KT_CUDA(cudaMemsetAsync(a.work, 0, 16, e->stream));
             KT_CUDA(cudaMemsetAsync(a.barrier, 0, 16, e->stream));
             a.it0 = it;
@@ -1863,8 +1954,10 @@ struct KmeansSession {
             for (int it = 0; it + 1 < std::min(100, mp); ++it) {
                 const long long* t = tl + it * 8;
                 std::fprintf(stderr, "[lloyd] pass %d: centroids %.1f us, scan %.1f us, eval %.1f us, flush %.1f us, "
-                             "barrier %.1f us, rest %.1f us\n", it, (t[1] - t[0]) * 1e-3, (t[2] - t[1]) * 1e-3,
-                             (t[3] - t[2]) * 1e-3, (t[4] - t[3]) * 1e-3, (t[5] - t[4]) * 1e-3, (t[8] - t[5]) * 1e-3);
+                             "barrier %.1f us, rest %.1f us (update %.1f us, sync %.1f us, decide+commit %.1f us)\n",
+                             it, (t[1] - t[0]) * 1e-3, (t[2] - t[1]) * 1e-3, (t[3] - t[2]) * 1e-3, (t[4] - t[3]) * 1e-3,
+                             (t[5] - t[4]) * 1e-3, (t[8] - t[5]) * 1e-3, (t[6] - t[5]) * 1e-3, (t[7] - t[6]) * 1e-3,
+                             (t[8] - t[7]) * 1e-3);
             }
         }
         int max_passes = 0;
@@ -2220,8 +2313,8 @@ int kt_lloyd_create(kt_engine* e, const uint64_t* shard_pts_dev, int64_t shard_m
     a.dcum = static_cast<float*>(l->alloc(size_t(K) * 4));
     a.cent = static_cast<double*>(l->alloc(size_t(K) * kMaxKnobs * 8));
     a.S = static_cast<long long*>(l->alloc(size_t(K) * kSumW * 8));
-    a.D = static_cast<unsigned long long*>(l->alloc(size_t(3) * K * kSumW * 8));
-    a.chg = static_cast<unsigned int*>(l->alloc(3 * kMaxRuns * 4));
+    a.D = static_cast<unsigned long long*>(l->alloc(size_t(3) * K * kSumW * kDStride * 8));
+    a.chg = static_cast<unsigned int*>(l->alloc(3 * kMaxRuns * kChgStride * 4));
     a.work = static_cast<unsigned int*>(l->alloc(16));
     a.run_state = static_cast<int*>(l->alloc(kMaxRuns * 4));
     a.run_iter = static_cast<int*>(l->alloc(kMaxRuns * 4));
