@@ -1051,7 +1051,15 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
     // the dynamic window is only guaranteed 8-byte aligned after static smem (tools add their
     // own static smem): align explicitly for the float4 centroid loads (16 spare bytes allocated)
     // generic pointer arithmetic measured faster here than align_shared<16> (1.60 vs 1.95 ms per 1M-point knee scan)
-    unsigned char* s_raw = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(s_dyn) + 15) & ~uintptr_t(15));
+#ifndef KT_SMEM_PROVENANCE
+#define KT_SMEM_PROVENANCE 0
+#endif
+    // KT_SMEM_PROVENANCE 1 offsets from s_dyn itself so every derived pointer keeps the shared
+    // address space (LDS / STS instead of generic LD / ST): measured SLOWER on B200 (1M-point
+    // knee scan 1.20 -> 1.59 ms; heavy-pass evaluation 33 -> 45 us, grid-barrier wait 2 -> 5 us)
+    unsigned char* s_raw = KT_SMEM_PROVENANCE
+        ? s_dyn + ((16u - (unsigned(__cvta_generic_to_shared(s_dyn)) & 15u)) & 15u)
+        : reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(s_dyn) + 15) & ~uintptr_t(15));
     const LloydLayout L = lloyd_layout(a.K);
     double* c64 = reinterpret_cast<double*>(s_raw + L.c64);
     long long* S = reinterpret_cast<long long*>(s_raw + L.S);
