@@ -501,6 +501,11 @@ def run_rl(args, rank: int, world: int, local_rank: int) -> None:
 
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
 
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+
     line = bench_rl.run(args, rank, world, local_rank, kt, torch, dist, {"barrier": barrier, "clock": ClockSampler})
     if line is not None:
         print(json.dumps(line), flush=True)

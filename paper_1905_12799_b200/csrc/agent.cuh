@@ -53,7 +53,11 @@ struct PaddedWeights64 {
 static_assert(sizeof(PaddedWeights64) % 16 == 0, "bulk-copy granularity");
 
 constexpr int kAgentsPerCta = 32;   // one agent per lane
-constexpr int kRolloutThreads = 256;  // warp w: outputs [16w, 16w+16) of each layer, knob w when sampling
+// warp w: outputs [8w, 8w+8) of each layer (16 warps: 2x the latency hiding of 8 warps x 16
+// outputs, half the accumulator registers), knob w when sampling, warp 8 the value head
+constexpr int kRolloutThreads = 512;
+constexpr int kRolloutWarps = kRolloutThreads / 32;
+constexpr int kRolloutOut = kH / kRolloutWarps;
 
 struct RolloutArgs {
     const PaddedWeights64* w64;

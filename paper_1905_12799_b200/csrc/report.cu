@@ -110,7 +110,7 @@ int kt_step_best(kt_engine* e, const double* scores_dev, const int32_t* steps_de
     auto* best = static_cast<unsigned long long*>(e->scratch("report.best", size_t(cap) * 8 + 8));
     int* hz = reinterpret_cast<int*>(best + cap);
     KT_CUDA(cudaMemsetAsync(best, 0, size_t(cap) * 8, e->stream));  // key 0 < every encoded double
-    KT_CUDA(cudaMemsetAsync(hz, 0xff, 4, e->stream));
+    KT_CUDA(cudaMemsetAsync(hz, 0xff, 8, e->stream));  // the whole trailing word (read back)
     const int grid = int(std::min<int64_t>(ceil_div(count, 256), int64_t(e->num_sms) * 4));
     e->pre_launch("step_best");
     step_best_kernel<<<grid, 256, 0, e->stream>>>(scores_dev, steps_dev, count, cap, best, hz);

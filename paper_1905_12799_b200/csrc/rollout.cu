@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(kRolloutThreads, 1) rollout_kernel(RolloutArgs
     }
     umma::mbar_wait(mbar, 0);
     int steps = 0;
-    const int o0 = warp * 16;
+    const int o0 = warp * kRolloutOut;
 
     for (int s = 0; s < a.S; ++s) {
         if (warp == 0) {
@@ -94,35 +94,35 @@ __global__ void __launch_bounds__(kRolloutThreads, 1) rollout_kernel(RolloutArgs
 
         // ---- h1 = tanh(x W1^T + b1)
         {
-            double acc[16];
+            double acc[kRolloutOut];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+            for (int j = 0; j < kRolloutOut; ++j) acc[j] = 0.0;
             for (int k = 0; k < n; ++k) {
                 const double xk = sm.xt[k][lane];
                 const double2* wr = reinterpret_cast<const double2*>(&sm.w.w1t[k][o0]);
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
+                for (int q = 0; q < kRolloutOut / 2; ++q) {
                     const double2 w2 = wr[q];
                     acc[2 * q] = fma(xk, w2.x, acc[2 * q]);
                     acc[2 * q + 1] = fma(xk, w2.y, acc[2 * q + 1]);
                 }
             }
 #pragma unroll
-            for (int j = 0; j < 16; ++j) sm.h[o0 + j][lane] = tanh(acc[j] + sm.w.b1[o0 + j]);
+            for (int j = 0; j < kRolloutOut; ++j) sm.h[o0 + j][lane] = tanh(acc[j] + sm.w.b1[o0 + j]);
         }
         __syncthreads();
         // ---- [hp | hv] = tanh(h1 [W2p | W2v]^T + [b2p | b2v])
         {
-            double acc[16];
+            double acc[kRolloutOut];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+            for (int j = 0; j < kRolloutOut; ++j) acc[j] = 0.0;
             if ((o0 & (kG - 1)) < a.g) {  // warps wholly inside the zero padding have nothing to add
 #pragma unroll 4
                 for (int k = 0; k < a.h; ++k) {
                     const double hk = sm.h[k][lane];
                     const double2* wr = reinterpret_cast<const double2*>(&sm.w.w2t[k][o0]);
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) {
+                    for (int q = 0; q < kRolloutOut / 2; ++q) {
                         const double2 w2 = wr[q];
                         acc[2 * q] = fma(hk, w2.x, acc[2 * q]);
                         acc[2 * q + 1] = fma(hk, w2.y, acc[2 * q + 1]);
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(kRolloutThreads, 1) rollout_kernel(RolloutArgs
             }
             __syncthreads();  // every warp has read h1
 #pragma unroll
-            for (int j = 0; j < 16; ++j) sm.h[o0 + j][lane] = tanh(acc[j] + sm.w.b2[o0 + j]);
+            for (int j = 0; j < kRolloutOut; ++j) sm.h[o0 + j][lane] = tanh(acc[j] + sm.w.b2[o0 + j]);
         }
         __syncthreads();
         // ---- logits (warp w: knob w's three) and the value (warp n, or warp 7 when n == 8)
@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(kRolloutThreads, 1) rollout_kernel(RolloutArgs
                 sm.z[lane][3 * warp + 1] = z1 + sm.w.b3p[3 * warp + 1];
                 sm.z[lane][3 * warp + 2] = z2 + sm.w.b3p[3 * warp + 2];
             }
-            if (warp == (n < kMaxKnobs ? n : kMaxKnobs - 1)) {
+            if (warp == (kRolloutWarps > kMaxKnobs ? kMaxKnobs : (n < kMaxKnobs ? n : kMaxKnobs - 1))) {
                 double v = 0.0;
                 for (int k = 0; k < a.g; ++k) v = fma(sm.h[kG + k][lane], sm.w.w3v[k], v);
                 sm.z[lane][kN3] = v + sm.w.b3v;

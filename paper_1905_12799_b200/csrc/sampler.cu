@@ -1117,9 +1117,11 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
     for (int i = tid; i < (K + kMaxRuns) * kMaxKnobs; i += blockDim.x) c2[i] = __int_as_float(0x7fc00000);  // NaN pads
     if (RESIDENT) {
         for (int r = 0; r < R; ++r) {
+            // budgets are only meaningful (and only written) once a run has bounds
+            const bool bounds = a.run_state[r] == kActiveFromSums;
             for (int i = tid; i < np; i += blockDim.x) {
                 s_asg[r * P + i] = a.assign[int64_t(r) * a.stride + b0 + i];
-                s_bud[r * P + i] = a.budget[int64_t(r) * a.stride + b0 + i];
+                s_bud[r * P + i] = bounds ? a.budget[int64_t(r) * a.stride + b0 + i] : 0.0f;
             }
             for (int i = np + tid; i < ((np + 3) & ~3); i += blockDim.x) s_asg[r * P + i] = 255;  // quad padding
         }
@@ -1518,6 +1520,7 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
                         if (lane + 32 < k)
                             dcum[co + lane + 32] = __fadd_ru(dcum[co + lane + 32], __fadd_ru(d1, lane + 32 == am ? m2 : m1));
                     }
+                    __syncwarp();  // every lane has read rs.state[r]
                     if (lane == 0) {
                         rs.state[r] = st;
                         rs.changed[r] = 0;

@@ -187,6 +187,7 @@ int kt_top_unvisited(kt_engine* e, const uint64_t* rows_dev, const double* score
     allow_dynamic_smem((const void*)top_final_kernel);
     auto* d_out = static_cast<uint64_t*>(e->scratch("top.out", kTopMax * 8 + 8));
     int* d_n = reinterpret_cast<int*>(d_out + kTopMax);
+    KT_CUDA(cudaMemsetAsync(d_out, 0, kTopMax * 8 + 8, e->stream));  // read back whole (initcheck-clean)
     e->pre_launch("top_final");
     top_final_kernel<<<1, 1024, smem, e->stream>>>(bkey, bidx, n, blocks, cap, rows_dev, d_out, d_n);
     e->check_launch("top_final");
