@@ -293,6 +293,16 @@ int kt_fit_trees(const double* features, const double* targets, int64_t m, int n
                  int32_t* right_out, double* value_out, int64_t node_capacity, int32_t* tree_offsets_out,
                  double* base_out);
 
+/* Same contract and bytes as kt_fit_trees, with the boosting loop on the GPU: one single-CTA
+ * kernel grows every tree (a warp per node of a level, a lane per feature for the split scans,
+ * float64 in the reference's operation order); the host only sorts (canonical lexsort order,
+ * per-feature stable argsorts).  depth <= 7, n_features <= 8 (else KT_ERR_UNSUPPORTED).
+ * Replaces cost_model.py:367-398 (fit) on the device path of the tuning loop (driver.py:142-148). */
+int kt_fit_trees_device(kt_engine* engine, const double* features, const double* targets, int64_t m, int n,
+                        int rounds, int depth, double learning_rate, int32_t* feature_out, double* threshold_out,
+                        int32_t* left_out, int32_t* right_out, double* value_out, int64_t node_capacity,
+                        int32_t* tree_offsets_out, double* base_out);
+
 /* ------------------------------------------------ trajectory analysis
  * per_step_best (report.py:53-69): best_out[s] = max score of the entries landing at step s
  * (-inf if none), s < cap; *horizon_out = max step index.  pca_project (report.py:227-253):

@@ -121,6 +121,8 @@ SIGNATURES = {
     "kt_lloyd_leaf_losses": (C.c_int, [P, P, C.c_int, pi64, C.c_int, pf64]),
     "kt_fit_trees": (C.c_int, [pf64, pf64, i64, C.c_int, C.c_int, C.c_int, f64, pi32, pf64, pi32, pi32, pf64, i64,
                                pi32, pf64]),
+    "kt_fit_trees_device": (C.c_int, [P, pf64, pf64, i64, C.c_int, C.c_int, C.c_int, f64, pi32, pf64, pi32, pi32,
+                                      pf64, i64, pi32, pf64]),
     "kt_step_best": (C.c_int, [P, P, P, i64, C.c_int, pf64, pi32]),
     "kt_pca_moments": (C.c_int, [P, P, i64, C.c_int, pi32, pi64, pi64]),
     "kt_pca_project": (C.c_int, [P, P, i64, C.c_int, pi32, pf64, pf64, pf64, P, P]),

@@ -18,6 +18,8 @@ from __future__ import annotations
 import json
 from dataclasses import dataclass
 
+import os
+
 import numpy as np
 
 from . import _lib, errors
@@ -217,11 +219,23 @@ class BoostParams:
             raise ValueError(f"learning_rate must be in (0, 1], got {self.learning_rate}")
 
 
-def fit(training, params=BoostParams(), seed: int = 0) -> CostModel:
+def _use_device_fit(params, n: int) -> bool:
+    """The device engine is opt-in: byte-identical, but the split search's exact float64 cumsums
+    are one sequential chain per (node, feature), and measured on B200 the single-CTA kernel is
+    ~3x slower than the native host engine at every size tried (m = 100 .. 20,000 rows:
+    profiles/r2/fit_device.txt), so the tuning loop keeps the host engine."""
+    return os.environ.get("KT_FIT_DEVICE", "") == "1" and int(params.depth) <= 7 and n <= 8
+
+
+def fit(training, params=BoostParams(), seed: int = 0, engine=None, device: bool | None = None) -> CostModel:
     """Gradient boosting under squared error (fit, cost_model.py:367-398) — native exact-greedy
     restatement (csrc/fit.cu) in numpy's operation order: the model is byte-identical to the
     reference's (its JSON compares equal).  ``training`` is the reference's TrainingSet (or any
     object with ``features`` (m, n) and ``targets`` (m,)); ``seed`` is unused, as in the reference.
+
+    ``device=True`` runs the boosting loop on the GPU (kt_fit_trees_device: one single-CTA
+    kernel grows every tree); the default runs the same algorithm natively on the host
+    (kt_fit_trees), which measured faster at tuning sizes.  Both give the same bytes.
     """
     params.validate()
     X = np.ascontiguousarray(np.asarray(training.features, dtype=np.float64))
@@ -241,10 +255,17 @@ def fit(training, params=BoostParams(), seed: int = 0) -> CostModel:
     offs = np.zeros(int(params.rounds) + 1, dtype=np.int32)
     base = _lib.C.c_double(0.0)
     C = _lib.C
-    _lib.call("kt_fit_trees", _lib.as_ptr(X, C.c_double), _lib.as_ptr(y, C.c_double), m, n, int(params.rounds),
-              int(params.depth), float(params.learning_rate), _lib.as_ptr(feat, C.c_int32),
-              _lib.as_ptr(thr, C.c_double), _lib.as_ptr(left, C.c_int32), _lib.as_ptr(right, C.c_int32),
-              _lib.as_ptr(val, C.c_double), cap, _lib.as_ptr(offs, C.c_int32), C.byref(base))
+    args = (_lib.as_ptr(X, C.c_double), _lib.as_ptr(y, C.c_double), m, n, int(params.rounds), int(params.depth),
+            float(params.learning_rate), _lib.as_ptr(feat, C.c_int32), _lib.as_ptr(thr, C.c_double),
+            _lib.as_ptr(left, C.c_int32), _lib.as_ptr(right, C.c_int32), _lib.as_ptr(val, C.c_double), cap,
+            _lib.as_ptr(offs, C.c_int32), C.byref(base))
+    if device is None:
+        device = _use_device_fit(params, n)
+    if device:
+        eng = engine if engine is not None else _lib.engine()
+        _lib.call("kt_fit_trees_device", eng.handle, *args)
+    else:
+        _lib.call("kt_fit_trees", *args)
     trees = []
     for r in range(int(params.rounds)):
         a, b = int(offs[r]), int(offs[r + 1])
