@@ -242,6 +242,24 @@ int kt_lloyd_clusters(const kt_lloyd* l, int32_t* n_clusters);
 int kt_lloyd_pass(kt_engine* e, kt_lloyd* l, uint64_t* ext_dev);
 /* states_out[r]: 0/1/5 active, 2 converged, 3 maxed (100 passes), 4 needs reseed. */
 int kt_lloyd_apply(kt_engine* e, kt_lloyd* l, const uint64_t* ext_dev, int32_t* states_out, int32_t* passes_out);
+/* Native NCCL communicator (loaded with dlopen; the unique id travels over the caller's
+ * process group) for the two exchanges north_star names, both on the engine stream with no
+ * host round trip: the k-means partial sums (sampler.py:94-115) and the PPO gradient /
+ * round-statistics all-reduce (agent.py:245-257).  kt_comm_all_reduce_f64 has the
+ * kt_all_reduce_f64_fn signature: pass it with user = the kt_comm* in a kt_collective.      */
+typedef struct kt_comm kt_comm;
+int kt_comm_unique_id(uint8_t* id_out /* 128 bytes */);
+int kt_comm_create(kt_engine* e, const uint8_t* id, int rank, int world, kt_comm** out);
+int kt_comm_destroy(kt_comm* c);
+int kt_comm_all_reduce_f64(void* comm, double* dev_buf, int64_t count);
+int kt_comm_all_reduce_i64(kt_comm* c, int64_t* dev_buf, int64_t count);
+/* Device-driven sharded Lloyd loop: enqueues `batch` rounds of pass -> ncclAllReduce(int64,
+ * comm; NULL = one rank) -> apply per host check (the iteration counter lives on the device);
+ * returns when no run is active or a run needs a reseed (*reseed_out = 1: do the host reseed
+ * with kt_lloyd_sums / kt_lloyd_farthest / kt_lloyd_set_centroids, then call again).
+ * Replaces the per-pass kt_lloyd_pass / all-reduce / kt_lloyd_apply host loop. */
+int kt_lloyd_run(kt_engine* e, kt_lloyd* l, kt_comm* comm, int batch, int32_t* states_out, int32_t* passes_out,
+                 int32_t* reseed_out);
 /* Global cluster sums (host int64 [K][9]: 8 coordinate sums, count). */
 int kt_lloyd_sums(kt_engine* e, kt_lloyd* l, int64_t* sums_out);
 /* Empty-cluster reseed (sampler.py:108-115): the shard's farthest point from its

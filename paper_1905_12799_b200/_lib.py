@@ -114,6 +114,12 @@ SIGNATURES = {
     "kt_lloyd_pass": (C.c_int, [P, P, P]),
     "kt_lloyd_apply": (C.c_int, [P, P, P, pi32, pi32]),
     "kt_lloyd_sums": (C.c_int, [P, P, pi64]),
+    "kt_lloyd_run": (C.c_int, [P, P, P, C.c_int, pi32, pi32, pi32]),
+    "kt_comm_unique_id": (C.c_int, [P]),
+    "kt_comm_create": (C.c_int, [P, P, C.c_int, C.c_int, C.POINTER(P)]),
+    "kt_comm_destroy": (C.c_int, [P]),
+    "kt_comm_all_reduce_f64": (C.c_int, [P, P, i64]),
+    "kt_comm_all_reduce_i64": (C.c_int, [P, P, i64]),
     "kt_lloyd_farthest": (C.c_int, [P, P, C.c_int, pi64, C.c_int, pf64, pi64]),
     "kt_lloyd_set_centroids": (C.c_int, [P, P, C.c_int, pf64]),
     "kt_lloyd_centroids": (C.c_int, [P, P, C.c_int, pf64]),

@@ -206,7 +206,7 @@ PPOHyper = _lib.PPOHyper
 
 
 def run_search_rows(agent, model, space, start_rows, engine=None, info: RoundInfo | None = None,
-                    rollout_out: dict | None = None, all_reduce=None, episode_offset: int = 0):
+                    rollout_out: dict | None = None, all_reduce=None, episode_offset: int = 0, collective=None):
     """Array path: CUDA int64 start rows -> (rows, scores, step indices) CUDA tensors; mutates ``agent``.
 
     ``rollout_out`` (optional dict) receives the rollout's per-step log-probs and
@@ -243,8 +243,8 @@ def run_search_rows(agent, model, space, start_rows, engine=None, info: RoundInf
         if rollout_out is not None:
             lp = torch.empty(E * S, dtype=torch.float64, device=start_rows.device)
             vals = torch.empty(E * S, dtype=torch.float64, device=start_rows.device)
-        coll = None
-        if all_reduce is not None:
+        coll = collective  # a ready kt_collective (e.g. shard.NativeComm: NCCL inside the library)
+        if coll is None and all_reduce is not None:
             errors_seen = []
 
             def _cb(user, ptr, count):

@@ -643,6 +643,7 @@ struct LloydArgs {
     int* ctrl;                 // [0] next iteration
     unsigned long long* stats; // optional [R][3]: point visits, unused, evaluations
     long long* timeline;       // optional [100][4] globaltimer stamps of block 0 per pass
+    const int* freeze;         // optional (device-driven sharded loop): nonzero -> the launch is a no-op
 };
 
 struct LloydLayout {
@@ -1044,6 +1045,7 @@ template <bool RESIDENT, bool BYTES>
 __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, RESIDENT ? 1 : 3)
     lloyd_kernel(LloydArgs a) {
     extern __shared__ __align__(16) unsigned char s_dyn[];
+    if (a.freeze && *a.freeze) return;  // every block reads the same flag: uniform exit
     __shared__ RunShared rs;
     __shared__ uint8_t run_of[kMaxClusters];
     __shared__ LloydQueueEntry wqueue[RESIDENT ? 1 : kLloydThreads / 32 * 128];
@@ -1578,6 +1580,36 @@ __global__ void lloyd_apply_kernel(LloydArgs a, const long long* __restrict__ ex
             if (ns != kActiveFromSums) a.run_iter[r] = it;
             a.run_state[r] = ns;
         }
+    }
+}
+
+// Device-driven variant for kt_lloyd_run: the iteration counter and a freeze flag live in
+// device memory, so the host can enqueue several pass -> all-reduce -> apply rounds ahead:
+// once a run needs a reseed (host work) every later enqueued pass and apply is a no-op.
+__global__ void lloyd_apply_dev_kernel(LloydArgs a, const long long* __restrict__ ext, int* it_dev, int* freeze) {
+    __shared__ long long S[kMaxClusters * kSumW];
+    __shared__ int any_reseed;
+    if (*freeze) return;
+    const int K = a.K;
+    const int it = *it_dev;
+    if (threadIdx.x == 0) any_reseed = 0;
+    for (int i = threadIdx.x; i < K * kSumW; i += blockDim.x) S[i] = a.S[i] + ext[i];
+    __syncthreads();
+    for (int i = threadIdx.x; i < K * kSumW; i += blockDim.x) a.S[i] = S[i];
+    if (threadIdx.x < a.R) {
+        const int r = threadIdx.x;
+        const int st = a.run_state[r];
+        if (run_active(st)) {
+            const int ns = lloyd_decide(a, S, r, st, ext[size_t(K) * kSumW + r] != 0, it);
+            if (ns != kActiveFromSums) a.run_iter[r] = it;
+            if (ns == kNeedsReseed) atomicOr(&any_reseed, 1);
+            a.run_state[r] = ns;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        *it_dev = it + 1;
+        if (any_reseed) *freeze = 1;
     }
 }
 
@@ -2263,6 +2295,11 @@ int kt_adaptive_sample(kt_engine* e, const uint64_t* rows_dev, int64_t count, in
 // and all-reduces (sum) the int64 buffer [K][9] cluster deltas + [R] changed counts
 // between kt_lloyd_pass and kt_lloyd_apply; every rank then holds the same global
 // sums, so decisions and centroids are identical everywhere (exact integers).
+struct kt_comm;
+namespace kt {
+void comm_all_reduce_i64(kt_comm* c, int64_t* buf, int64_t count);  // comm.cu
+}
+
 struct kt_lloyd {
     kt_engine* e = nullptr;
     const uint64_t* pts = nullptr;
@@ -2274,6 +2311,8 @@ struct kt_lloyd {
     int it = 0;
     std::vector<void*> bufs;
     double* pd2 = nullptr;
+    int* it_dev = nullptr;     // device-driven loop: [0] iteration, [1] freeze flag
+    uint64_t* ext_dev = nullptr;
 
     void* alloc(size_t bytes) {
         void* p = nullptr;
@@ -2378,6 +2417,60 @@ int kt_lloyd_pass(kt_engine* e, kt_lloyd* l, uint64_t* ext_dev) {
     e->pre_launch("lloyd");
     KT_CUDA(cudaLaunchCooperativeKernel(l->plan.kern, l->plan.grid, l->plan.threads, params, l->plan.smem, e->stream));
     e->check_launch("lloyd");
+    KT_API_END
+}
+
+int kt_lloyd_run(kt_engine* e, kt_lloyd* l, kt_comm* comm, int batch, int32_t* states_out, int32_t* passes_out,
+                 int32_t* reseed_out) {
+    KT_API_BEGIN
+    LloydArgs& a = l->a;
+    if (batch < 1) fail(KT_ERR_VALUE, "batch must be >= 1");
+    const int64_t next = int64_t(a.K) * kSumW + a.R;
+    if (!l->it_dev) l->it_dev = static_cast<int*>(l->alloc(16));
+    if (!l->ext_dev) l->ext_dev = static_cast<uint64_t*>(l->alloc(size_t(next) * 8));
+    auto* hs = static_cast<int*>(e->staging("lloyd.run", (2 * kMaxRuns + 4) * 4));
+    hs[0] = l->it;
+    hs[1] = 0;
+    KT_CUDA(cudaMemcpyAsync(l->it_dev, hs, 8, cudaMemcpyHostToDevice, e->stream));
+    a.ext = reinterpret_cast<unsigned long long*>(l->ext_dev);
+    a.freeze = l->it_dev + 1;
+    a.stats = nullptr;
+    a.timeline = nullptr;
+    allow_dynamic_smem((const void*)l->plan.kern);
+    *reseed_out = 0;
+    for (;;) {
+        for (int c = 0; c < batch; ++c) {  // enqueued ahead: no host synchronisation inside a batch
+            KT_CUDA(cudaMemsetAsync(l->ext_dev, 0, size_t(next) * 8, e->stream));
+            KT_CUDA(cudaMemsetAsync(a.work, 0, 16, e->stream));
+            KT_CUDA(cudaMemsetAsync(a.barrier, 0, 16, e->stream));
+            a.it0 = l->it + c;  // only indexes scratch in the external pass; the decision reads it_dev
+            a.it_end = a.it0 + 1;
+            void* params[] = {&a};
+            e->pre_launch("lloyd");
+            KT_CUDA(cudaLaunchCooperativeKernel(l->plan.kern, l->plan.grid, l->plan.threads, params, l->plan.smem,
+                                                e->stream));
+            e->check_launch("lloyd");
+            if (comm) comm_all_reduce_i64(comm, reinterpret_cast<int64_t*>(l->ext_dev), next);
+            e->pre_launch("lloyd_apply_dev");
+            lloyd_apply_dev_kernel<<<1, 256, 0, e->stream>>>(a, reinterpret_cast<const long long*>(l->ext_dev),
+                                                             l->it_dev, l->it_dev + 1);
+            e->check_launch("lloyd_apply_dev");
+        }
+        KT_CUDA(cudaMemcpyAsync(hs, l->it_dev, 8, cudaMemcpyDeviceToHost, e->stream));
+        KT_CUDA(cudaMemcpyAsync(hs + 2, a.run_state, a.R * 4, cudaMemcpyDeviceToHost, e->stream));
+        KT_CUDA(cudaMemcpyAsync(hs + 2 + kMaxRuns, a.run_iter, a.R * 4, cudaMemcpyDeviceToHost, e->stream));
+        e->sync();
+        l->it = hs[0];
+        bool active = false;
+        for (int r = 0; r < a.R; ++r) active |= run_active(hs[2 + r]);
+        if (hs[1] || !active) break;
+    }
+    a.freeze = nullptr;
+    for (int r = 0; r < a.R; ++r) {
+        states_out[r] = hs[2 + r];
+        if (passes_out) passes_out[r] = run_active(hs[2 + r]) ? l->it : hs[2 + kMaxRuns + r] + 1;
+    }
+    *reseed_out = hs[1];
     KT_API_END
 }
 

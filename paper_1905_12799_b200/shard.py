@@ -30,6 +30,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -155,6 +156,7 @@ class Comm:
         self.world = dist.get_world_size(group)
         self.device = device
         self.scope = stream_scope
+        self.native = None  # NativeComm when the group is an NCCL group (set by the GPU entry points)
 
     def all_reduce_sum(self, t) -> None:
         self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
@@ -183,6 +185,50 @@ class Comm:
         outs = [torch.empty_like(buf) for _ in range(self.world)]
         self.dist.all_gather(outs, buf, group=self.group)
         return torch.cat([o[:s] for o, s in zip(outs, sizes)])
+
+
+class NativeComm:
+    """kt_comm: an NCCL communicator of the engine library over the ranks of ``group`` (the
+    unique id is broadcast over the torch process group).  Its all-reduces run on the engine
+    stream inside the library: kt_lloyd_run's per-pass k-means exchange and, as a kt_collective
+    callback, the PPO statistics / gradient all-reduce — no Python per exchange."""
+
+    _cache: dict = {}
+
+    def __init__(self, eng, group=None):
+        import torch.distributed as dist
+
+        self.eng = eng
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        uid = np.zeros(128, dtype=np.uint8)
+        if self.rank == 0:
+            _lib.call("kt_comm_unique_id", _lib.as_ptr(uid, C.c_uint8))
+        obj = [uid.tobytes()]
+        src = dist.get_global_rank(group, 0) if group is not None else 0
+        dist.broadcast_object_list(obj, src=src, group=group)
+        uid = np.frombuffer(obj[0], dtype=np.uint8).copy()
+        h = _lib.P()
+        _lib.call("kt_comm_create", eng.handle, _lib.as_ptr(uid, C.c_uint8), self.rank, self.world, C.byref(h))
+        self.handle = h
+
+    @classmethod
+    def for_group(cls, eng, group=None):
+        """One communicator per (engine, group) for the life of the process, or None when the
+        group is not an NCCL group (gloo / CPU tests keep the torch.distributed path)."""
+        import torch.distributed as dist
+
+        if dist.get_backend(group) != "nccl" or os.environ.get("KT_NATIVE_COMM", "1") == "0":
+            return None
+        key = (id(eng), id(group), dist.get_rank(group), dist.get_world_size(group))
+        if key not in cls._cache:
+            cls._cache[key] = cls(eng, group)
+        return cls._cache[key]
+
+    def collective(self, episode_offset: int):
+        """kt_collective whose callback is kt_comm_all_reduce_f64 itself (a C function)."""
+        fn = C.cast(_lib.load().kt_comm_all_reduce_f64, C.c_void_p).value
+        return _lib.Collective(_lib.ALL_REDUCE_F64(fn), self.handle, int(episode_offset))
 
 
 # ------------------------------------------------------------------ GPU backend
@@ -217,6 +263,15 @@ class GpuLloydShard:
     def local_pass(self):
         _lib.call("kt_lloyd_pass", self.eng.handle, self.h, _lib.ptr(self.ext))
         return self.ext
+
+    def run(self, native: "NativeComm", batch: int = 8):
+        """Device-driven passes (kt_lloyd_run) until convergence or a reseed."""
+        st = np.zeros(len(self.ks), dtype=np.int32)
+        ps = np.zeros(len(self.ks), dtype=np.int32)
+        reseed = C.c_int32(0)
+        _lib.call("kt_lloyd_run", self.eng.handle, self.h, native.handle if native is not None else None, int(batch),
+                  _lib.as_ptr(st, C.c_int32), _lib.as_ptr(ps, C.c_int32), C.byref(reseed))
+        return st.tolist(), ps.tolist()
 
     def apply(self, ext):
         st = np.zeros(len(self.ks), dtype=np.int32)
@@ -286,11 +341,15 @@ def lloyd_runs(backend, comm: Comm, shards: PointShards, full_rows_host: np.ndar
     offs = np.concatenate([[0], np.cumsum(ks)]).astype(int)
     states = [1] * len(ks)
     passes = [0] * len(ks)
+    native = getattr(comm, "native", None)
     while any(s in ACTIVE_STATES for s in states):
         with scope():
-            ext = backend.local_pass()
-            comm.all_reduce_sum(ext)
-            states, passes = backend.apply(ext)
+            if native is not None and hasattr(backend, "run"):
+                states, passes = backend.run(native)  # passes + NCCL exchange on the device
+            else:
+                ext = backend.local_pass()
+                comm.all_reduce_sum(ext)
+                states, passes = backend.apply(ext)
         if NEEDS_RESEED in states:
             S = backend.sums()
             for r, st in enumerate(states):
@@ -386,6 +445,7 @@ def adaptive_sample_sharded(rows_local, visited, space, seed: int, group=None,
 
     eng = _lib.engine()
     comm = Comm(group, device=f"cuda:{eng.device}")
+    comm.native = NativeComm.for_group(eng, group)
     cards = np.ascontiguousarray(sp.check_engine_space(space), dtype=np.int32)
     n = cards.size
     with eng.scope():
@@ -464,6 +524,11 @@ def run_search_rows_sharded(agent, model, space, start_rows_local, episode_offse
     """
     from .agent import run_search_rows
 
+    eng = engine if engine is not None else _lib.engine()
+    native = NativeComm.for_group(eng, group)
+    if native is not None:  # statistics and gradients all-reduced by NCCL inside the library
+        return run_search_rows(agent, model, space, start_rows_local, engine=eng, info=info,
+                               collective=native.collective(episode_offset), episode_offset=episode_offset)
     comm = Comm(group)
-    return run_search_rows(agent, model, space, start_rows_local, engine=engine, info=info,
+    return run_search_rows(agent, model, space, start_rows_local, engine=eng, info=info,
                            all_reduce=comm.all_reduce_sum, episode_offset=episode_offset)

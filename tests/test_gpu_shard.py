@@ -203,7 +203,14 @@ def test_adaptive_sample_sharded_world1_nccl():
         idx = np.vstack([idx, idx[:3000]])
         rows = dev_rows(idx)
         visited = sp.pack(idx[:20])
+        eng = kt.engine()
+        eng.set_timing(True)
+        eng.kernel_stats(reset=True)
         got = shard.adaptive_sample_sharded(rows, visited, space, seed=17)
+        stats = eng.kernel_stats(reset=True)
+        eng.set_timing(False)
+        # the device-driven loop ran: pass -> ncclAllReduce -> apply on the engine stream
+        assert "lloyd_apply_dev" in stats and shard.NativeComm.for_group(eng) is not None
         ref = kt.adaptive_sample_rows(rows, visited, space, seed=17)
         assert got.tolist() == np.asarray(ref).tolist()
         want = osamp.adaptive_sample(idx, {tuple(r) for r in idx[:20].tolist()}, cards.tolist(), 17)
@@ -289,10 +296,60 @@ def test_sharded_search_round_world1_nccl_equals_unsharded():
     os.environ["MASTER_PORT"] = str(_free_port())
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
     try:
-        r2, s2, t2 = shard.run_search_rows_sharded(a2, model, space, rows, episode_offset=0)
+        def no_torch_collectives(*_a, **_k):  # the native kt_comm path must carry every exchange
+            raise AssertionError("torch.distributed all_reduce used on the sharded PPO path")
+
+        orig = shard.Comm.all_reduce_sum
+        shard.Comm.all_reduce_sum = no_torch_collectives
+        try:
+            r2, s2, t2 = shard.run_search_rows_sharded(a2, model, space, rows, episode_offset=0)
+        finally:
+            shard.Comm.all_reduce_sum = orig
     finally:
         dist.destroy_process_group()
     assert torch.equal(r1, r2) and torch.equal(s1, s2) and torch.equal(t1, t2)
     from paper_1905_12799_b200.agent import _flat
 
     assert np.array_equal(_flat(a1.params), _flat(a2.params))
+
+
+@pytest.mark.parametrize("batch", [1, 3, 8])
+def test_device_driven_reseed_world1_nccl(batch, monkeypatch):
+    """kt_lloyd_run (pass -> ncclAllReduce -> apply enqueued `batch` rounds ahead, device-side
+    iteration counter and freeze flag) through an empty-cluster reseed: bit-exact vs the
+    oracle's Lloyd from the same init (sampler.py:94-116)."""
+    import torch.distributed as dist
+
+    from test_shard import lloyd_from_init
+
+    rng = np.random.default_rng(11)
+    idx = osamp.distinct_rows(rng.integers(0, 30, size=(2500, 4)))
+    pts = idx.astype(np.float64)
+    init = np.vstack([idx[:5], idx[:3]])  # centroids 5..7 duplicate 0..2 -> empty clusters
+    cent, asg, hist = lloyd_from_init(pts, init.astype(np.float64))
+    cards = np.full(4, 30, dtype=np.int32)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(_free_port())
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+    try:
+        eng = kt.engine(0)
+        distinct = dev_rows(idx, cards)
+        ps = shard.point_shards(len(idx), 1)
+        be = shard.GpuLloydShard(eng, distinct, 4, cards, [8], sp.pack(init, cards))
+        orig_run = be.run
+        monkeypatch.setattr(be, "run", lambda native: orig_run(native, batch))
+        comm = shard.Comm(None, device="cuda:0")
+        comm.native = shard.NativeComm.for_group(eng)
+        assert comm.native is not None
+        eng.set_timing(True)
+        eng.kernel_stats(reset=True)
+        res = shard.lloyd_runs(be, comm, ps, sp.pack(idx, cards), 4, lambda r: rows_to_float(r, 4, cards))
+        stats = eng.kernel_stats(reset=True)
+        eng.set_timing(False)
+        assert "lloyd_apply_dev" in stats
+        assert np.array_equal(be.assignment(0), asg)
+        assert np.array_equal(res[0].centroids, cent)
+        assert res[0].loss == hist[-1] and res[0].passes == len(hist)
+    finally:
+        dist.destroy_process_group()
