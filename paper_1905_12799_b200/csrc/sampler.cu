@@ -823,7 +823,9 @@ __device__ __forceinline__ int full_assign(const float* c32, const float* c2, co
     }
     if (k > 1 && !(second - best > d2_bound(best, k1) + d2_bound(second, k1))) {
         // ambiguous: the reference's own float64 expression decides (ties -> lowest j)
-        // (rare: rolled loops keep the resident kernel's loop body small)
+        // (rare: rolled loops keep the resident kernel's loop body small; an out-of-line
+        // __noinline__ version and a compile-time delta variant both measured slower:
+        // 1.18 -> 1.33 / 1.26 ms per 1M-point knee scan)
         double bd = INFINITY;
 #pragma unroll 1
         for (int j = 0; j < k; ++j) {
@@ -1146,7 +1148,7 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
         if (kLloydProbes && a.timeline && blockIdx.x == 0 && tid == 0 && it < 100) {
             long long t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            a.timeline[it * 8 + phase] = t;
+            a.timeline[it * 16 + phase] = t;
         }
     };
     int tile_parity = 0;  // queue counter in use (alternates per tile, across passes too)
@@ -1282,6 +1284,7 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
                         }
                     }
                 }
+                if (t0 == 0) stamp(10);
                 __syncthreads();
                 if (t0 == 0) stamp(2);
                 if (tid == 0) s_qn[tile_parity ^ 1] = 0;
@@ -1333,6 +1336,7 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
                     }
                 }
                 tile_parity ^= 1;
+                if (t0 == 0) stamp(11);
                 __syncthreads();
                 if (t0 == 0) stamp(3);
             }
@@ -1530,6 +1534,7 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
                 }
             }
         }
+        stamp(8);
         // same phase: commit the next pass's centroids of the runs that go on (converged /
         // maxed runs keep the centroids of their last pass: the reference's result; reseeds
         // are set by the host).  "Goes on" is decided from inputs this phase does not write
@@ -1544,6 +1549,7 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
                 if (blockIdx.x == 0) a.cent[x] = c;
             }
         }
+        stamp(9);
         __syncthreads();
         const bool stop = rs.exit_flag[it & 1] || rs.n_active[it & 1] == 0;
         ++it;
@@ -1679,6 +1685,9 @@ static LloydPlan plan_lloyd(kt_engine* e, int64_t m, int K, int R, LloydArgs& a)
     const bool force_stream = mode && std::strcmp(mode, "stream") == 0;
     const int64_t P = ((ceil_div(m, int64_t(e->num_sms)) + 15) & ~int64_t(15));
     const bool bytes = a.fmt.bytes != 0;
+    // byte rows: the byte kernel packs all 8 bytes (unused knobs are 0), field bound 255
+    const int64_t field_max = bytes ? 255 : std::max<int64_t>(1, a.fmt.cmax);
+    const bool pack3 = P * field_max < (int64_t(1) << 21) && !std::getenv("KT_LLOYD_PACK5");
     const void* kres = bytes ? (const void*)lloyd_kernel<true, true> : (const void*)lloyd_kernel<true, false>;
     const void* kstr = bytes ? (const void*)lloyd_kernel<false, true> : (const void*)lloyd_kernel<false, false>;
     cudaFuncAttributes fa{};
@@ -1713,9 +1722,7 @@ static LloydPlan plan_lloyd(kt_engine* e, int64_t m, int K, int R, LloydArgs& a)
         a.per_block = P;
         a.tile = int(tile);
         a.rows_resident = rows_res ? 1 : 0;
-        // byte rows: the byte kernel packs all 8 bytes (unused knobs are 0), field bound 255
-        const int64_t field_max = bytes ? 255 : std::max<int64_t>(1, a.fmt.cmax);
-        a.pack3 = (P * field_max < (int64_t(1) << 21) && !std::getenv("KT_LLOYD_PACK5")) ? 1 : 0;
+        a.pack3 = pack3 ? 1 : 0;
         if (const char* t = std::getenv("KT_LLOYD_TILE"))  // tests: force many tiles per block
             a.tile = std::max(4, std::min(a.tile, std::atoi(t) & ~3));
     } else {
@@ -1906,7 +1913,7 @@ struct KmeansSession {
             KT_CUDA(cudaMemsetAsync(a.stats, 0, kMaxRuns * 3 * 8, e->stream));
         }
         static const bool want_timeline = kLloydProbes && std::getenv("KT_LLOYD_TIMELINE") != nullptr;
-        a.timeline = want_timeline ? static_cast<long long*>(e->scratch("km.timeline", 800 * 8)) : nullptr;
+        a.timeline = want_timeline ? static_cast<long long*>(e->scratch("km.timeline", 1600 * 8)) : nullptr;
         double* d_loss = static_cast<double*>(e->scratch("km.loss", kMaxRuns * 8));
         a.budget = static_cast<float*>(e->scratch("km.budget", size_t(R) * a.stride * sizeof(float)));
         a.dcum = static_cast<float*>(e->scratch("km.dcum", size_t(K) * sizeof(float)));
@@ -1990,17 +1997,19 @@ struct KmeansSession {
                              hs[r * 3], hs[r * 3 + 1], hs[r * 3 + 2]);
         }
         if (a.timeline) {
-            long long tl[800];
+            long long tl[1600];
             KT_CUDA(cudaMemcpy(tl, a.timeline, sizeof(tl), cudaMemcpyDeviceToHost));
             int mp = 0;
             for (int r = 0; r < R; ++r) mp = std::max(mp, h_iter[r] + 1);
             for (int it = 0; it + 1 < std::min(100, mp); ++it) {
-                const long long* t = tl + it * 8;
+                const long long* t = tl + it * 16;
                 std::fprintf(stderr, "[lloyd] pass %d: centroids %.1f us, scan %.1f us, eval %.1f us, flush %.1f us, "
-                             "barrier %.1f us, rest %.1f us (update %.1f us, sync %.1f us, decide+commit %.1f us)\n",
+                             "barrier %.1f us, rest %.1f us (update %.1f us, sync %.1f us, decide %.1f us, commit %.1f us, "
+                             "final sync %.1f us; own scan %.1f us, own eval %.1f us)\n",
                              it, (t[1] - t[0]) * 1e-3, (t[2] - t[1]) * 1e-3, (t[3] - t[2]) * 1e-3, (t[4] - t[3]) * 1e-3,
-                             (t[5] - t[4]) * 1e-3, (t[8] - t[5]) * 1e-3, (t[6] - t[5]) * 1e-3, (t[7] - t[6]) * 1e-3,
-                             (t[8] - t[7]) * 1e-3);
+                             (t[5] - t[4]) * 1e-3, (t[16] - t[5]) * 1e-3, (t[6] - t[5]) * 1e-3, (t[7] - t[6]) * 1e-3,
+                             (t[8] - t[7]) * 1e-3, (t[9] - t[8]) * 1e-3, (t[16] - t[9]) * 1e-3, (t[10] - t[1]) * 1e-3,
+                             (t[11] - t[2]) * 1e-3);
             }
         }
         int max_passes = 0;
