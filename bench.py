@@ -37,7 +37,7 @@ WORKLOAD = ("resnet18.c2_3x3_64x64_56 space (S2: 84x80x80x7x2x2x3x2 = 90,316,800
             "the step's own rounded centroids (measured in an earlier round) + 62 earlier measurements, so batch "
             "assembly takes the reference's mode branch (sampler.py:203-209) every step")
 GOLDEN = ROOT / "tests" / "golden" / "bench_golden.json"
-TRAFFIC_ROUND = "r1"  # profiles/<round>/traffic.json: ncu --set full DRAM bytes per launch
+TRAFFIC_ROUND = "r2"  # profiles/<round>/traffic.json: ncu --set full DRAM bytes per launch
 
 
 def load_model():
@@ -551,6 +551,7 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cpu-full", action="store_true", help="skip the one full-size (1M) CPU step (~2 min)")
     ap.add_argument("--no-wall95", action="store_true", help="skip the wall-time-to-95%%-best tune runs")
+    ap.add_argument("--rl-serial", action="store_true", help="--workload rl: tasks in sequence on one engine")
     ap.add_argument("--workload", choices=("s2", "rl", "c4"), default="s2",
                     help="s2: the headline scored+clustered step; rl: 5 tasks x 4096 PPO agents per step; "
                          "c4: ResNet-18's 12 tasks x 1M candidates placed over the ranks (configs[3])")

@@ -4,7 +4,9 @@ Per step and rank: AlexNet's 5 conv tasks (workloads.ALEXNET_TASKS; surrogates
 and landscapes in data/models/alexnet_task*.json), each runs one search round
 with 4096 PPO agents (K1 rollout, K2 scoring, K4 GAE, K5 PPO update) followed by
 adaptive_sample on its trajectory (K6/K7/K8/K9).  Metric: trajectory candidates
-scored + clustered per second.  conv3/conv4 have tile_f cardinality 480, so
+scored + clustered per second.  The tasks are independent (configs[1]), so by default each runs
+on its own engine (stream) from its own host thread: one task's host-side work and
+latency-bound kernels overlap the others' (--rl-serial: one engine, tasks in sequence).  conv3/conv4 have tile_f cardinality 480, so
 their rows use the bit-field layout (space.row_layout).
 """
 
@@ -43,9 +45,13 @@ def cpu_rl_step(docs, rng_seed: int, agents: int):
 
 def run(args, rank: int, world: int, local_rank: int, kt, torch, dist, helpers) -> dict | None:
     """GPU arm; returns the JSON line (rank 0) or None."""
+    import threading
+
     sp = kt.space
     docs = task_docs()
     eng = kt.engine(local_rank)
+    serial = bool(getattr(args, "rl_serial", False))
+    engines = [eng] * N_TASKS if serial else [eng] + [kt._lib.Engine(local_rank) for _ in range(N_TASKS - 1)]
     dev = f"cuda:{local_rank}"
     tasks = []
     for i, d in enumerate(docs):
@@ -61,47 +67,88 @@ def run(args, rank: int, world: int, local_rank: int, kt, torch, dist, helpers) 
     no_visited = np.zeros(0, dtype=np.uint64)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
-    def step(s, e2e_batch=None, infos=None):
-        n = 0
-        for space, model, agent, host_starts in tasks:
-            with eng.scope():
+    def task_step(i, s, out, infos):
+        space, model, agent, host_starts = tasks[i]
+        e = engines[i]
+        with torch.cuda.stream(e.stream):  # this thread's current stream = its engine's
+            with e.scope():
                 starts = host_starts[s % 2].to(dev, non_blocking=True)
-            rows, scores, _ = kt.run_search_rows(agent, model, space, starts, engine=eng)
+            rows, scores, _ = kt.run_search_rows(agent, model, space, starts, engine=e)
             info = kt._lib.SampleInfo() if infos is not None else None
-            batch = kt.adaptive_sample_rows(rows, no_visited, space, seed=s, engine=eng, info=info)
-            if infos is not None:
-                infos.append({"entries": int(rows.numel()), "distinct": int(info.n_distinct), "k": int(info.chosen_k),
-                              "lloyd_passes": int(info.lloyd_passes), "lloyd_launches": int(info.lloyd_launches)})
-            n += int(rows.numel())
-            if e2e_batch is not None:
-                e2e_batch.append(batch.nbytes)
-        return n
+            batch = kt.adaptive_sample_rows(rows, no_visited, space, seed=s, engine=e, info=info)
+        if infos is not None:
+            infos[i] = {"entries": int(rows.numel()), "distinct": int(info.n_distinct), "k": int(info.chosen_k),
+                        "lloyd_passes": int(info.lloyd_passes), "lloyd_launches": int(info.lloyd_launches)}
+        out[i] = (int(rows.numel()), batch.nbytes)
+
+    def step(s, e2e_batch=None, infos=None):
+        """One step of all tasks, ordered after the caller's stream and joined back into it."""
+        main = torch.cuda.current_stream(local_rank)
+        go = torch.cuda.Event()
+        go.record(main)
+        for e in set(engines):
+            e.stream.wait_event(go)
+        out = [None] * N_TASKS
+        if serial:
+            for i in range(N_TASKS):
+                task_step(i, s, out, infos)
+        else:
+            errs = []
+
+            def body(i):
+                try:
+                    task_step(i, s, out, infos)
+                except BaseException as ex:  # pragma: no cover - surfaced below
+                    errs.append(ex)
+
+            th = [threading.Thread(target=body, args=(i,)) for i in range(N_TASKS)]
+            for t in th:
+                t.start()
+            for t in th:
+                t.join()
+            if errs:
+                raise errs[0]
+        for e in set(engines):
+            done = torch.cuda.Event()
+            done.record(e.stream)
+            main.wait_event(done)
+        if e2e_batch is not None:
+            e2e_batch.extend(b for _, b in out)
+        return sum(c for c, _ in out)
 
     for w in range(args.warmup):
         step(w)
     helpers["barrier"]()
-    launches0 = eng.launches
+    uniq = list({id(e): e for e in engines}.values())
+    launches0 = sum(e.launches for e in uniq)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     n_total = 0
     d2h = []
+    main = torch.cuda.current_stream(local_rank)
     with helpers["clock"](local_rank) as clk:
         helpers["barrier"]()
         for s in range(args.steps):
             flush.fill_(float(s))
-            with eng.scope():
-                ev[s][0].record(eng.stream)
+            ev[s][0].record(main)
             n_total += step(s, d2h)
-            with eng.scope():
-                ev[s][1].record(eng.stream)
+            ev[s][1].record(main)
         helpers["barrier"]()
-    launches = eng.launches - launches0
+    launches = sum(e.launches for e in uniq) - launches0
     t = sum(a.elapsed_time(b) for a, b in ev) / 1e3
-    eng.set_timing(True)
-    eng.kernel_stats(reset=True)
-    infos = []
+    # per-kernel device times: one serial step (the engines' timing events would overlap otherwise)
+    for e in uniq:
+        e.set_timing(True)
+        e.kernel_stats(reset=True)
+    infos = [None] * N_TASKS
+    serial_saved, serial = serial, True
     step(0, infos=infos)
-    stats = eng.kernel_stats(reset=True)
-    eng.set_timing(False)
+    serial = serial_saved
+    stats = {}
+    for e in uniq:
+        for k, (c, ms) in e.kernel_stats(reset=True).items():
+            c0, m0 = stats.get(k, (0, 0.0))
+            stats[k] = (c0 + c, m0 + ms)
+        e.set_timing(False)
     times = torch.tensor([t, float(n_total)], dtype=torch.float64, device=dev)
     if dist is not None:
         tt = times.clone()
@@ -147,6 +194,7 @@ def run(args, rank: int, world: int, local_rank: int, kt, torch, dist, helpers) 
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+fp32/tf32", "data": "synthetic",
         "config": {"workload": f"AlexNet's {N_TASKS} conv tasks x {AGENTS} PPO agents per step: run_search_round "
                                f"(rollout, scoring, GAE, 3 PPO epochs) + adaptive_sample per task",
+                   "tasks": "serial on one engine" if serial else f"{N_TASKS} engines (streams) + host threads, concurrent",
                    "candidates_per_step": n_total / args.steps / world, "parallelism": f"tasks x{world}",
                    "l2": "flushed between steps"},
         "e2e": {"value": value, "unit": "candidates/s", "h2d_bytes_per_step": N_TASKS * AGENTS * 8,

@@ -18,6 +18,10 @@ WANT = [
     "smsp__average_warp_latency_issue_stalled_math_pipe_throttle", "smsp__average_warp_latency_issue_stalled_mio_throttle",
     "smsp__average_warp_latency_issue_stalled_no_instruction",
     "smsp__sass_inst_executed_op_local_ld.sum", "smsp__sass_inst_executed_op_local_st.sum",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+    "sm__inst_executed_pipe_tensor.sum", "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_elapsed",
 ]
 
 for path in sys.argv[1:]:

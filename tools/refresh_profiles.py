@@ -1,7 +1,7 @@
-"""Copy one gpu_session.sh run into profiles/r1/: ncu summaries, per-launch DRAM traffic, the launch
+"""Copy one gpu_session.sh run into profiles/<round>/ (default r2): ncu summaries, per-launch DRAM traffic, the launch
 list summary and the bench JSON lines.
 
-    python tools/refresh_profiles.py TAG      (reads gpurun_out/TAG/)
+    python tools/refresh_profiles.py TAG [ROUND]      (reads gpurun_out/TAG/)
 """
 
 import collections
@@ -16,7 +16,10 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent.parent
 tag = sys.argv[1]
 src = ROOT / "gpurun_out" / tag
-dst = ROOT / "profiles" / "r1"
+dst = ROOT / "profiles" / (sys.argv[2] if len(sys.argv) > 2 else "r2")
+dst.mkdir(parents=True, exist_ok=True)
+if not (dst / "traffic.json").exists():
+    shutil.copy(ROOT / "profiles" / "r1" / "traffic.json", dst / "traffic.json")
 CAPTURES = {"lloyd": "lloyd", "score_trees": "score_trees", "dedup_insert": "dedup_insert",
             "kmeanspp_init": "init_kernel"}
 UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
@@ -63,7 +66,7 @@ if launches.exists():
 
 for name, out in (("bench.json", "bench"), ("bench_ref.json", "bench_ref"), ("bench_rl.json", "bench_rl")):
     if (src / name).exists():
-        for old in dst.glob(f"{out}_r1*.json"):
+        for old in dst.glob(f"{out}_{dst.name}*.json"):
             old.unlink()
         shutil.copy(src / name, dst / f"{out}_{tag}.json")
-print("profiles/r1 refreshed from", src)
+print(f"profiles/{dst.name} refreshed from", src)
