@@ -106,7 +106,15 @@ __device__ __forceinline__ void warp_leaf(int l, const int64_t* leaf_start, cons
     const int lane = threadIdx.x & 31;
     const int64_t s = leaf_start[l];
     const int len = leaf_len[l];
-    for (int i = lane; i < len; i += 32) buf[i] = value(s + i);
+    double v[4];  // a leaf holds <= 128 values: all four per lane in flight at once
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int i = lane + 32 * q;
+        v[q] = i < len ? value(s + i) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        if (lane + 32 * q < len) buf[lane + 32 * q] = v[q];
     __syncwarp();
     double r = 0.0;
     const int body = len - (len % 8);

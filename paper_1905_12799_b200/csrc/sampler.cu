@@ -200,6 +200,10 @@ struct ModeArgs {
     int off[kMaxKnobs + 1];
 };
 
+// Knobs with <= 32 settings are counted with one warp ballot per setting (lane v keeps setting
+// v's running count in a register, flushed once per launch); wider knobs (tile_f / tile_y /
+// tile_x: 80-84 settings) use shared-memory atomics, whose conflicts across 32 random rows over
+// ~80 bins are rare.  (Per-row __match_any_sync aggregation: 38 us per 1M rows.)
 __global__ void __launch_bounds__(256) mode_hist_kernel(const uint64_t* __restrict__ rows, int64_t count,
                                                         const ModeArgs a, unsigned int* __restrict__ hist) {
     extern __shared__ unsigned int s_hist[];
@@ -207,27 +211,44 @@ __global__ void __launch_bounds__(256) mode_hist_kernel(const uint64_t* __restri
     for (int i = threadIdx.x; i < bins; i += blockDim.x) s_hist[i] = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31;
+    unsigned int acc[kMaxKnobs];
+#pragma unroll
+    for (int d = 0; d < kMaxKnobs; ++d) acc[d] = 0;
     const int64_t warps_total = int64_t(gridDim.x) * (blockDim.x >> 5);
     const int64_t gw = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
     for (int64_t base = gw * 32; base < count; base += warps_total * 32) {
         const int64_t i = base + lane;
         const bool valid = i < count;
-        const unsigned active = __ballot_sync(0xffffffffu, valid);
-        if (!valid) continue;
-        const uint64_t row = rows[i];
-        for (int d = 0; d < n; ++d) {
-            const int v = a.off[d] + a.fmt.get(row, d);
-            const unsigned peers = __match_any_sync(active, v);
-            if (lane == __ffs(peers) - 1) atomicAdd(&s_hist[v], unsigned(__popc(peers)));
+        const uint64_t row = valid ? rows[i] : 0ull;
+#pragma unroll
+        for (int d = 0; d < kMaxKnobs; ++d) {
+            if (d >= n) break;
+            const int c = a.off[d + 1] - a.off[d];
+            const int v = a.fmt.get(row, d);
+            if (c <= 32) {
+                for (int u = 0; u < c; ++u) {
+                    const unsigned b = __ballot_sync(0xffffffffu, valid && v == u);
+                    if (lane == u) acc[d] += __popc(b);
+                }
+            } else if (valid) {
+                atomicAdd(&s_hist[a.off[d] + v], 1u);
+            }
         }
     }
+#pragma unroll
+    for (int d = 0; d < kMaxKnobs; ++d)
+        if (d < n && a.off[d + 1] - a.off[d] <= 32 && lane < a.off[d + 1] - a.off[d] && acc[d])
+            atomicAdd(&s_hist[a.off[d] + lane], acc[d]);
     __syncthreads();
     for (int i = threadIdx.x; i < bins; i += blockDim.x)
         if (s_hist[i]) atomicAdd(&hist[i], s_hist[i]);
 }
 
-void mode_vote(kt_engine* e, const uint64_t* rows, int64_t count, int n, const RowFmt& fmt, const int32_t* cards,
-               int32_t* mode_out) {
+// Histograms of every knob on the device, copied back asynchronously into a pinned staging
+// buffer (read after the caller's next synchronisation): adaptive_sample enqueues this before
+// its knee scan, so the mode vote costs no synchronisation of its own.
+static const unsigned int* mode_hist_async(kt_engine* e, const uint64_t* rows, int64_t count, int n,
+                                           const RowFmt& fmt, const int32_t* cards) {
     if (count <= 0) fail(KT_ERR_VALUE, "mode vote needs at least one row");
     if (count >= (int64_t(1) << 32)) fail(KT_ERR_UNSUPPORTED, "mode vote supports < 2^32 rows");
     ModeArgs a{};
@@ -246,14 +267,27 @@ void mode_vote(kt_engine* e, const uint64_t* rows, int64_t count, int n, const R
     e->check_launch("mode_hist");
     auto* h = static_cast<unsigned int*>(e->staging("mode.hist", smem));
     KT_CUDA(cudaMemcpyAsync(h, hist, smem, cudaMemcpyDeviceToHost, e->stream));
-    e->sync();
+    return h;
+}
+
+// mode_config's per-knob argmax (ties -> smallest index) from a copied-back histogram
+static void mode_from_hist(const unsigned int* h, int n, const int32_t* cards, int32_t* mode_out) {
+    int off = 0;
     for (int d = 0; d < n; ++d) {
-        const unsigned int* hd = h + a.off[d];
+        const unsigned int* hd = h + off;
         int best = 0;
         for (int v = 1; v < cards[d]; ++v)
             if (hd[v] > hd[best]) best = v;  // ties -> smallest index
         mode_out[d] = best;
+        off += cards[d];
     }
+}
+
+void mode_vote(kt_engine* e, const uint64_t* rows, int64_t count, int n, const RowFmt& fmt, const int32_t* cards,
+               int32_t* mode_out) {
+    const unsigned int* h = mode_hist_async(e, rows, count, n, fmt, cards);
+    e->sync();
+    mode_from_hist(h, n, cards, mode_out);
 }
 
 // ====================================================== k-means++ init (K7)
@@ -2255,6 +2289,9 @@ int kt_adaptive_sample(kt_engine* e, const uint64_t* rows_dev, int64_t count, in
         *batch_len = len;
         return KT_OK;
     }
+    // the mode is needed only if a centroid rounds onto a visited config: with a visited set,
+    // enqueue the vote now (its histograms ride back with the knee scan's synchronisations)
+    const unsigned int* mode_h = n_visited > 0 ? mode_hist_async(e, rows_dev, count, n_knobs, fmt, cards) : nullptr;
     KneeResult r = knee_scan(e, distinct, m, n_knobs, fmt, seed, knee_constant, 63);
     inf.chosen_k = r.chosen_k;
     inf.n_scanned = int32_t(r.ks.size());
@@ -2280,7 +2317,8 @@ int kt_adaptive_sample(kt_engine* e, const uint64_t* rows_dev, int64_t count, in
         if (visited.count(row)) {
             if (!have_mode) {
                 int32_t md[kMaxKnobs];
-                mode_vote(e, rows_dev, count, n_knobs, fmt, cards, md);
+                e->sync();  // (already idle: the knee scan ended with one)
+                mode_from_hist(mode_h, n_knobs, cards, md);
                 mode_row = 0;
                 for (int i = 0; i < n_knobs; ++i) mode_row = fmt.set(mode_row, i, md[i]);
                 have_mode = true;
