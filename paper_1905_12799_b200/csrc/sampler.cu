@@ -678,6 +678,7 @@ struct LloydArgs {
     unsigned long long* stats; // optional [R][3]: point visits, unused, evaluations
     long long* timeline;       // optional [100][4] globaltimer stamps of block 0 per pass
     const int* freeze;         // optional (device-driven sharded loop): nonzero -> the launch is a no-op
+    unsigned long long* slack; // optional probe [100][kMaxRuns][8]: points by budget slack b - D_a per pass
 };
 
 struct LloydLayout {
@@ -1256,6 +1257,24 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
         }
 
         stamp(1);
+        if (kLloydProbes && RESIDENT && a.slack && it < 100) {
+            // slack histogram of this block's points (run r, bucket: < margin, 0.25, 0.5, 1, 2, 4, 8, more)
+            for (int r = 0; r < R; ++r) {
+                if (rs.state[r] != kActiveFromSums) continue;
+                unsigned cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                for (int i = tid; i < np; i += blockDim.x) {
+                    const int old = s_asg[r * P + i];
+                    const float sl = old == 255 ? -1.0f : __fsub_rd(s_bud[r * P + i], dcum[a.coff[r] + old]);
+                    const int bkt = sl <= kSettleMargin ? 0 : sl < 0.25f ? 1 : sl < 0.5f ? 2 : sl < 1.0f ? 3
+                                  : sl < 2.0f ? 4 : sl < 4.0f ? 5 : sl < 8.0f ? 6 : 7;
+                    ++cnt[bkt];
+                }
+                for (int b = 0; b < 8; ++b) {
+                    const unsigned v = __reduce_add_sync(0xffffffffu, cnt[b]);
+                    if (lane == 0 && v) atomicAdd(a.slack + (size_t(it) * kMaxRuns + r) * 8 + b, (unsigned long long)v);
+                }
+            }
+        }
         if constexpr (RESIDENT) {
             // ---- assignment pass over this block's resident points, one tile at a time
             for (int t0 = 0; t0 < np; t0 += a.tile) {
@@ -1941,6 +1960,12 @@ struct KmeansSession {
         a.ctrl = static_cast<int*>(e->scratch("km.ctrl", 16));
         a.barrier = static_cast<unsigned int*>(e->scratch("km.barrier", 16));
         static const bool want_stats = kLloydProbes && std::getenv("KT_LLOYD_STATS") != nullptr;
+        static const bool want_slack = kLloydProbes && std::getenv("KT_LLOYD_SLACK") != nullptr;
+        a.slack = nullptr;
+        if (want_slack) {
+            a.slack = static_cast<unsigned long long*>(e->scratch("km.slack", size_t(100) * kMaxRuns * 8 * 8));
+            KT_CUDA(cudaMemsetAsync(a.slack, 0, size_t(100) * kMaxRuns * 8 * 8, e->stream));
+        }
         a.stats = nullptr;
         if (want_stats) {
             a.stats = static_cast<unsigned long long*>(e->scratch("km.stats", kMaxRuns * 3 * 8));
@@ -2022,6 +2047,19 @@ struct KmeansSession {
             KT_CUDA(cudaMemcpyAsync(h_iter, a.run_iter, R * 4, cudaMemcpyDeviceToHost, e->stream));
             KT_CUDA(cudaMemcpyAsync(h_cent, a.cent, size_t(K) * kMaxKnobs * 8, cudaMemcpyDeviceToHost, e->stream));
             e->sync();
+        }
+        if (a.slack) {
+            std::vector<unsigned long long> hsl(size_t(100) * kMaxRuns * 8);
+            KT_CUDA(cudaMemcpy(hsl.data(), a.slack, hsl.size() * 8, cudaMemcpyDeviceToHost));
+            for (int it2 = 0; it2 < 100; ++it2)
+                for (int r = 0; r < R; ++r) {
+                    const unsigned long long* c = hsl.data() + (size_t(it2) * kMaxRuns + r) * 8;
+                    unsigned long long t = 0;
+                    for (int b = 0; b < 8; ++b) t += c[b];
+                    if (!t) continue;
+                    std::fprintf(stderr, "[slack] k=%d pass %d: <=margin %llu <0.25 %llu <0.5 %llu <1 %llu <2 %llu <4 %llu <8 %llu more %llu\n",
+                                 ks[r], it2, c[0], c[1], c[2], c[3], c[4], c[5], c[6], c[7]);
+                }
         }
         if (a.stats) {
             unsigned long long hs[kMaxRuns * 3];
