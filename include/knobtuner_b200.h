@@ -299,6 +299,12 @@ int kt_search_round_ex(kt_engine* e, kt_agent* a, const kt_forest* f, const uint
                        double* scores_out_dev, int32_t* steps_out_dev, int64_t* n_out, kt_round_info* info,
                        double* logp_out_dev, double* values_out_dev, const kt_collective* coll /* NULL: 1 rank */);
 
+/* compute_gae (agent.py:191-210) of E episodes laid out episode-major: rewards / values [T]
+ * float64 (device), lengths [E] int32 (device), terminal value 0; adv_out [T] (device).
+ * The same kernel the PPO update runs (float64, the reference's reverse recurrence). */
+int kt_gae(kt_engine* e, const double* rewards_dev, const double* values_dev, const int32_t* lengths_dev, int32_t E,
+           double discount, double gae_parameter, double* adv_out_dev);
+
 /* ------------------------------------------------ surrogate refit
  * Gradient-boosted regression trees, exact greedy squared error (fit,
  * cost_model.py:367-398; _grow :328-364; _best_split :292-325), host code in

@@ -242,8 +242,9 @@ def search_round(agent: dict, model: dict, knob_values, starts, hyper: dict, ret
         values=np.array([x for ep in vb for x in ep], dtype=np.float64),
         bounds=bounds,
     )
-    ppo_update(agent, rollout["states"], rollout["actions"], rollout["logp"], rollout["rewards"],
-               rollout["values"], rollout["bounds"], hyper)
+    # the loss report of the last epoch (policy, value, entropy, total), as ppo_update returns it
+    rollout["report"] = ppo_update(agent, rollout["states"], rollout["actions"], rollout["logp"], rollout["rewards"],
+                                   rollout["values"], rollout["bounds"], hyper)
     agent["rounds"] += 1
     if return_rollout:
         return flat, scores, steps_idx, rollout

@@ -125,6 +125,7 @@ SIGNATURES = {
     "kt_lloyd_centroids": (C.c_int, [P, P, C.c_int, pf64]),
     "kt_lloyd_assignment": (C.c_int, [P, P, C.c_int, pi64]),
     "kt_lloyd_leaf_losses": (C.c_int, [P, P, C.c_int, pi64, C.c_int, pf64]),
+    "kt_gae": (C.c_int, [P, P, P, P, C.c_int32, f64, f64, P]),
     "kt_fit_trees": (C.c_int, [pf64, pf64, i64, C.c_int, C.c_int, C.c_int, f64, pi32, pf64, pi32, pi32, pf64, i64,
                                pi32, pf64]),
     "kt_fit_trees_device": (C.c_int, [P, pf64, pf64, i64, C.c_int, C.c_int, C.c_int, f64, pi32, pf64, pi32, pi32,

@@ -658,4 +658,25 @@ int kt_search_round_ex(kt_engine* e, kt_agent* ag, const kt_forest* f, const uin
     KT_API_END
 }
 
+
+// compute_gae (agent.py:191-210) per episode on the device, terminal value 0: exposed for
+// direct parity tests of gae_kernel.  rewards / values: [T] float64, episode-major; lengths: [E].
+int kt_gae(kt_engine* e, const double* rewards_dev, const double* values_dev, const int32_t* lengths_dev, int32_t E,
+           double discount, double gae_parameter, double* adv_out_dev) {
+    KT_API_BEGIN
+    using namespace kt;
+    if (E < 1) fail(KT_ERR_VALUE, "compute_gae needs at least one episode");
+    auto* lens = static_cast<int64_t*>(e->scratch("gae.lens", size_t(E) * 8));
+    auto* lens2 = static_cast<int64_t*>(e->scratch("gae.lens2", size_t(E) * 8));
+    auto* off = static_cast<int64_t*>(e->scratch("gae.off", size_t(E + 1) * 8));
+    e->pre_launch("round_lengths");
+    lengths_kernel<<<int(std::min<int64_t>(1024, ceil_div(E, 256))), 256, 0, e->stream>>>(lengths_dev, E, lens, lens2);
+    e->check_launch("round_lengths");
+    exclusive_scan(e, lens, off, E);
+    e->pre_launch("gae");
+    gae_kernel<<<int(ceil_div(E, 128)), 128, 0, e->stream>>>(rewards_dev, values_dev, lengths_dev, off, E, discount,
+                                                              gae_parameter, adv_out_dev);
+    e->check_launch("gae");
+    KT_API_END
+}
 }  // extern "C"
