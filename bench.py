@@ -483,6 +483,13 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     }
     if not args.no_wall95:
         line["wall_to_95"] = w95_ours(eng)
+    if not args.no_extra_configs and world == 1:  # configs[1..4] beside the headline (after its timing)
+        from tools import extra_configs
+
+        try:
+            line["other_configs"] = extra_configs.run_all(kt, torch, steps=2, local_rank=local_rank)
+        except Exception as ex:  # informational: never lose the headline line over it
+            line["other_configs"] = {"error": f"{type(ex).__name__}: {ex}"[:300]}
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
@@ -551,6 +558,8 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cpu-full", action="store_true", help="skip the one full-size (1M) CPU step (~2 min)")
     ap.add_argument("--no-wall95", action="store_true", help="skip the wall-time-to-95%%-best tune runs")
+    ap.add_argument("--no-extra-configs", action="store_true",
+                    help="skip the short runs of BASELINE configs[1..4] reported beside the headline")
     ap.add_argument("--rl-concurrent", action="store_true",
                     help="--workload rl: the 5 tasks on 5 engines from 5 host threads (default: in sequence)")
     ap.add_argument("--workload", choices=("s2", "rl", "c4"), default="s2",
