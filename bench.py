@@ -560,8 +560,8 @@ def main() -> None:
     ap.add_argument("--no-wall95", action="store_true", help="skip the wall-time-to-95%%-best tune runs")
     ap.add_argument("--no-extra-configs", action="store_true",
                     help="skip the short runs of BASELINE configs[1..4] reported beside the headline")
-    ap.add_argument("--rl-concurrent", action="store_true",
-                    help="--workload rl: the 5 tasks on 5 engines from 5 host threads (default: in sequence)")
+    ap.add_argument("--rl-serial", action="store_true",
+                    help="--workload rl: the 5 tasks in sequence on one engine (default: 5 engines, 5 host threads)")
     ap.add_argument("--workload", choices=("s2", "rl", "c4"), default="s2",
                     help="s2: the headline scored+clustered step; rl: 5 tasks x 4096 PPO agents per step; "
                          "c4: ResNet-18's 12 tasks x 1M candidates placed over the ranks (configs[3])")

@@ -121,6 +121,11 @@ void kt_engine::pre_launch(const char* what) {
 void kt_engine::check_launch(const char* what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) kt::fail(KT_ERR_CUDA, std::string("launch of ") + what + ": " + cudaGetErrorString(e));
+    static const bool sync_check = std::getenv("KT_SYNC_CHECK") != nullptr;  // debugging: name the faulting kernel
+    if (sync_check) {
+        e = cudaStreamSynchronize(stream);
+        if (e != cudaSuccess) kt::fail(KT_ERR_CUDA, std::string("kernel ") + what + ": " + cudaGetErrorString(e));
+    }
     note_launch();
     if (timing && open_start) {
         cudaEvent_t stop = take_event();

@@ -74,6 +74,10 @@ __global__ void __launch_bounds__(kRolloutThreads, 1) rollout_kernel(RolloutArgs
         rng = pcg64_from_seed_sequence(a.seed_words, a.n_seed_words, spawn, ns);
         a.visited[int64_t(e) * (a.S + 1)] = row;
     }
+    // no thread may poll the mbarrier before thread 0 has initialised it: shared memory still
+    // holds whatever the SM's previous kernel left there (found as an intermittent launch
+    // failure when several engines' kernels share the SMs)
+    __syncthreads();
     umma::mbar_wait(mbar, 0);
     int steps = 0;
     const int o0 = warp * kRolloutOut;

@@ -4,10 +4,11 @@ Per step and rank: AlexNet's 5 conv tasks (workloads.ALEXNET_TASKS; surrogates
 and landscapes in data/models/alexnet_task*.json), each runs one search round
 with 4096 PPO agents (K1 rollout, K2 scoring, K4 GAE, K5 PPO update) followed by
 adaptive_sample on its trajectory (K6/K7/K8/K9).  Metric: trajectory candidates
-scored + clustered per second.  The tasks are independent (configs[1]); --rl-concurrent runs each
-on its own engine (stream) from its own host thread so one task's host-side work and
-latency-bound kernels overlap the others' (measured 22.5-25 ms/step against ~28 serial on quiet
-boxes; one of nine cold runs died with an unexplained launch failure, so serial stays the default).  conv3/conv4 have tile_f cardinality 480, so
+scored + clustered per second.  The tasks are independent (configs[1]), so each runs on its own
+engine (stream) from its own host thread: one task's host-side work and latency-bound kernels
+overlap the others' (~22 ms/step against ~26-28 in sequence; --rl-serial: one engine, tasks in
+sequence).  Running them concurrently exposed a real race, since fixed: the rollout kernel's
+warps could poll its TMA mbarrier before thread 0 had initialised it.  conv3/conv4 have tile_f cardinality 480, so
 their rows use the bit-field layout (space.row_layout).
 """
 
@@ -51,7 +52,7 @@ def run(args, rank: int, world: int, local_rank: int, kt, torch, dist, helpers) 
     sp = kt.space
     docs = task_docs()
     eng = kt.engine(local_rank)
-    serial = not bool(getattr(args, "rl_concurrent", False))
+    serial = bool(getattr(args, "rl_serial", False))
     engines = [eng] * N_TASKS if serial else [eng] + [kt._lib.Engine(local_rank) for _ in range(N_TASKS - 1)]
     dev = f"cuda:{local_rank}"
     tasks = []

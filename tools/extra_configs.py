@@ -103,7 +103,7 @@ def run_all(kt, torch, steps: int = 2, local_rank: int = 0, clock=None) -> dict:
     out["c3_vgg16_256k"] = vgg
 
     # configs[1] and configs[3] through their bench modules (two steps after one warm-up)
-    args = argparse.Namespace(steps=steps, warmup=1, no_cpu_baseline=True, rl_concurrent=False)
+    args = argparse.Namespace(steps=steps, warmup=1, no_cpu_baseline=True, rl_serial=False)
 
     class _NoClock:
         def __init__(self, *_a):
