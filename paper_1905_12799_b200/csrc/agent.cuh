@@ -86,6 +86,7 @@ void launch_rollout(kt_engine* e, const RolloutArgs& a);
 
 // fp32 GEMM on tcgen05 (gemm_tc.cu): C = epi(A(m,k) B(k,n)), TA: A MN-major, TB: B K-major.
 void tc_gemm(kt_engine* e, bool TA, bool TB, int M, int N, int K, const float* A, int lda, const float* B, int ldb,
-             float* C, int ldc, int epi, const float* bias, const float* aux, int ldaux, int splits);
+             float* C, int ldc, int epi, const float* bias, const float* aux, int ldaux, int splits,
+             double* colpart = nullptr);
 
 }  // namespace kt

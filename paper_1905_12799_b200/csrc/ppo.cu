@@ -366,6 +366,13 @@ static void colsum(kt_engine* e, const Tv* X, int64_t rows, int cols, int ld, do
     e->check_launch("colsum_final");
 }
 
+// out[c] = sum over the (row tile, warp) partials of column c (fixed order: colsum_final)
+static void colsum_parts(kt_engine* e, const double* part, int parts, int cols, double* out) {
+    e->pre_launch("colsum_final");
+    colsum_final_kernel<<<cols, 256, 0, e->stream>>>(part, parts, cols, out);
+    e->check_launch("colsum_final");
+}
+
 // weight gradient out[M][N] (float64) = A^T B over T rows, deterministic split-K
 static void wgrad(kt_engine* e, int M, int N, int64_t T, const float* A, int lda, const float* B, int ldb,
                   double* out) {
@@ -578,11 +585,14 @@ int kt_search_round_ex(kt_engine* e, kt_agent* ag, const kt_forest* f, const uin
 
     // ---- K5 PPO epochs (nets.py:94-200)
     const int h = ag->h, g2 = 2 * ag->g, n3 = 3 * n + 1;
+    // Z / dZ rows padded to a multiple of 4 floats: the GEMMs that read them (wgrad, dgrad of
+    // layer 3) take the 16-byte vector-load path instead of scalar loads (25 -> 28 columns)
+    const int n3p = (n3 + 3) & ~3;
     auto* X = static_cast<float*>(e->scratch("ppo.X", size_t(T) * n * 4));
     auto* H1 = static_cast<float*>(e->scratch("ppo.H1", size_t(T) * h * 4));
     auto* H2 = static_cast<float*>(e->scratch("ppo.H2", size_t(T) * g2 * 4));
-    auto* Z = static_cast<float*>(e->scratch("ppo.Z", size_t(T) * n3 * 4));
-    auto* dZ = static_cast<float*>(e->scratch("ppo.dZ", size_t(T) * n3 * 4));
+    auto* Z = static_cast<float*>(e->scratch("ppo.Z", size_t(T) * n3p * 4));
+    auto* dZ = static_cast<float*>(e->scratch("ppo.dZ", size_t(T) * n3p * 4));
     auto* dP2 = static_cast<float*>(e->scratch("ppo.dP2", size_t(T) * g2 * 4));
     auto* dP1 = static_cast<float*>(e->scratch("ppo.dP1", size_t(T) * h * 4));
     auto* terms = static_cast<double*>(e->scratch("ppo.terms", size_t(T) * 3 * 8));
@@ -594,6 +604,8 @@ int kt_search_round_ex(kt_engine* e, kt_agent* ag, const kt_forest* f, const uin
     double* gw3 = gb2 + g2;
     double* gb3 = gw3 + n3 * g2;
     auto* gflat = static_cast<double*>(e->scratch("ppo.gflat", size_t(ag->P) * 8));
+    const int tiles4 = int(ceil_div(T, 128)) * 4;  // dgrad epilogue partials: (row tile, warp)
+    auto* colpart = static_cast<double*>(e->scratch("ppo.colpart", size_t(tiles4) * 128 * 8));
     auto* cards_dev = static_cast<int32_t*>(e->scratch("ppo.cards", 64));
     KT_CUDA(cudaMemcpyAsync(cards_dev, cards, size_t(n) * 4, cudaMemcpyHostToDevice, e->stream));
     e->pre_launch("encode_states");
@@ -605,19 +617,22 @@ int kt_search_round_ex(kt_engine* e, kt_agent* ag, const kt_forest* f, const uin
         const DenseWeights& w = ag->dw;
         tc_gemm(e, false, true, int(T), h, n, X, n, w.w1, n, H1, h, kEpiBiasTanh, w.b1, nullptr, 0, 1);
         tc_gemm(e, false, true, int(T), g2, h, H1, h, w.w2, h, H2, g2, kEpiBiasTanh, w.b2, nullptr, 0, 1);
-        tc_gemm(e, false, true, int(T), n3, g2, H2, g2, w.w3, g2, Z, n3, kEpiBias, w.b3, nullptr, 0, 1);
+        tc_gemm(e, false, true, int(T), n3, g2, H2, g2, w.w3, g2, Z, n3p, kEpiBias, w.b3, nullptr, 0, 1);
         e->pre_launch("ppo_rows");
-        ppo_rows_kernel<<<nb, 256, 0, e->stream>>>(Z, n3, n, T, T_all, ac_c, lp_c, adv, ret, hp->clip, hp->value_coef,
+        ppo_rows_kernel<<<nb, 256, 0, e->stream>>>(Z, n3p, n, T, T_all, ac_c, lp_c, adv, ret, hp->clip, hp->value_coef,
                                                     hp->entropy_coef, dZ, terms);
         e->check_launch("ppo_rows");
-        wgrad(e, n3, g2, T, dZ, n3, H2, g2, gw3);
-        colsum(e, dZ, T, n3, n3, gb3);
-        tc_gemm(e, false, false, int(T), g2, n3, dZ, n3, w.w3, g2, dP2, g2, kEpiTanhDeriv, nullptr, H2, g2, 1);
+        wgrad(e, n3, g2, T, dZ, n3p, H2, g2, gw3);
+        colsum(e, dZ, T, n3, n3p, gb3);
+        // bias gradients of layers 2 and 1 = column sums of dP2 / dP1, accumulated by the dgrad
+        // epilogues (float64 per row tile and warp) instead of re-reading T x 128 from HBM
+        tc_gemm(e, false, false, int(T), g2, n3, dZ, n3p, w.w3, g2, dP2, g2, kEpiTanhDeriv, nullptr, H2, g2, 1,
+                colpart);
         wgrad(e, g2, h, T, dP2, g2, H1, h, gw2);
-        colsum(e, dP2, T, g2, g2, gb2);
-        tc_gemm(e, false, false, int(T), h, g2, dP2, g2, w.w2, h, dP1, h, kEpiTanhDeriv, nullptr, H1, h, 1);
+        colsum_parts(e, colpart, tiles4, g2, gb2);
+        tc_gemm(e, false, false, int(T), h, g2, dP2, g2, w.w2, h, dP1, h, kEpiTanhDeriv, nullptr, H1, h, 1, colpart);
         wgrad(e, h, n, T, dP1, h, X, n, gw1);
-        colsum(e, dP1, T, h, h, gb1);
+        colsum_parts(e, colpart, tiles4, h, gb1);
         e->pre_launch("gather_grads");
         gather_grads_kernel<<<32, 256, 0, e->stream>>>(n, ag->h, ag->g, gw1, gb1, gw2, gb2, gw3, gb3, gflat);
         e->check_launch("gather_grads");

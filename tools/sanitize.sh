@@ -15,7 +15,7 @@ for tool in $TOOLS; do
   # racecheck / synccheck abort kernels that use cp.async.bulk + mbarrier (K1 rollout) or
   # tcgen05 (K5 GEMMs) with "unspecified launch failure"; memcheck / initcheck cover those
   if [ $tool = racecheck ] || [ $tool = synccheck ]; then sel="($SEL) and not test_first_round and not test_gemm"; fi
-  timeout 1500 compute-sanitizer --tool $tool $extra --target-processes all --print-limit 2000 \
+  timeout 2400 compute-sanitizer --tool $tool $extra --target-processes all --print-limit 200 \
     python -m pytest $FILES -m gpu -q -x -p no:cacheprovider -k "$sel" > $T/san_$tool.txt 2>&1
   rc=$?
   grep -h "hazard detected\|Read Thread\|Write Thread\|^=========     at " $T/san_$tool.txt | sed 's/block ([0-9,]*)//; s/__shared__ 0x[0-9a-f]*//; s/Thread ([0-9,]*)//; s/+0x[0-9a-f]*//' | sort | uniq -c | sort -rn | head -20 > $T/san_${tool}_sites.txt
