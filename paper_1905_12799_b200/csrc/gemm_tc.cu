@@ -185,7 +185,10 @@ __global__ void __launch_bounds__(kTcThreads, 3) tc_gemm_kernel(TcGemmArgs g) {
     const bool b_vec = (g.ldb % 4) == 0 && (reinterpret_cast<uintptr_t>(g.B) % 16) == 0;
 
     // one chunk's MMAs: split into tf32 hi/lo in stage s, then one thread issues them
-    auto stage_and_issue = [&](const Frag<kTcBM>& A, const Frag<128>& B, int cc) {
+    // `prefetch` runs between the proxy fence and the block barrier: the fence waits for every
+    // outstanding memory operation of the thread, so loads issued before it would be drained
+    // there (the next chunk's global loads are only in flight across the MMA if issued after)
+    auto stage_and_issue = [&](const Frag<kTcBM>& A, const Frag<128>& B, int cc, auto&& prefetch) {
         const int s = cc & 1;
         if (cc >= 2) umma::mbar_wait(umma::smem_addr(&mma_bar[s]), uint32_t((cc - 2) >> 1) & 1u);
         float* st = base + s * stage_floats;
@@ -193,6 +196,7 @@ __global__ void __launch_bounds__(kTcThreads, 3) tc_gemm_kernel(TcGemmArgs g) {
         store_tile<A_MN, kTcBM>(A, a_hi, a_lo, kTcBM);
         store_tile<B_MN, 128>(B, b_hi, b_lo, BN);
         umma::fence_async_smem();
+        prefetch();
         __syncthreads();
         if (tid == 0) {
             umma::fence_after();
@@ -228,8 +232,9 @@ __global__ void __launch_bounds__(kTcThreads, 3) tc_gemm_kernel(TcGemmArgs g) {
         for (int t = 0; t < 3; ++t) {
             const int cc = c + t;
             if (cc >= nchunks) break;
-            if (cc + 2 < nchunks) load_chunk(fa[(t + 2) % 3], fb[(t + 2) % 3], cc + 2);
-            stage_and_issue(fa[t], fb[t], cc);
+            stage_and_issue(fa[t], fb[t], cc, [&] {
+                if (cc + 2 < nchunks) load_chunk(fa[(t + 2) % 3], fb[(t + 2) % 3], cc + 2);
+            });
         }
     }
 #else
@@ -243,8 +248,9 @@ __global__ void __launch_bounds__(kTcThreads, 3) tc_gemm_kernel(TcGemmArgs g) {
         for (int half = 0; half < 2; ++half) {
             const int cc = c + half;
             if (cc >= nchunks) break;
-            if (cc + 1 < nchunks) load_chunk(fa[half ^ 1], fb[half ^ 1], cc + 1);  // overlaps this chunk's MMA
-            stage_and_issue(fa[half], fb[half], cc);
+            stage_and_issue(fa[half], fb[half], cc, [&] {  // overlaps this chunk's MMA
+                if (cc + 1 < nchunks) load_chunk(fa[half ^ 1], fb[half ^ 1], cc + 1);
+            });
         }
     }
 #endif
