@@ -1089,6 +1089,7 @@ extern "C" int kt_fit_trees_device(kt_engine* e, const double* features, const d
     a.tree_offsets = reinterpret_cast<int32_t*>(takeo(size_t(rounds + 1) * 4));
     a.threshold = reinterpret_cast<double*>(takeo(cap * 8));
     a.value = reinterpret_cast<double*>(takeo(cap * 8));
+    KT_CUDA(cudaMemsetAsync(dout, 0, oo, e->stream));  // read back whole: trees use <= the capacity
     const size_t smem = fit_smem_bytes(m, n);
     int optin = 0;
     KT_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
