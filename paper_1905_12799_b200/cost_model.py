@@ -221,8 +221,8 @@ class BoostParams:
 
 def _use_device_fit(params, n: int) -> bool:
     """The device engine is opt-in: byte-identical, but the split search's exact float64 cumsums
-    are one sequential chain per (node, feature), and measured on B200 the single-CTA kernel is
-    ~3x slower than the native host engine at every size tried (m = 100 .. 20,000 rows:
+    are one sequential chain per (node, feature); measured on B200 the single-CTA kernel is at
+    parity with the native host engine at the tuning loop's sizes (m = 1,000: 9.0 vs 9.3 ms;
     profiles/r2/fit_device.txt), so the tuning loop keeps the host engine."""
     return os.environ.get("KT_FIT_DEVICE", "") == "1" and int(params.depth) <= 7 and n <= 8
 

@@ -228,6 +228,7 @@ struct FitDevArgs {
     double* pred;        // [m]
     double* buf;         // [m] per-node segments
     uint8_t* in_left;    // [m]
+    const uint16_t* codes;  // [n][m] rank of each row's value among the feature's distinct values (or null)
     double* xs;          // [n][m] the node's feature values in its per-feature order (segment-local)
     double* rs;          // [n][m] residuals in the same order
     double* csum;        // [n][m] np.cumsum(rs) of the segment
@@ -682,7 +683,8 @@ __global__ void __launch_bounds__(kFitThreads, 1) fit_kernel(FitDevArgs a) {
 // runs it again with every lane keeping the prefix at its own position and evaluating the gain
 // there (boundaries in parallel), then a first-maximum argmax across the warp.
 __host__ __device__ inline size_t fit_smem_bytes(int64_t m, int n) {
-    return size_t(2) * n * m * 8 + size_t(m) * 8 * 2 + size_t(2) * m * 2 + size_t(2) * n * m * 2 + size_t(m) + 64;
+    return size_t(2) * n * m * 8 + size_t(m) * 8 * 2 + size_t(2) * m * 2 + size_t(2) * n * m * 2 + size_t(n) * m * 2 +
+           size_t(m) + 64;
 }
 
 __global__ void __launch_bounds__(kFitThreads, 1) fit_smem_kernel(FitDevArgs a) {
@@ -704,13 +706,15 @@ __global__ void __launch_bounds__(kFitThreads, 1) fit_smem_kernel(FitDevArgs a) 
     double* pred = resid + m;                              // [m]
     uint16_t* rows2 = reinterpret_cast<uint16_t*>(pred + m);  // [2][m]
     uint16_t* ord2 = rows2 + 2 * m;                        // [2][n][m]
-    uint8_t* in_left = reinterpret_cast<uint8_t*>(ord2 + size_t(2) * n * m);
+    uint16_t* codes = ord2 + size_t(2) * n * m;            // [n][m] value ranks: boundary tests on chip
+    uint8_t* in_left = reinterpret_cast<uint8_t*>(codes + size_t(n) * m);
     const double* Xg = a.xs;  // feature-major copy in global memory (L2-resident), [n][m]
     for (int i = tid; i < n * m; i += blockDim.x) {
         const int f = i / m, r = i - f * m;
         a.xs[i] = a.X[int64_t(r) * n + f];
     }
     for (int i = tid; i < m; i += blockDim.x) pred[i] = a.base;
+    for (int i = tid; i < n * m; i += blockDim.x) codes[i] = a.codes[i];
     if (tid == 0) used = 0;
     __syncthreads();
     for (int round = 0; round < a.rounds; ++round) {
@@ -757,16 +761,31 @@ __global__ void __launch_bounds__(kFitThreads, 1) fit_smem_kernel(FitDevArgs a) 
                 const int li = pair / n, f = pair - li * n, q = lb + li;
                 if (!node_try[li]) continue;
                 const int off = nodes[q].off, cnt = nodes[q].cnt;
-                const uint16_t* o = ord_d + size_t(f) * m + off;
-                double* cs = csum + size_t(f) * m + off;
-                double* cq = csq + size_t(f) * m + off;
-                double c = resid[o[0]];
+                const uint16_t* __restrict__ o = ord_d + size_t(f) * m + off;
+                double* __restrict__ cs = csum + size_t(f) * m + off;
+                double* __restrict__ cq = csq + size_t(f) * m + off;
+                const double* __restrict__ rsd = resid;
+                double c = rsd[o[0]];
                 double qq = __dmul_rn(c, c);
                 cs[0] = c;
                 cq[0] = qq;
-#pragma unroll 8
-                for (int kk = 1; kk < cnt; ++kk) {
-                    const double rv = resid[o[kk]];
+                // the residuals of 8 positions are gathered before their 8 chain steps, so the
+                // two dependent shared-memory loads per element overlap the float64 add chain
+                int kk = 1;
+                for (; kk + 8 <= cnt; kk += 8) {
+                    double rv[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) rv[u] = rsd[o[kk + u]];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        c = __dadd_rn(c, rv[u]);
+                        qq = __dadd_rn(qq, __dmul_rn(rv[u], rv[u]));
+                        cs[kk + u] = c;
+                        cq[kk + u] = qq;
+                    }
+                }
+                for (; kk < cnt; ++kk) {
+                    const double rv = rsd[o[kk]];
                     c = __dadd_rn(c, rv);
                     qq = __dadd_rn(qq, __dmul_rn(rv, rv));
                     cs[kk] = c;
@@ -786,14 +805,14 @@ __global__ void __launch_bounds__(kFitThreads, 1) fit_smem_kernel(FitDevArgs a) 
                 const double* cs = csum + size_t(f) * m + off;
                 const double* cq = csq + size_t(f) * m + off;
                 const double* xf = Xg + size_t(f) * m;
+                const uint16_t* cf = codes + size_t(f) * m;
                 const double total = cs[cnt - 1], total_sq = cq[cnt - 1];
                 const double parent_sse = __dsub_rn(total_sq, __ddiv_rn(__dmul_rn(total, total), double(cnt)));
                 double gb = 0.0, tb = 0.0;
                 int64_t ib = -1;
                 bool any = false;
                 for (int kk = lane; kk + 1 < cnt; kk += 32) {
-                    const double xv = xf[o[kk]], xn = xf[o[kk + 1]];
-                    if (!(xv != xn)) continue;
+                    if (cf[o[kk]] == cf[o[kk + 1]]) continue;  // equal values (distinct values have distinct ranks)
                     any = true;
                     const double ln = double(kk + 1), rn = double(cnt - (kk + 1));
                     const double ls = cs[kk], lq = cq[kk];
@@ -804,7 +823,6 @@ __global__ void __launch_bounds__(kFitThreads, 1) fit_smem_kernel(FitDevArgs a) 
                     if (argmax_better(gain, kk, gb, ib)) {
                         gb = gain;
                         ib = kk;
-                        tb = __ddiv_rn(__dadd_rn(xv, xn), 2.0);
                     }
                 }
                 any = __any_sync(0xffffffffu, any);
@@ -812,16 +830,16 @@ __global__ void __launch_bounds__(kFitThreads, 1) fit_smem_kernel(FitDevArgs a) 
                 for (int s2 = 16; s2 > 0; s2 >>= 1) {
                     const double g2 = __shfl_xor_sync(0xffffffffu, gb, s2);
                     const int64_t i2 = __shfl_xor_sync(0xffffffffu, ib, s2);
-                    const double t2 = __shfl_xor_sync(0xffffffffu, tb, s2);
                     if (argmax_better(g2, i2, gb, ib)) {
                         gb = g2;
                         ib = i2;
-                        tb = t2;
                     }
                 }
                 if (lane == 0) {
                     feat_have[li][f] = any;
                     feat_gain[li][f] = gb;
+                    // the winning boundary's midpoint (float64 values from the global copy)
+                    if (any) tb = __ddiv_rn(__dadd_rn(xf[o[ib]], xf[o[ib + 1]]), 2.0);
                     feat_thr[li][f] = tb;
                 }
             }
@@ -865,7 +883,9 @@ __global__ void __launch_bounds__(kFitThreads, 1) fit_smem_kernel(FitDevArgs a) 
                 n_nodes = nn;
             }
             __syncthreads();
-            // ---- stable partitions into the other level buffers (left part first)
+            // ---- stable partitions into the other level buffers (left part first): the left
+            // flags and counts per split node (a warp per node), then every (node, array) pair —
+            // the rows and each feature's order — partitioned by its own warp
             uint16_t* rows_n = rows2 + ((d + 1) & 1) * m;
             uint16_t* ord_n = ord2 + size_t((d + 1) & 1) * n * m;
             for (int q = lb + warp; q < le; q += kFitWarps) {
@@ -885,30 +905,32 @@ __global__ void __launch_bounds__(kFitThreads, 1) fit_smem_kernel(FitDevArgs a) 
                     }
                     nl += __popc(__ballot_sync(0xffffffffu, lft));
                 }
-                __syncwarp();
-                const int nordered = d + 1 < a.depth ? n : 0;
-                for (int f = -1; f < nordered; ++f) {
-                    const uint16_t* src = f < 0 ? rows_d + off : ord_d + size_t(f) * m + off;
-                    uint16_t* dst = f < 0 ? rows_n + off : ord_n + size_t(f) * m + off;
-                    int li2 = 0, ri2 = nl;
-                    for (int i0 = 0; i0 < cnt; i0 += 32) {
-                        const int i = i0 + lane;
-                        const int r = i < cnt ? src[i] : 0;
-                        const bool lft = i < cnt && in_left[r];
-                        const unsigned bl = __ballot_sync(0xffffffffu, lft);
-                        const unsigned br = __ballot_sync(0xffffffffu, i < cnt && !lft);
-                        const unsigned below = (1u << lane) - 1u;
-                        if (i < cnt) dst[lft ? li2 + __popc(bl & below) : ri2 + __popc(br & below)] = uint16_t(r);
-                        li2 += __popc(bl);
-                        ri2 += __popc(br);
-                    }
-                }
-                __syncwarp();
                 if (lane == 0) {
                     FitNode& L = nodes[nodes[q].lchild];
                     FitNode& R = nodes[nodes[q].rchild];
                     L.off = off, L.cnt = nl;
                     R.off = off + nl, R.cnt = cnt - nl;
+                }
+            }
+            __syncthreads();
+            const int narr = 1 + (d + 1 < a.depth ? n : 0);  // children at max depth are leaves: no orders
+            for (int pair = warp; pair < (le - lb) * narr; pair += kFitWarps) {
+                const int q = lb + pair / narr, f = pair % narr - 1;
+                if (nodes[q].feature < 0) continue;
+                const int off = nodes[q].off, cnt = nodes[q].cnt, nl = nodes[nodes[q].lchild].cnt;
+                const uint16_t* src = f < 0 ? rows_d + off : ord_d + size_t(f) * m + off;
+                uint16_t* dst = f < 0 ? rows_n + off : ord_n + size_t(f) * m + off;
+                int li2 = 0, ri2 = nl;
+                for (int i0 = 0; i0 < cnt; i0 += 32) {
+                    const int i = i0 + lane;
+                    const int r = i < cnt ? src[i] : 0;
+                    const bool lft = i < cnt && in_left[r];
+                    const unsigned bl = __ballot_sync(0xffffffffu, lft);
+                    const unsigned br = __ballot_sync(0xffffffffu, i < cnt && !lft);
+                    const unsigned below = (1u << lane) - 1u;
+                    if (i < cnt) dst[lft ? li2 + __popc(bl & below) : ri2 + __popc(br & below)] = uint16_t(r);
+                    li2 += __popc(bl);
+                    ri2 += __popc(br);
                 }
             }
             __syncthreads();
@@ -1052,18 +1074,34 @@ extern "C" int kt_fit_trees_device(kt_engine* e, const double* features, const d
     const size_t xb = size_t(m) * n * 8, yb = size_t(m) * 8, ob = size_t(n) * m * 4;
     const size_t cap = size_t(rounds) * size_t(per_tree);
     const size_t outb = cap * (4 + 8 + 4 + 4 + 8) + size_t(rounds + 1) * 4 + 6 * 16;
-    auto* h = static_cast<unsigned char*>(e->staging("fit.host", xb + yb + ob + outb + 64));
+    auto* h = static_cast<unsigned char*>(e->staging("fit.host", xb + yb + ob + size_t(n) * m * 2 + outb + 64));
     std::memcpy(h, c.X.data(), xb);
     std::memcpy(h + xb, c.y.data(), yb);
     auto* ho = reinterpret_cast<int32_t*>(h + xb + yb);
     for (int j = 0; j < n; ++j)
         for (int64_t i = 0; i < m; ++i) ho[size_t(j) * m + i] = int32_t(c.root[j][i]);
-    auto* d = static_cast<unsigned char*>(e->scratch("fit.in", xb + yb + ob + 64));
-    KT_CUDA(cudaMemcpyAsync(d, h, xb + yb + ob, cudaMemcpyHostToDevice, e->stream));
+    // value ranks per feature (walk each stable argsort; NaN-free inputs only — NaN compares unequal
+    // to itself, which ranks cannot express, so such inputs take the global kernel)
+    bool finite = m < 65536;
+    for (size_t i = 0; i < c.X.size() && finite; ++i) finite = !std::isnan(c.X[i]);
+    auto* hcodes = reinterpret_cast<uint16_t*>(ho + size_t(n) * m);
+    if (finite)
+        for (int j = 0; j < n; ++j) {
+            int code = 0;
+            for (int64_t i = 0; i < m; ++i) {
+                const int64_t r = c.root[j][i];
+                if (i && c.X[size_t(r) * n + j] != c.X[size_t(c.root[j][i - 1]) * n + j]) ++code;
+                hcodes[size_t(j) * m + r] = uint16_t(code);
+            }
+        }
+    const size_t cb = size_t(n) * m * 2;
+    auto* d = static_cast<unsigned char*>(e->scratch("fit.in", xb + yb + ob + cb + 64));
+    KT_CUDA(cudaMemcpyAsync(d, h, xb + yb + ob + cb, cudaMemcpyHostToDevice, e->stream));
     FitDevArgs a{};
     a.X = reinterpret_cast<const double*>(d);
     a.y = reinterpret_cast<const double*>(d + xb);
     a.root_ord = reinterpret_cast<const int32_t*>(d + xb + yb);
+    a.codes = finite ? reinterpret_cast<const uint16_t*>(d + xb + yb + ob) : nullptr;
     a.m = m, a.n = n, a.rounds = rounds, a.depth = depth, a.lr = learning_rate, a.base = c.base;
     const size_t wb = size_t(depth + 1) * m * 4 + size_t(depth + 1) * n * m * 4 + size_t(m) * (8 * 3 + 1) +
                       size_t(4) * n * m * 8 + 10 * 16;
@@ -1095,7 +1133,7 @@ extern "C" int kt_fit_trees_device(kt_engine* e, const double* features, const d
     KT_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
     cudaFuncAttributes fa{};
     KT_CUDA(cudaFuncGetAttributes(&fa, (const void*)fit_smem_kernel));
-    const bool on_chip = m <= 65535 && smem + fa.sharedSizeBytes <= size_t(optin) && !std::getenv("KT_FIT_GLOBAL");
+    const bool on_chip = finite && smem + fa.sharedSizeBytes <= size_t(optin) && !std::getenv("KT_FIT_GLOBAL");
     e->pre_launch("fit_trees");
     if (on_chip) {
         allow_dynamic_smem((const void*)fit_smem_kernel);
@@ -1104,7 +1142,7 @@ extern "C" int kt_fit_trees_device(kt_engine* e, const double* features, const d
         fit_kernel<<<1, kFitThreads, 0, e->stream>>>(a);
     }
     e->check_launch("fit_trees");
-    unsigned char* hout = h + xb + yb + ob;
+    unsigned char* hout = h + xb + yb + ob + cb;
     KT_CUDA(cudaMemcpyAsync(hout, dout, oo, cudaMemcpyDeviceToHost, e->stream));
     e->sync();
     const int32_t* offs = reinterpret_cast<const int32_t*>(hout + (reinterpret_cast<unsigned char*>(a.tree_offsets) - dout));
