@@ -336,3 +336,16 @@ def test_assemble_batch_matches_oracle_rules():
         seen.add(cand)
         want.append(cand)
     assert got == want and (2, 2, 2) in got and len(got) == 3
+
+
+def _native_comm_job(rank, world):
+    class _Eng:  # stands in for an engine: for_group must decide before touching it
+        pass
+
+    return shard.NativeComm.for_group(_Eng()) is None and shard.Comm().native is None
+
+
+def test_native_comm_only_on_nccl_groups():
+    """gloo groups (these CPU tests) keep the torch.distributed path: NativeComm.for_group
+    returns None there and Comm carries no native communicator."""
+    assert run_group(_native_comm_job, 2) == [True, True]
