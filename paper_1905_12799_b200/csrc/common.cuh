@@ -180,7 +180,9 @@ struct kt_engine {
 namespace kt {
 // Launch helpers shared across translation units.
 void allow_dynamic_smem(const void* kernel);
-int occupancy_blocks(const void* kernel, int threads, size_t smem);
+int occupancy_blocks(const void* kernel, int threads, size_t smem);  // cached per (device, kernel, shape)
+int smem_optin(int device);             // cudaDevAttrMaxSharedMemoryPerBlockOptin, cached
+size_t static_smem(const void* kernel);  // cudaFuncAttributes::sharedSizeBytes, cached
 // out[i] = sum(in[0..i)), out[n] = total; n <= 16M (single-block scan).
 void exclusive_scan(kt_engine* e, const int64_t* in, int64_t* out, int n);
 // K6's first-occurrence hash table over rows[0, count): *first = per-slot lowest row index,

@@ -7,7 +7,9 @@
 #include "common.cuh"
 #include "rng.cuh"
 
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <set>
 #include <utility>
 
@@ -37,10 +39,49 @@ void allow_dynamic_smem(const void* kernel) {
     done.insert({dev, kernel});
 }
 
+// Launch-planning queries are constant per (device, kernel, shape): cached, because a driver
+// round trip each (cudaOccupancy*, cudaFuncGetAttributes, cudaDeviceGetAttribute: ~5-20 us)
+// on every launch of an adaptive_sample step left the GPU idle between kernels.
 int occupancy_blocks(const void* kernel, int threads, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, const void*, int, size_t>, int> cache;
+    int dev = 0;
+    KT_CUDA(cudaGetDevice(&dev));
+    const auto key = std::make_tuple(dev, kernel, threads, smem);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) return it->second;
+    }
     int blocks = 0;
     KT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, threads, smem));
+    std::lock_guard<std::mutex> lk(mu);
+    cache[key] = blocks;
     return blocks;
+}
+
+int smem_optin(int device) {
+    static std::mutex mu;
+    static std::map<int, int> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(device);
+    if (it != cache.end()) return it->second;
+    int optin = 0;
+    KT_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    cache[device] = optin;
+    return optin;
+}
+
+size_t static_smem(const void* kernel) {
+    static std::mutex mu;
+    static std::map<const void*, size_t> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(kernel);
+    if (it != cache.end()) return it->second;
+    cudaFuncAttributes fa{};
+    KT_CUDA(cudaFuncGetAttributes(&fa, kernel));
+    cache[kernel] = fa.sharedSizeBytes;
+    return fa.sharedSizeBytes;
 }
 
 RowFmt row_fmt(const int32_t* cards, int n) {

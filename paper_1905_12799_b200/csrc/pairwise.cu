@@ -226,8 +226,7 @@ static void combine(kt_engine* e, const PairwiseTree& t, double* vals, double* o
     const int L = int(t.leaf_start.size());
     const int I = int(t.node_left.size());
     const size_t smem = size_t(L + I) * 8 + size_t(I) * 8 + size_t(t.n_levels + 1) * 4;
-    static int optin = -1;  // per process; every device in the pool is a B200
-    if (optin < 0) KT_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
+    const int optin = smem_optin(e->device);
     e->pre_launch("pairwise_combine");
     if (smem <= size_t(optin)) {
         allow_dynamic_smem((const void*)combine_smem_kernel);

@@ -1744,9 +1744,8 @@ static LloydPlan plan_lloyd(kt_engine* e, int64_t m, int K, int R, LloydArgs& a)
     const void* kres = bytes ? (const void*)lloyd_kernel<true, true> : (const void*)lloyd_kernel<true, false>;
     const void* kstr = bytes ? (const void*)lloyd_kernel<false, true> : (const void*)lloyd_kernel<false, false>;
     cudaFuncAttributes fa{};
-    KT_CUDA(cudaFuncGetAttributes(&fa, kres));
-    int optin = 0;
-    KT_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
+    fa.sharedSizeBytes = static_smem(kres);
+    const int optin = smem_optin(e->device);
     // smem plan: state (+ rows when they fit) + a queue of >= kLloydQueueMin entries
     const int64_t dw_bytes = kDeltaMode == 2 ? int64_t(kLloydResThreads / 32) * K * kDeltaW * 4 : 0;
     const int64_t avail = int64_t(optin) - int64_t(fa.sharedSizeBytes) - 16 - dw_bytes;
@@ -1855,11 +1854,10 @@ struct KmeansSession {
                            ~int64_t(31));
             init_nsub = int(ceil_div(init_P, int64_t(init_sub)));
             init_smem = size_t(init_P) * 12;
-            int optin = 0;
-            KT_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
+            const int optin = smem_optin(e->device);
             cudaFuncAttributes fa{};
             init_kern = f.bytes ? (const void*)init_res_kernel<true> : (const void*)init_res_kernel<false>;
-            KT_CUDA(cudaFuncGetAttributes(&fa, init_kern));
+            fa.sharedSizeBytes = static_smem(init_kern);
             init_res = !(mode && std::strcmp(mode, "chunked") == 0) && init_nsub <= kInitMaxSub &&
                        int64_t(init_nsub) * e->num_sms <= int64_t(kInitSelPer) * kInitResThreads &&
                        init_sub <= kInitFinPer * kInitResThreads &&
