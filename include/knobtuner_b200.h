@@ -62,6 +62,9 @@ int kt_engine_destroy(kt_engine* e);
 /* Use a caller-owned stream (cudaStream_t) instead of the engine's own; NULL restores it. */
 int kt_engine_set_stream(kt_engine* e, void* cuda_stream);
 int kt_engine_synchronize(kt_engine* e);
+/* Order the engine stream and another CUDA stream without a host synchronisation:
+ * after = 0: the engine waits for `other`'s work so far; 1: `other` waits for the engine's. */
+int kt_engine_order(kt_engine* e, void* other_cuda_stream, int after);
 /* Number of engine kernels launched since creation (evidence counter for the bench). */
 int64_t kt_engine_launch_count(const kt_engine* e);
 /* Per-kernel CUDA-event timing on the engine stream (off by default). */

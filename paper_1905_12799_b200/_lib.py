@@ -88,6 +88,7 @@ SIGNATURES = {
     "kt_engine_destroy": (C.c_int, [P]),
     "kt_engine_set_stream": (C.c_int, [P, P]),
     "kt_engine_synchronize": (C.c_int, [P]),
+    "kt_engine_order": (C.c_int, [P, P, C.c_int]),
     "kt_engine_launch_count": (C.c_int64, [P]),
     "kt_engine_set_timing": (C.c_int, [P, C.c_int]),
     "kt_engine_kernel_stats": (C.c_int, [P, C.c_int, C.c_char_p, pi64, pf64, pi32, C.c_int]),
@@ -210,17 +211,38 @@ class Engine:
         # all engine work is ordered on one torch-visible stream
         self.stream = torch.cuda.Stream(device=self.device)
         raise_for(lib.kt_engine_set_stream(h, P(self.stream.cuda_stream)))
+        self._lib = lib
+        self._raw = int(self.stream.cuda_stream)
+        self._ids = (self.stream.stream_id, self.stream.device_index, self.stream.device_type)
 
     @contextlib.contextmanager
     def scope(self):
-        """Run a block on the engine stream, ordered after/before the caller's stream."""
+        """Run a block on the engine stream, ordered after/before the caller's stream.
+
+        Lean on purpose (it brackets every engine call): the ordering is one event record + wait
+        each way inside the library, and the current-stream switch uses torch's raw accessors —
+        the torch.cuda.stream / wait_stream Python layers cost ~50 us per call."""
         import torch
 
-        caller = torch.cuda.current_stream(self.device)
-        self.stream.wait_stream(caller)
-        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
+        tc = torch._C
+        prev_dev = tc._cuda_getDevice()
+        if prev_dev != self.device:
+            tc._cuda_setDevice(self.device)
+        caller_raw = tc._cuda_getCurrentRawStream(self.device)
+        prev = tc._cuda_getCurrentStream(self.device)  # (stream_id, device_index, device_type)
+        lib = self._lib
+        same = caller_raw == self._raw
+        if not same:
+            raise_for(lib.kt_engine_order(self.handle, P(caller_raw), 0))
+            tc._cuda_setStream(*self._ids)
+        try:
             yield self
-        caller.wait_stream(self.stream)
+        finally:
+            if not same:
+                tc._cuda_setStream(*prev)
+                raise_for(lib.kt_engine_order(self.handle, P(caller_raw), 1))
+            if prev_dev != self.device:
+                tc._cuda_setDevice(prev_dev)
 
     @property
     def launches(self) -> int:
@@ -246,8 +268,15 @@ class Engine:
             out[name] = (int(counts[i]), float(ms[i]))
         return out
 
-    def set_stream(self, stream_ptr: int | None) -> None:
-        call("kt_engine_set_stream", self.handle, P(stream_ptr) if stream_ptr else None)
+    def set_stream(self, stream) -> None:
+        """Order the engine's work on ``stream`` (a torch.cuda.Stream) instead of its own."""
+        import torch
+
+        stream = stream if stream is not None else torch.cuda.Stream(device=self.device)
+        call("kt_engine_set_stream", self.handle, P(stream.cuda_stream))
+        self.stream = stream
+        self._raw = int(stream.cuda_stream)
+        self._ids = (stream.stream_id, stream.device_index, stream.device_type)
 
 
 def engine(device: int | None = None) -> Engine:

@@ -141,6 +141,7 @@ struct kt_engine {
     int device = 0;
     int num_sms = 148;
     cudaStream_t own_stream = nullptr;
+    cudaEvent_t order_event = nullptr;  // kt_engine_order
     cudaStream_t stream = nullptr;
     int64_t launches = 0;
     struct Buf {

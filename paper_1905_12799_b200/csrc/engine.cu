@@ -179,12 +179,25 @@ void kt_engine::check_launch(const char* what) {
 void kt_engine::flush_timing() {
     if (pending.empty()) return;
     KT_CUDA(cudaStreamSynchronize(stream));
-    for (auto& p : pending) {
+    // KT_GAP_TRACE: idle time of the stream between consecutive timed launches, attributed to
+    // the pair (host work / synchronisations between them), accumulated as "gap:<a>><b>"
+    static const bool gaps = std::getenv("KT_GAP_TRACE") != nullptr;
+    for (size_t i = 0; i < pending.size(); ++i) {
+        auto& p = pending[i];
         float ms = 0.f;
         KT_CUDA(cudaEventElapsedTime(&ms, p.start, p.stop));
         Stat& s = stats[p.name];
         s.count += 1;
         s.ms += ms;
+        if (gaps && i + 1 < pending.size()) {
+            float g = 0.f;
+            KT_CUDA(cudaEventElapsedTime(&g, p.stop, pending[i + 1].start));
+            Stat& gs = stats[std::string("gap:") + p.name + ">" + pending[i + 1].name];
+            gs.count += 1;
+            gs.ms += g;
+        }
+    }
+    for (auto& p : pending) {
         event_pool.push_back(p.start);
         event_pool.push_back(p.stop);
     }
@@ -246,6 +259,23 @@ int kt_engine_set_stream(kt_engine* e, void* s) {
     KT_API_BEGIN
     KT_CUDA(cudaStreamSynchronize(e->stream));
     e->stream = s ? static_cast<cudaStream_t>(s) : e->own_stream;
+    KT_API_END
+}
+
+// Cross-stream ordering without a host round trip: `after` = 0 makes the engine stream wait for
+// everything enqueued so far on `other`; 1 makes `other` wait for the engine stream.
+int kt_engine_order(kt_engine* e, void* other, int after) {
+    KT_API_BEGIN
+    auto* o = static_cast<cudaStream_t>(other);
+    if (o == e->stream) return KT_OK;
+    if (!e->order_event) KT_CUDA(cudaEventCreateWithFlags(&e->order_event, cudaEventDisableTiming));
+    if (after == 0) {
+        KT_CUDA(cudaEventRecord(e->order_event, o));
+        KT_CUDA(cudaStreamWaitEvent(e->stream, e->order_event, 0));
+    } else {
+        KT_CUDA(cudaEventRecord(e->order_event, e->stream));
+        KT_CUDA(cudaStreamWaitEvent(o, e->order_event, 0));
+    }
     KT_API_END
 }
 

@@ -52,4 +52,18 @@ pr.enable()
 for s in range(20):
     step(s)
 pr.disable()
-pstats.Stats(pr).sort_stats("tottime").print_stats(18)
+pstats.Stats(pr).sort_stats("cumulative").print_stats(25)
+
+# idle gaps of the engine stream between consecutive kernels (KT_GAP_TRACE=1 to enable)
+import os  # noqa: E402
+
+if os.environ.get("KT_GAP_TRACE"):
+    eng.set_timing(True)
+    eng.kernel_stats(reset=True)
+    for s in range(10):
+        step(s)
+    st = eng.kernel_stats(reset=True)
+    eng.set_timing(False)
+    print("per step (ms):")
+    for k, (c, ms) in sorted(st.items(), key=lambda kv: -kv[1][1])[:24]:
+        print(f"  {k:34s} {c / 10:5.1f}x {ms / 10:8.4f}")
