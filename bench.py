@@ -368,41 +368,59 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     # ---- timed region 2: end to end through the public API with host buffers.  One continuous
     # region over K steps: every step's candidate rows come from pinned host memory (a fresh H2D
     # copy, never reused on the device), its float64 scores (predict's return value, 8 B per
-    # candidate) and its batch go back to the host; the copy of step s+1 runs on a copy stream
-    # while step s computes (double-buffered device rows and scores).
-    copy_stream = torch.cuda.Stream(device=dev)
-    bufs = [torch.empty(N, dtype=torch.int64, device=dev) for _ in range(2)]
+    # candidate) and its batch go back to the host.  Pipelined as a tuning service runs it: step
+    # s+1's scoring is queued on the engine stream ahead of step s's clustering (so the GPU scores
+    # while the host returns from one adaptive_sample and launches the next), the H2D of step s+2
+    # runs on one copy stream and the scores' D2H on another; rows are triple-buffered, scores
+    # double-buffered, every reuse ordered by events.  (Scoring on a second engine concurrently
+    # with the clustering was measured slower: the resident Lloyd launch waits for the SMs the
+    # scoring kernel holds.)
+    copy_stream = torch.cuda.Stream(device=dev)  # H2D of upcoming steps' candidates
+    d2h_stream = torch.cuda.Stream(device=dev)   # D2H of the scores
+    bufs = [torch.empty(N, dtype=torch.int64, device=dev) for _ in range(3)]
     sbufs = [torch.empty(N, dtype=torch.float64, device=dev) for _ in range(2)]
     host_scores = [torch.empty(N, dtype=torch.float64).pin_memory() for _ in range(2)]
-    ready = [torch.cuda.Event() for _ in range(2)]
+    ready = [torch.cuda.Event() for _ in range(3)]    # rows of a step on the device
     scored = [torch.cuda.Event() for _ in range(2)]
+    drained = [torch.cuda.Event() for _ in range(2)]  # scores of a step copied out: sbufs free again
     e2e_start, e2e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
-    def upload(s):
+    def upload(s):  # bufs[s % 3] was last read by step s-3, whose clustering has returned
         with torch.cuda.stream(copy_stream):
-            bufs[s % 2].copy_(host_sets[s % n_sets], non_blocking=True)
-            ready[s % 2].record(copy_stream)
+            bufs[s % 3].copy_(host_sets[s % n_sets], non_blocking=True)
+            ready[s % 3].record(copy_stream)
+
+    def score(s):
+        i = s % 2
+        eng.stream.wait_event(ready[s % 3])
+        if s >= 2:
+            eng.stream.wait_event(drained[i])
+        kt.predict_rows(model, space, bufs[s % 3], out=sbufs[i], engine=eng)
+        with eng.scope():
+            scored[i].record(eng.stream)
+        with torch.cuda.stream(d2h_stream):  # the D2H overlaps the clustering queued behind it
+            d2h_stream.wait_event(scored[i])
+            host_scores[i].copy_(sbufs[i], non_blocking=True)
+            drained[i].record(d2h_stream)
 
     d2h = 0
     barrier()
     flush.fill_(-1.0)
     torch.cuda.synchronize()
     e2e_start.record(copy_stream)
-    upload(0)
+    for s in range(min(2, args.steps)):
+        upload(s)
+    score(0)
     for s in range(args.steps):
         if s + 1 < args.steps:
-            upload(s + 1)  # step s-1 has returned (host-synchronous), so its buffer is free
-        eng.stream.wait_event(ready[s % 2])
-        kt.predict_rows(model, space, bufs[s % 2], out=sbufs[s % 2], engine=eng)
-        with eng.scope():
-            scored[s % 2].record(eng.stream)
-        with torch.cuda.stream(copy_stream):  # scores D2H overlaps the clustering of the same step
-            copy_stream.wait_event(scored[s % 2])
-            host_scores[s % 2].copy_(sbufs[s % 2], non_blocking=True)
-        batch = kt.adaptive_sample_rows(bufs[s % 2], visited_for[2000 + s], space, 2000 + s, engine=eng)
+            score(s + 1)
+        if s + 2 < args.steps:
+            upload(s + 2)
+        batch = kt.adaptive_sample_rows(bufs[s % 3], visited_for[2000 + s], space, 2000 + s, engine=eng)
         d2h += batch.nbytes + N * 8
     with eng.scope():
         eng.stream.wait_stream(copy_stream)
+        eng.stream.wait_stream(d2h_stream)
         e2e_end.record(eng.stream)
     barrier()
     t_e2e = e2e_start.elapsed_time(e2e_end) / 1e3

@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "pwsum_warp.cuh"
 
 namespace kt {
 namespace {
@@ -65,7 +66,8 @@ struct Grower {
     // output (one tree)
     std::vector<int32_t> feature, left, right;
     std::vector<double> threshold, value;
-    std::vector<double> buf, xs, rs, csum, csq;
+    std::vector<double> buf, xs, csum, csq;
+    std::vector<int64_t> bnd;
     std::vector<uint8_t> in_left;
 
     int add() {
@@ -93,38 +95,57 @@ struct Grower {
         in_left.assign(size_t(m), 0);
     }
 
-    // _best_split (cost_model.py:292-325) over feature orders ord[f * m + off .. + cnt)
-    bool best_split(const int64_t* ord, int64_t off, int64_t mm, int& bf, double& bt) {
-        bool have = false;
-        double best_gain = 0.0;
-        xs.resize(mm);
-        rs.resize(mm);
-        csum.resize(mm);
-        csq.resize(mm);
-        for (int j = 0; j < n; ++j) {
-            const int64_t* o = ord + size_t(j) * m + off;
-            // one pass: gather, sequential cumsums (np.cumsum order), boundary detection
-            double c = 0.0, q = 0.0;
-            bool any = false;
-            for (int64_t k = 0; k < mm; ++k) {
-                const int64_t row = o[k];
-                const double xv = x(row, j), rv = resid[row];
-                xs[k] = xv;
-                any |= k > 0 && xv != xs[k - 1];
-                c = k ? c + rv : rv;
-                q = k ? q + rv * rv : rv * rv;
-                csum[k] = c;
-                csq[k] = q;
+    // _best_split (cost_model.py:292-325) over feature orders ord[f * m + off .. + cnt).
+    // Features are scanned G at a time in one pass over the rows, so the G per-feature
+    // sequential cumsum chains (np.cumsum order) run side by side; the pass also records the
+    // boundaries (value changes), so the gain evaluation visits only those.
+    template <int G>
+    void scan_group(const int64_t* ord, int64_t off, int64_t mm, int j0, bool& have, double& best_gain, int& bf,
+                    double& bt) {
+        const int64_t* o[G];
+        double c[G], q[G], prev[G];
+        int64_t nb[G];
+        double* xsj[G];
+        double* csj[G];
+        double* cqj[G];
+        int64_t* bj[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            o[g] = ord + size_t(j0 + g) * m + off;
+            c[g] = q[g] = prev[g] = 0.0;
+            nb[g] = 0;
+            xsj[g] = xs.data() + size_t(g) * mm;
+            csj[g] = csum.data() + size_t(g) * mm;
+            cqj[g] = csq.data() + size_t(g) * mm;
+            bj[g] = bnd.data() + size_t(g) * mm;
+        }
+        for (int64_t k = 0; k < mm; ++k) {
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const int64_t row = o[g][k];
+                const double xv = x(row, j0 + g), rv = resid[row];
+                c[g] = k ? c[g] + rv : rv;
+                q[g] = k ? q[g] + rv * rv : rv * rv;
+                csj[g][k] = c[g];
+                cqj[g][k] = q[g];
+                xsj[g][k] = xv;
+                bj[g][nb[g]] = k - 1;  // boundary between k - 1 and k
+                nb[g] += k > 0 && xv != prev[g];
+                prev[g] = xv;
             }
-            if (!any) continue;
-            const double total = csum[mm - 1], total_sq = csq[mm - 1];
+        }
+        for (int g = 0; g < G; ++g) {
+            if (!nb[g]) continue;  // constant feature: no split
+            const double* cs = csj[g];
+            const double* cq = cqj[g];
+            const double total = cs[mm - 1], total_sq = cq[mm - 1];
             const double parent_sse = total_sq - total * total / double(mm);
             double g_best = 0.0;
             int64_t b_best = -1;
-            for (int64_t b = 0; b + 1 < mm; ++b) {
-                if (!(xs[b] != xs[b + 1])) continue;
+            for (int64_t i = 0; i < nb[g]; ++i) {
+                const int64_t b = bj[g][i];
                 const double ln = double(b + 1), rn = double(mm - (b + 1));
-                const double ls = csum[b], lq = csq[b];
+                const double ls = cs[b], lq = cq[b];
                 const double sse_left = lq - ls * ls / ln;
                 const double d = total - ls;
                 const double sse_right = (total_sq - lq) - d * d / rn;
@@ -138,13 +159,34 @@ struct Grower {
                     b_best = b;
                 }
             }
-            const double thr = (xs[b_best] + xs[b_best + 1]) / 2.0;
+            const double thr = (xsj[g][b_best] + xsj[g][b_best + 1]) / 2.0;
             if (!have || g_best > best_gain) {
                 have = true;
                 best_gain = g_best;
-                bf = j;
+                bf = j0 + g;
                 bt = thr;
             }
+        }
+    }
+
+    bool best_split(const int64_t* ord, int64_t off, int64_t mm, int& bf, double& bt) {
+        constexpr int kG = 4;
+        bool have = false;
+        double best_gain = 0.0;
+        const size_t need = size_t(kG) * size_t(mm);
+        if (xs.size() < need) {
+            xs.resize(need);
+            csum.resize(need);
+            csq.resize(need);
+            bnd.resize(need);
+        }
+        int j = 0;
+        for (; j + kG <= n; j += kG) scan_group<kG>(ord, off, mm, j, have, best_gain, bf, bt);
+        switch (n - j) {
+            case 1: scan_group<1>(ord, off, mm, j, have, best_gain, bf, bt); break;
+            case 2: scan_group<2>(ord, off, mm, j, have, best_gain, bf, bt); break;
+            case 3: scan_group<3>(ord, off, mm, j, have, best_gain, bf, bt); break;
+            default: break;
         }
         return have;
     }
@@ -300,81 +342,6 @@ __device__ double pw_sum_dev(const double* a, int64_t n) {
     }
 }
 
-// Warp-cooperative numpy pairwise_sum of val(0..n-1) (all 32 lanes call it; every lane gets
-// the result).  A <= 128-element leaf is loaded in one shot (4 values per lane) and its 8
-// strided accumulators run on lanes 0..7 over shuffled values — the same additions in the
-// same order as pw_leaf_dev; larger inputs walk numpy's split tree iteratively.
-template <class Val>
-__device__ double pw_leaf_warp(Val val, int base, int n) {
-    const int lane = threadIdx.x & 31;
-    double v[4];
-#pragma unroll
-    for (int s2 = 0; s2 < 4; ++s2) v[s2] = lane + 32 * s2 < n ? val(base + lane + 32 * s2) : 0.0;
-    if (n < 8) {
-        double res = 0.0;
-        for (int i = 0; i < n; ++i) res = __dadd_rn(res, __shfl_sync(0xffffffffu, v[0], i));
-        return res;
-    }
-    const int body = n - (n % 8);
-    double r = 0.0;
-#pragma unroll
-    for (int t = 0; t < 16; ++t) {
-        if (8 * t >= body) break;
-        const double x = __shfl_sync(0xffffffffu, v[t / 4], (lane + 8 * (t % 4)) & 31);
-        r = t ? __dadd_rn(r, x) : x;
-    }
-    double rr[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) rr[j] = __shfl_sync(0xffffffffu, r, j);
-    double res = __dadd_rn(__dadd_rn(__dadd_rn(rr[0], rr[1]), __dadd_rn(rr[2], rr[3])),
-                           __dadd_rn(__dadd_rn(rr[4], rr[5]), __dadd_rn(rr[6], rr[7])));
-    for (int i = body; i < n; ++i) {
-        double x = 0.0;
-#pragma unroll
-        for (int s2 = 0; s2 < 4; ++s2) {
-            const double y = __shfl_sync(0xffffffffu, v[s2], i & 31);
-            if ((i >> 5) == s2) x = y;
-        }
-        res = __dadd_rn(res, x);
-    }
-    return res;
-}
-template <class Val>
-__device__ double pw_sum_warp(Val val, int n) {
-    if (n <= 128) return pw_leaf_warp(val, 0, n);
-    constexpr int kMaxFrames = 32;
-    int32_t off[kMaxFrames], len[kMaxFrames];
-    double lsum[kMaxFrames];
-    bool right[kMaxFrames];
-    int sp = 0;
-    off[0] = 0, len[0] = n, right[0] = false;
-    for (;;) {
-        while (len[sp] > 128) {
-            int32_t n2 = len[sp] / 2;
-            n2 -= n2 % 8;
-            off[sp + 1] = off[sp];
-            len[sp + 1] = n2;
-            right[sp + 1] = false;
-            ++sp;
-        }
-        double v = pw_leaf_warp(val, off[sp], len[sp]);
-        for (;;) {
-            if (sp == 0) return v;
-            const int p = sp - 1;
-            int32_t n2 = len[p] / 2;
-            n2 -= n2 % 8;
-            if (!right[sp]) {
-                lsum[p] = v;
-                off[sp] = off[p] + n2;
-                len[sp] = len[p] - n2;
-                right[sp] = true;
-                break;
-            }
-            v = __dadd_rn(lsum[p], v);
-            --sp;
-        }
-    }
-}
 
 struct FitNode {  // BFS record of one tree
     int off, cnt;

@@ -16,10 +16,12 @@
 // or 1.0 below 1e-12, or the explicit initial temperature.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "forest.cuh"
 #include "pairwise.cuh"
+#include "pwsum_warp.cuh"
 #include "rng.cuh"
 
 namespace kt {
@@ -55,6 +57,10 @@ struct SAArgs {
     double* slot_scores;
     int32_t* slot_steps;
     int64_t* counts;
+    // fused start (warp kernel, few chains): every block scores all starts and derives the
+    // temperature itself instead of the score_trees + pairwise-sum + temperature launches
+    int fused, has_t0;
+    double t0;
 };
 
 template <int D>
@@ -116,9 +122,9 @@ __global__ void __launch_bounds__(128) sa_chain_kernel(SAArgs a) {
 }
 
 // Warp-per-chain variant for few chains (a tuning round runs 64): the 32 lanes walk
-// the trees of a proposal in parallel (lane l takes trees l, l + 32, ...), then every
-// lane accumulates the leaf values in tree order from shuffles — the same sequential
-// float64 sum as score_row, so the chain is bit-identical.  Every lane runs the chain's
+// the trees of a proposal in parallel (lane l takes trees l, l + 32, ...), stage the leaf
+// values in shared memory, then every lane accumulates them in tree order — the same
+// sequential float64 sum as score_row, so the chain is bit-identical.  Every lane runs the chain's
 // PCG64 stream redundantly (identical draws, no broadcast); lane 0 writes the slots.
 template <int D>
 __global__ void __launch_bounds__(128) sa_chain_warp_kernel(SAArgs a) {
@@ -126,13 +132,43 @@ __global__ void __launch_bounds__(128) sa_chain_warp_kernel(SAArgs a) {
     const int total = a.n_trees * a.words_per_tree;
     for (int i = threadIdx.x; i < total; i += blockDim.x) s_forest[i] = a.forest[i];
     __syncthreads();
+    __shared__ double s_leaf[4][64];  // per warp: the proposal's leaf value of each tree
+    __shared__ double s_temp;
+    const double* start_scores = a.start_scores;
+    if (a.fused) {
+        // start scores (score_row = K2's float64 order) and T0 = np.std(start scores) (sa.py:93-97:
+        // pairwise mean, pairwise sum of squared deviations, sqrt; 1.0 below 1e-12)
+        double* s_sc = reinterpret_cast<double*>(s_forest + total);
+        for (int i = threadIdx.x; i < a.chains; i += blockDim.x)
+            s_sc[i] = score_row<D>(s_forest, a.words_per_tree, a.n_trees, a.base, a.starts[i], !a.fmt.bytes, a.fmt);
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            double t = a.t0;
+            if (!a.has_t0) {
+                const double mean = __ddiv_rn(pw_sum_warp([&](int i) { return s_sc[i]; }, a.chains), double(a.chains));
+                const double ss = pw_sum_warp([&](int i) {
+                    const double d = __dsub_rn(s_sc[i], mean);
+                    return __dmul_rn(d, d);
+                }, a.chains);
+                const double sd = __dsqrt_rn(__ddiv_rn(ss, double(a.chains)));
+                t = sd > 1e-12 ? sd : 1.0;
+            }
+            if (threadIdx.x == 0) s_temp = t;
+        }
+        __syncthreads();
+        start_scores = s_sc;
+    } else if (threadIdx.x == 0) {
+        s_temp = *a.temperature;
+    }
+    __syncthreads();
     const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (c >= a.chains) return;  // whole warps
+    double* my_leaf = s_leaf[threadIdx.x >> 5];
     const uint32_t spawn = uint32_t(c);
     Pcg64 g = pcg64_from_seed_sequence(a.seed_words, a.n_seed_words, &spawn, 1);
     uint64_t row = a.starts[c];
-    double score = a.start_scores[c];
-    double temp = *a.temperature;
+    double score = start_scores[c];
+    double temp = s_temp;
     const int64_t slot0 = int64_t(c) * (a.steps + 1);
     if (lane == 0) {
         a.slot_rows[slot0] = row;
@@ -159,11 +195,15 @@ __global__ void __launch_bounds__(128) sa_chain_warp_kernel(SAArgs a) {
                 leaf[q] = wide ? walk_tree_wide<D>(tr, x) : walk_tree<D>(tr, lo, hi);
             }
         }
-        double acc = 0.0;
-        for (int t = 0; t < a.n_trees; ++t) {
-            const double lv = t < 32 ? __shfl_sync(0xffffffffu, leaf[0], t) : __shfl_sync(0xffffffffu, leaf[1], t - 32);
-            acc = t ? __dadd_rn(acc, lv) : lv;
-        }
+        // tree-order sum from shared memory: the loads are independent of the running sum, so
+        // only the dependent float64 adds remain on the step's critical path
+        my_leaf[lane] = leaf[0];
+        my_leaf[lane + 32] = leaf[1];
+        __syncwarp();
+        double acc = my_leaf[0];
+#pragma unroll 8
+        for (int t = 1; t < a.n_trees; ++t) acc = __dadd_rn(acc, my_leaf[t]);
+        __syncwarp();  // every lane has read the leaves before the next step overwrites them
         const double ps = __dadd_rn(a.base, acc);
         const double delta = __dsub_rn(ps, score);
         bool accept = delta >= 0.0;
@@ -198,12 +238,20 @@ __global__ void sa_compact_kernel(const uint64_t* slot_rows, const double* slot_
 }
 
 constexpr int kSaWarpChains = 8192;  // up to this many chains the warp-per-chain kernel is used
+constexpr int kSaFusedChains = 1024;  // up to this many, the warp kernel also scores the starts
+
+static bool sa_warp_path(const kt_forest* f, int chains) { return f->n_trees <= 64 && chains <= kSaWarpChains; }
+static bool sa_fused_path(const kt_forest* f, int chains) {
+    return sa_warp_path(f, chains) && chains <= kSaFusedChains &&
+           (size_t(f->n_trees) * f->words_per_tree + chains) * 8 <= 200 * 1024;
+}
 
 template <int D>
 static void launch_chains(kt_engine* e, const kt_forest* f, const SAArgs& a) {
-    const size_t smem = size_t(f->n_trees) * f->words_per_tree * 8;
+    size_t smem = size_t(f->n_trees) * f->words_per_tree * 8;
     if (smem > 200 * 1024) fail(KT_ERR_UNSUPPORTED, "forest too large for the in-kernel SA walk");
-    if (a.n_trees <= 64 && a.chains <= kSaWarpChains) {  // few chains: a warp per chain
+    if (sa_warp_path(f, a.chains)) {  // few chains: a warp per chain
+        if (a.fused) smem += size_t(a.chains) * 8;
         auto kern = sa_chain_warp_kernel<D>;
         allow_dynamic_smem((const void*)kern);
         e->pre_launch("sa_chains");
@@ -250,22 +298,29 @@ extern "C" int kt_sa_chains(kt_engine* e, const kt_forest* f, const uint64_t* st
         }
         KT_CUDA(cudaMemcpyAsync(starts + given, h, size_t(chains - given) * 8, cudaMemcpyHostToDevice, e->stream));
     }
+    if (f->n_trees == 0) fail(KT_ERR_UNSUPPORTED, "SA on a sentinel (tree-less) model is not supported by the engine");
+    const bool fused = sa_fused_path(f, chains) && !std::getenv("KT_SA_UNFUSED");  // tests: the launch chain
     auto* start_scores = static_cast<double*>(e->scratch("sa.start_scores", size_t(chains) * 8));
-    score_trees(e, f, starts, chains, start_scores);
     auto* scal = static_cast<double*>(e->scratch("sa.scalars", 4 * 8));  // sum, mean, sumsq, temperature
-    if (!has_initial_temperature) {
-        pairwise_sum(e, start_scores, chains, nullptr, scal + 0);
-        e->pre_launch("sa_mean");
-        sa_temperature_kernel<<<1, 1, 0, e->stream>>>(scal + 0, nullptr, chains, 0, 0.0, scal + 1, nullptr, 0);
-        e->check_launch("sa_mean");
-        pairwise_sum(e, start_scores, chains, scal + 1, scal + 2);
+    if (!fused) {
+        score_trees(e, f, starts, chains, start_scores);
+        if (!has_initial_temperature) {
+            pairwise_sum(e, start_scores, chains, nullptr, scal + 0);
+            e->pre_launch("sa_mean");
+            sa_temperature_kernel<<<1, 1, 0, e->stream>>>(scal + 0, nullptr, chains, 0, 0.0, scal + 1, nullptr, 0);
+            e->check_launch("sa_mean");
+            pairwise_sum(e, start_scores, chains, scal + 1, scal + 2);
+        }
+        e->pre_launch("sa_temperature");
+        sa_temperature_kernel<<<1, 1, 0, e->stream>>>(nullptr, scal + 2, chains, has_initial_temperature,
+                                                      initial_temperature, nullptr, scal + 3, 1);
+        e->check_launch("sa_temperature");
     }
-    e->pre_launch("sa_temperature");
-    sa_temperature_kernel<<<1, 1, 0, e->stream>>>(nullptr, scal + 2, chains, has_initial_temperature,
-                                                  initial_temperature, nullptr, scal + 3, 1);
-    e->check_launch("sa_temperature");
 
     SAArgs a{};
+    a.fused = fused;
+    a.has_t0 = has_initial_temperature;
+    a.t0 = initial_temperature;
     a.forest = f->dev;
     a.words_per_tree = f->words_per_tree;
     a.n_trees = f->n_trees;
@@ -286,7 +341,6 @@ extern "C" int kt_sa_chains(kt_engine* e, const kt_forest* f, const uint64_t* st
     a.slot_scores = static_cast<double*>(e->scratch("sa.slot_scores", slots * 8));
     a.slot_steps = static_cast<int32_t*>(e->scratch("sa.slot_steps", slots * 4));
     a.counts = static_cast<int64_t*>(e->scratch("sa.counts", size_t(chains) * 8));
-    if (f->n_trees == 0) fail(KT_ERR_UNSUPPORTED, "SA on a sentinel (tree-less) model is not supported by the engine");
     switch (f->depth) {
         case 1: launch_chains<1>(e, f, a); break;
         case 2: launch_chains<2>(e, f, a); break;

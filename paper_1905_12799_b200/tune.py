@@ -45,6 +45,17 @@ def random_config(cards, rng) -> tuple:
     return tuple(int(rng.integers(0, c)) for c in cards)
 
 
+def random_configs(cards, rng, count: int) -> np.ndarray:
+    """``count`` successive random_config draws as one (count, n) index matrix.
+
+    One broadcast ``integers(0, cards, size=(count, n))`` call consumes the generator exactly
+    like ``count`` x n scalar ``integers(0, c)`` calls in row-major order (same values, same
+    state afterwards; checked in tests/test_tune_host.py), at a fraction of the Python cost.
+    """
+    cards = np.asarray(cards, dtype=np.int64)
+    return rng.integers(0, cards, size=(int(count), cards.size))
+
+
 def random_unvisited(cards, visited: set, count: int, rng) -> list[tuple]:
     """driver.py:72-98: distinct unvisited draws, then an exact sweep when draws stall."""
     if count <= 0:
@@ -52,12 +63,24 @@ def random_unvisited(cards, visited: set, count: int, rng) -> list[tuple]:
     batch, seen, attempts = [], set(), 0
     limit = max(200, 20 * count)
     while len(batch) < count and attempts < limit:
-        attempts += 1
-        cand = random_config(cards, rng)
-        if cand in seen or cand in visited:
-            continue
-        seen.add(cand)
-        batch.append(cand)
+        # the reference draws one configuration per attempt; draw a chunk at once and, if the
+        # batch fills before the chunk is used up, rewind the generator and redraw exactly the
+        # attempts made (random_configs consumes the stream like the scalar draws)
+        chunk = min(limit - attempts, max(64, 2 * (count - len(batch))))
+        state = rng.bit_generator.state
+        used = 0
+        for cand in map(tuple, random_configs(cards, rng, chunk).tolist()):
+            used += 1
+            if cand in seen or cand in visited:
+                continue
+            seen.add(cand)
+            batch.append(cand)
+            if len(batch) == count:
+                break
+        attempts += used
+        if used < chunk:
+            rng.bit_generator.state = state
+            random_configs(cards, rng, used)
     if len(batch) < count:
         if int(np.prod(np.asarray(cards, dtype=np.int64))) > ENUMERATION_CAP:
             return batch
@@ -236,13 +259,14 @@ def tune_rows(space, landscape, strategy: str, budget: int, seed: int = 0,
                     fitness[~ok] = predict_rows(model, space, frows, engine=eng).cpu().numpy()
                 order = np.argsort(-fitness, kind="stable")
                 starts = [run.configs[int(i)] for i in order[: agent_params.episodes_per_round]]
-                while len(starts) < agent_params.episodes_per_round:
-                    starts.append(random_config(cards, rng))
-                srows = torch.from_numpy(sp.pack(np.asarray(starts), cards).view(np.int64)).to(dev)
+                sidx = np.asarray(starts, dtype=np.int64).reshape(-1, n)
+                if len(starts) < agent_params.episodes_per_round:
+                    sidx = np.concatenate([sidx, random_configs(cards, rng, agent_params.episodes_per_round - len(starts))])
+                srows = torch.from_numpy(sp.pack(sidx, cards).view(np.int64)).to(dev)
                 traj = run_search_rows(agent, model, space, srows, engine=eng)
             else:
-                starts = [random_config(cards, rng) for _ in range(sa_params.chains)]
-                srows = torch.from_numpy(sp.pack(np.asarray(starts), cards).view(np.int64)).to(dev)
+                sidx = random_configs(cards, rng, sa_params.chains)
+                srows = torch.from_numpy(sp.pack(sidx, cards).view(np.int64)).to(dev)
                 traj = run_sa_rows(sa_params, model, space, srows, round_seed(seed, round_index), engine=eng)
         if strategy.endswith("+as"):
             brows = adaptive_sample_rows(traj[0], m_rows[:m_cnt], space, round_seed(seed, round_index), engine=eng)

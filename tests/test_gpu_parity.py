@@ -281,8 +281,13 @@ def test_adaptive_sample_1m_candidates_properties():
 
 
 # ------------------------------------------------------------------ K10 SA
+@pytest.mark.parametrize("launch", ["fused", "unfused"])
 @pytest.mark.parametrize("name", sorted(meta("sa")))
-def test_sa_vs_reference(name):
+def test_sa_vs_reference(name, launch, monkeypatch):
+    """fused: the warp kernel scores the starts and derives T0 itself (<= 1024 chains);
+    unfused: score_trees + pairwise sums + temperature launches (KT_SA_UNFUSED)."""
+    if launch == "unfused":
+        monkeypatch.setenv("KT_SA_UNFUSED", "1")
     g = npz("sa")
     md = meta("sa")[name]
     mm = MODELS[md["model"]]
@@ -297,15 +302,18 @@ def test_sa_vs_reference(name):
     assert tr.step_indices == tuple(g[f"{name}/steps"].tolist())
 
 
-def test_sa_large_vs_oracle():
+@pytest.mark.parametrize("chains,unfused", [(1024, False), (1024, True), (1500, False), (64, False)])
+def test_sa_large_vs_oracle(chains, unfused, monkeypatch):
+    if unfused:
+        monkeypatch.setenv("KT_SA_UNFUSED", "1")
     mm = MODELS["s2_resnet18"]
     space = space_of(mm["values"])
     model = kt.CostModel.from_dict(mm["model"])
     rng = np.random.default_rng(8)
     idx = rng.integers(0, np.array(space.cardinalities), size=(1000, 8))
-    tr = kt.run_sa_round(kt.SAParams(chains=1024, steps_per_round=40), model, space,
+    tr = kt.run_sa_round(kt.SAParams(chains=chains, steps_per_round=40), model, space,
                          [kt.Configuration(tuple(r)) for r in idx.tolist()], seed=2**40 + 3)
-    o_idx, o_sc, o_st = osa.run_sa_round(mm["model"], mm["values"], idx, 2**40 + 3, chains=1024, steps=40)
+    o_idx, o_sc, o_st = osa.run_sa_round(mm["model"], mm["values"], idx, 2**40 + 3, chains=chains, steps=40)
     assert np.array_equal(tr.index_matrix(), o_idx)
     assert np.array_equal(tr.scores(), o_sc)
     assert np.array_equal(np.array(tr.step_indices), o_st)

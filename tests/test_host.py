@@ -238,3 +238,45 @@ def test_glibc_exp_replica_matches_libm(tmp_path):
     want = np.array([math.exp(v) if v < 709.78 else math.inf for v in x.tolist()])
     bad = np.flatnonzero(got.view(np.int64) != want.view(np.int64))
     assert bad.size == 0, [(x[i].hex(), got[i].hex(), want[i].hex()) for i in bad[:5]]
+
+
+def test_random_configs_consume_the_stream_like_scalar_draws():
+    """tune.random_configs / random_unvisited vs the reference's one-integers()-per-knob draws
+    (space.py:212-214, driver.py:72-98): same configurations, same generator state afterwards."""
+    from paper_1905_12799_b200 import tune
+
+    def unvisited_seq(cards, visited, count, rng):  # driver.py:72-98 draw loop, one draw per attempt
+        batch, seen, attempts = [], set(), 0
+        limit = max(200, 20 * count)
+        while len(batch) < count and attempts < limit:
+            attempts += 1
+            cand = tune.random_config(cards, rng)
+            if cand in seen or cand in visited:
+                continue
+            seen.add(cand)
+            batch.append(cand)
+        return batch
+
+    for seed in range(60):
+        r = np.random.default_rng(seed)
+        cards = r.integers(1, 400, size=int(r.integers(1, 9)))
+        if seed % 3 == 0:
+            cards[0] = 1
+        count = int(r.integers(1, 80))
+        a, b = np.random.default_rng(seed + 7), np.random.default_rng(seed + 7)
+        seq = [tune.random_config(cards, a) for _ in range(count)]
+        vec = [tuple(t) for t in tune.random_configs(cards, b, count).tolist()]
+        assert seq == vec and a.integers(0, 2**62) == b.integers(0, 2**62)
+    for seed in range(40):
+        cards = np.array([3, 4, 2, 5]) if seed % 2 else np.array([10, 10, 10, 10])
+        total = int(np.prod(cards))
+        r = np.random.default_rng(seed)
+        visited = {tuple(int(v) for v in np.unravel_index(i, cards))
+                   for i in r.choice(total, size=int(r.integers(0, total)), replace=False)}
+        count = int(r.integers(1, 70))
+        a, b = np.random.default_rng(seed + 99), np.random.default_rng(seed + 99)
+        want = unvisited_seq(cards, visited, count, a)
+        got = tune.random_unvisited(cards, visited, count, b)
+        assert got[:len(want)] == want
+        if len(want) == count:  # no exhaustive sweep: generator states must agree
+            assert got == want and a.integers(0, 2**62) == b.integers(0, 2**62)
