@@ -4,7 +4,7 @@
 // the CUDA-core gemm in ppo.cu:
 //   A(m,k) = TA ? A[k*lda + m] (MN-major) : A[m*lda + k] (K-major)
 //   B(k,n) = TB ? B[n*ldb + k] (K-major)  : B[k*ldb + n] (MN-major)
-// One CTA (128 threads) owns a 128 x BN output tile whose fp32 accumulator
+// One CTA (256 threads) owns a 128 x BN output tile whose fp32 accumulator
 // lives in TMEM.  K is consumed in chunks of 16: all threads stage the chunk
 // into shared memory in the canonical no-swizzle UMMA layout (umma.cuh), split
 // into tf32 hi and lo parts (MN-major global operands are transposed while
@@ -22,7 +22,16 @@
 
 namespace kt {
 
-constexpr int kTcBM = 128, kTcBK = 16, kTcThreads = 128;
+#ifndef KT_TC_THREADS
+#define KT_TC_THREADS 256  // A/B on the RL step (GEMM ms per step): 128 threads x 3 CTAs 9.14, 256 x 3 8.29, 256 x 2 10.2
+#endif
+#ifndef KT_TC_MINB
+#define KT_TC_MINB 3
+#endif
+// 128 threads: one warp per TMEM lane quadrant.  256: two warps per quadrant (they split the
+// tile's columns in the epilogue; MN-major operands are staged by one half each).
+constexpr int kTcBM = 128, kTcBK = 16, kTcThreads = KT_TC_THREADS;
+static_assert(kTcThreads == 128 || kTcThreads == 256, "one or two warps per TMEM lane quadrant");
 #ifndef KT_TC_LOOKAHEAD
 #define KT_TC_LOOKAHEAD 1  // chunks of global loads in flight ahead of the MMA issue (2 measured slower: fwd 3.55 -> 3.70 ms per RL step)
 #endif
@@ -48,23 +57,27 @@ struct TcGemmArgs {
 // current chunk is converted and handed to the tensor core: load_tile fills a
 // per-thread register fragment, store_tile splits it into tf32 hi/lo and writes
 // the canonical K-major layout.  A thread owns `kPer` 4-element vectors per tile.
-template <int ROWS_MAX>
+template <int ROWS_MAX, bool MN = false>
 struct Frag {
-    static constexpr int kPer = ROWS_MAX * (kTcBK / 4) / kTcThreads;
+    // K-major: every thread holds kPer 4-vectors; MN-major: a 4 x 4 block (threads of one half)
+    static constexpr int kPer = MN ? 4 : ROWS_MAX * (kTcBK / 4) / kTcThreads;
     float4 v[kPer];
 };
+// MN-major staging: the thread half that stages operand `b_op` (both halves of a 128-thread CTA)
+__device__ __forceinline__ int mn_thread(bool b_op) {
+    return kTcThreads == 256 && b_op ? int(threadIdx.x) - 128 : int(threadIdx.x);
+}
 
 template <bool MN_MAJOR, int ROWS_MAX>
-__device__ __forceinline__ void load_tile(Frag<ROWS_MAX>& fr, const float* __restrict__ G, int ld, int rows, int r0,
-                                          int rlimit, int k0, int klimit, bool vec_ok) {
+__device__ __forceinline__ void load_tile(Frag<ROWS_MAX, MN_MAJOR>& fr, const float* __restrict__ G, int ld, int rows,
+                                          int r0, int rlimit, int k0, int klimit, bool vec_ok, bool b_op) {
     if constexpr (MN_MAJOR) {
         // MN-major G[k * ld + r]: a thread owns a 4-row x 4-k block — four 16-byte loads along r
         // (coalesced across lanes), transposed to K-major in store_tile
-        static_assert(Frag<ROWS_MAX>::kPer == 4, "one 4x4 block per thread");
-        const int b = threadIdx.x, rgn = rows >> 2;
+        const int b = mn_thread(b_op), rgn = rows >> 2;
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) fr.v[kk] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (b < rows) {
+        if (b >= 0 && b < rows) {
             const int rb = b % rgn, kb = b / rgn;
             const int gr = r0 + 4 * rb;
 #pragma unroll
@@ -110,10 +123,11 @@ __device__ __forceinline__ void load_tile(Frag<ROWS_MAX>& fr, const float* __res
 }
 
 template <bool MN_MAJOR, int ROWS_MAX>
-__device__ __forceinline__ void store_tile(const Frag<ROWS_MAX>& fr, float* hi, float* lo, int rows) {
+__device__ __forceinline__ void store_tile(const Frag<ROWS_MAX, MN_MAJOR>& fr, float* hi, float* lo, int rows,
+                                           bool b_op) {
     if constexpr (MN_MAJOR) {
-        const int b = threadIdx.x, rgn = rows >> 2;
-        if (b >= rows) return;
+        const int b = mn_thread(b_op), rgn = rows >> 2;
+        if (b < 0 || b >= rows) return;
         const int rb = b % rgn, kb = b / rgn;
         const float* f0 = reinterpret_cast<const float*>(&fr.v[0]);
         const float* f1 = reinterpret_cast<const float*>(&fr.v[1]);
@@ -155,7 +169,7 @@ __device__ __forceinline__ uint64_t tile_desc(uint32_t base, int rows, int j) {
 }
 
 template <bool TA, bool TB>
-__global__ void __launch_bounds__(kTcThreads, 3) tc_gemm_kernel(TcGemmArgs g) {
+__global__ void __launch_bounds__(kTcThreads, KT_TC_MINB) tc_gemm_kernel(TcGemmArgs g) {
     extern __shared__ __align__(1024) unsigned char s_dyn[];
     __shared__ uint64_t mma_bar[2];
     __shared__ uint32_t tmem_slot;
@@ -188,13 +202,15 @@ __global__ void __launch_bounds__(kTcThreads, 3) tc_gemm_kernel(TcGemmArgs g) {
     // `prefetch` runs between the proxy fence and the block barrier: the fence waits for every
     // outstanding memory operation of the thread, so loads issued before it would be drained
     // there (the next chunk's global loads are only in flight across the MMA if issued after)
-    auto stage_and_issue = [&](const Frag<kTcBM>& A, const Frag<128>& B, int cc, auto&& prefetch) {
+    using FragA = Frag<kTcBM, A_MN>;
+    using FragB = Frag<128, B_MN>;
+    auto stage_and_issue = [&](const FragA& A, const FragB& B, int cc, auto&& prefetch) {
         const int s = cc & 1;
         if (cc >= 2) umma::mbar_wait(umma::smem_addr(&mma_bar[s]), uint32_t((cc - 2) >> 1) & 1u);
         float* st = base + s * stage_floats;
         float *a_hi = st, *a_lo = st + a_floats, *b_hi = st + 2 * a_floats, *b_lo = b_hi + b_floats;
-        store_tile<A_MN, kTcBM>(A, a_hi, a_lo, kTcBM);
-        store_tile<B_MN, 128>(B, b_hi, b_lo, BN);
+        store_tile<A_MN, kTcBM>(A, a_hi, a_lo, kTcBM, false);
+        store_tile<B_MN, 128>(B, b_hi, b_lo, BN, true);
         umma::fence_async_smem();
         prefetch();
         __syncthreads();
@@ -214,16 +230,16 @@ __global__ void __launch_bounds__(kTcThreads, 3) tc_gemm_kernel(TcGemmArgs g) {
         }
         __syncwarp();
     };
-    auto load_chunk = [&](Frag<kTcBM>& A, Frag<128>& B, int cc) {
+    auto load_chunk = [&](FragA& A, FragB& B, int cc) {
         const int k1 = kbeg + cc * kTcBK;
-        load_tile<A_MN, kTcBM>(A, g.A, g.lda, kTcBM, m0, g.M, k1, kend, a_vec);
-        load_tile<B_MN, 128>(B, g.B, g.ldb, BN, n0, g.N, k1, kend, b_vec);
+        load_tile<A_MN, kTcBM>(A, g.A, g.lda, kTcBM, m0, g.M, k1, kend, a_vec, false);
+        load_tile<B_MN, 128>(B, g.B, g.ldb, BN, n0, g.N, k1, kend, b_vec, true);
     };
 #if KT_TC_LOOKAHEAD == 2
     // global loads run two chunks ahead of the split + MMA issue (three register fragments,
     // statically indexed by unrolling the chunk loop by three)
-    Frag<kTcBM> fa[3];
-    Frag<128> fb[3];
+    FragA fa[3];
+    FragB fb[3];
     if (nchunks > 0) load_chunk(fa[0], fb[0], 0);
     if (nchunks > 1) load_chunk(fa[1], fb[1], 1);
 #pragma unroll 1
@@ -238,8 +254,8 @@ __global__ void __launch_bounds__(kTcThreads, 3) tc_gemm_kernel(TcGemmArgs g) {
         }
     }
 #else
-    Frag<kTcBM> fa[2];
-    Frag<128> fb[2];
+    FragA fa[2];
+    FragB fb[2];
     if (nchunks > 0) load_chunk(fa[0], fb[0], 0);
 #pragma unroll 1
     for (int c = 0; c < nchunks; c += 2) {
@@ -261,12 +277,14 @@ __global__ void __launch_bounds__(kTcThreads, 3) tc_gemm_kernel(TcGemmArgs g) {
     // transposes through shared memory (the stage buffers are free now) and writes
     // full 128-byte row segments, applying bias / tanh / tanh' per element.
     const int lane = tid & 31;
+    const int quad = warp & 3;                      // TMEM lane quadrant = the tile's rows 32q..32q+31
+    constexpr int kHalves = kTcThreads / 128;       // warps per quadrant, interleaved over 32-column groups
     float* scratch = base + warp * (32 * 33);
     float* Cz = g.C + size_t(blockIdx.z) * size_t(g.M) * g.ldc;
-    for (int c0 = 0; c0 < BN; c0 += 32) {
+    for (int c0 = 32 * (warp >> 2); c0 < BN; c0 += 32 * kHalves) {
         float v[32];
         if (nchunks > 0) {
-            umma::tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + uint32_t(c0), v);
+            umma::tmem_ld32(tmem + (uint32_t(quad * 32) << 16) + uint32_t(c0), v);
         } else {
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = 0.f;
@@ -277,7 +295,7 @@ __global__ void __launch_bounds__(kTcThreads, 3) tc_gemm_kernel(TcGemmArgs g) {
         const int n = n0 + c0 + lane;
         const bool col_ok = c0 + lane < BN && n < g.N;
         const float bias = col_ok && (g.epi == 1 || g.epi == 3) ? g.bias[n] : 0.f;
-        const int mbase = m0 + warp * 32;
+        const int mbase = m0 + quad * 32;
         float hv[32];
         if (g.epi == 2) {  // all 32 aux loads in flight before any store
 #pragma unroll
@@ -296,7 +314,7 @@ __global__ void __launch_bounds__(kTcThreads, 3) tc_gemm_kernel(TcGemmArgs g) {
             Cz[size_t(mm) * g.ldc + n] = x;
             csum += double(x);
         }
-        if (g.colpart && col_ok) g.colpart[size_t(blockIdx.y * 4 + warp) * g.N + n] = csum;
+        if (g.colpart && col_ok) g.colpart[size_t(blockIdx.y * 4 + quad) * g.N + n] = csum;
         __syncwarp();
     }
     umma::fence_before();
