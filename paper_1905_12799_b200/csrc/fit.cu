@@ -66,7 +66,7 @@ struct Grower {
     // output (one tree)
     std::vector<int32_t> feature, left, right;
     std::vector<double> threshold, value;
-    std::vector<double> buf, xs, csum, csq;
+    std::vector<double> buf, xs, csum, csq, gbuf;
     std::vector<int64_t> bnd;
     std::vector<uint8_t> in_left;
 
@@ -140,25 +140,29 @@ struct Grower {
             const double* cq = cqj[g];
             const double total = cs[mm - 1], total_sq = cq[mm - 1];
             const double parent_sse = total_sq - total * total / double(mm);
-            double g_best = 0.0;
-            int64_t b_best = -1;
-            for (int64_t i = 0; i < nb[g]; ++i) {
+            // gains at every boundary first (independent divisions pipeline), then np.argmax
+            const int64_t nbg = nb[g];
+            double* gains = gbuf.data();
+            for (int64_t i = 0; i < nbg; ++i) {
                 const int64_t b = bj[g][i];
                 const double ln = double(b + 1), rn = double(mm - (b + 1));
                 const double ls = cs[b], lq = cq[b];
                 const double sse_left = lq - ls * ls / ln;
                 const double d = total - ls;
                 const double sse_right = (total_sq - lq) - d * d / rn;
-                const double gain = parent_sse - sse_left - sse_right;
-                // np.argmax: first maximum; a NaN is the maximum (first NaN wins)
-                if (b_best < 0) {
+                gains[i] = parent_sse - sse_left - sse_right;
+            }
+            // np.argmax: first maximum; a NaN is the maximum (first NaN wins)
+            double g_best = gains[0];
+            int64_t i_best = 0;
+            for (int64_t i = 1; i < nbg && !std::isnan(g_best); ++i) {
+                const double gain = gains[i];
+                if (std::isnan(gain) || gain > g_best) {
                     g_best = gain;
-                    b_best = b;
-                } else if (!std::isnan(g_best) && (std::isnan(gain) || gain > g_best)) {
-                    g_best = gain;
-                    b_best = b;
+                    i_best = i;
                 }
             }
+            const int64_t b_best = bj[g][i_best];
             const double thr = (xsj[g][b_best] + xsj[g][b_best + 1]) / 2.0;
             if (!have || g_best > best_gain) {
                 have = true;
@@ -180,6 +184,7 @@ struct Grower {
             csq.resize(need);
             bnd.resize(need);
         }
+        if (gbuf.size() < size_t(mm)) gbuf.resize(size_t(mm));
         int j = 0;
         for (; j + kG <= n; j += kG) scan_group<kG>(ord, off, mm, j, have, best_gain, bf, bt);
         switch (n - j) {
@@ -223,20 +228,20 @@ struct Grower {
             in_left[r] = lft;
             nl += lft;
         }
-        int64_t li = 0, ri = nl;
-        for (int64_t i = 0; i < cnt; ++i) {
-            const int64_t r = rows[i];
-            nrows[in_left[r] ? li++ : ri++] = r;
-        }
-        for (int f = 0; f < n && depth + 1 < max_depth; ++f) {  // children at max depth are leaves: no orders
-            const int64_t* o = lvl_ord[depth].data() + size_t(f) * m + off;
-            int64_t* no = lvl_ord[depth + 1].data() + size_t(f) * m + off;
+        // branch-free (the side of a row is data-dependent: branches mispredict half the time)
+        auto partition = [&](const int64_t* src, int64_t* dst) {
             int64_t a2 = 0, b2 = nl;
             for (int64_t i = 0; i < cnt; ++i) {
-                const int64_t r = o[i];
-                no[in_left[r] ? a2++ : b2++] = r;
+                const int64_t r = src[i];
+                const int64_t lft = in_left[r];
+                dst[b2 + (a2 - b2) * lft] = r;
+                a2 += lft;
+                b2 += 1 - lft;
             }
-        }
+        };
+        partition(rows, nrows);
+        for (int f = 0; f < n && depth + 1 < max_depth; ++f)  // children at max depth are leaves: no orders
+            partition(lvl_ord[depth].data() + size_t(f) * m + off, lvl_ord[depth + 1].data() + size_t(f) * m + off);
         feature[node] = j;
         threshold[node] = t;
         const int l = grow(off, nl, depth + 1);
