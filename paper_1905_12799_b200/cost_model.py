@@ -90,9 +90,34 @@ class CostModel:
                            "trees": [t.to_dict() for t in self.trees]}, sort_keys=True)
 
 
-def feature_table(space) -> tuple[np.ndarray, np.ndarray]:
-    """log2(1 + value) lookup and negative-prefix counts (cost_model.py:235-249)."""
+_TABLES: dict = {}  # knob values -> (table, neg, forest table), read-only arrays
+
+
+def _tables(space):
     vals = sp.knob_values(space)
+    key = tuple(tuple(v) for v in vals)
+    hit = _TABLES.get(key)
+    if hit is None:
+        table, neg = _feature_table(vals)
+        ftab = table.copy()
+        for j, k in enumerate(neg):  # negative settings are rejected before scoring;
+            ftab[j, :k] = -np.inf    # -inf keeps the cut-point search monotone
+        for a in (table, neg, ftab):
+            a.setflags(write=False)
+        if len(_TABLES) > 256:
+            _TABLES.clear()
+        hit = _TABLES[key] = (table, neg, np.ascontiguousarray(ftab))
+    return hit
+
+
+def feature_table(space) -> tuple[np.ndarray, np.ndarray]:
+    """log2(1 + value) lookup and negative-prefix counts (cost_model.py:235-249); cached per
+    knob-value tuple, returned read-only."""
+    table, neg, _ = _tables(space)
+    return table, neg
+
+
+def _feature_table(vals) -> tuple[np.ndarray, np.ndarray]:
     width = max(len(v) for v in vals)
     table = np.zeros((len(vals), width), dtype=np.float64)
     neg = np.zeros(len(vals), dtype=np.int64)
@@ -109,20 +134,21 @@ class DeviceForest:
 
     def __init__(self, model, space, engine: _lib.Engine):
         cards = sp.check_engine_space(space)
-        table, neg = feature_table(space)
-        table = table.copy()
-        for j, k in enumerate(neg):  # negative settings are rejected before scoring;
-            table[j, :k] = -np.inf   # -inf keeps the cut-point search monotone
+        _, neg, table = _tables(space)
         trees = list(model.trees)
-        offs = [0]
-        for t in trees:
-            offs.append(offs[-1] + int(np.asarray(t.feature).size))
-        cat = lambda attr, dt: (np.ascontiguousarray(np.concatenate([np.asarray(getattr(t, attr), dtype=dt) for t in trees]))
-                                if trees else np.zeros(1, dtype=dt))
-        feat, thr = cat("feature", np.int32), cat("threshold", np.float64)
-        left, right, val = cat("child_left", np.int32), cat("child_right", np.int32), cat("value", np.float64)
-        node_off = np.asarray(offs, dtype=np.int32)
-        table = np.ascontiguousarray(table)
+        flat = getattr(model, "__dict__", {}).get("_b200_flat")  # set by fit(): the same nodes, flat
+        if flat is not None:
+            node_off, feat, thr, left, right, val = flat
+        else:
+            offs = [0]
+            for t in trees:
+                offs.append(offs[-1] + int(np.asarray(t.feature).size))
+            cat = lambda attr, dt: (np.ascontiguousarray(np.concatenate([np.asarray(getattr(t, attr), dtype=dt)
+                                                                         for t in trees]))
+                                    if trees else np.zeros(1, dtype=dt))
+            feat, thr = cat("feature", np.int32), cat("threshold", np.float64)
+            left, right, val = cat("child_left", np.int32), cat("child_right", np.int32), cat("value", np.float64)
+            node_off = np.asarray(offs, dtype=np.int32)
         h = _lib.P()
         _lib.call("kt_forest_create", engine.handle, int(cards.size), _lib.as_ptr(cards, _lib.C.c_int32),
                   _lib.as_ptr(table, _lib.C.c_double), int(table.shape[1]), len(trees),
@@ -269,6 +295,14 @@ def fit(training, params=BoostParams(), seed: int = 0, engine=None, device: bool
     trees = []
     for r in range(int(params.rounds)):
         a, b = int(offs[r]), int(offs[r + 1])
-        trees.append(Tree(feature=feat[a:b].copy(), threshold=thr[a:b].copy(), child_left=left[a:b].copy(),
-                          child_right=right[a:b].copy(), value=val[a:b].copy()))
-    return CostModel(trees=tuple(trees), base_score=float(base.value), feature_count=n)
+        # views of the flat node arrays (the model owns them; DeviceForest packs the same arrays)
+        trees.append(Tree(feature=feat[a:b], threshold=thr[a:b], child_left=left[a:b], child_right=right[a:b],
+                          value=val[a:b]))
+    model = CostModel(trees=tuple(trees), base_score=float(base.value), feature_count=n)
+    used = int(offs[int(params.rounds)])
+    flat = (offs, feat[:used], thr[:used], left[:used], right[:used], val[:used])
+    try:  # DeviceForest packs these directly instead of re-concatenating the trees
+        object.__setattr__(model, "_b200_flat", flat)
+    except (AttributeError, TypeError):
+        pass
+    return model

@@ -1722,6 +1722,8 @@ __global__ void __launch_bounds__(256) argmax_kernel(const double* __restrict__ 
 
 
 // ============================================================ orchestration
+constexpr int64_t kLloydMinPerBlock = 1;  // resident kernel: fewest points per block before shrinking the grid
+
 // Launch plan of one Lloyd launch over m points and K clusters in R runs: the resident
 // kernel whenever the state fits shared memory, else the streaming kernel.
 struct LloydPlan {
@@ -1736,7 +1738,11 @@ static LloydPlan plan_lloyd(kt_engine* e, int64_t m, int K, int R, LloydArgs& a)
     // streaming kernel (state in global memory, dynamic chunk scheduling).
     const char* mode = std::getenv("KT_LLOYD_MODE");
     const bool force_stream = mode && std::strcmp(mode, "stream") == 0;
-    const int64_t P = ((ceil_div(m, int64_t(e->num_sms)) + 15) & ~int64_t(15));
+    // blocks of the resident kernel: one per SM, fewer for small point sets (a pass is then
+    // latency-bound and its grid barrier gets cheaper with fewer arrivals)
+    int blocks = int(std::max<int64_t>(1, std::min<int64_t>(e->num_sms, ceil_div(m, kLloydMinPerBlock))));
+    if (const char* b = std::getenv("KT_LLOYD_BLOCKS")) blocks = std::max(1, std::min(e->num_sms, std::atoi(b)));
+    const int64_t P = ((ceil_div(m, int64_t(blocks)) + 15) & ~int64_t(15));
     const bool bytes = a.fmt.bytes != 0;
     // byte rows: the byte kernel packs all 8 bytes (unused knobs are 0), field bound 255
     const int64_t field_max = bytes ? 255 : std::max<int64_t>(1, a.fmt.cmax);
@@ -1768,7 +1774,7 @@ static LloydPlan plan_lloyd(kt_engine* e, int64_t m, int K, int R, LloydArgs& a)
     }
     if (resident) {
         smem = res_smem;
-        grid = e->num_sms;
+        grid = blocks;
         threads = kLloydResThreads;
         kern = kres;
         a.per_block = P;

@@ -244,6 +244,7 @@ def tune_rows(space, landscape, strategy: str, budget: int, seed: int = 0,
         rounds = 1
     while len(run.configs) < budget and not (stop_fitness is not None and best >= stop_fitness):
         round_index = rounds
+        rseed = round_seed(seed, round_index)
         remaining = budget - len(run.configs)
         traj = None
         if strategy in ("rl", "rl+as", "sa", "sa+as"):
@@ -267,9 +268,9 @@ def tune_rows(space, landscape, strategy: str, budget: int, seed: int = 0,
             else:
                 sidx = random_configs(cards, rng, sa_params.chains)
                 srows = torch.from_numpy(sp.pack(sidx, cards).view(np.int64)).to(dev)
-                traj = run_sa_rows(sa_params, model, space, srows, round_seed(seed, round_index), engine=eng)
+                traj = run_sa_rows(sa_params, model, space, srows, rseed, engine=eng)
         if strategy.endswith("+as"):
-            brows = adaptive_sample_rows(traj[0], m_rows[:m_cnt], space, round_seed(seed, round_index), engine=eng)
+            brows = adaptive_sample_rows(traj[0], m_rows[:m_cnt], space, rseed, engine=eng)
             batch = [tuple(r) for r in sp.unpack(brows, n, cards).tolist()]
         elif traj is not None:  # _top_unvisited, driver.py:101-115, on the device
             brows = top_unvisited_rows(traj[0], traj[1], m_rows[:m_cnt], GREEDY_BATCH, engine=eng)

@@ -31,9 +31,12 @@ def main() -> None:
     for sync in (False, True):
         acc = collections.defaultdict(lambda: [0, 0.0])
         orig = {}
-        for name in ("fit", "run_sa_rows", "adaptive_sample_rows", "runtimes_rows", "random_unvisited"):
-            fn = getattr(tune, name)
-            orig[name] = fn
+        from paper_1905_12799_b200 import sa as sa_mod
+        targets = [(tune, n) for n in ("fit", "run_sa_rows", "adaptive_sample_rows", "runtimes_rows",
+                                       "random_unvisited")] + [(sa_mod, "device_forest")]
+        for mod, name in targets:
+            fn = getattr(mod, name)
+            orig[(mod, name)] = fn
 
             def wrapped(*a, _fn=fn, _name=name, **k):
                 t = time.perf_counter()
@@ -44,7 +47,7 @@ def main() -> None:
                 acc[_name][1] += time.perf_counter() - t
                 return out
 
-            setattr(tune, name, wrapped)
+            setattr(mod, name, wrapped)
         try:
             tune.tune_rows(space, landscape_from_dict(fx["landscapes"][0], space), bench.W95_STRATEGY, 100, 1,
                            engine=eng)
@@ -60,13 +63,13 @@ def main() -> None:
                 total += time.perf_counter() - t
                 rounds += run.rounds
         finally:
-            for name, fn in orig.items():
-                setattr(tune, name, fn)
+            for (mod, name), fn in orig.items():
+                setattr(mod, name, fn)
         print(f"sync={sync}: {total * 1e3:.2f} ms over 5 landscapes, {rounds} rounds "
               f"({total / rounds * 1e6:.0f} us/round)")
         for name, (cnt, sec) in sorted(acc.items(), key=lambda kv: -kv[1][1]):
             print(f"  {name:22s} {cnt:4d} calls {sec * 1e3:8.2f} ms  {sec / max(cnt, 1) * 1e6:8.1f} us/call")
-        other = total - sum(v[1] for v in acc.values())
+        other = total - sum(v[1] for k, v in acc.items() if k != "device_forest")
         print(f"  {'(loop body / host)':22s}           {other * 1e3:8.2f} ms")
 
     # kernel time per round (engine CUDA-event timing; serialises launches, so only the split counts)
