@@ -208,12 +208,20 @@ def test_adaptive_sample_uniform_s2_vs_oracle(seed):
     assert [tuple(r) for r in sp.unpack(got, 8).tolist()] == want
 
 
-@pytest.mark.parametrize("mode", ["stream", "tile64", "gather", "init_chunked", "pack5"])
+@pytest.mark.parametrize("mode", ["stream", "tile64", "gather", "init_chunked", "pack5", "grid", "cluster8", "blocks7"])
 @pytest.mark.parametrize("seed", [0, 1, 2])
 def test_lloyd_variants_vs_oracle(mode, seed, monkeypatch):
     """Both Lloyd kernels (streaming, and resident with many queue tiles per block) and both k-means++
-    kernels (resident, chunked) agree with the oracle."""
-    if mode == "init_chunked":
+    kernels (resident, chunked) agree with the oracle; small point sets also through the cooperative
+    grid (grid: no cluster), an 8-block cluster, and a 7-block cooperative grid."""
+    if mode == "grid":
+        monkeypatch.setenv("KT_LLOYD_CLUSTER", "0")
+    elif mode == "cluster8":
+        monkeypatch.setenv("KT_LLOYD_CLUSTER", "8")
+    elif mode == "blocks7":
+        monkeypatch.setenv("KT_LLOYD_CLUSTER", "0")
+        monkeypatch.setenv("KT_LLOYD_BLOCKS", "7")
+    elif mode == "init_chunked":
         monkeypatch.setenv("KT_INIT_MODE", "chunked")
     elif mode == "stream":
         monkeypatch.setenv("KT_LLOYD_MODE", "stream")

@@ -10,6 +10,7 @@ continuous CUDA-event-timed region of K steps in variants:
   chunked   full, the scores' D2H split into 16 copies
   zerocopy  H2D rows; predict writes the scores straight into pinned host memory (UVA), no D2H
   prio      full, the engine on a high-priority stream and the D2H on a low-priority one
+  late      full, but step s's scores D2H is issued once step s's clustering has returned
 usage: python tools/e2e_probe.py [steps]
 """
 
@@ -59,8 +60,8 @@ def main() -> None:
         scored = [torch.cuda.Event() for _ in range(2)]
         drained = [torch.cuda.Event() for _ in range(2)]
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        copies = variant in ("full", "no_d2h", "chunked", "zerocopy", "prio")
-        d2h = variant in ("full", "chunked", "prio")
+        copies = variant in ("full", "no_d2h", "chunked", "zerocopy", "prio", "late")
+        d2h = variant in ("full", "chunked", "prio", "late")
         d2h_stream = lo_stream if variant == "prio" else d2h_plain
         eng.set_stream(hi_stream if variant == "prio" else eng_stream0)
 
@@ -88,6 +89,12 @@ def main() -> None:
             if d2h:
                 with eng.scope():
                     scored[i].record(eng.stream)
+                if variant != "late":
+                    drain(s)
+
+        def drain(s):
+            i = s % 2
+            if True:
                 with torch.cuda.stream(d2h_stream):
                     d2h_stream.wait_event(scored[i])
                     if variant == "chunked":
@@ -110,6 +117,8 @@ def main() -> None:
             if s + 2 < K:
                 upload(s + 2)
             kt.adaptive_sample_rows(rows(s), vis[s], space, 2000 + s, engine=eng)
+            if variant == "late":
+                drain(s)
             if variant == "flushed":
                 with eng.scope():
                     flush.fill_(float(s))
@@ -120,7 +129,7 @@ def main() -> None:
         torch.cuda.synchronize()
         return a.elapsed_time(b) / K
 
-    for v in ("full", "no_d2h", "resident", "flushed", "chunked", "zerocopy", "prio", "full", "resident"):
+    for v in ("full", "no_d2h", "resident", "flushed", "chunked", "zerocopy", "prio", "late", "full", "resident"):
         run(v)  # warm
         ms = sorted(run(v) for _ in range(3))[1]
         print(f"{v:10s} {ms:.4f} ms/step  {N / ms * 1e3:.3e} cand/s")
