@@ -472,7 +472,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     kernel_table = {k: {"launches": c, "ms_total": round(ms, 4), "ms_per_step": round(ms / K, 4)}
                     for k, (c, ms) in sorted(stats.items(), key=lambda kv: -kv[1][1])}
     base = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:  # the CPU baseline is reported at N = 1 only
         base = cpu_baseline(doc, cards, args.cpu_sample, full=0 if args.no_cpu_full else N)
     chosen = sorted({i.chosen_k for i in infos})
     line = {
@@ -499,7 +499,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         "cpu_baseline": base,
         "parity": parity,
     }
-    if not args.no_wall95:
+    if not args.no_wall95 and world == 1:  # metric 2 is a single-task, single-GPU number
         line["wall_to_95"] = w95_ours(eng)
     if not args.no_extra_configs and world == 1:  # configs[1..4] beside the headline (after its timing)
         from tools import extra_configs
