@@ -18,12 +18,12 @@ for w in $WHAT; do
       timeout 900 python bench.py --impl reference > "$OUT/bench_ref.json" 2> "$OUT/bench_ref.err"; echo "ref rc=$?"; cut -c1-300 "$OUT/bench_ref.json";;
     launches)
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$OUT/launches.csv" \
-        python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-wall95 > "$OUT/launches_bench.log" 2>&1; echo "launches rc=$?";;
+        python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-wall95 --no-extra-configs > "$OUT/launches_bench.log" 2>&1; echo "launches rc=$?";;
     full)
       for kr in lloyd:lloyd score_trees:score_trees dedup_insert:dedup_insert init_kernel:init_res_kernel; do
         k=${kr%%:*}; re=${kr#*:}
         timeout 900 ncu --set full --clock-control none --import-source on -k regex:$re -s 2 -c 1 -o "$OUT/prof_$k" \
-          python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-wall95 > "$OUT/prof_$k.log" 2>&1; echo "full $k rc=$?"
+          python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-wall95 --no-extra-configs > "$OUT/prof_$k.log" 2>&1; echo "full $k rc=$?"
       done;;
     timeline)
       KT_LIB_PATH=build/ab/probes.so KT_LLOYD_TIMELINE=1 timeout 300 python tools/lloyd_probe.py > "$OUT/timeline.txt" 2>&1; echo "timeline rc=$?"

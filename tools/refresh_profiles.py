@@ -57,7 +57,7 @@ if launches.exists():
     tot = sum(v for _, v in agg.values())
     with open(dst / "launches_summary.txt", "w") as f:
         f.write("# ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised); "
-                f"bench.py --steps 2 --warmup 1 --no-wall95 (capture {tag})\n# kernel, launches, total ns, share\n")
+                f"bench.py --steps 2 --warmup 1 --no-wall95 --no-extra-configs (capture {tag})\n# kernel, launches, total ns, share\n")
         for k, (c, v) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
             f.write(f"{k:60s} {c:6d} {v:14.1f} {100 * v / tot:6.2f}%\n")
     for old in dst.glob("launches_bench_*.csv"):
