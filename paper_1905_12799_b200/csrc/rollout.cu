@@ -9,7 +9,9 @@
 // float64) fit in shared memory, where one TMA bulk copy stages them while the
 // threads derive their PCG64 streams.  Activations live transposed
 // ([feature][agent]); warp w computes outputs [16w, 16w+16) of a layer for its
-// 32 agents, reading each weight row as a broadcast 16-byte load.
+// 32 agents — a lane two agents x 8 outputs, so each broadcast 16-byte weight load
+// feeds four FMAs (the shared-load issue rate, not the FP64 pipe, bounded the
+// one-agent-per-lane mapping: MIO throttle was its top stall).
 //
 // Determinism / parity.  Episode e draws its uniforms from
 // PCG64(SeedSequence(seed, spawn_key=(round, e))) on the device, n per step
@@ -96,6 +98,65 @@ __global__ void __launch_bounds__(kRolloutThreads, 1) rollout_kernel(RolloutArgs
         __syncthreads();
         if (!sm.any_active) break;
 
+#if KT_ROLLOUT_PAIR
+        // lane (half, p): agents 2p and 2p + 1, outputs [o1, o1 + 8) — every broadcast weight load
+        // feeds both agents (half the shared loads per FMA of one agent per lane); per (output,
+        // agent) the same sequential fma chain over k as the one-agent mapping
+        const int half = lane >> 4, p2 = 2 * (lane & 15);
+        const int o1 = o0 + 8 * half;
+        // ---- h1 = tanh(x W1^T + b1)
+        {
+            double acc0[8], acc1[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc0[j] = acc1[j] = 0.0;
+            for (int k = 0; k < n; ++k) {
+                const double2 x2 = *reinterpret_cast<const double2*>(&sm.xt[k][p2]);
+                const double2* wr = reinterpret_cast<const double2*>(&sm.w.w1t[k][o1]);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const double2 w2 = wr[q];
+                    acc0[2 * q] = fma(x2.x, w2.x, acc0[2 * q]);
+                    acc0[2 * q + 1] = fma(x2.x, w2.y, acc0[2 * q + 1]);
+                    acc1[2 * q] = fma(x2.y, w2.x, acc1[2 * q]);
+                    acc1[2 * q + 1] = fma(x2.y, w2.y, acc1[2 * q + 1]);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const double b = sm.w.b1[o1 + j];
+                *reinterpret_cast<double2*>(&sm.h[o1 + j][p2]) = make_double2(tanh(acc0[j] + b), tanh(acc1[j] + b));
+            }
+        }
+        __syncthreads();
+        // ---- [hp | hv] = tanh(h1 [W2p | W2v]^T + [b2p | b2v])
+        {
+            double acc0[8], acc1[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc0[j] = acc1[j] = 0.0;
+            if ((o1 & (kG - 1)) < a.g) {  // outputs wholly inside the zero padding have nothing to add
+#pragma unroll 4
+                for (int k = 0; k < a.h; ++k) {
+                    const double2 h2 = *reinterpret_cast<const double2*>(&sm.h[k][p2]);
+                    const double2* wr = reinterpret_cast<const double2*>(&sm.w.w2t[k][o1]);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const double2 w2 = wr[q];
+                        acc0[2 * q] = fma(h2.x, w2.x, acc0[2 * q]);
+                        acc0[2 * q + 1] = fma(h2.x, w2.y, acc0[2 * q + 1]);
+                        acc1[2 * q] = fma(h2.y, w2.x, acc1[2 * q]);
+                        acc1[2 * q + 1] = fma(h2.y, w2.y, acc1[2 * q + 1]);
+                    }
+                }
+            }
+            __syncthreads();  // every warp has read h1
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const double b = sm.w.b2[o1 + j];
+                *reinterpret_cast<double2*>(&sm.h[o1 + j][p2]) = make_double2(tanh(acc0[j] + b), tanh(acc1[j] + b));
+            }
+        }
+        __syncthreads();
+#else
         // ---- h1 = tanh(x W1^T + b1)
         {
             double acc[kRolloutOut];
@@ -138,6 +199,7 @@ __global__ void __launch_bounds__(kRolloutThreads, 1) rollout_kernel(RolloutArgs
             for (int j = 0; j < kRolloutOut; ++j) sm.h[o0 + j][lane] = tanh(acc[j] + sm.w.b2[o0 + j]);
         }
         __syncthreads();
+#endif
         // ---- logits (warp w: knob w's three) and the value (warp n, or warp 7 when n == 8)
         {
             if (warp < n) {
