@@ -16,6 +16,7 @@
 // fp32 in TMEM.  The epilogue (bias + tanh, tanh derivative, or split-K
 // partial store) reads TMEM with tcgen05.ld, one row per thread.
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 #include "umma.cuh"
@@ -23,7 +24,7 @@
 namespace kt {
 
 #ifndef KT_TC_THREADS
-#define KT_TC_THREADS 256  // A/B on the RL step (GEMM ms per step): 128 threads x 3 CTAs 9.14, 256 x 3 8.29, 256 x 2 10.2
+#define KT_TC_THREADS 256  // A/B on the RL step (GEMM ms per step): 128 threads x 3 CTAs 9.14, 256 x 3 8.29, 256 x 2 10.2; + specialised epilogue loops 7.78
 #endif
 #ifndef KT_TC_MINB
 #define KT_TC_MINB 3
@@ -302,19 +303,32 @@ __global__ void __launch_bounds__(kTcThreads, KT_TC_MINB) tc_gemm_kernel(TcGemmA
             for (int r = 0; r < 32; ++r)
                 hv[r] = (col_ok && mbase + r < g.M) ? __ldg(g.aux + size_t(mbase + r) * g.ldaux + n) : 0.f;
         }
-        double csum = 0.0;  // this warp's 32 rows of column n, in row order (bias gradients)
+        // one specialised store loop per epilogue (uniform branch outside the 32-row loop);
+        // csum = this warp's 32 rows of column n in row order (bias gradients), only if wanted
+        auto store_rows = [&](auto op, auto want_csum) {
+            double csum = 0.0;
 #pragma unroll
-        for (int r = 0; r < 32; ++r) {
-            const int mm = mbase + r;
-            if (mm >= g.M || !col_ok) continue;
-            float x = scratch[r * 33 + lane];
-            if (g.epi == 1) x = tanhf(x + bias);
-            else if (g.epi == 3) x = x + bias;
-            else if (g.epi == 2) x = x * (1.0f - hv[r] * hv[r]);
-            Cz[size_t(mm) * g.ldc + n] = x;
-            csum += double(x);
-        }
-        if (g.colpart && col_ok) g.colpart[size_t(blockIdx.y * 4 + quad) * g.N + n] = csum;
+            for (int r = 0; r < 32; ++r) {
+                const int mm = mbase + r;
+                if (mm >= g.M || !col_ok) continue;
+                const float x = op(scratch[r * 33 + lane], r);
+                Cz[size_t(mm) * g.ldc + n] = x;
+                if constexpr (decltype(want_csum)::value) csum += double(x);
+            }
+            return csum;
+        };
+        auto store = [&](auto op) {
+            if (g.colpart) {
+                const double cs = store_rows(op, std::true_type{});
+                if (col_ok) g.colpart[size_t(blockIdx.y * 4 + quad) * g.N + n] = cs;
+            } else {
+                store_rows(op, std::false_type{});
+            }
+        };
+        if (g.epi == 1) store([&](float x, int) { return tanhf(x + bias); });
+        else if (g.epi == 3) store([&](float x, int) { return x + bias; });
+        else if (g.epi == 2) store([&](float x, int r) { return x * (1.0f - hv[r] * hv[r]); });
+        else store([](float x, int) { return x; });
         __syncwarp();
     }
     umma::fence_before();
