@@ -726,7 +726,30 @@ struct RunShared {
     unsigned int chg_g[kMaxRuns];  // changed flags of the whole grid (after the barrier)
     int empty[kMaxRuns];           // a cluster of the run ended the pass empty
     float dmax[kMaxRuns];          // largest shrink D_j of the run's clusters (scan prefilter)
+    int spec_bad[2];               // by pass parity: a run's shrink outgrew the speculative scan's table
 };
+
+// Speculative scan (resident kernel, one tile per block): while a block waits at the grid
+// barrier of pass t it already scans its points for pass t+1 against s_dspec[g] = D_a(t+1)
+// estimate = D_a(t) + G (G = kSpecFactor x the run's largest shrink step of the last pass).
+// The decision phase checks the real D_a(t+1) <= s_dspec for every cluster of every run
+// that goes on; then every point the scan settled has b - D_a(t+1) >= b - s_dspec > margin
+// (rounded down), so the speculative queue holds every unsettled point (and a few settled
+// ones, which an evaluation leaves unchanged: evaluations are exact).  Otherwise the queue
+// is dropped and the pass scans as before.
+#ifndef KT_LLOYD_SPEC
+#define KT_LLOYD_SPEC 1
+#endif
+#ifndef KT_SPEC_FACTOR
+#define KT_SPEC_FACTOR 1.25f
+#endif
+constexpr float kSpecFactor = KT_SPEC_FACTOR;
+#ifndef KT_SPEC_RETEST
+#define KT_SPEC_RETEST 0
+#endif
+#ifndef KT_SPEC_PERCLUSTER
+#define KT_SPEC_PERCLUSTER 1
+#endif
 
 // Conservative |fp32 - exact| bound for sum_i (p_i - c_i)^2 with p_i, |c_i| <= 255
 // (derivation in DESIGN.md §K8).
@@ -1088,6 +1111,7 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
     __shared__ uint8_t run_of[kMaxClusters];
     __shared__ LloydQueueEntry wqueue[RESIDENT ? 1 : kLloydThreads / 32 * 128];
     __shared__ int s_qn[2];  // resident kernel: queue counters (alternating tiles)
+    __shared__ float s_dspec[RESIDENT && KT_LLOYD_SPEC ? kMaxClusters : 1];  // speculative shrink table
     // the dynamic window is only guaranteed 8-byte aligned after static smem (tools add their
     // own static smem): align explicitly for the float4 centroid loads (16 spare bytes allocated)
     // generic pointer arithmetic measured faster here than align_shared<16> (1.60 vs 1.95 ms per 1M-point knee scan)
@@ -1183,6 +1207,30 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
             grid.sync();
         }
     };
+    // the same barrier split in two, so a block can work between its arrival and its wait
+    auto grid_arrive = [&]() {
+        if (RESIDENT && a.cluster) {
+            asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        } else {
+            __syncthreads();
+            if (threadIdx.x == 0) asm volatile("atom.add.release.gpu.u32 _, [%0], 1;" ::"l"(a.barrier) : "memory");
+        }
+    };
+    auto grid_wait = [&]() {
+        if (RESIDENT && a.cluster) {
+            asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+        } else {
+            const unsigned int target = ++n_bar * gridDim.x;
+            if (threadIdx.x == 0) {
+                unsigned int cur;
+                do {
+                    asm volatile("ld.relaxed.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(a.barrier) : "memory");
+                } while (cur < target);
+                asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(a.barrier) : "memory");
+            }
+            __syncthreads();
+        }
+    };
     grid_barrier();  // every block has read a.cent / a.dcum before block 0 overwrites them
 
     int it = a.it0;
@@ -1193,13 +1241,76 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
             a.timeline[it * 16 + phase] = t;
         }
     };
+    // scan of points [t0, t1): kScanQuads quads per thread and round (independent loads, one
+    // warp scan + one queue atomic per warp and round); unsettled (point, run, old) -> queue.
+    // dtab: the shrink table the budgets are tested against (dcum, or the speculative s_dspec)
+    auto scan_tile = [&](int t0, int t1, int* qn, const float* dtab) {
+        const int tq1 = (t1 + 3) >> 2;
+        for (int qd0 = t0 >> 2; qd0 < tq1; qd0 += kScanQuads * blockDim.x) {
+            for (int r = 0; r < R; ++r) {
+                const int st = rs.state[r];
+                if (!run_active(st)) continue;
+                const int co = a.coff[r];
+                unsigned todo = 0;  // bit 4q + e: point e of quad q
+                uint32_t as4[kScanQuads];
+#pragma unroll
+                for (int q = 0; q < kScanQuads; ++q) {
+                    const int qd = qd0 + q * blockDim.x + tid;
+                    const int p0 = qd << 2;
+                    const int cnt = qd < tq1 ? (t1 - p0 < 4 ? t1 - p0 : 4) : 0;
+                    as4[q] = 0xffffffffu;
+                    if (cnt > 0) {
+                        as4[q] = *reinterpret_cast<const uint32_t*>(s_asg + r * P + p0);
+                        if (st == kActiveFromSums) {
+                            const float4 b4 = *reinterpret_cast<const float4*>(s_bud + r * P + p0);
+                            const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const int old = (as4[q] >> (8 * e)) & 0xff;
+                                if (e >= cnt) continue;
+                                if (old == 255 || !(__fsub_rd(bb[e], dtab[co + old]) > kSettleMargin))
+                                    todo |= 1u << (4 * q + e);
+                            }
+                        } else {
+                            todo |= ((1u << cnt) - 1u) << (4 * q);
+                        }
+                    }
+                }
+                // warp-aggregated append
+                const int c = __popc(todo);
+                int incl = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                int wbase = 0;
+                if (lane == 31 && incl) wbase = atomicAdd(qn, incl);
+                wbase = __shfl_sync(0xffffffffu, wbase, 31);
+                int pos = wbase + incl - c;
+                while (todo) {
+                    const int bit = __ffs(todo) - 1;
+                    todo &= todo - 1;
+                    const int q = bit >> 2, e = bit & 3;
+                    const int p0 = (qd0 + q * int(blockDim.x) + tid) << 2;
+                    uint32_t aq = as4[0];  // select without dynamic register indexing
+#pragma unroll
+                    for (int qq = 1; qq < kScanQuads; ++qq) aq = q == qq ? as4[qq] : aq;
+                    s_queue[pos++] = uint32_t(p0 + e) | (uint32_t(r) << 16) | (((aq >> (8 * e)) & 0xffu) << 24);
+                }
+            }
+        }
+    };
     int tile_parity = 0;  // queue counter in use (alternates per tile, across passes too)
     bool entry = true;
+    bool spec_hit = false;    // this pass's queue was built by the previous pass's speculative scan
+    bool spec_ready = false;  // s_dspec holds the next pass's table (after a decision phase)
     while (it < a.it_end) {
         stamp(0);
         if (tid == 0) {  // written by this pass's update, read after its final barrier
             rs.exit_flag[it & 1] = 0;
             rs.n_active[it & 1] = 0;
+            rs.spec_bad[it & 1] = 0;
         }
         if (tid < kMaxRuns) rs.empty[tid] = 0;  // likewise (ordered by the tile / grid barriers)
         if (entry) {  // launch entry; later passes get their centroids from the fused update below
@@ -1287,63 +1398,9 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
             for (int t0 = 0; t0 < np; t0 += a.tile) {
                 const int t1 = t0 + a.tile < np ? t0 + a.tile : np;
                 int* qn = s_qn + tile_parity;
-                // scan: kScanQuads quads per thread and round (independent loads, one warp
-                // scan + one queue atomic per warp and round); unsettled (point, run, old) -> queue
-                const int tq1 = (t1 + 3) >> 2;
-                for (int qd0 = t0 >> 2; qd0 < tq1; qd0 += kScanQuads * blockDim.x) {
-                    for (int r = 0; r < R; ++r) {
-                        const int st = rs.state[r];
-                        if (!run_active(st)) continue;
-                        const int co = a.coff[r];
-                        unsigned todo = 0;  // bit 4q + e: point e of quad q
-                        uint32_t as4[kScanQuads];
-#pragma unroll
-                        for (int q = 0; q < kScanQuads; ++q) {
-                            const int qd = qd0 + q * blockDim.x + tid;
-                            const int p0 = qd << 2;
-                            const int cnt = qd < tq1 ? (t1 - p0 < 4 ? t1 - p0 : 4) : 0;
-                            as4[q] = 0xffffffffu;
-                            if (cnt > 0) {
-                                as4[q] = *reinterpret_cast<const uint32_t*>(s_asg + r * P + p0);
-                                if (st == kActiveFromSums) {
-                                    const float4 b4 = *reinterpret_cast<const float4*>(s_bud + r * P + p0);
-                                    const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
-#pragma unroll
-                                    for (int e = 0; e < 4; ++e) {
-                                        const int old = (as4[q] >> (8 * e)) & 0xff;
-                                        if (e >= cnt) continue;
-                                        if (old == 255 || !(__fsub_rd(bb[e], dcum[co + old]) > kSettleMargin))
-                                            todo |= 1u << (4 * q + e);
-                                    }
-                                } else {
-                                    todo |= ((1u << cnt) - 1u) << (4 * q);
-                                }
-                            }
-                        }
-                        // warp-aggregated append
-                        const int c = __popc(todo);
-                        int incl = c;
-#pragma unroll
-                        for (int o = 1; o < 32; o <<= 1) {
-                            const int y = __shfl_up_sync(0xffffffffu, incl, o);
-                            if (lane >= o) incl += y;
-                        }
-                        int wbase = 0;
-                        if (lane == 31 && incl) wbase = atomicAdd(qn, incl);
-                        wbase = __shfl_sync(0xffffffffu, wbase, 31);
-                        int pos = wbase + incl - c;
-                        while (todo) {
-                            const int bit = __ffs(todo) - 1;
-                            todo &= todo - 1;
-                            const int q = bit >> 2, e = bit & 3;
-                            const int p0 = (qd0 + q * int(blockDim.x) + tid) << 2;
-                            uint32_t aq = as4[0];  // select without dynamic register indexing
-#pragma unroll
-                            for (int qq = 1; qq < kScanQuads; ++qq) aq = q == qq ? as4[qq] : aq;
-                            s_queue[pos++] = uint32_t(p0 + e) | (uint32_t(r) << 16) | (((aq >> (8 * e)) & 0xffu) << 24);
-                        }
-                    }
-                }
+                const bool spec_pass = spec_hit;  // the queue holds candidates tested against s_dspec
+                if (!spec_hit) scan_tile(t0, t1, qn, dcum);
+                spec_hit = false;
                 if (t0 == 0) stamp(10);
                 __syncthreads();
                 if (t0 == 0) stamp(2);
@@ -1368,6 +1425,13 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
                     for (int u = 0; u < kEvalUnroll; ++u) {
                         if (ent[u] == 0xffffffffu) continue;
                         const int pl = int(ent[u] & 0xffffu), r = int((ent[u] >> 16) & 0xff), old = int(ent[u] >> 24);
+                        if (KT_LLOYD_SPEC && spec_pass) {
+                            if (!run_active(rs.state[r])) continue;  // a speculative entry of a run that stopped
+                            // re-test against the real shrink table: the scan's guard let it through
+                            if (KT_SPEC_RETEST && old != 255 &&
+                                __fsub_rd(s_bud[r * P + pl], dcum[a.coff[r] + old]) > kSettleMargin)
+                                continue;
+                        }
                         float bud;
                         const int j = lloyd_assign(a, fmt, c32, c2, s_pcoff, c64, dcum, r, row[u], bud);
                         s_bud[r * P + pl] = bud;
@@ -1509,7 +1573,20 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
             if (tid == 0) a.work[nb] = 0u;
         }
         stamp(4);
-        grid_barrier();
+        bool spec_scanned = false;
+        if (RESIDENT && KT_LLOYD_SPEC) {
+            grid_arrive();
+            // speculative scan for the next pass (every active run must continue from sums)
+            bool ok = spec_ready && np <= a.tile && it + 1 < a.it_end && it + 1 < a.max_iters;
+            for (int r = 0; r < R && ok; ++r) ok = !run_active(rs.state[r]) || rs.state[r] == kActiveFromSums;
+            if (ok) {
+                scan_tile(0, np, s_qn + tile_parity, s_dspec);
+                spec_scanned = true;
+            }
+            grid_wait();
+        } else {
+            grid_barrier();
+        }
         stamp(5);
 
         // ---- fused update (identical in every block): sums += grid deltas, the next pass's
@@ -1581,10 +1658,32 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
                         const unsigned o1 = (lane + 32 < k && lane + 32 != am) ? b1 : 0u;
                         const float m1 = __uint_as_float(mx);
                         const float m2 = __uint_as_float(__reduce_max_sync(0xffffffffu, o0 > o1 ? o0 : o1));
-                        if (lane < k)
-                            dcum[co + lane] = __fadd_ru(dcum[co + lane], __fadd_ru(d0, lane == am ? m2 : m1));
-                        if (lane + 32 < k)
-                            dcum[co + lane + 32] = __fadd_ru(dcum[co + lane + 32], __fadd_ru(d1, lane + 32 == am ? m2 : m1));
+                        const float s0 = __fadd_ru(d0, lane == am ? m2 : m1), s1 = __fadd_ru(d1, lane + 32 == am ? m2 : m1);
+                        const float n0 = lane < k ? __fadd_ru(dcum[co + lane], s0) : 0.0f;
+                        const float n1 = lane + 32 < k ? __fadd_ru(dcum[co + lane + 32], s1) : 0.0f;
+                        if (lane < k) dcum[co + lane] = n0;
+                        if (lane + 32 < k) dcum[co + lane + 32] = n1;
+                        if (KT_LLOYD_SPEC && RESIDENT) {
+                            // check the speculative table this pass's scan used, then the next one:
+                            // D_a(t+2) estimate = D_a(t+1) + kSpecFactor x this pass's largest step
+                            const bool bad = (lane < k && !(n0 <= s_dspec[co + lane])) ||
+                                             (lane + 32 < k && !(n1 <= s_dspec[co + lane + 32]));
+                            if (__any_sync(0xffffffffu, bad) && lane == 0) {
+                                rs.spec_bad[it & 1] = 1;
+                                s_qn[tile_parity] = 0;  // drop the speculative queue (its scan ended before the wait)
+                            }
+                            float G0, G1;
+                            if (KT_SPEC_PERCLUSTER) {  // each cluster's own last step
+                                G0 = __fmul_ru(s0, kSpecFactor);
+                                G1 = __fmul_ru(s1, kSpecFactor);
+                            } else {  // the run's largest last step
+                                const float stepmax = __uint_as_float(__reduce_max_sync(
+                                    0xffffffffu, __float_as_uint(fmaxf(lane < k ? s0 : 0.0f, lane + 32 < k ? s1 : 0.0f))));
+                                G0 = G1 = __fmul_ru(stepmax, kSpecFactor);
+                            }
+                            if (lane < k) s_dspec[co + lane] = __fadd_ru(n0, G0);
+                            if (lane + 32 < k) s_dspec[co + lane + 32] = __fadd_ru(n1, G1);
+                        }
                     }
                     __syncwarp();  // every lane has read rs.state[r]
                     if (lane == 0) {
@@ -1612,6 +1711,9 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
         stamp(9);
         __syncthreads();
         const bool stop = rs.exit_flag[it & 1] || rs.n_active[it & 1] == 0;
+        spec_hit = spec_scanned && !rs.spec_bad[it & 1];
+        if (kLloydProbes && a.stats && tid == 0 && spec_scanned) rs.cnt[0][1] += spec_hit ? 1u : 1000u;  // hits + 1000 x misses
+        spec_ready = true;
         ++it;
         if (stop) break;
     }
