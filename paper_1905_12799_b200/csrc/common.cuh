@@ -170,6 +170,10 @@ struct kt_engine {
     void* scratch(const std::string& name, size_t bytes);
     // Named, growable pinned host staging buffer.
     void* staging(const std::string& name, size_t bytes);
+    // Small device -> pinned-host read-back on the engine stream, written by a one-block kernel
+    // through the pinned buffer's UVA mapping: it never queues behind a large D2H copy on the
+    // copy engine (the e2e leg's 8 MB score copies).  host_dst must come from staging().
+    void d2h(void* host_dst, const void* dev_src, size_t bytes);
     void note_launch(int n = 1) { launches += n; }
     void pre_launch(const char* what);    // call right before a kernel launch
     void check_launch(const char* what);  // call right after it

@@ -141,6 +141,27 @@ void* kt_engine::staging(const std::string& name, size_t bytes) {
     return b.ptr;
 }
 
+namespace {
+__global__ void readback_kernel(uint32_t* __restrict__ dst, const uint32_t* __restrict__ src, size_t words) {
+    for (size_t i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+}
+}  // namespace
+
+void kt_engine::d2h(void* host_dst, const void* dev_src, size_t bytes) {
+    // KT_D2H_COPY=1: plain cudaMemcpyAsync (A/B switch)
+    static const bool use_copy = std::getenv("KT_D2H_COPY") != nullptr;
+    if (use_copy || (bytes & 3) || (reinterpret_cast<uintptr_t>(host_dst) & 3) ||
+        (reinterpret_cast<uintptr_t>(dev_src) & 3)) {
+        KT_CUDA(cudaMemcpyAsync(host_dst, dev_src, bytes, cudaMemcpyDeviceToHost, stream));
+        return;
+    }
+    if (bytes == 0) return;
+    pre_launch("readback");
+    readback_kernel<<<1, 256, 0, stream>>>(static_cast<uint32_t*>(host_dst), static_cast<const uint32_t*>(dev_src),
+                                           bytes / 4);
+    check_launch("readback");
+}
+
 cudaEvent_t kt_engine::take_event() {
     if (!event_pool.empty()) {
         cudaEvent_t ev = event_pool.back();

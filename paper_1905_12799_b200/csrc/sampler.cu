@@ -187,7 +187,7 @@ int64_t dedup(kt_engine* e, const uint64_t* rows, int64_t count, uint64_t* out) 
     dedup_scatter_kernel<<<nb, 256, 0, e->stream>>>(rows, count, bits, offsets, out);
     e->check_launch("dedup_scatter");
     auto* h_total = static_cast<int64_t*>(e->staging("dedup.total", 8));
-    KT_CUDA(cudaMemcpyAsync(h_total, offsets + nb, 8, cudaMemcpyDeviceToHost, e->stream));
+    e->d2h(h_total, offsets + nb, 8);
     e->sync();
     return *h_total;
 }
@@ -266,7 +266,7 @@ static const unsigned int* mode_hist_async(kt_engine* e, const uint64_t* rows, i
     mode_hist_kernel<<<grid, 256, smem, e->stream>>>(rows, count, a, hist);
     e->check_launch("mode_hist");
     auto* h = static_cast<unsigned int*>(e->staging("mode.hist", smem));
-    KT_CUDA(cudaMemcpyAsync(h, hist, smem, cudaMemcpyDeviceToHost, e->stream));
+    e->d2h(h, hist, smem);
     return h;
 }
 
@@ -2178,18 +2178,18 @@ struct KmeansSession {
             launch_lloyd(e, plan, a);
             e->check_launch("lloyd");
             ++lloyd_launches;
-            KT_CUDA(cudaMemcpyAsync(h_ctrl, a.ctrl, 4, cudaMemcpyDeviceToHost, e->stream));
-            KT_CUDA(cudaMemcpyAsync(h_state, a.run_state, R * 4, cudaMemcpyDeviceToHost, e->stream));
+            e->d2h(h_ctrl, a.ctrl, 4);
+            e->d2h(h_state, a.run_state, R * 4);
             if (history) {
                 pairwise_loss(e, pts, m, n, fmt, a.assign, a.cent, d_loss);
-                KT_CUDA(cudaMemcpyAsync(h_loss, d_loss, 8, cudaMemcpyDeviceToHost, e->stream));
+                e->d2h(h_loss, d_loss, 8);
             } else {
                 // speculatively finish (no reseed is the common case): losses, pass counts and
                 // centroids come back with the launch state in one synchronisation
                 pairwise_loss_runs(e, pts, m, n, fmt, a.assign, a.stride, a.cent, a.coff, R, d_loss);
-                KT_CUDA(cudaMemcpyAsync(h_loss, d_loss, R * 8, cudaMemcpyDeviceToHost, e->stream));
-                KT_CUDA(cudaMemcpyAsync(h_iter, a.run_iter, R * 4, cudaMemcpyDeviceToHost, e->stream));
-                KT_CUDA(cudaMemcpyAsync(h_cent, a.cent, size_t(K) * kMaxKnobs * 8, cudaMemcpyDeviceToHost, e->stream));
+                e->d2h(h_loss, d_loss, R * 8);
+                e->d2h(h_iter, a.run_iter, R * 4);
+                e->d2h(h_cent, a.cent, size_t(K) * kMaxKnobs * 8);
             }
             e->sync();
             it = h_ctrl[0];
@@ -2200,7 +2200,7 @@ struct KmeansSession {
                 active |= run_active(h_state[r]);
             }
             if (reseed) {
-                KT_CUDA(cudaMemcpyAsync(h_S, a.S, size_t(K) * kSumW * 8, cudaMemcpyDeviceToHost, e->stream));
+                e->d2h(h_S, a.S, size_t(K) * kSumW * 8);
                 e->sync();
                 for (int r = 0; r < R; ++r)
                     if (h_state[r] == kNeedsReseed) reseed_run(a, r, h_S);
@@ -2214,9 +2214,9 @@ struct KmeansSession {
         std::vector<RunResult> out(R);
         if (history) {
             pairwise_loss_runs(e, pts, m, n, fmt, a.assign, a.stride, a.cent, a.coff, R, d_loss);
-            KT_CUDA(cudaMemcpyAsync(h_loss, d_loss, R * 8, cudaMemcpyDeviceToHost, e->stream));
-            KT_CUDA(cudaMemcpyAsync(h_iter, a.run_iter, R * 4, cudaMemcpyDeviceToHost, e->stream));
-            KT_CUDA(cudaMemcpyAsync(h_cent, a.cent, size_t(K) * kMaxKnobs * 8, cudaMemcpyDeviceToHost, e->stream));
+            e->d2h(h_loss, d_loss, R * 8);
+            e->d2h(h_iter, a.run_iter, R * 4);
+            e->d2h(h_cent, a.cent, size_t(K) * kMaxKnobs * 8);
             e->sync();
         }
         if (a.slack) {
@@ -2303,8 +2303,8 @@ struct KmeansSession {
             e->pre_launch("argmax");
             argmax_kernel<<<grid, 256, 0, e->stream>>>(pd2, m, d_blocked, int(blocked.size()), pv, pi);
             e->check_launch("argmax");
-            KT_CUDA(cudaMemcpyAsync(h_pv, pv, size_t(grid) * 8, cudaMemcpyDeviceToHost, e->stream));
-            KT_CUDA(cudaMemcpyAsync(h_pi, pi, size_t(grid) * 8, cudaMemcpyDeviceToHost, e->stream));
+            e->d2h(h_pv, pv, size_t(grid) * 8);
+            e->d2h(h_pi, pi, size_t(grid) * 8);
             e->sync();
             double bv = -1.0;
             int64_t bi = -1;
@@ -2318,7 +2318,7 @@ struct KmeansSession {
         }
         // fetch the chosen points' rows
         for (size_t q = 0; q < blocked.size(); ++q)
-            KT_CUDA(cudaMemcpyAsync(h_rows + q, pts + blocked[q], 8, cudaMemcpyDeviceToHost, e->stream));
+            e->d2h(h_rows + q, pts + blocked[q], 8);
         e->sync();
         for (size_t q = 0; q < empties.size(); ++q)
             for (int i = 0; i < n; ++i) newc[size_t(empties[q]) * kMaxKnobs + i] = double(fmt.get(h_rows[q], i));
@@ -2712,9 +2712,9 @@ int kt_lloyd_run(kt_engine* e, kt_lloyd* l, kt_comm* comm, int batch, int32_t* s
                                                              l->it_dev, l->it_dev + 1);
             e->check_launch("lloyd_apply_dev");
         }
-        KT_CUDA(cudaMemcpyAsync(hs, l->it_dev, 8, cudaMemcpyDeviceToHost, e->stream));
-        KT_CUDA(cudaMemcpyAsync(hs + 2, a.run_state, a.R * 4, cudaMemcpyDeviceToHost, e->stream));
-        KT_CUDA(cudaMemcpyAsync(hs + 2 + kMaxRuns, a.run_iter, a.R * 4, cudaMemcpyDeviceToHost, e->stream));
+        e->d2h(hs, l->it_dev, 8);
+        e->d2h(hs + 2, a.run_state, a.R * 4);
+        e->d2h(hs + 2 + kMaxRuns, a.run_iter, a.R * 4);
         e->sync();
         l->it = hs[0];
         bool active = false;
@@ -2738,8 +2738,8 @@ int kt_lloyd_apply(kt_engine* e, kt_lloyd* l, const uint64_t* ext_dev, int32_t* 
     e->check_launch("lloyd_apply");
     ++l->it;
     auto* hs = static_cast<int*>(e->staging("lloyd.state", 2 * kMaxRuns * 4));
-    KT_CUDA(cudaMemcpyAsync(hs, a.run_state, a.R * 4, cudaMemcpyDeviceToHost, e->stream));
-    KT_CUDA(cudaMemcpyAsync(hs + kMaxRuns, a.run_iter, a.R * 4, cudaMemcpyDeviceToHost, e->stream));
+    e->d2h(hs, a.run_state, a.R * 4);
+    e->d2h(hs + kMaxRuns, a.run_iter, a.R * 4);
     e->sync();
     for (int r = 0; r < a.R; ++r) {
         states_out[r] = hs[r];
