@@ -142,7 +142,10 @@ void* kt_engine::staging(const std::string& name, size_t bytes) {
 }
 
 namespace {
-__global__ void readback_kernel(uint32_t* __restrict__ dst, const uint32_t* __restrict__ src, size_t words) {
+// one warp, few registers: it fits beside a resident Lloyd / GEMM block on a busy SM, so an engine's
+// read-back never waits for another engine's cooperative launch to drain (concurrent engines)
+__global__ void __launch_bounds__(32) readback_kernel(uint32_t* __restrict__ dst, const uint32_t* __restrict__ src,
+                                                      size_t words) {
     for (size_t i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
 }
 }  // namespace
@@ -157,7 +160,7 @@ void kt_engine::d2h(void* host_dst, const void* dev_src, size_t bytes) {
     }
     if (bytes == 0) return;
     pre_launch("readback");
-    readback_kernel<<<1, 256, 0, stream>>>(static_cast<uint32_t*>(host_dst), static_cast<const uint32_t*>(dev_src),
+    readback_kernel<<<1, 32, 0, stream>>>(static_cast<uint32_t*>(host_dst), static_cast<const uint32_t*>(dev_src),
                                            bytes / 4);
     check_launch("readback");
 }
