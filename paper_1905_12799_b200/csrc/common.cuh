@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <map>
+#include <initializer_list>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -174,6 +175,13 @@ struct kt_engine {
     // through the pinned buffer's UVA mapping: it never queues behind a large D2H copy on the
     // copy engine (the e2e leg's 8 MB score copies).  host_dst must come from staging().
     void d2h(void* host_dst, const void* dev_src, size_t bytes);
+    // up to 8 such read-backs in one launch
+    struct D2H {
+        void* dst;
+        const void* src;
+        size_t bytes;
+    };
+    void d2h(std::initializer_list<D2H> regions);
     void note_launch(int n = 1) { launches += n; }
     void pre_launch(const char* what);    // call right before a kernel launch
     void check_launch(const char* what);  // call right after it

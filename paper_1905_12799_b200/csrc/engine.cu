@@ -148,7 +148,39 @@ __global__ void __launch_bounds__(32) readback_kernel(uint32_t* __restrict__ dst
                                                       size_t words) {
     for (size_t i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
 }
+struct ReadbackList {
+    uint32_t* dst[8];
+    const uint32_t* src[8];
+    uint32_t words[8];
+    int n;
+};
+__global__ void __launch_bounds__(32) readback_list_kernel(ReadbackList l) {
+    for (int r = 0; r < l.n; ++r)
+        for (uint32_t i = threadIdx.x; i < l.words[r]; i += blockDim.x) l.dst[r][i] = l.src[r][i];
+}
 }  // namespace
+
+void kt_engine::d2h(std::initializer_list<D2H> regions) {
+    static const bool use_copy = std::getenv("KT_D2H_COPY") != nullptr;
+    ReadbackList l{};
+    for (const D2H& d : regions) {
+        const bool ok = !use_copy && !(d.bytes & 3) && !(reinterpret_cast<uintptr_t>(d.dst) & 3) &&
+                        !(reinterpret_cast<uintptr_t>(d.src) & 3) && d.bytes / 4 < (size_t(1) << 31) && l.n < 8;
+        if (!ok) {
+            KT_CUDA(cudaMemcpyAsync(d.dst, d.src, d.bytes, cudaMemcpyDeviceToHost, stream));
+            continue;
+        }
+        if (!d.bytes) continue;
+        l.dst[l.n] = static_cast<uint32_t*>(d.dst);
+        l.src[l.n] = static_cast<const uint32_t*>(d.src);
+        l.words[l.n] = uint32_t(d.bytes / 4);
+        ++l.n;
+    }
+    if (!l.n) return;
+    pre_launch("readback");
+    readback_list_kernel<<<1, 32, 0, stream>>>(l);
+    check_launch("readback");
+}
 
 void kt_engine::d2h(void* host_dst, const void* dev_src, size_t bytes) {
     // KT_D2H_COPY=1: plain cudaMemcpyAsync (A/B switch)

@@ -2178,18 +2178,15 @@ struct KmeansSession {
             launch_lloyd(e, plan, a);
             e->check_launch("lloyd");
             ++lloyd_launches;
-            e->d2h(h_ctrl, a.ctrl, 4);
-            e->d2h(h_state, a.run_state, R * 4);
             if (history) {
                 pairwise_loss(e, pts, m, n, fmt, a.assign, a.cent, d_loss);
-                e->d2h(h_loss, d_loss, 8);
+                e->d2h({{h_ctrl, a.ctrl, 4}, {h_state, a.run_state, size_t(R) * 4}, {h_loss, d_loss, 8}});
             } else {
                 // speculatively finish (no reseed is the common case): losses, pass counts and
-                // centroids come back with the launch state in one synchronisation
+                // centroids come back with the launch state in one read-back and one synchronisation
                 pairwise_loss_runs(e, pts, m, n, fmt, a.assign, a.stride, a.cent, a.coff, R, d_loss);
-                e->d2h(h_loss, d_loss, R * 8);
-                e->d2h(h_iter, a.run_iter, R * 4);
-                e->d2h(h_cent, a.cent, size_t(K) * kMaxKnobs * 8);
+                e->d2h({{h_ctrl, a.ctrl, 4}, {h_state, a.run_state, size_t(R) * 4}, {h_loss, d_loss, size_t(R) * 8},
+                        {h_iter, a.run_iter, size_t(R) * 4}, {h_cent, a.cent, size_t(K) * kMaxKnobs * 8}});
             }
             e->sync();
             it = h_ctrl[0];
@@ -2214,9 +2211,8 @@ struct KmeansSession {
         std::vector<RunResult> out(R);
         if (history) {
             pairwise_loss_runs(e, pts, m, n, fmt, a.assign, a.stride, a.cent, a.coff, R, d_loss);
-            e->d2h(h_loss, d_loss, R * 8);
-            e->d2h(h_iter, a.run_iter, R * 4);
-            e->d2h(h_cent, a.cent, size_t(K) * kMaxKnobs * 8);
+            e->d2h({{h_loss, d_loss, size_t(R) * 8}, {h_iter, a.run_iter, size_t(R) * 4},
+                    {h_cent, a.cent, size_t(K) * kMaxKnobs * 8}});
             e->sync();
         }
         if (a.slack) {
