@@ -744,6 +744,14 @@ struct RunShared {
 #define KT_SPEC_FACTOR 1.25f
 #endif
 constexpr float kSpecFactor = KT_SPEC_FACTOR;
+// Only where the scan is long enough to hide: blocks of >= 1536 points (1M points, 7,056 per
+// block: 1.19 -> 1.13 ms per knee scan; 262K, 1,772 per block: 0.83 -> 0.78).  With fewer points
+// per block the scan is short and the extra evaluations cost more than the overlap saves
+// (AlexNet RL tasks, ~900 points per block: Lloyd 4.51 -> 4.81 ms per RL step with speculation).
+#ifndef KT_SPEC_MIN_POINTS
+#define KT_SPEC_MIN_POINTS 1536
+#endif
+constexpr int kSpecMinPoints = KT_SPEC_MIN_POINTS;
 #ifndef KT_SPEC_RETEST
 #define KT_SPEC_RETEST 0
 #endif
@@ -1574,7 +1582,7 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
         }
         stamp(4);
         bool spec_scanned = false;
-        if (RESIDENT && KT_LLOYD_SPEC) {
+        if (RESIDENT && KT_LLOYD_SPEC && P >= kSpecMinPoints) {
             grid_arrive();
             // speculative scan for the next pass (every active run must continue from sums)
             bool ok = spec_ready && np <= a.tile && it + 1 < a.it_end && it + 1 < a.max_iters;
@@ -1663,7 +1671,7 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
                         const float n1 = lane + 32 < k ? __fadd_ru(dcum[co + lane + 32], s1) : 0.0f;
                         if (lane < k) dcum[co + lane] = n0;
                         if (lane + 32 < k) dcum[co + lane + 32] = n1;
-                        if (KT_LLOYD_SPEC && RESIDENT) {
+                        if (KT_LLOYD_SPEC && RESIDENT && P >= kSpecMinPoints) {
                             // check the speculative table this pass's scan used, then the next one:
                             // D_a(t+2) estimate = D_a(t+1) + kSpecFactor x this pass's largest step
                             const bool bad = (lane < k && !(n0 <= s_dspec[co + lane])) ||
