@@ -661,6 +661,7 @@ struct LloydArgs {
     float* dcum;               // [K] cumulative bound shrink D_j (carried across launches)
     int64_t per_block;         // resident kernel: points owned by each block (multiple of 16)
     int tile;                  // resident kernel: points per queue tile (multiple of 4)
+    float spec_factor;         // speculative scan guard (kSpecFactor; KT_LLOYD_SPEC_FACTOR in tests)
     int rows_resident;         // resident kernel: the block's rows live in shared memory too
     int external;              // 1: one pass, deltas + changed counts -> ext, no in-kernel decisions
     int pack3;                 // resident kernel, P * largest knob index < 2^21: 3-word cluster deltas
@@ -1682,12 +1683,12 @@ __global__ void __launch_bounds__(RESIDENT ? kLloydResThreads : kLloydThreads, R
                             }
                             float G0, G1;
                             if (KT_SPEC_PERCLUSTER) {  // each cluster's own last step
-                                G0 = __fmul_ru(s0, kSpecFactor);
-                                G1 = __fmul_ru(s1, kSpecFactor);
+                                G0 = __fmul_ru(s0, a.spec_factor);
+                                G1 = __fmul_ru(s1, a.spec_factor);
                             } else {  // the run's largest last step
                                 const float stepmax = __uint_as_float(__reduce_max_sync(
                                     0xffffffffu, __float_as_uint(fmaxf(lane < k ? s0 : 0.0f, lane + 32 < k ? s1 : 0.0f))));
-                                G0 = G1 = __fmul_ru(stepmax, kSpecFactor);
+                                G0 = G1 = __fmul_ru(stepmax, a.spec_factor);
                             }
                             if (lane < k) s_dspec[co + lane] = __fadd_ru(n0, G0);
                             if (lane + 32 < k) s_dspec[co + lane + 32] = __fadd_ru(n1, G1);
@@ -1933,6 +1934,10 @@ static LloydPlan plan_lloyd(kt_engine* e, int64_t m, int K, int R, LloydArgs& a,
         a.tile = int(tile);
         a.rows_resident = rows_res ? 1 : 0;
         a.pack3 = pack3 ? 1 : 0;
+        a.spec_factor = kSpecFactor;
+        // tests: 0 makes nearly every speculative scan miss (rescan path), a large factor makes
+        // every one hit with many extra evaluations — both must stay bit-exact
+        if (const char* f = std::getenv("KT_LLOYD_SPEC_FACTOR")) a.spec_factor = std::max(0.0f, float(std::atof(f)));
         a.cluster = cluster;
         if (const char* t = std::getenv("KT_LLOYD_TILE"))  // tests: force many tiles per block
             a.tile = std::max(4, std::min(a.tile, std::atoi(t) & ~3));
@@ -1951,6 +1956,7 @@ static LloydPlan plan_lloyd(kt_engine* e, int64_t m, int K, int R, LloydArgs& a,
         a.tile = 0;
         a.rows_resident = 0;
         a.pack3 = 0;
+        a.spec_factor = kSpecFactor;
         a.cluster = 0;
     }
     return pl;

@@ -240,7 +240,10 @@ LARGE = json.loads((GOLDEN / "large.json").read_text())
 
 LLOYD_MODES = {"resident": {}, "stream": {"KT_LLOYD_MODE": "stream"}, "tile64": {"KT_LLOYD_TILE": "64"},
                "gather": {"KT_LLOYD_ROWS": "global"}, "init_chunked": {"KT_INIT_MODE": "chunked"},
-               "pack5": {"KT_LLOYD_PACK5": "1"}}
+               "pack5": {"KT_LLOYD_PACK5": "1"},
+               # speculative scan (blocks of >= 1536 points): guard 0 -> almost every pass rescans,
+               # guard 16 -> every speculative queue is used, with many extra (exact) evaluations
+               "spec_miss": {"KT_LLOYD_SPEC_FACTOR": "0"}, "spec_wide": {"KT_LLOYD_SPEC_FACTOR": "16"}}
 
 
 @pytest.mark.parametrize("mode", sorted(LLOYD_MODES))
@@ -367,7 +370,7 @@ def _bench_case(name, mode, monkeypatch):
     assert hashlib.sha256(asg.tobytes()).hexdigest() == g["assignment_sha256"]
 
 
-@pytest.mark.parametrize("mode", ["resident", "tile64", "pack5"])
+@pytest.mark.parametrize("mode", ["resident", "tile64", "pack5", "spec_miss", "spec_wide"])
 def test_bench_headline_config_bit_exact(mode, monkeypatch):
     """bench.py's exact headline step (1,048,576 uniform S2 candidates, candidate seed 0, seed 1000):
     distinct count, knee curve, centroids, assignment, batch with and without the bench's visited set
