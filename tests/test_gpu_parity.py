@@ -208,13 +208,21 @@ def test_adaptive_sample_uniform_s2_vs_oracle(seed):
     assert [tuple(r) for r in sp.unpack(got, 8).tolist()] == want
 
 
-@pytest.mark.parametrize("mode", ["stream", "tile64", "gather", "init_chunked", "pack5", "grid", "cluster8", "blocks7"])
+@pytest.mark.parametrize("mode", ["stream", "tile64", "gather", "init_chunked", "pack5", "grid", "cluster8", "blocks7",
+                                  "blocks7_miss", "cluster1"])
 @pytest.mark.parametrize("seed", [0, 1, 2])
 def test_lloyd_variants_vs_oracle(mode, seed, monkeypatch):
     """Both Lloyd kernels (streaming, and resident with many queue tiles per block) and both k-means++
     kernels (resident, chunked) agree with the oracle; small point sets also through the cooperative
-    grid (grid: no cluster), an 8-block cluster, and a 7-block cooperative grid."""
-    if mode == "grid":
+    grid (grid: no cluster), an 8-block cluster, and a 7-block cooperative grid.  The 7-block grid
+    (>= 1,536 points per block from 20K candidates on) and the one-block cluster run the speculative
+    scan at small sizes, blocks7_miss with a zero guard (almost every pass drops its queue)."""
+    if mode == "blocks7_miss":
+        monkeypatch.setenv("KT_LLOYD_SPEC_FACTOR", "0")
+        mode = "blocks7"
+    if mode == "cluster1":
+        monkeypatch.setenv("KT_LLOYD_CLUSTER", "1")
+    elif mode == "grid":
         monkeypatch.setenv("KT_LLOYD_CLUSTER", "0")
     elif mode == "cluster8":
         monkeypatch.setenv("KT_LLOYD_CLUSTER", "8")
