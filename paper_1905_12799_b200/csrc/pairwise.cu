@@ -1,5 +1,6 @@
 // pairwise.cu — see pairwise.cuh.
 #include <algorithm>
+#include <cstring>
 #include <map>
 #include <mutex>
 #include <string>
@@ -63,18 +64,27 @@ std::shared_ptr<PairwiseTree> make_tree(int64_t m) {
     t->level_start.push_back(I);
     t->n_levels = int(t->level_start.size()) - 1;
     t->root = enc(root);
-    KT_CUDA(cudaMalloc(&t->d_leaf_start, std::max<size_t>(1, L) * 8));
-    KT_CUDA(cudaMalloc(&t->d_leaf_len, std::max<size_t>(1, L) * 4));
-    KT_CUDA(cudaMalloc(&t->d_left, std::max<size_t>(1, I) * 4));
-    KT_CUDA(cudaMalloc(&t->d_right, std::max<size_t>(1, I) * 4));
-    KT_CUDA(cudaMalloc(&t->d_level, t->level_start.size() * 4));
-    KT_CUDA(cudaMemcpy(t->d_level, t->level_start.data(), t->level_start.size() * 4, cudaMemcpyHostToDevice));
-    KT_CUDA(cudaMemcpy(t->d_leaf_start, t->leaf_start.data(), L * 8, cudaMemcpyHostToDevice));
-    KT_CUDA(cudaMemcpy(t->d_leaf_len, t->leaf_len.data(), L * 4, cudaMemcpyHostToDevice));
+    // one device allocation and one copy for the five arrays (a new length costs one cudaMalloc
+    // and one synchronous copy instead of five each: the tuning loop's lengths change every round)
+    const size_t o_len = size_t(std::max(1, L)) * 8, o_left = o_len + size_t(std::max(1, L)) * 4;
+    const size_t o_right = o_left + size_t(std::max(1, I)) * 4, o_level = o_right + size_t(std::max(1, I)) * 4;
+    const size_t total = o_level + t->level_start.size() * 4;
+    std::vector<unsigned char> hb(total, 0);
+    std::memcpy(hb.data(), t->leaf_start.data(), size_t(L) * 8);
+    std::memcpy(hb.data() + o_len, t->leaf_len.data(), size_t(L) * 4);
     if (I) {
-        KT_CUDA(cudaMemcpy(t->d_left, t->node_left.data(), I * 4, cudaMemcpyHostToDevice));
-        KT_CUDA(cudaMemcpy(t->d_right, t->node_right.data(), I * 4, cudaMemcpyHostToDevice));
+        std::memcpy(hb.data() + o_left, t->node_left.data(), size_t(I) * 4);
+        std::memcpy(hb.data() + o_right, t->node_right.data(), size_t(I) * 4);
     }
+    std::memcpy(hb.data() + o_level, t->level_start.data(), t->level_start.size() * 4);
+    KT_CUDA(cudaMalloc(&t->d_block, total));
+    KT_CUDA(cudaMemcpy(t->d_block, hb.data(), total, cudaMemcpyHostToDevice));
+    auto* base = static_cast<unsigned char*>(t->d_block);
+    t->d_leaf_start = reinterpret_cast<int64_t*>(base);
+    t->d_leaf_len = reinterpret_cast<int32_t*>(base + o_len);
+    t->d_left = reinterpret_cast<int32_t*>(base + o_left);
+    t->d_right = reinterpret_cast<int32_t*>(base + o_right);
+    t->d_level = reinterpret_cast<int32_t*>(base + o_level);
     return t;
 }
 

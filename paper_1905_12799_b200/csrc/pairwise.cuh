@@ -29,13 +29,8 @@ struct PairwiseTree {
     int32_t* d_level = nullptr;
     int root = 0;
     int n_levels = 0;
-    ~PairwiseTree() {
-        cudaFree(d_leaf_start);
-        cudaFree(d_leaf_len);
-        cudaFree(d_left);
-        cudaFree(d_right);
-        cudaFree(d_level);
-    }
+    void* d_block = nullptr;  // the five device arrays above, one allocation
+    ~PairwiseTree() { cudaFree(d_block); }
 };
 
 std::shared_ptr<const PairwiseTree> pairwise_tree(int device, int64_t m);
